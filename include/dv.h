@@ -1,0 +1,262 @@
+/*
+ * dv.h -- C ABI of dvstream, a B200-native implementation of DejaVuLib's KV-cache streaming
+ * hot path (Strati et al., "DejaVu: KV-cache Streaming for Fast, Fault-tolerant Generative LLM
+ * Serving", arXiv 2403.01876).
+ *
+ * The three levels follow the paper's primitives (Table 1):
+ *   dv_stream_out / dv_stream_in   "Given a source (or destination) worker, the KV cache, and the
+ *                                   inference setup ... find the proper destinations (or sources)
+ *                                   for the different chunks of KV cache. This might involve
+ *                                   splitting the cache at the source or merging cache chunks at
+ *                                   the destination."
+ *   dv_scatter / dv_gather         "Given a non-contiguous region of KV cache, and a local or
+ *                                   remote destination (or source), chunk the region to
+ *                                   contiguous transfers and orchestrate movement."
+ *   dv_flush / dv_fetch            "Copy a contiguous chunk of KV cache, on the same or remote
+ *                                   host."
+ * Note the naming: the paper's `scatter` is the SEND side (non-contiguous region -> contiguous
+ * chunk); its kernel is called "pack" inside the library, `gather`'s kernel "unpack".
+ *
+ * Conventions (all calls):
+ *   - Every function returns a dv_status; on failure dv_last_error() holds a message (thread-local).
+ *   - Validation happens before anything is enqueued: an error has no partial effect.
+ *   - Data calls are asynchronous and stream-ordered on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream). No call synchronises the device except dv_destroy and the
+ *     explicitly blocking dv_query on device-resident flags.
+ *   - The caller owns KV caches, inboxes it allocated, and streams. The library owns its staging
+ *     pool, ticket counters and anything returned by dv_host_alloc/dv_device_alloc until freed.
+ *   - There is no CPU fallback: without a usable CUDA device every data call fails (DV_ECUDA).
+ *
+ * Data layout (reading Q1 of DESIGN.md; PAPER.md:131 fn 5, PAPER.md:119 preallocation):
+ *   DV_LAYOUT_KV5D: K and V are each [n_layers][n_reqs][n_heads][max_seq][head_dim] arrays of
+ *   elem_bytes-wide words, dense, row-major; element (l, r, h, s, d) (cache-local l, r) sits at
+ *   byte ((((l*n_reqs + r)*n_heads + h)*max_seq + s)*head_dim + d)*elem_bytes.
+ *   Words are opaque (fp16/bf16 bit patterns are moved, never converted; NaN payloads survive).
+ *
+ * Wire format (reading Q3): a region [l0,l1)x[r0,r1)x[s0,s1) packs to the dense array
+ *   [l-l0][kv][r-r0][h][s-s0][d]  (kv: 0 = K, 1 = V), i.e. 2*nL*nR*H*n*D*e bytes, d fastest.
+ *
+ * Alignment: cache bases, endpoint bases/offsets and head_dim*elem_bytes must be multiples of
+ * 16 bytes (else DV_EALIGN).
+ */
+#ifndef DV_H_
+#define DV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DV_API __attribute__((visibility("default")))
+#else
+#define DV_API
+#endif
+
+typedef enum dv_status {
+  DV_OK = 0,
+  DV_EINVAL = 1,  /* malformed argument (NULL pointer, negative extent, bad enum, capacity)   */
+  DV_EMAP = 2,    /* setups / caches do not hold the region's layers or requests */
+  DV_ERANGE = 3,  /* pos_end exceeds max_seq on a side; message names the limit  */
+  DV_EALIGN = 4,  /* a base/offset or head_dim*elem_bytes is not a multiple of 16 bytes        */
+  DV_ENOMEM = 5,  /* staging pool or an allocation could not be satisfied                     */
+  DV_EPEER = 6,   /* IPC export/open failed or a blob is malformed                            */
+  DV_EBUSY = 7,   /* reserved: inbox without credit                                           */
+  DV_ECUDA = 8,   /* a CUDA runtime/driver call failed; its text is in dv_last_error()        */
+  DV_ENOTSUP = 9  /* valid request this build does not implement                              */
+} dv_status;
+
+enum { DV_LAYOUT_KV5D = 0 };
+
+/* A worker's K and V cache, preallocated to max_seq. Descriptor only: the library
+ * never allocates or frees caches. */
+typedef struct dv_cache {
+  void* k;             /* K base (device, mapped pinned host, or IPC-mapped peer memory)        */
+  void* v;             /* V base                                                                 */
+  int32_t device;      /* owning CUDA device ordinal, or -1 for pinned host memory              */
+  int32_t layout;      /* DV_LAYOUT_*                                                           */
+  int32_t elem_bytes;  /* bytes per word (2 for fp16/bf16); head_dim*elem_bytes % 16 == 0       */
+  int32_t layer_begin; /* global id of the first layer held (a pipeline stage's layers)         */
+  int32_t n_layers;
+  int32_t req_begin;   /* global id of the first request held (a microbatch's requests)         */
+  int32_t n_reqs;
+  int32_t n_heads;
+  int32_t max_seq;     /* preallocated positions S                                              */
+  int32_t head_dim;
+} dv_cache;
+
+/* Half-open box of GLOBAL layer ids x GLOBAL request ids x absolute positions (reading Q5). */
+typedef struct dv_region {
+  int32_t layer_begin, layer_end;
+  int32_t req_begin, req_end;
+  int32_t pos_begin, pos_end;
+} dv_region;
+
+/* A pipeline configuration: layers partitioned over n_stages stages,
+ * requests split into n_micro microbatches; bounds are global ids, strictly increasing. */
+typedef struct dv_setup {
+  int32_t n_stages;
+  const int32_t* layer_bounds; /* n_stages + 1 entries */
+  int32_t n_micro;
+  const int32_t* req_bounds;   /* n_micro + 1 entries  */
+  int32_t max_seq;
+} dv_setup;
+
+/* One route piece = region x source block (stage, micro) x destination block (stage, micro).
+ * Pieces come in lexicographic order of (src_stage, src_micro, dst_stage, dst_micro).
+ * src_wire_off / dst_wire_off: byte offset of this piece's wire chunk among the pieces leaving
+ * the source block / entering the destination block, cumulative in piece order. */
+typedef struct dv_piece {
+  int32_t src_stage, src_micro, dst_stage, dst_micro;
+  int32_t layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end;
+  uint64_t bytes;
+  uint64_t src_wire_off;
+  uint64_t dst_wire_off;
+} dv_piece;
+
+/* Where contiguous chunks go / come from (the paper's flush/fetch targets). */
+enum {
+  DV_EP_DEVICE = 0, /* local device memory (e.g. a staging buffer or local inbox)                */
+  DV_EP_HOST = 1,   /* pinned, device-mapped host memory (swap arena / host log)  */
+  DV_EP_PEER = 2    /* another GPU's memory mapped into this process (CUDA IPC) over NVLink     */
+};
+
+typedef struct dv_endpoint {
+  int32_t kind;     /* DV_EP_*                                                                  */
+  int32_t device;   /* device owning the memory (-1 for host)                                  */
+  void* base;       /* address usable from the calling device (device/host-mapped/IPC-mapped)  */
+  uint64_t bytes;   /* capacity                                                                */
+  uint64_t* flags;  /* n_flags monotone 64-bit sequence words (same accessibility as base), or NULL */
+  int32_t n_flags;
+  int32_t reserved;
+} dv_endpoint;
+
+/* Transfer-method flags for the data calls. DV_XFER_AUTO lets the library pick. */
+enum {
+  DV_XFER_AUTO = 0,
+  DV_XFER_FUSED = 1u << 0,  /* SM kernel reads/writes the endpoint memory directly (zero-copy / P2P) */
+  DV_XFER_STAGED = 1u << 1, /* kernel <-> local staging, copy engine DMA for the contiguous chunk */
+  DV_NO_FLAG = 1u << 8      /* do not publish / wait on sequence flags                           */
+};
+
+typedef struct dv_ctx dv_ctx;
+
+typedef struct dv_config {
+  uint64_t staging_bytes; /* device staging pool for DV_XFER_STAGED (0 = 256 MiB)                */
+  int32_t max_ctas;       /* cap on CTAs per copy kernel (0 = 148 * 8)                           */
+  int32_t reserved;
+} dv_config;
+
+/* ---- errors ------------------------------------------------------------------------------ */
+DV_API const char* dv_last_error(void);                 /* thread-local message of the last failure     */
+DV_API const char* dv_status_str(dv_status s);
+DV_API int32_t dv_abi_version(void);
+
+/* ---- pure host functions (no GPU needed) ------------------------------------------------- */
+/* Bytes of K and V in a region: 2*nL*nR*(pos_end-pos_begin)*n_heads*head_dim*elem_bytes
+ * ("2*L*hidden*element_bytes*batch*seq"). */
+DV_API dv_status dv_region_bytes(const dv_region* region, int32_t n_heads, int32_t head_dim,
+                          int32_t elem_bytes, uint64_t* out_bytes);
+
+/* Route a region from src setup to dst setup (Table 1 stream_out/stream_in).
+ * Writes up to `cap` pieces to `out` and the total count to *n (call with cap=0 to size).
+ * Errors in order: DV_EINVAL (malformed setup/region), DV_EMAP (a setup does not hold the
+ * region's layers/requests), DV_ERANGE (pos_end > max_seq on either side). An empty region
+ * (any zero extent) yields 0 pieces. */
+DV_API dv_status dv_route(const dv_setup* src, const dv_setup* dst, const dv_region* region,
+                   int32_t n_heads, int32_t head_dim, int32_t elem_bytes, dv_piece* out,
+                   uint64_t cap, uint64_t* n);
+
+/* ---- context ----------------------------------------------------------------------------- */
+/* One context per (process, device). Owns the staging pool, the release tickets and the CUDA
+ * driver entry points it needs. `cfg` may be NULL. */
+DV_API dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out);
+DV_API dv_status dv_destroy(dv_ctx* ctx); /* synchronises the device, frees library-owned memory */
+
+/* ---- memory and peers -------------------------------------------------------------------- */
+DV_API dv_status dv_host_alloc(uint64_t bytes, void** out);  /* pinned, portable, device-mapped */
+DV_API dv_status dv_host_free(void* p);
+DV_API dv_status dv_device_alloc(int32_t device, uint64_t bytes, void** out); /* IPC-exportable */
+DV_API dv_status dv_device_free(void* p);
+
+typedef struct dv_ipc_blob { uint8_t bytes[96]; } dv_ipc_blob; /* opaque, copyable between processes */
+/* Export device memory at `ptr` (any address inside a cudaMalloc allocation). */
+DV_API dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out);
+/* Map a blob exported by another process (same or other GPU) into this process; returns the
+ * address corresponding to the exported `ptr`. Same-process blobs map to the original pointer. */
+DV_API dv_status dv_ipc_open(const dv_ipc_blob* blob, void** out);
+DV_API dv_status dv_ipc_close(void* mapped);
+
+/* ---- level 3: flush / fetch ----------------------------------------------- */
+/* Copy `bytes` contiguous bytes from local device memory `src` to `dst` at `dst_off`; then, if
+ * flag_slot >= 0 and dst->flags, publish dst->flags[flag_slot] = seq (release, after the data). */
+DV_API dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoint* dst,
+                   uint64_t dst_off, int32_t flag_slot, uint64_t seq, uint32_t xfer, void* stream);
+/* Wait (stream-ordered) until src->flags[flag_slot] >= wait_seq when flag_slot >= 0, then copy
+ * `bytes` from `src` at `src_off` to local device memory `dst`. */
+DV_API dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_t flag_slot,
+                   uint64_t wait_seq, void* dst, uint64_t bytes, uint32_t xfer, void* stream);
+
+/* ---- level 2: scatter / gather (Opt (1) "buffered copies") --- */
+/* Pack `region` of `src` into the wire format at dst->base + dst_off, then publish
+ * dst->flags[flag_slot] = seq if flag_slot >= 0. DV_XFER_FUSED: one kernel stores straight into
+ * the endpoint memory (device, pinned host over PCIe, or peer over NVLink) and publishes the flag
+ * itself; DV_XFER_STAGED: kernel packs into library staging, the copy engine moves the chunk. */
+DV_API dv_status dv_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                     const dv_endpoint* dst, uint64_t dst_off, int32_t flag_slot, uint64_t seq,
+                     uint32_t xfer, void* stream);
+/* Wait until src->flags[flag_slot] >= wait_seq (if flag_slot >= 0), then unpack the wire chunk
+ * at src->base + src_off into `region` of `dst`. Words of `dst` outside the region are untouched. */
+DV_API dv_status dv_gather(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_t flag_slot,
+                    uint64_t wait_seq, const dv_cache* dst, const dv_region* region,
+                    uint32_t xfer, void* stream);
+/* Direct layout-to-layout copy of `region` (pack and unpack fused, no wire buffer). Either cache
+ * may live in local device memory, pinned host memory (mirror-form arena) or mapped peer memory.
+ * If `signal` is non-NULL and flag_slot >= 0, publishes signal->flags[flag_slot] = seq after. */
+DV_API dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const dv_region* region,
+                   const dv_endpoint* signal, int32_t flag_slot, uint64_t seq, uint32_t xfer,
+                   void* stream);
+
+/* ---- level 1: stream_out / stream_in ------------------------------ */
+/* Sender side. `src` is the cache of source block (my_stage, my_micro) of `src_setup`. Routes
+ * `region`; for every piece leaving this block, scatters it into inboxes[dst_stage*n_micro_dst +
+ * dst_micro] at the piece's dst_wire_off and publishes flag slot (my_stage*n_micro_src +
+ * my_micro) = seq in that inbox. `inboxes` has dst_setup->n_stages*dst_setup->n_micro entries
+ * (entries never addressed may be zeroed). */
+DV_API dv_status dv_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                        const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
+                        const dv_setup* dst_setup, const dv_endpoint* inboxes, int32_t n_inboxes,
+                        uint64_t seq, uint32_t xfer, void* stream);
+/* Receiver side. For every piece entering block (my_stage, my_micro) of `dst_setup`: wait for
+ * inbox->flags[src_stage*n_micro_src + src_micro] >= wait_seq, then gather the piece from
+ * inbox at its dst_wire_off into `dst`. */
+DV_API dv_status dv_stream_in(dv_ctx* ctx, const dv_cache* dst, const dv_region* region,
+                       const dv_setup* src_setup, const dv_setup* dst_setup, int32_t my_stage,
+                       int32_t my_micro, const dv_endpoint* inbox, uint64_t wait_seq,
+                       uint32_t xfer, void* stream);
+/* Sender side, direct form: every piece leaving (my_stage, my_micro) is remapped straight into
+ * dst_caches[dst block] (mapped peer, host or local memory), then flag slot
+ * (my_stage*n_micro_src + my_micro) of signals[dst block] (if non-NULL) is set to seq. */
+DV_API dv_status dv_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                               const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
+                               const dv_setup* dst_setup, const dv_cache* dst_caches,
+                               const dv_endpoint* signals, int32_t n_dst, uint64_t seq,
+                               uint32_t xfer, void* stream);
+
+/* ---- completion / ordering ---------------------------------------------- */
+/* Stream-ordered wait until ep->flags[flag_slot] >= seq (64-bit unsigned compare). */
+DV_API dv_status dv_wait(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq, void* stream);
+/* Stream-ordered publish ep->flags[flag_slot] = seq after all prior work on `stream`. */
+DV_API dv_status dv_signal(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq, void* stream);
+/* Non-blocking poll from the host: *done = (flags[flag_slot] >= seq). Host-memory flags are read
+ * directly; device-memory flags with a small synchronous copy. */
+DV_API dv_status dv_query(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq, int32_t* done);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DV_H_ */

@@ -1,0 +1,33 @@
+/*
+ * dv_testing.h -- test-only utilities of dvstream. NOT part of the streaming
+ * path: a synthetic KV "writer" that fills caches with the seeded generator of kvgen/__init__.py
+ * (same counter-based splitmix64 coordinate hash, implemented independently on the device), and a
+ * synthetic compute kernel for overlap measurements.
+ */
+#ifndef DV_TESTING_H_
+#define DV_TESTING_H_
+#include "dv.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { DVT_FILL_HASH = 0, DVT_FILL_UID = 1, DVT_FILL_CONST = 2 };
+
+/* Write the generator's word at every (kv, l, r, h, s, d) of `region` of cache `c` (global layer
+ * and request ids; NULL region = the whole cache). Positions outside [valid_begin, valid_end) get
+ * the POISON word 0xFFFE. kind:
+ *   DVT_FILL_HASH  word = bits 48..63 of splitmix64(key XOR seed*0xD1B54A32D192ED03), key =
+ *                  kv<<62 | l<<52 | r<<40 | h<<30 | s<<10 | d  (elem_bytes must be 2);
+ *   DVT_FILL_UID   word = ((((kv*L + l)*R + r)*H + h)*S + s)*D + d with box = {L,R,H,S,D};
+ *   DVT_FILL_CONST word = (uint16_t)seed.
+ * Stream-ordered; no synchronisation. */
+DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                   int32_t valid_begin, int32_t valid_end, const dv_region* region, void* stream);
+
+/* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */
+DV_API dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

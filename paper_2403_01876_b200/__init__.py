@@ -1,0 +1,417 @@
+"""dvstream: B200-native KV-cache streaming (DejaVuLib hot path, arXiv 2403.01876).
+
+Thin ctypes binding over the C ABI in include/dv.h (libdvstream.so, built in-tree for sm_100a).
+Argument marshalling only: every step of the path (route, pack, transfer, unpack, publish) runs
+in the library. Function names equal the C entry points. There is no CPU fallback: if the
+library is missing every call raises.
+
+torch is used only to hand over device memory (``tensor.data_ptr()``) and streams
+(``torch.cuda.current_stream().cuda_stream``); it is imported lazily by the helpers that take
+tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdvstream.so")
+
+# ---- constants mirrored from include/dv.h --------------------------------------------------------
+DV_OK, DV_EINVAL, DV_EMAP, DV_ERANGE, DV_EALIGN, DV_ENOMEM, DV_EPEER, DV_EBUSY, DV_ECUDA, \
+    DV_ENOTSUP = range(10)
+DV_LAYOUT_KV5D = 0
+DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
+DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_NO_FLAG = 0, 1, 2, 256
+DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
+
+
+class dv_cache(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("device", C.c_int32), ("layout", C.c_int32),
+                ("elem_bytes", C.c_int32), ("layer_begin", C.c_int32), ("n_layers", C.c_int32),
+                ("req_begin", C.c_int32), ("n_reqs", C.c_int32), ("n_heads", C.c_int32),
+                ("max_seq", C.c_int32), ("head_dim", C.c_int32)]
+
+
+class dv_region(C.Structure):
+    _fields_ = [("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("req_begin", C.c_int32),
+                ("req_end", C.c_int32), ("pos_begin", C.c_int32), ("pos_end", C.c_int32)]
+
+
+class dv_setup(C.Structure):
+    _fields_ = [("n_stages", C.c_int32), ("layer_bounds", C.POINTER(C.c_int32)),
+                ("n_micro", C.c_int32), ("req_bounds", C.POINTER(C.c_int32)), ("max_seq", C.c_int32)]
+
+
+class dv_piece(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("src_stage", "src_micro", "dst_stage", "dst_micro",
+                                         "layer_begin", "layer_end", "req_begin", "req_end",
+                                         "pos_begin", "pos_end")] + \
+               [("bytes", C.c_uint64), ("src_wire_off", C.c_uint64), ("dst_wire_off", C.c_uint64)]
+
+
+class dv_endpoint(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("device", C.c_int32), ("base", C.c_void_p),
+                ("bytes", C.c_uint64), ("flags", C.c_void_p), ("n_flags", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class dv_config(C.Structure):
+    _fields_ = [("staging_bytes", C.c_uint64), ("max_ctas", C.c_int32), ("reserved", C.c_int32)]
+
+
+class dv_ipc_blob(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 96)]
+
+
+class DVError(RuntimeError):
+    def __init__(self, status: int, func: str, msg: str):
+        super().__init__(f"{func}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "DV_OK", 1: "DV_EINVAL", 2: "DV_EMAP", 3: "DV_ERANGE", 4: "DV_EALIGN",
+           5: "DV_ENOMEM", 6: "DV_EPEER", 7: "DV_EBUSY", 8: "DV_ECUDA", 9: "DV_ENOTSUP"}
+
+P = C.POINTER
+_SIGS = {
+    "dv_last_error": (C.c_char_p, []),
+    "dv_status_str": (C.c_char_p, [C.c_int]),
+    "dv_abi_version": (C.c_int32, []),
+    "dv_region_bytes": (C.c_int, [P(dv_region), C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64)]),
+    "dv_route": (C.c_int, [P(dv_setup), P(dv_setup), P(dv_region), C.c_int32, C.c_int32, C.c_int32,
+                           P(dv_piece), C.c_uint64, P(C.c_uint64)]),
+    "dv_create": (C.c_int, [C.c_int32, P(dv_config), P(C.c_void_p)]),
+    "dv_destroy": (C.c_int, [C.c_void_p]),
+    "dv_host_alloc": (C.c_int, [C.c_uint64, P(C.c_void_p)]),
+    "dv_host_free": (C.c_int, [C.c_void_p]),
+    "dv_device_alloc": (C.c_int, [C.c_int32, C.c_uint64, P(C.c_void_p)]),
+    "dv_device_free": (C.c_int, [C.c_void_p]),
+    "dv_ipc_export": (C.c_int, [C.c_void_p, P(dv_ipc_blob)]),
+    "dv_ipc_open": (C.c_int, [P(dv_ipc_blob), P(C.c_void_p)]),
+    "dv_ipc_close": (C.c_int, [C.c_void_p]),
+    "dv_flush": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(dv_endpoint), C.c_uint64,
+                           C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "dv_fetch": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_uint64, C.c_int32, C.c_uint64,
+                           C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "dv_scatter": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_endpoint), C.c_uint64,
+                             C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "dv_gather": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_uint64, C.c_int32, C.c_uint64,
+                            P(dv_cache), P(dv_region), C.c_uint32, C.c_void_p]),
+    "dv_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint),
+                           C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "dv_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
+                                C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32, C.c_uint64,
+                                C.c_uint32, C.c_void_p]),
+    "dv_stream_in": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), P(dv_setup),
+                               C.c_int32, C.c_int32, P(dv_endpoint), C.c_uint64, C.c_uint32,
+                               C.c_void_p]),
+    "dv_stream_out_direct": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup),
+                                       C.c_int32, C.c_int32, P(dv_setup), P(dv_cache),
+                                       P(dv_endpoint), C.c_int32, C.c_uint64, C.c_uint32,
+                                       C.c_void_p]),
+    "dv_wait": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
+    "dv_signal": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
+    "dv_query": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, P(C.c_int32)]),
+    "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
+                           P(dv_region), C.c_void_p]),
+    "dvt_spin": (C.c_int, [C.c_uint64, C.c_int32, C.c_void_p]),
+    "dvb_per_run_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, P(C.c_uint64)]),
+    "dvb_buffered_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, C.c_void_p,
+                                    P(C.c_uint64)]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdvstream.so (in-tree). Raises if it has not been built -- no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _call(name, *args):
+    st = getattr(lib(), name)(*args)
+    if st != DV_OK:
+        raise DVError(st, name, lib().dv_last_error().decode())
+    return st
+
+
+def _stream(s):
+    if s is None:
+        try:
+            import torch
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:  # pragma: no cover
+            return C.c_void_p(0)
+    if hasattr(s, "cuda_stream"):
+        return C.c_void_p(s.cuda_stream)
+    return C.c_void_p(int(s))
+
+
+def _ref(x):
+    return None if x is None else C.byref(x)
+
+
+# ---- descriptor helpers --------------------------------------------------------------------------
+def region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end) -> dv_region:
+    return dv_region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end)
+
+
+class Setup:
+    """Owns the bound arrays of a dv_setup."""
+
+    def __init__(self, layer_bounds, req_bounds, max_seq):
+        self.lb = (C.c_int32 * len(layer_bounds))(*layer_bounds)
+        self.rb = (C.c_int32 * len(req_bounds))(*req_bounds)
+        self.c = dv_setup(len(layer_bounds) - 1, self.lb, len(req_bounds) - 1, self.rb, max_seq)
+        self.layer_bounds, self.req_bounds, self.max_seq = list(layer_bounds), list(req_bounds), max_seq
+
+    @property
+    def n_stages(self):
+        return self.c.n_stages
+
+    @property
+    def n_micro(self):
+        return self.c.n_micro
+
+
+def cache(k, v, layer_begin=0, req_begin=0, device=None) -> dv_cache:
+    """Descriptor of a KV5D cache held in two tensors (or raw pointers with explicit shapes via
+    cache_raw). Tensors must be [n_layers][n_reqs][n_heads][max_seq][head_dim], contiguous."""
+    assert k.shape == v.shape and k.dtype == v.dtype and k.dim() == 5
+    assert k.is_contiguous() and v.is_contiguous()
+    nL, nR, H, S, D = k.shape
+    if device is None:
+        device = k.device.index if k.is_cuda else -1
+    return dv_cache(k.data_ptr(), v.data_ptr(), device, DV_LAYOUT_KV5D, k.element_size(),
+                    layer_begin, nL, req_begin, nR, H, S, D)
+
+
+def cache_raw(k_ptr, v_ptr, device, elem_bytes, layer_begin, n_layers, req_begin, n_reqs, n_heads,
+              max_seq, head_dim) -> dv_cache:
+    return dv_cache(k_ptr, v_ptr, device, DV_LAYOUT_KV5D, elem_bytes, layer_begin, n_layers,
+                    req_begin, n_reqs, n_heads, max_seq, head_dim)
+
+
+def endpoint(kind, base_ptr, nbytes, flags_ptr=0, n_flags=0, device=-1) -> dv_endpoint:
+    return dv_endpoint(kind, device, base_ptr, nbytes, flags_ptr, n_flags, 0)
+
+
+def endpoint_of(buf, flags=None, kind=None) -> dv_endpoint:
+    """Endpoint over a torch buffer (device or pinned host) and an optional uint64/int64 flag
+    tensor in the same kind of memory."""
+    if kind is None:
+        kind = DV_EP_DEVICE if buf.is_cuda else DV_EP_HOST
+    dev = buf.device.index if buf.is_cuda else -1
+    nb = buf.numel() * buf.element_size()
+    fp, nf = (flags.data_ptr(), flags.numel()) if flags is not None else (0, 0)
+    return dv_endpoint(kind, dev, buf.data_ptr(), nb, fp, nf, 0)
+
+
+def endpoint_array(eps):
+    arr = (dv_endpoint * max(1, len(eps)))()
+    for i, e in enumerate(eps):
+        if e is not None:
+            arr[i] = e
+    return arr
+
+
+def cache_array(cs):
+    arr = (dv_cache * max(1, len(cs)))()
+    for i, c in enumerate(cs):
+        if c is not None:
+            arr[i] = c
+    return arr
+
+
+# ---- C entry points with the same names ----------------------------------------------------------
+def dv_last_error() -> str:
+    return lib().dv_last_error().decode()
+
+
+def dv_abi_version() -> int:
+    return lib().dv_abi_version()
+
+
+def dv_region_bytes(reg: dv_region, n_heads, head_dim, elem_bytes) -> int:
+    out = C.c_uint64()
+    _call("dv_region_bytes", C.byref(reg), n_heads, head_dim, elem_bytes, C.byref(out))
+    return out.value
+
+
+def dv_route(src: Setup, dst: Setup, reg: dv_region, n_heads, head_dim, elem_bytes):
+    n = C.c_uint64()
+    _call("dv_route", C.byref(src.c), C.byref(dst.c), C.byref(reg), n_heads, head_dim, elem_bytes,
+          None, 0, C.byref(n))
+    arr = (dv_piece * max(1, n.value))()
+    _call("dv_route", C.byref(src.c), C.byref(dst.c), C.byref(reg), n_heads, head_dim, elem_bytes,
+          arr, n.value, C.byref(n))
+    return [arr[i] for i in range(n.value)]
+
+
+class Context:
+    """Owns a dv_ctx* (one per process and device)."""
+
+    def __init__(self, device: int = 0, staging_bytes: int = 0, max_ctas: int = 0):
+        h = C.c_void_p()
+        cfg = dv_config(staging_bytes, max_ctas, 0)
+        _call("dv_create", device, C.byref(cfg), C.byref(h))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _call("dv_destroy", self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dv_create(device=0, staging_bytes=0, max_ctas=0) -> Context:
+    return Context(device, staging_bytes, max_ctas)
+
+
+def dv_destroy(ctx: Context):
+    ctx.close()
+
+
+def dv_host_alloc(nbytes) -> int:
+    p = C.c_void_p()
+    _call("dv_host_alloc", nbytes, C.byref(p))
+    return p.value
+
+
+def dv_host_free(p):
+    _call("dv_host_free", C.c_void_p(p))
+
+
+def dv_device_alloc(device, nbytes) -> int:
+    p = C.c_void_p()
+    _call("dv_device_alloc", device, nbytes, C.byref(p))
+    return p.value
+
+
+def dv_device_free(p):
+    _call("dv_device_free", C.c_void_p(p))
+
+
+def dv_ipc_export(ptr) -> bytes:
+    b = dv_ipc_blob()
+    _call("dv_ipc_export", C.c_void_p(ptr), C.byref(b))
+    return bytes(b.bytes)
+
+
+def dv_ipc_open(blob: bytes) -> int:
+    b = dv_ipc_blob()
+    C.memmove(b.bytes, blob, len(b.bytes))
+    p = C.c_void_p()
+    _call("dv_ipc_open", C.byref(b), C.byref(p))
+    return p.value
+
+
+def dv_ipc_close(p):
+    _call("dv_ipc_close", C.c_void_p(p))
+
+
+def dv_flush(ctx, src_ptr, nbytes, dst: dv_endpoint, dst_off=0, flag_slot=-1, seq=0, xfer=0, stream=None):
+    _call("dv_flush", ctx.h, C.c_void_p(src_ptr), nbytes, C.byref(dst), dst_off, flag_slot, seq, xfer,
+          _stream(stream))
+
+
+def dv_fetch(ctx, src: dv_endpoint, src_off, dst_ptr, nbytes, flag_slot=-1, wait_seq=0, xfer=0, stream=None):
+    _call("dv_fetch", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.c_void_p(dst_ptr), nbytes,
+          xfer, _stream(stream))
+
+
+def dv_scatter(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off=0, flag_slot=-1, seq=0,
+               xfer=0, stream=None):
+    _call("dv_scatter", ctx.h, C.byref(src), C.byref(reg), C.byref(dst), dst_off, flag_slot, seq, xfer,
+          _stream(stream))
+
+
+def dv_gather(ctx, src: dv_endpoint, src_off, dst: dv_cache, reg: dv_region, flag_slot=-1, wait_seq=0,
+              xfer=0, stream=None):
+    _call("dv_gather", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), C.byref(reg),
+          xfer, _stream(stream))
+
+
+def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpoint = None, flag_slot=-1,
+             seq=0, xfer=0, stream=None):
+    _call("dv_remap", ctx.h, C.byref(src), C.byref(dst), C.byref(reg), _ref(signal), flag_slot, seq,
+          xfer, _stream(stream))
+
+
+def dv_stream_out(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
+                  dst_setup: Setup, inboxes, seq, xfer=0, stream=None):
+    arr = endpoint_array(inboxes)
+    _call("dv_stream_out", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage, my_micro,
+          C.byref(dst_setup.c), arr, len(inboxes), seq, xfer, _stream(stream))
+
+
+def dv_stream_in(ctx, dst: dv_cache, reg: dv_region, src_setup: Setup, dst_setup: Setup, my_stage,
+                 my_micro, inbox: dv_endpoint, wait_seq, xfer=0, stream=None):
+    _call("dv_stream_in", ctx.h, C.byref(dst), C.byref(reg), C.byref(src_setup.c), C.byref(dst_setup.c),
+          my_stage, my_micro, C.byref(inbox), wait_seq, xfer, _stream(stream))
+
+
+def dv_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
+                         dst_setup: Setup, dst_caches, signals=None, seq=0, xfer=0, stream=None):
+    carr = cache_array(dst_caches)
+    sarr = endpoint_array(signals) if signals is not None else None
+    _call("dv_stream_out_direct", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage,
+          my_micro, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, xfer, _stream(stream))
+
+
+def dv_wait(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):
+    _call("dv_wait", ctx.h, C.byref(ep), flag_slot, seq, _stream(stream))
+
+
+def dv_signal(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):
+    _call("dv_signal", ctx.h, C.byref(ep), flag_slot, seq, _stream(stream))
+
+
+def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
+    d = C.c_int32()
+    _call("dv_query", ctx.h, C.byref(ep), flag_slot, seq, C.byref(d))
+    return bool(d.value)
+
+
+# ---- test-only utilities (include/dv_testing.h) and baselines (include/dv_baselines.h) -----------
+def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_region = None, stream=None):
+    b = (C.c_int32 * 5)(*box) if box is not None else None
+    _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], _ref(reg), _stream(stream))
+
+
+def dvt_spin(ns, ctas, stream=None):
+    _call("dvt_spin", ns, ctas, _stream(stream))
+
+
+def dvb_per_run_copy(src: dv_cache, reg: dv_region, dst_ptr, stream=None) -> int:
+    n = C.c_uint64()
+    _call("dvb_per_run_copy", C.byref(src), C.byref(reg), C.c_void_p(dst_ptr), _stream(stream), C.byref(n))
+    return n.value
+
+
+def dvb_buffered_copy(src: dv_cache, reg: dv_region, staging_ptr, dst_ptr, stream=None) -> int:
+    n = C.c_uint64()
+    _call("dvb_buffered_copy", C.byref(src), C.byref(reg), C.c_void_p(staging_ptr), C.c_void_p(dst_ptr),
+          _stream(stream), C.byref(n))
+    return n.value

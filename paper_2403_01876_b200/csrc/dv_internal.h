@@ -1,0 +1,127 @@
+// Internal declarations of dvstream (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dv.h"
+
+namespace dv {
+
+// ---- error state (thread-local message behind dv_last_error) --------------------------------
+dv_status fail(dv_status s, const char* fmt, ...);
+dv_status cuda_fail(cudaError_t e, const char* what);
+#define DV_TRY(expr)                         \
+  do {                                       \
+    dv_status _s = (expr);                   \
+    if (_s != DV_OK) return _s;              \
+  } while (0)
+#define DV_CUDA(expr)                                   \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+// ---- fast unsigned division by a run-time constant (dividend < 2^31) ------------------------
+// Round-up multiply-shift (Granlund & Montgomery 1994); d == 1 handled by mul == 0.
+struct FastDiv {
+  uint32_t d;
+  uint32_t mul;
+  uint32_t shr;
+};
+FastDiv make_fastdiv(uint32_t d);
+
+// ---- a batched strided copy: up to 4 loop dims of contiguous runs ---------------------------
+// Run q (row-major over n[0..3], n[3] innermost) starts at src + sum_k i_k*ss[k] and
+// dst + sum_k i_k*ds[k]; every run is run_bytes contiguous bytes on both sides.
+struct CopyPlan {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint32_t n[4];
+  int64_t ss[4];
+  int64_t ds[4];
+  uint64_t run_bytes;
+  uint64_t runs() const { return (uint64_t)n[0] * n[1] * n[2] * n[3]; }
+  uint64_t bytes() const { return runs() * run_bytes; }
+};
+
+// Merge contiguous dims into the run (and adjacent dims into each other) on both sides.
+void collapse(CopyPlan& p);
+
+// Release of a 64-bit sequence flag after a kernel's stores (fused publish).
+struct Release {
+  unsigned long long* flag;  // NULL = none
+  unsigned long long seq;
+  unsigned int* ticket;      // per-launch CTA counter (library-owned, zero between uses)
+};
+
+// Enqueue the copy kernel(s) for runs [q_first, q_last) of the (collapsed) plan `p` on `stream`;
+// the last launch carries `rel` (an empty range still publishes the flag).
+dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, const Release& rel,
+                      int max_ctas, cudaStream_t stream);
+
+// ---- CUDA driver entry points (resolved through the runtime; no -lcuda) --------------------
+struct Driver {
+  int (*streamWaitValue64)(void* stream, unsigned long long addr, unsigned long long value,
+                           unsigned int flags) = nullptr;
+  int (*streamWriteValue64)(void* stream, unsigned long long addr, unsigned long long value,
+                            unsigned int flags) = nullptr;
+  int (*memGetAddressRange)(unsigned long long* base, size_t* size,
+                            unsigned long long dptr) = nullptr;
+  int (*getErrorString)(int err, const char** str) = nullptr;
+};
+dv_status driver(const Driver** out);
+
+// ---- staging pool (device), stream-ordered reuse via events ---------------------------------
+class Staging {
+ public:
+  dv_status init(int device, uint64_t bytes);
+  void destroy();
+  uint64_t capacity() const { return cap_; }
+  // Reserve n bytes for work about to be enqueued on `stream`; makes `stream` wait for earlier
+  // users of the same bytes.
+  dv_status acquire(uint64_t n, cudaStream_t stream, uint8_t** out, uint64_t* off);
+  // Mark the range as in use until all work currently enqueued on `stream` completes.
+  dv_status release(uint64_t off, uint64_t n, cudaStream_t stream);
+
+ private:
+  struct Rec {
+    uint64_t off, len;
+    cudaEvent_t ev;
+  };
+  uint8_t* base_ = nullptr;
+  uint64_t cap_ = 0, head_ = 0;
+  std::deque<Rec> recs_;
+  std::vector<cudaEvent_t> free_ev_;
+  std::mutex mu_;
+};
+
+}  // namespace dv
+
+struct dv_ctx {
+  int device;
+  int max_ctas;
+  int sm_count;
+  dv::Staging staging;
+  unsigned int* tickets;  // device array of kTickets counters
+  std::atomic<uint32_t> next_ticket{0};
+  cudaStream_t aux;       // private stream for dv_query on device flags
+  static constexpr uint32_t kTickets = 4096;
+};
+
+namespace dv {
+// Validation + descriptor helpers shared by the API translation units (route.cpp, api.cu).
+dv_status check_setup(const dv_setup* s, const char* name);
+dv_status check_region_shape(const dv_region* r);
+dv_status check_cache(const dv_cache* c, const char* name);
+dv_status check_cache_holds(const dv_cache* c, const dv_region* r, const char* name);
+dv_status route(const dv_setup* src, const dv_setup* dst, const dv_region* region,
+                int32_t n_heads, int32_t head_dim, int32_t elem_bytes,
+                std::vector<dv_piece>* out);
+}  // namespace dv

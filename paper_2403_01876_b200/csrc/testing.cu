@@ -1,0 +1,118 @@
+// Test-only kernels (include/dv_testing.h): synthetic KV writer with the kvgen generator, spin.
+#include "../../include/dv_testing.h"
+#include "dv_internal.h"
+
+namespace dv {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct FillParams {
+  uint16_t* k;
+  uint16_t* v;
+  int64_t s_l, s_r, s_h;  // element strides of the cache
+  int32_t lb, rb;         // cache layer_begin / req_begin
+  int32_t l0, r0, s0;     // region origin
+  int32_t nR, H, n, D;    // region extents
+  int32_t kind;
+  uint64_t seedmix;
+  int32_t box[5];
+  int32_t vlo, vhi;
+};
+
+__global__ void k_fill(const FillParams p) {
+  // blockIdx.x = slab (l, r, h) of the region, blockIdx.y = kv
+  uint32_t slab = blockIdx.x;
+  const int h = slab % p.H;
+  slab /= p.H;
+  const int r = p.r0 + (int)(slab % p.nR);
+  const int l = p.l0 + (int)(slab / p.nR);
+  const int kv = blockIdx.y;
+  uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
+                   (int64_t)h * p.s_h;
+  const int64_t words = (int64_t)p.n * p.D;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) {
+    const int s = p.s0 + (int)(i / p.D);
+    const int d = (int)(i % p.D);
+    uint16_t w;
+    if (s < p.vlo || s >= p.vhi) {
+      w = 0xFFFE;
+    } else if (p.kind == DVT_FILL_HASH) {
+      const uint64_t key = ((uint64_t)kv << 62) | ((uint64_t)l << 52) | ((uint64_t)r << 40) |
+                           ((uint64_t)h << 30) | ((uint64_t)s << 10) | (uint64_t)d;
+      w = (uint16_t)(splitmix64(key ^ p.seedmix) >> 48);
+    } else if (p.kind == DVT_FILL_UID) {
+      const int64_t id =
+          (((((int64_t)kv * p.box[0] + l) * p.box[1] + r) * p.box[2] + h) * p.box[3] + s) *
+              p.box[4] + d;
+      w = (uint16_t)id;
+    } else {
+      w = (uint16_t)p.seedmix;
+    }
+    base[(int64_t)s * p.D + d] = w;
+  }
+}
+
+__global__ void k_spin(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+}  // namespace dv
+
+using namespace dv;
+
+extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                              int32_t valid_begin, int32_t valid_end, const dv_region* region,
+                              void* stream) {
+  DV_TRY(check_cache(c, "cache"));
+  if (c->elem_bytes != 2) return fail(DV_ENOTSUP, "dvt_fill supports 16-bit words only");
+  dv_region whole{c->layer_begin, c->layer_begin + c->n_layers, c->req_begin,
+                  c->req_begin + c->n_reqs, 0, c->max_seq};
+  const dv_region* r = region ? region : &whole;
+  DV_TRY(check_region_shape(r));
+  DV_TRY(check_cache_holds(c, r, "cache"));
+  if (kind == DVT_FILL_UID && !box) return fail(DV_EINVAL, "uid fill needs a box");
+  FillParams p{};
+  p.k = (uint16_t*)c->k;
+  p.v = (uint16_t*)c->v;
+  p.s_h = (int64_t)c->max_seq * c->head_dim;
+  p.s_r = p.s_h * c->n_heads;
+  p.s_l = p.s_r * c->n_reqs;
+  p.lb = c->layer_begin;
+  p.rb = c->req_begin;
+  p.l0 = r->layer_begin;
+  p.r0 = r->req_begin;
+  p.s0 = r->pos_begin;
+  p.nR = r->req_end - r->req_begin;
+  p.H = c->n_heads;
+  p.n = r->pos_end - r->pos_begin;
+  p.D = c->head_dim;
+  p.kind = kind;
+  p.seedmix = kind == DVT_FILL_CONST ? seed : seed * 0xD1B54A32D192ED03ull;
+  if (box)
+    for (int i = 0; i < 5; ++i) p.box[i] = box[i];
+  p.vlo = valid_begin;
+  p.vhi = valid_end;
+  const uint64_t slabs = (uint64_t)(r->layer_end - r->layer_begin) * p.nR * p.H;
+  if (!slabs || !p.n) return DV_OK;
+  if (slabs >= (1ull << 31)) return fail(DV_ENOTSUP, "region too large for dvt_fill");
+  const int threads = p.n * p.D >= 256 ? 256 : 128;
+  k_fill<<<dim3((unsigned)slabs, 2), threads, 0, (cudaStream_t)stream>>>(p);
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream) {
+  if (ctas < 1) return fail(DV_EINVAL, "ctas must be >= 1");
+  k_spin<<<ctas, 128, 0, (cudaStream_t)stream>>>(ns);
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}

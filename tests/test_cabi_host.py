@@ -1,0 +1,120 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/*.h declares,
+and its host-only logic (route planner, byte counts, validation) agrees with the oracle.
+
+The route is independent code on each side (C++ in csrc/route.cpp, numpy loops in oracle/), so
+agreement on random setups is a real cross-check; the oracle itself is pinned in
+test_oracle_pins.py.
+"""
+import glob
+import os
+import random
+import re
+
+import pytest
+
+import paper_2403_01876_b200 as dv
+from oracle import kvstream as ok
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        for m in re.finditer(r"DV_API\s+[\w\s\*]+?\b(dv[tb]?_\w+)\s*\(", open(h).read()):
+            syms.add(m.group(1))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = dv.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 29
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(dv.exported_symbols()) == syms
+    assert dv.dv_abi_version() == 1
+
+
+def test_no_cpu_fallback_without_gpu():
+    """dv_create must fail loudly (DV_ECUDA) when no GPU is usable -- never run on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_create(0)
+    assert ei.value.status == dv.DV_ECUDA
+
+
+def _region_bytes_oracle(r, H, D, e):
+    return ok.region_bytes(r.layer_begin, r.layer_end, r.req_begin, r.req_end, r.pos_begin, r.pos_end, H, D, e)
+
+
+def test_region_bytes_matches_spec_example(golden):
+    ex = golden("spec_kv_bytes.json")["kv_cache_bytes"][0]
+    assert dv.dv_region_bytes(dv.region(0, 12, 0, 1, 0, 1024), 12, 64, 2) == ex["bytes"]
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_region_bytes(dv.region(0, 12, 3, 1, 0, 1024), 12, 64, 2)
+    assert ei.value.status == dv.DV_EINVAL
+
+
+def _bounds(rng, lo, hi, k):
+    cuts = sorted(rng.sample(range(lo + 1, hi), k - 1)) if k > 1 else []
+    return [lo] + cuts + [hi]
+
+
+FIELDS = ["src_stage", "src_micro", "dst_stage", "dst_micro", "layer_begin", "layer_end", "req_begin",
+          "req_end", "pos_begin", "pos_end", "bytes", "src_wire_off", "dst_wire_off"]
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_route_matches_oracle(seed):
+    rng = random.Random(1000 + seed)
+    L, R = rng.randint(1, 80), rng.randint(1, 40)
+    lo_l, lo_r = rng.randint(0, 3), rng.randint(0, 3)
+    sl = _bounds(rng, lo_l, lo_l + L, rng.randint(1, min(L, 8)))
+    dl = _bounds(rng, lo_l, lo_l + L, rng.randint(1, min(L, 8)))
+    sr = _bounds(rng, lo_r, lo_r + R, rng.randint(1, min(R, 4)))
+    dr = _bounds(rng, lo_r, lo_r + R, rng.randint(1, min(R, 4)))
+    S1, S2 = rng.randint(1, 4096), rng.randint(1, 4096)
+    l0 = rng.randint(lo_l, lo_l + L - 1); l1 = rng.randint(l0 + 1, lo_l + L)
+    r0 = rng.randint(lo_r, lo_r + R - 1); r1 = rng.randint(r0 + 1, lo_r + R)
+    s0 = rng.randint(0, min(S1, S2) - 1); s1 = rng.randint(s0, min(S1, S2))
+    H, D, e = rng.choice([(40, 128, 2), (72, 128, 2), (112, 128, 2), (4, 16, 2), (3, 8, 4)])
+    if rng.random() < 0.1:   # sometimes out of range -> both sides must raise the same error
+        s1 = max(S1, S2) + 1
+    reg = (l0, l1, r0, r1, s0, s1)
+    try:
+        exp = ok.route(ok.Setup(sl, sr, S1), ok.Setup(dl, dr, S2), reg, H, D, e)
+        exp_err = None
+    except (ok.MappingError, ok.RangeError, ValueError) as ex:
+        exp_err = type(ex)
+    if exp_err is not None:
+        with pytest.raises(dv.DVError) as ei:
+            dv.dv_route(dv.Setup(sl, sr, S1), dv.Setup(dl, dr, S2), dv.region(*reg), H, D, e)
+        want = {ok.MappingError: dv.DV_EMAP, ok.RangeError: dv.DV_ERANGE, ValueError: dv.DV_EINVAL}[exp_err]
+        assert ei.value.status == want
+        return
+    got = dv.dv_route(dv.Setup(sl, sr, S1), dv.Setup(dl, dr, S2), dv.region(*reg), H, D, e)
+    assert [[getattr(p, f) for f in FIELDS] for p in got] == [[getattr(p, f) for f in FIELDS] for p in exp]
+
+
+def test_route_c3_and_errors_match_golden(golden):
+    g = golden("c3_pieces.json")
+    got = dv.dv_route(dv.Setup(g["prompt_layer_bounds"], [0, 8], 1024), dv.Setup(g["token_layer_bounds"], [0, 8], 2048),
+                      dv.region(0, 64, 0, 8, 0, 1000), 72, 128, 2)
+    assert [[p.src_stage, p.dst_stage, p.layer_begin, p.layer_end] for p in got] == g["pieces"]
+    s = dv.Setup([0, 4, 8], [0, 4], 32)
+    cases = [
+        (dv.Setup([0, 10], [0, 4], 32), s, dv.region(0, 10, 0, 4, 0, 8), dv.DV_EMAP),
+        (s, s, dv.region(0, 8, 0, 5, 0, 8), dv.DV_EMAP),
+        (s, dv.Setup([0, 8], [0, 4], 16), dv.region(0, 8, 0, 4, 0, 17), dv.DV_ERANGE),
+        (dv.Setup([0, 4, 4], [0, 4], 8), s, dv.region(0, 4, 0, 4, 0, 2), dv.DV_EINVAL),
+    ]
+    for a, b, r, st in cases:
+        with pytest.raises(dv.DVError) as ei:
+            dv.dv_route(a, b, r, 2, 8, 2)
+        assert ei.value.status == st
+    with pytest.raises(dv.DVError, match="max_seq 16"):
+        dv.dv_route(s, dv.Setup([0, 8], [0, 4], 16), dv.region(0, 8, 0, 4, 0, 17), 2, 8, 2)
+    assert dv.dv_route(s, s, dv.region(0, 8, 0, 4, 5, 5), 2, 8, 2) == []

@@ -1,0 +1,478 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Inputs come from kvgen only (numpy on the host side; the device fill kernel is itself pinned to
+kvgen here). Expected values come from oracle/ only.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import paper_2403_01876_b200 as dv
+from oracle import kvstream as ok
+from oracle import scenarios
+
+from gpu_util import ctx, flags, pinned_u16, sentinel_like, to_dev, to_np, to_pinned
+
+pytestmark = pytest.mark.gpu
+
+XFERS = [dv.DV_XFER_FUSED, dv.DV_XFER_STAGED]
+
+
+def dev_cache(K, V, lb, rb, pinned=False):
+    k = to_pinned(K) if pinned else to_dev(K)
+    v = to_pinned(V) if pinned else to_dev(V)
+    return k, v, dv.cache(k, v, lb, rb)
+
+
+def oc(K, V, lb, rb, S):
+    return ok.Cache(K, V, lb, rb, K.shape[2], S, K.shape[4])
+
+
+# ------------------------------------------------------------------------------------------------
+def test_device_fill_matches_kvgen():
+    """The device-side writer (dvt_fill) implements kvgen's generator bit-exactly."""
+    L, B, H, S, D = 3, 2, 5, 24, 16
+    k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
+    v = torch.empty_like(k)
+    c = dv.cache(k, v, 7, 3)
+    dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=kvgen.config_seed(1), valid=(2, 20))
+    torch.cuda.synchronize()
+    K, V = kvgen.kv5d_cache("hash", 7, L, 3, B, H, S, D, seed=kvgen.config_seed(1), valid_pos=(2, 20))
+    assert np.array_equal(to_np(k), K) and np.array_equal(to_np(v), V)
+    L, B, H, S, D = 2, 2, 2, 16, 16
+    k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
+    v = torch.empty_like(k)
+    c = dv.cache(k, v, 2, 1)
+    box = (4, 3, H, S, D)
+    dv.dvt_fill(c, dv.DVT_FILL_UID, box=box)
+    torch.cuda.synchronize()
+    K, V = kvgen.kv5d_cache("uid", 2, L, 1, B, H, S, D, box=box)
+    assert np.array_equal(to_np(k), K) and np.array_equal(to_np(v), V)
+
+
+# ------------------------------------------------------------------------------------------------
+def _rand_case(rng):
+    H = rng.choice([1, 3, 4, 8])
+    D = rng.choice([8, 16, 64, 128])          # D*e in {16, 32, 128, 256} bytes
+    nL, nR = rng.randint(1, 5), rng.randint(1, 4)
+    S = rng.randint(2, 70)
+    lb, rb = rng.randint(0, 9), rng.randint(0, 9)
+    l0 = lb + rng.randint(0, nL - 1); l1 = rng.randint(l0 + 1, lb + nL)
+    r0 = rb + rng.randint(0, nR - 1); r1 = rng.randint(r0 + 1, rb + nR)
+    s0 = rng.randint(0, S - 1); s1 = rng.randint(s0 + 1, S)
+    return H, D, nL, nR, S, lb, rb, (l0, l1, r0, r1, s0, s1)
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("xfer", XFERS)
+@pytest.mark.parametrize("host", [False, True])
+def test_scatter_gather_random_shapes(seed, xfer, host):
+    """pack into a device/host endpoint == oracle.pack; unpack from it into a sentinel cache with
+    another max_seq == oracle.unpack; bytes around the chunk in the endpoint stay untouched."""
+    rng = random.Random(seed)
+    H, D, nL, nR, S, lb, rb, reg = _rand_case(rng)
+    K, V = kvgen.kv5d_cache("hash", lb, nL, rb, nR, H, S, D, seed=seed)
+    k, v, c = dev_cache(K, V, lb, rb)
+    wire_words = ok.region_bytes(*reg, H, D, 2) // 2
+    pad = 64
+    buf = pinned_u16(wire_words + 2 * pad) if host else sentinel_like((wire_words + 2 * pad,))
+    ep = dv.endpoint_of(buf)
+    ctx_ = ctx()
+    dv.dv_scatter(ctx_, c, dv.region(*reg), ep, dst_off=pad * 2, xfer=xfer)
+    torch.cuda.synchronize()
+    got = to_np(buf)
+    exp = ok.pack(oc(K, V, lb, rb, S), reg)
+    assert np.array_equal(got[pad:pad + wire_words], exp)
+    assert np.all(got[:pad] == kvgen.SENTINEL) and np.all(got[pad + wire_words:] == kvgen.SENTINEL)
+    # gather into a destination with a different max_seq
+    S2 = max(reg[5], S + rng.randint(-3, 9))
+    dk = sentinel_like((nL, nR, H, S2, D))
+    dvv = sentinel_like((nL, nR, H, S2, D))
+    dc = dv.cache(dk, dvv, lb, rb)
+    dv.dv_gather(ctx_, ep, pad * 2, dc, dv.region(*reg), xfer=xfer)
+    torch.cuda.synchronize()
+    o = oc(*kvgen.sentinel_cache(nL, nR, H, S2, D), lb, rb, S2)
+    ok.unpack(o, reg, exp)
+    assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)
+
+
+@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("mode", ["dev-dev", "dev-host", "host-dev-fused", "host-dev-staged"])
+def test_remap_random_shapes(seed, mode):
+    """Direct layout-to-layout copy (different S, layer and request offsets) == oracle.remap."""
+    rng = random.Random(100 + seed)
+    H, D, nL, nR, S, lb, rb, reg = _rand_case(rng)
+    K, V = kvgen.kv5d_cache("hash", lb, nL, rb, nR, H, S, D, seed=seed)
+    src_host = mode.startswith("host")
+    dst_host = mode == "dev-host"
+    k, v, c = dev_cache(K, V, lb, rb, pinned=src_host)
+    # destination holds a superset of the region's layers/requests at other offsets
+    dlb, drb = reg[0] - rng.randint(0, 2), reg[2] - rng.randint(0, 2)
+    dlb, drb = max(dlb, 0), max(drb, 0)
+    dnL, dnR = reg[1] - dlb + rng.randint(0, 2), reg[3] - drb + rng.randint(0, 2)
+    S2 = reg[5] + rng.randint(0, 20)
+    dk = sentinel_like((dnL, dnR, H, S2, D), pinned=dst_host)
+    dvv = sentinel_like((dnL, dnR, H, S2, D), pinned=dst_host)
+    dc = dv.cache(dk, dvv, dlb, drb)
+    xfer = dv.DV_XFER_STAGED if mode.endswith("staged") else dv.DV_XFER_FUSED
+    dv.dv_remap(ctx(), c, dc, dv.region(*reg), xfer=xfer)
+    torch.cuda.synchronize()
+    o = oc(*kvgen.sentinel_cache(dnL, dnR, H, S2, D), dlb, drb, S2)
+    ok.remap(oc(K, V, lb, rb, S), o, reg)
+    assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)
+    assert np.array_equal(to_np(k), K) and np.array_equal(to_np(v), V)   # source untouched
+
+
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("xfer", XFERS)
+def test_c1_toy_round_trip_through_host(xfer):
+    """C1 (BASELINE.json configs[0]): L2 H4 D16 b2, prompt 32 + 8 tokens, fp16. Prompt streamed out
+    layer by layer to a pinned-host log, then 8 token steps; stream_in of [0,40) into a sentinel
+    cache with S=64. uid fill: every word decodes to its coordinate; poison never crosses."""
+    L, B, H, S, D, p, T = 2, 2, 4, 40, 16, 32, 8
+    box = (L, B, H, S, D)
+    K, V = kvgen.kv5d_cache("uid", 0, L, 0, B, H, S, D, box=box)
+    k, v, c = dev_cache(K, V, 0, 0)
+    one = dv.Setup([0, L], [0, B], S)
+    big = dv.Setup([0, L], [0, B], 64)
+    C = 2 * H * D * 2  # bytes per layer.token.request
+    log = pinned_u16(L * B * (p + T) * C // 2)
+    fl = flags(1, pinned=True)
+    cx = ctx()
+    # prompt, layer by layer (Opt 2): each layer's chunk appended to the log
+    off = 0
+    regions = [(l, l + 1, 0, B, 0, p) for l in range(L)] + \
+              [(0, L, 0, B, ok.token_position(p, t), ok.token_position(p, t) + 1) for t in range(1, T + 1)]
+    offs = []
+    seq = 0
+    for reg in regions:
+        seq += 1
+        ep = dv.endpoint_of(log, fl)
+        dv.dv_scatter(cx, c, dv.region(*reg), ep, dst_off=off, flag_slot=0, seq=seq, xfer=xfer)
+        offs.append(off)
+        off += ok.region_bytes(*reg, H, D, 2)
+    torch.cuda.synchronize()
+    assert int(fl[0]) == seq and dv.dv_query(cx, dv.endpoint_of(log, fl), 0, seq)
+    # oracle: the same sequence of chunks
+    osrc = oc(K, V, 0, 0, S)
+    exp_log = np.concatenate([ok.pack(osrc, reg) for reg in regions])
+    assert np.array_equal(to_np(log)[:exp_log.size], exp_log)
+    # stream back in (each chunk at its offset) into S=64
+    dk = sentinel_like((L, B, H, 64, D)); dvv = sentinel_like((L, B, H, 64, D))
+    dc = dv.cache(dk, dvv, 0, 0)
+    for reg, o in zip(regions, offs):
+        dv.dv_gather(cx, dv.endpoint_of(log, fl), o, dc, dv.region(*reg), flag_slot=0, wait_seq=seq, xfer=xfer)
+    torch.cuda.synchronize()
+    odst = oc(*kvgen.sentinel_cache(L, B, H, 64, D), 0, 0, 64)
+    for reg, o in zip(regions, offs):
+        ok.unpack(odst, reg, exp_log[o // 2:(o + ok.region_bytes(*reg, H, D, 2)) // 2])
+    assert np.array_equal(to_np(dk), odst.K) and np.array_equal(to_np(dvv), odst.V)
+    # independent of the oracle: every word decodes to its own coordinate (definition C-1)
+    g = to_np(dk)[:, :, :, :40]
+    kv_, l_, r_, h_, s_, d_ = kvgen.uid_decode(g, box)
+    ll, rr, hh, ss, dd = np.meshgrid(*[np.arange(n) for n in g.shape], indexing="ij")
+    assert np.all(kv_ == 0) and np.all(l_ == ll) and np.all(r_ == rr) and np.all(s_ == ss) and np.all(d_ == dd)
+    assert np.all(to_np(dk)[:, :, :, 40:] == kvgen.SENTINEL)
+    # level 1 form on the same data: stream_out -> host inbox, stream_in -> S=64 cache
+    inbox = pinned_u16(L * B * (p + T) * C // 2)
+    ifl = flags(1, pinned=True)
+    iep = dv.endpoint_of(inbox, ifl)
+    dv.dv_stream_out(cx, c, dv.region(0, L, 0, B, 0, p + T), one, 0, 0, big, [iep], seq=5, xfer=xfer)
+    dk2 = sentinel_like((L, B, H, 64, D)); dv2 = sentinel_like((L, B, H, 64, D))
+    dv.dv_stream_in(cx, dv.cache(dk2, dv2), dv.region(0, L, 0, B, 0, p + T), one, big, 0, 0, iep, 5, xfer=xfer)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(dk2), odst.K) and np.array_equal(to_np(dv2), odst.V)
+
+
+def test_flag_orders_consumer_after_producer():
+    """A5: the consumer's stream waits on the producer's seq flag. The producer is delayed by a
+    2 ms spin on another stream; without the wait the gather would read the sentinel."""
+    L, B, H, S, D = 2, 2, 4, 16, 16
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=5)
+    k, v, c = dev_cache(K, V, 0, 0)
+    reg = (0, L, 0, B, 0, S)
+    nbytes = ok.region_bytes(*reg, H, D, 2)
+    for host in (False, True):
+        inbox = pinned_u16(nbytes // 2) if host else sentinel_like((nbytes // 2,))
+        fl = flags(4, pinned=host)
+        ep = dv.endpoint_of(inbox, fl)
+        prod, cons = torch.cuda.Stream(), torch.cuda.Stream()
+        cx = ctx()
+        dk = sentinel_like((L, B, H, S, D)); dvv = sentinel_like((L, B, H, S, D))
+        torch.cuda.synchronize()
+        dv.dvt_spin(2_000_000, 1, stream=prod)
+        dv.dv_scatter(cx, c, dv.region(*reg), ep, 0, flag_slot=2, seq=7, xfer=dv.DV_XFER_FUSED, stream=prod)
+        dv.dv_gather(cx, ep, 0, dv.cache(dk, dvv), dv.region(*reg), flag_slot=2, wait_seq=7, stream=cons)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(dk), K) and np.array_equal(to_np(dvv), V)
+        assert int(fl[2]) == 7
+
+
+def test_staged_publish_and_fetch_flush():
+    L, B, H, S, D = 1, 1, 2, 8, 16
+    cx = ctx()
+    src = torch.arange(4096, dtype=torch.int16, device="cuda")
+    host = pinned_u16(4096 + 64)
+    fl = flags(2, pinned=True)
+    ep = dv.endpoint_of(host, fl)
+    for xfer in XFERS:
+        host.fill_(-1)
+        dv.dv_flush(cx, src.data_ptr(), 8192, ep, dst_off=64, flag_slot=1, seq=3 + xfer, xfer=xfer)
+        torch.cuda.synchronize()
+        assert int(fl[1]) == 3 + xfer
+        assert np.array_equal(to_np(host)[32:32 + 4096], np.arange(4096, dtype=np.uint16))
+        back = torch.zeros(4096, dtype=torch.int16, device="cuda")
+        dv.dv_fetch(cx, ep, 64, back.data_ptr(), 8192, flag_slot=1, wait_seq=3 + xfer, xfer=xfer)
+        torch.cuda.synchronize()
+        assert torch.equal(back, src)
+
+
+# ------------------------------------------------------------------------------------------------
+def _blocks(setup: ok.Setup):
+    for i in range(setup.n_stages):
+        for u in range(setup.n_micro):
+            yield i, u, setup.layer_bounds[i], setup.layer_bounds[i + 1], setup.req_bounds[u], setup.req_bounds[u + 1]
+
+
+@pytest.mark.parametrize("form", ["inbox-fused", "inbox-staged-host", "direct"])
+@pytest.mark.parametrize("psplit,tsplit,preq,treq", [
+    ([0, 16, 32, 48, 64], [0, 13, 30, 47, 64], [0, 4], [0, 4]),        # C3 partitions (7 pieces)
+    ([0, 16, 32, 48, 64], [0, 13, 30, 47, 64], [0, 4], [0, 2, 4]),     # + batch split (14 pieces)
+    ([0, 9, 18, 27, 36, 45, 54, 62, 70], [0, 35, 70], [0, 2, 4], [0, 4]),  # merge
+])
+def test_disaggregation_stream_out_in(form, psplit, tsplit, preq, treq):
+    """C3 shape shrunk (H=3, D=16, p=12, S 16 -> 24), all blocks on one GPU: every prompt block
+    calls dv_stream_out, every token block dv_stream_in; token caches == oracle.disaggregate."""
+    H, D, p, Sp, St, seed = 3, 16, 12, 16, 24, 21
+    ps, ts = ok.Setup(psplit, preq, Sp), ok.Setup(tsplit, treq, St)
+    dps, dts = dv.Setup(psplit, preq, Sp), dv.Setup(tsplit, treq, St)
+    prompt, oprompt = {}, {}
+    for i, u, a, b, c0, c1 in _blocks(ps):
+        K, V = kvgen.kv5d_cache("hash", a, b - a, c0, c1 - c0, H, Sp, D, seed=seed, valid_pos=(0, p))
+        prompt[(i, u)] = dev_cache(K, V, a, c0)
+        oprompt[(i, u)] = oc(K, V, a, c0, Sp)
+    token, otoken = {}, {}
+    for j, w, a, b, c0, c1 in _blocks(ts):
+        k = sentinel_like((b - a, c1 - c0, H, St, D)); v = sentinel_like((b - a, c1 - c0, H, St, D))
+        token[(j, w)] = (k, v, dv.cache(k, v, a, c0))
+        otoken[(j, w)] = oc(*kvgen.sentinel_cache(b - a, c1 - c0, H, St, D), a, c0, St)
+    reg = dv.region(psplit[0], psplit[-1], preq[0], preq[-1], 0, p)
+    cx = ctx()
+    nblk_t = ts.n_stages * ts.n_micro
+    if form == "direct":
+        dcs = [token[(j, w)][2] for j, w, *_ in _blocks(ts)]
+        nblk_p = ps.n_stages * ps.n_micro
+        sigf = flags(nblk_t * nblk_p)
+        sig = [dv.endpoint_of(sigf[:1], sigf[k * nblk_p:(k + 1) * nblk_p]) for k in range(nblk_t)]
+        for (i, u), (_, _, c) in prompt.items():
+            dv.dv_stream_out_direct(cx, c, reg, dps, i, u, dts, dcs, sig, seq=1)
+    else:
+        host = form.endswith("host")
+        xfer = dv.DV_XFER_STAGED if "staged" in form else dv.DV_XFER_FUSED
+        inb, eps = {}, []
+        for j, w, a, b, c0, c1 in _blocks(ts):
+            words = (b - a) * (c1 - c0) * H * p * D * 2
+            buf = pinned_u16(words) if host else sentinel_like((words,))
+            fl = flags(ps.n_stages * ps.n_micro, pinned=host)
+            inb[(j, w)] = (buf, fl)
+            eps.append(dv.endpoint_of(buf, fl))
+        for (i, u), (_, _, c) in prompt.items():
+            dv.dv_stream_out(cx, c, reg, dps, i, u, dts, eps, seq=1, xfer=xfer)
+        for k_, (j, w, *_r) in enumerate(_blocks(ts)):
+            dv.dv_stream_in(cx, token[(j, w)][2], reg, dps, dts, j, w, eps[k_], 1, xfer=xfer)
+    torch.cuda.synchronize()
+    scenarios.disaggregate(oprompt, ps, otoken, ts, p)
+    for key, (k, v, _) in token.items():
+        assert np.array_equal(to_np(k), otoken[key].K) and np.array_equal(to_np(v), otoken[key].V), key
+
+
+def test_validation_has_no_partial_effect():
+    """An invalid piece anywhere in a stream_out rejects the whole call before anything is
+    enqueued (DESIGN.md conventions): the first inbox stays untouched."""
+    H, D, p, S = 2, 16, 4, 8
+    K, V = kvgen.kv5d_cache("hash", 0, 4, 0, 2, H, S, D, seed=3)
+    k, v, c = dev_cache(K, V, 0, 0)
+    src_s, dst_s = dv.Setup([0, 4], [0, 2], S), dv.Setup([0, 2, 4], [0, 2], S)
+    good = sentinel_like((2 * 2 * H * p * D * 2,))
+    small = sentinel_like((16,))
+    eps = [dv.endpoint_of(good, flags(1)), dv.endpoint_of(small, flags(1))]
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_stream_out(ctx(), c, dv.region(0, 4, 0, 2, 0, p), src_s, 0, 0, dst_s, eps, seq=1)
+    assert ei.value.status == dv.DV_EINVAL
+    torch.cuda.synchronize()
+    assert np.all(to_np(good) == kvgen.SENTINEL)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(ctx(), c, dv.region(0, 4, 0, 2, 0, S + 1), eps[0])
+    assert ei.value.status == dv.DV_ERANGE and "max_seq 8" in str(ei.value)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(ctx(), c, dv.region(0, 5, 0, 2, 0, 2), eps[0])
+    assert ei.value.status == dv.DV_EMAP
+    bad = dv.cache(k, v, 0, 0)
+    bad.head_dim = 12  # 24 bytes per row: not a multiple of 16
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(ctx(), bad, dv.region(0, 1, 0, 1, 0, 1), eps[0])
+    assert ei.value.status == dv.DV_EALIGN
+
+
+def test_empty_regions_are_noops_that_still_publish():
+    H, D, S = 2, 16, 8
+    K, V = kvgen.kv5d_cache("hash", 0, 2, 0, 2, H, S, D, seed=3)
+    k, v, c = dev_cache(K, V, 0, 0)
+    buf = sentinel_like((64,))
+    fl = flags(1)
+    dv.dv_scatter(ctx(), c, dv.region(0, 2, 0, 2, 3, 3), dv.endpoint_of(buf, fl), flag_slot=0, seq=9)
+    torch.cuda.synchronize()
+    assert int(fl[0]) == 9 and np.all(to_np(buf) == kvgen.SENTINEL)
+
+
+# ------------------------------------------------------------------------------------------------
+def _write_token_dev(c: dv.dv_cache, pos, seed):
+    reg = dv.region(c.layer_begin, c.layer_begin + c.n_layers, c.req_begin, c.req_begin + c.n_reqs, pos, pos + 1)
+    dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=seed, reg=reg)
+
+
+@pytest.mark.parametrize("depth,rounds,xfer", [(3, 2, dv.DV_XFER_FUSED), (4, 2, dv.DV_XFER_STAGED), (5, 1, dv.DV_XFER_FUSED)])
+def test_swap_rotation_matches_oracle(depth, rounds, xfer):
+    """C4 shape shrunk: one stage, D microbatches with pinned-host mirror arenas, two device slots;
+    rotation of PAPER.md:272 driven through dv_remap (swap-in: whole prefix host->slot; swap-out:
+    the step's position slot->host). Final arenas and slots == oracle.swap_simulate."""
+    L0, nL, b, H, S, D, p, seed = 9, 2, 2, 4, 24, 16, 6, 77
+    host_np, host_t = {}, {}
+    for x in range(depth):
+        K, V = kvgen.kv5d_cache("hash", L0, nL, x * b, b, H, S, D, seed=seed, valid_pos=(0, p))
+        K[:, :, :, p:] = kvgen.SENTINEL
+        V[:, :, :, p:] = kvgen.SENTINEL
+        host_np[x] = oc(K, V, L0, x * b, S)
+        host_t[x] = (to_pinned(K), to_pinned(V))
+    slots_t = [(sentinel_like((nL, b, H, S, D)), sentinel_like((nL, b, H, S, D))) for _ in range(2)]
+    cx = ctx()
+
+    def hc(x):
+        return dv.cache(host_t[x][0], host_t[x][1], L0, x * b)
+
+    def sc(s, x):
+        return dv.cache(slots_t[s][0], slots_t[s][1], L0, x * b)
+
+    # --- GPU driver of the rotation (independent of the oracle's loop) ---
+    length = {x: p for x in range(depth)}
+    slot_of = {0: 0}
+    dv.dv_remap(cx, hc(0), sc(0, 0), dv.region(L0, L0 + nL, 0, b, 0, p), xfer=xfer)
+    done = {x: 0 for x in range(depth)}
+    for t in range(1, rounds + 1):
+        for x in range(depth):
+            xin, xout = (x + 1) % depth, (x - 1) % depth
+            pos = p + t - 1
+            _write_token_dev(sc(slot_of[x], x), pos, seed)
+            done[x] += 1
+            length[x] = p + done[x]
+            if done[xout] > 0 and xout in slot_of:
+                q = length[xout] - 1
+                dv.dv_remap(cx, sc(slot_of[xout], xout), hc(xout),
+                            dv.region(L0, L0 + nL, xout * b, xout * b + b, q, q + 1), xfer=xfer)
+                free = slot_of.pop(xout)
+            else:
+                free = 1 - slot_of[x]
+            if not (t == rounds and x == depth - 1):
+                dv.dv_remap(cx, hc(xin), sc(free, xin), dv.region(L0, L0 + nL, xin * b, xin * b + b, 0, length[xin]),
+                            xfer=xfer)
+                slot_of[xin] = free
+    last = depth - 1
+    q = length[last] - 1
+    dv.dv_remap(cx, sc(slot_of[last], last), hc(last), dv.region(L0, L0 + nL, last * b, last * b + b, q, q + 1), xfer=xfer)
+    torch.cuda.synchronize()
+
+    oslots = [oc(*kvgen.sentinel_cache(nL, b, H, S, D), L0, 0, S) for _ in range(2)]
+
+    def write(cache, x, pos):
+        for kv in (0, 1):
+            blk = kvgen.logical_block("hash", kv, range(L0, L0 + nL), range(cache.req_begin, cache.req_begin + b),
+                                      H, [pos], D, seed)
+            cache.set_logical(kv, L0, L0 + nL, cache.req_begin, cache.req_begin + b, pos, pos + 1, blk)
+    scenarios.swap_simulate(host_np, oslots, p, rounds, write)
+    for x in range(depth):
+        assert np.array_equal(to_np(host_t[x][0]), host_np[x].K) and np.array_equal(to_np(host_t[x][1]), host_np[x].V)
+    for s in range(2):
+        assert np.array_equal(to_np(slots_t[s][0]), oslots[s].K) and np.array_equal(to_np(slots_t[s][1]), oslots[s].V)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_ring_replication_and_recovery_loopback(P):
+    """C5 shape shrunk, P stages on one GPU (loopback peers): prompt replica then per-token
+    stream_out_direct into the replica store at (x+1)%P with seq flags; then recovery of stage 1.
+    Replicas and restored caches == oracle (scenarios.ring_step / recover)."""
+    Ls, b, H, S, D, p, T, seed = 2, 3, 4, 20, 16, 7, 4, 91
+    L = Ls * P
+    setup = dv.Setup([x * Ls for x in range(P + 1)], [0, b], S)
+    own, rep, oown, orep = {}, {}, {}, {}
+    for x in range(P):
+        K, V = kvgen.kv5d_cache("hash", x * Ls, Ls, 0, b, H, S, D, seed=seed, valid_pos=(0, p))
+        own[x] = dev_cache(K, V, x * Ls, 0)
+        oown[x] = oc(K, V, x * Ls, 0, S)
+        px = (x - 1) % P
+        rk, rv = sentinel_like((Ls, b, H, S, D)), sentinel_like((Ls, b, H, S, D))
+        rep[x] = (rk, rv, dv.cache(rk, rv, px * Ls, 0))
+        orep[x] = oc(*kvgen.sentinel_cache(Ls, b, H, S, D), px * Ls, 0, S)
+    sigf = flags(P * P)
+    sig = [dv.endpoint_of(sigf[:1], sigf[y * P:(y + 1) * P]) for y in range(P)]
+    cx = ctx()
+
+    def replicate(reg_of, seq):
+        for x in range(P):
+            y = (x + 1) % P
+            # destination "setup" of the replica store: replica[y] holds stage x's layers
+            dcs = [None] * P
+            dcs[x] = rep[y][2]
+            dsig = [None] * P
+            dsig[x] = sig[y]
+            dv.dv_stream_out_direct(cx, own[x][2], dv.region(*reg_of(x)), setup, x, 0, setup, dcs, dsig, seq=seq)
+
+    replicate(lambda x: (x * Ls, x * Ls + Ls, 0, b, 0, p), 1)
+    scenarios.ring_step(oown, orep, lambda x: (x * Ls, x * Ls + Ls, 0, b, 0, p))
+    for t in range(1, T + 1):
+        q = p + t - 1
+        for x in range(P):
+            _write_token_dev(own[x][2], q, seed)
+            blkK = kvgen.logical_block("hash", 0, range(x * Ls, x * Ls + Ls), range(b), H, [q], D, seed)
+            blkV = kvgen.logical_block("hash", 1, range(x * Ls, x * Ls + Ls), range(b), H, [q], D, seed)
+            oown[x].set_logical(0, x * Ls, x * Ls + Ls, 0, b, q, q + 1, blkK)
+            oown[x].set_logical(1, x * Ls, x * Ls + Ls, 0, b, q, q + 1, blkV)
+        replicate(lambda x: (x * Ls, x * Ls + Ls, 0, b, q, q + 1), 1 + t)
+        scenarios.ring_step(oown, orep, lambda x: (x * Ls, x * Ls + Ls, 0, b, q, q + 1))
+    torch.cuda.synchronize()
+    for y in range(P):
+        assert np.array_equal(to_np(rep[y][0]), orep[y].K) and np.array_equal(to_np(rep[y][1]), orep[y].V)
+        x = (y - 1) % P
+        assert int(sigf[y * P + x]) == 1 + T   # the seq plays the (x, j, t) ack role
+    # failure of stage 1: wipe its cache and the replica it hosts, then the two recovery copies
+    own[1][0].fill_(-1); own[1][1].fill_(-1); rep[1][0].fill_(-1); rep[1][1].fill_(-1)
+    for a in (oown[1].K, oown[1].V, orep[1].K, orep[1].V):
+        a[...] = kvgen.SENTINEL
+    n = p + T
+    a_, b_ = (1 + 1) % P, (1 - 1) % P
+    dv.dv_remap(cx, rep[a_][2], own[1][2], dv.region(Ls, 2 * Ls, 0, b, 0, n))
+    dv.dv_remap(cx, own[b_][2], rep[1][2], dv.region(b_ * Ls, b_ * Ls + Ls, 0, b, 0, n))
+    torch.cuda.synchronize()
+    scenarios.recover(1, oown, orep, n)
+    assert np.array_equal(to_np(own[1][0]), oown[1].K) and np.array_equal(to_np(own[1][1]), oown[1].V)
+    assert np.array_equal(to_np(rep[1][0]), orep[1].K) and np.array_equal(to_np(rep[1][1]), orep[1].V)
+
+
+def test_paper_baselines_produce_the_wire():
+    """The prior-art baselines (per-run copies, 2-D buffered copies) produce the same wire chunk."""
+    H, D, nL, nR, S = 4, 16, 3, 2, 20
+    K, V = kvgen.kv5d_cache("hash", 0, nL, 0, nR, H, S, D, seed=8)
+    k, v, c = dev_cache(K, V, 0, 0)
+    reg = (0, nL, 0, nR, 5, 11)
+    exp = ok.pack(oc(K, V, 0, 0, S), reg)
+    out = sentinel_like((exp.size,))
+    calls = dv.dvb_per_run_copy(c, dv.region(*reg), out.data_ptr())
+    torch.cuda.synchronize()
+    assert calls == 2 * nL * nR * H and np.array_equal(to_np(out), exp)
+    out.fill_(-1)
+    stg = torch.empty(exp.size, dtype=torch.int16, device="cuda")
+    calls = dv.dvb_buffered_copy(c, dv.region(*reg), stg.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    assert calls == 2 * nL * nR + 1 and np.array_equal(to_np(out), exp)
