@@ -1,0 +1,502 @@
+#!/usr/bin/env python
+"""bench.py -- KV-cache streaming throughput on B200 (DejaVuLib hot path, arXiv 2403.01876).
+
+Workload (BASELINE.json configs[1], "C2"): OPT-13B shape (40 layers, 40 heads, head_dim 128, fp16
+words), batch 8, prompt 1000, max_seq 2048; token-by-token stream-out to pinned host memory on
+one B200. One STEP = one generated token: its K/V (position p+t-1 of every layer, request and
+head = 2*40*8*40 runs of 256 B = 6,553,600 B) is routed, packed and moved to a pinned-host log
+with its sequence flag published -- all hot-path rows of SURVEY §8(a) for the host path
+(route -> pack -> PCIe put -> completion flag). The paper streams tokens per step, not per layer
+(PAPER.md:133); the per-layer form ("us per token-stream per layer") is reported in `extras`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--xfer auto|fused|staged]
+
+N > 1 (torchrun): every rank is an independent pipeline stage streaming its own C2 cache to its own
+pinned host memory (weak scaling, no data-path collective); time = max over ranks.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ---- C2 workload ------------------------------------------------------------------------------------
+L, H, D, B, P, S, E = 40, 40, 128, 8, 1000, 2048, 2
+STEP_BYTES = 2 * L * B * H * D * E          # 6,553,600 B per token step
+LAYER_BYTES = STEP_BYTES // L               # 163,840 B per token per layer
+PROMPT_LAYER_BYTES = LAYER_BYTES * P        # 163,840,000 B per prompt layer
+CONFIG = {"workload": "C2 OPT-13B shape (L40 H40 D128, fp16 words) b8 p1000 S2048: token-by-token "
+                      "stream-out of every layer's new K/V to pinned host, 1 step = 1 token",
+          "model": "OPT-13B KV-cache shape (no weights: pure data movement)",
+          "global_batch": B, "seq_len": S, "prompt": P, "bytes_per_step": STEP_BYTES,
+          "l2": "inputs larger than L2: 13.4 GB device cache, every step reads a fresh position "
+                "(new 256-B lines); host log ring 64 steps = 419 MB"}
+METRIC = "KV stream GB/s (token-step stream-out to pinned host)"
+HBM_PEAK = 6534.8   # MEASURED_PEAKS.json hbm_gbs (copy, read+write)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the measured region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        busy = [float(r[1]) for r in rows if r[9].strip().isdigit() and int(r[9]) > 0
+                and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(busy or sm) if (busy or sm) else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(rows), "samples_busy": len(busy)}
+
+
+# =====================================================================================================
+# our arm
+# =====================================================================================================
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_01876_b200 as dv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    xfer = {"auto": dv.DV_XFER_AUTO, "fused": dv.DV_XFER_FUSED, "staged": dv.DV_XFER_STAGED}[args.xfer]
+    ctx = dv.dv_create(local)
+    k = torch.empty((L, B, H, S, D), dtype=torch.int16, device=dev)
+    v = torch.empty_like(k)
+    cache = dv.cache(k, v)
+    seed = 20240304 + 1
+    dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=seed)          # writer: every position written
+    RING = 64
+    log = torch.empty(RING * STEP_BYTES // 2, dtype=torch.int16, pin_memory=True)
+    fl = torch.zeros(4, dtype=torch.int64, pin_memory=True)
+    ep = dv.endpoint_of(log, fl)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    npos = S - P
+
+    def pos_of(t):            # token step t >= 1 writes p + t - 1 (reading Q4), wrapped inside S
+        return P + (t - 1) % npos
+
+    def step(t, xf=xfer):
+        q = pos_of(t)
+        dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
+                      flag_slot=0, seq=t, xfer=xf, stream=sp)
+
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    t_ = 0
+    for _ in range(args.warmup):
+        t_ += 1
+        step(t_)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st_all, en_all = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0, _ = dv.dv_stats()
+    st_all.record(stream)
+    for i in range(args.steps):
+        t_ += 1
+        step(t_)
+    en_all.record(stream)
+    torch.cuda.synchronize()
+    l1, dma1 = dv.dv_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed_ms = st_all.elapsed_time(en_all)
+    launches = l1 - l0
+    # parity spot check of the last step against kvgen (the writer's definition), not timed
+    last_q = pos_of(t_)
+    wire = log[(t_ % RING) * STEP_BYTES // 2:(t_ % RING + 1) * STEP_BYTES // 2]
+    assert int(fl[0]) == t_, "flag not published"
+    spot = _spot_check(wire, last_q, seed)
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+
+    # ---- e2e: host buffers through the public API (H2D of the step's new K/V -> cache, stream-out)
+    delta = torch.empty(RING * STEP_BYTES // 2, dtype=torch.int16, pin_memory=True)
+    dfl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    dep = dv.endpoint_of(delta, dfl)
+    for j in range(RING):   # the model's outputs for the next RING tokens, prepared on the host
+        q = pos_of(j + 1)
+        dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), dep, j * STEP_BYTES,
+                      xfer=dv.DV_XFER_FUSED, stream=sp)
+    torch.cuda.synchronize()
+
+    s_in = torch.cuda.Stream()
+    evs = [torch.cuda.Event() for _ in range(8)]
+
+    def e2e_step(t):
+        # H2D of step t's new K/V on s_in (overlaps the D2H of step t-1 on the main stream: PCIe is
+        # full duplex), then the stream-out of step t on the main stream once it has landed.
+        q = pos_of(t)
+        j = (t - 1) % RING
+        dv.dv_gather(ctx, dep, j * STEP_BYTES, cache, dv.region(0, L, 0, B, q, q + 1), stream=s_in)
+        e = evs[t % 8]
+        e.record(s_in)
+        stream.wait_event(e)
+        dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
+                      flag_slot=0, seq=10_000_000 + t, xfer=xfer, stream=sp)
+    for t in range(1, args.warmup + 1):
+        e2e_step(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s_in.wait_event(e0)
+    for t in range(1, args.steps + 1):
+        e2e_step(t)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras = run_extras(dv, ctx, cache, stream, args, pos_of)
+    clk = clocks.stop()
+
+    value = world * args.steps * STEP_BYTES / (elapsed_ms * 1e-3) / 1e9
+    e2e_val = world * args.steps * STEP_BYTES / (e2e_ms * 1e-3) / 1e9
+    # one fused kernel per step: its average duration <= elapsed / launches (gaps included, so the
+    # achieved figure below is a lower bound)
+    mean_kernel_ms = elapsed_ms / max(1, launches)
+    peaks = _peaks()
+    pcie_peak = extras.get("pcie_dma_d2h_gbs")
+    if rank != 0:
+        dv.dv_destroy(ctx)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    roof = {"bound": "pcie", "achieved": STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9,
+            "peak": pcie_peak, "unit": "GB/s",
+            "frac": (STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9 / pcie_peak) if pcie_peak else None,
+            "traffic": None,
+            "kernel": "k_run_copy (fused pack -> pinned host zero-copy PCIe stores + st.release.sys flag)",
+            "algorithmic_bytes_per_launch": STEP_BYTES,
+            "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
+                           "PCIe Gen5 x16 nominal 64 GB/s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
+        "data": "synthetic (splitmix64 coordinate-hash fill, seed 20240305)",
+        "config": dict(CONFIG, parallelism=f"independent stages x{world}" if world > 1 else "1 stage",
+                       xfer=args.xfer),
+        "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": STEP_BYTES,
+                "d2h_bytes_per_step": STEP_BYTES,
+                "how": "per step: dv_gather of the token's K/V from pinned host into the device cache "
+                       "(H2D, side stream) then dv_scatter to the pinned-host log (D2H, main stream); "
+                       "step t's H2D overlaps step t-1's D2H"},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clk,
+        "parity_spot_check": spot,
+        "extras": extras,
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    dv.dv_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _spot_check(wire, q, seed):
+    """Sampled parity of one streamed step vs kvgen's definition, positions via the oracle's wire
+    order (oracle.kvstream.wire_index)."""
+    import numpy as np
+
+    import kvgen
+    from oracle import kvstream as ok
+    w = wire.cpu().numpy().view(np.uint16)
+    rng = np.random.default_rng(0)
+    n = 4096
+    l = rng.integers(0, L, n); kv = rng.integers(0, 2, n); r = rng.integers(0, B, n)
+    h = rng.integers(0, H, n); d = rng.integers(0, D, n)
+    reg = (0, L, 0, B, q, q + 1)
+    idx = np.array([ok.wire_index(reg, H, D, int(l[i]), int(kv[i]), int(r[i]), int(h[i]), q, int(d[i]))
+                    for i in range(n)])
+    exp = kvgen.hash_words(kv, l, r, h, np.full(n, q), d, seed)
+    bad = int(np.sum(w[idx] != exp))
+    assert bad == 0, f"{bad} sampled words differ from the oracle"
+    return {"samples": n, "mismatches": bad}
+
+
+def _time(fn, stream, reps, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_extras(dv, ctx, cache, stream, args, pos_of):
+    """Secondary measurements reported beside the headline (same run, same box)."""
+    import torch
+    sp = stream.cuda_stream
+    ex = {}
+    # PCIe DMA peaks (roofline denominators for the host path), 256 MiB pinned
+    n = 256 << 20
+    hb = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    db = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ms = _time(lambda: hb.copy_(db, non_blocking=True), stream, 5)
+    ex["pcie_dma_d2h_gbs"] = n / ms / 1e6
+    ms = _time(lambda: db.copy_(hb, non_blocking=True), stream, 5)
+    ex["pcie_dma_h2d_gbs"] = n / ms / 1e6
+    del hb, db
+
+    # token step: fused vs staged (host), and pack-only into HBM
+    log = torch.empty(STEP_BYTES // 2 * 8, dtype=torch.int16, pin_memory=True)
+    ep = dv.endpoint_of(log)
+    dbuf = torch.empty(STEP_BYTES // 2 * 8, dtype=torch.int16, device="cuda")
+    dep = dv.endpoint_of(dbuf)
+    cnt = [0]
+
+    def tok(epx, xf):
+        def f():
+            cnt[0] += 1
+            q = pos_of(cnt[0])
+            dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), epx, (cnt[0] % 8) * STEP_BYTES,
+                          xfer=xf, stream=sp)
+        return f
+    reps = 200
+    for name, epx, xf in (("fused", ep, dv.DV_XFER_FUSED), ("staged", ep, dv.DV_XFER_STAGED)):
+        ms = _time(tok(epx, xf), stream, reps)
+        ex[f"token_step_host_{name}_gbs"] = STEP_BYTES / ms / 1e6
+        ex[f"token_step_host_{name}_us"] = ms * 1e3
+    for name, xf in (("fused", dv.DV_XFER_FUSED), ("staged", dv.DV_XFER_STAGED)):
+        def g(xf=xf):
+            cnt[0] += 1
+            q = pos_of(cnt[0])
+            dv.dv_gather(ctx, ep, (cnt[0] % 8) * STEP_BYTES, cache, dv.region(0, L, 0, B, q, q + 1), xfer=xf,
+                         stream=sp)
+        ms = _time(g, stream, reps)
+        ex[f"token_step_gather_host_{name}_gbs"] = STEP_BYTES / ms / 1e6
+    ms = _time(tok(dep, dv.DV_XFER_FUSED), stream, reps)
+    ex["token_step_pack_hbm_us"] = ms * 1e3
+    ex["token_step_pack_hbm_gbs_2R"] = 2 * STEP_BYTES / ms / 1e6
+    ex["token_step_pack_hbm_frac"] = ex["token_step_pack_hbm_gbs_2R"] / HBM_PEAK
+    ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else "staged"
+
+    # per-layer token latency: writer (fill of the layer's new position) -> stream_out done
+    lat = {}
+    fl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    lep = dv.endpoint_of(log, fl)
+    for name, xf in (("fused", dv.DV_XFER_FUSED), ("staged", dv.DV_XFER_STAGED)):
+        samples = []
+        seq = 0
+        for t in range(1, 11):
+            q = pos_of(t)
+            for layer in range(L):
+                reg = dv.region(layer, layer + 1, 0, B, q, q + 1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp)  # the writer
+                a.record(stream)
+                seq += 1
+                dv.dv_scatter(ctx, cache, reg, lep, layer * LAYER_BYTES, flag_slot=0, seq=seq, xfer=xf,
+                              stream=sp)
+                b.record(stream)
+                samples.append((a, b))
+        torch.cuda.synchronize()
+        us = sorted(a.elapsed_time(b) * 1e3 for a, b in samples)
+        lat[name] = {"p50_us": us[len(us) // 2], "p99_us": us[int(len(us) * 0.99)], "n": len(us)}
+    # host enqueue cost of one per-layer call
+    t0 = time.perf_counter()
+    for layer in range(L):
+        dv.dv_scatter(ctx, cache, dv.region(layer, layer + 1, 0, B, P, P + 1), lep, layer * LAYER_BYTES,
+                      flag_slot=0, seq=10 ** 9 + layer, xfer=dv.DV_XFER_FUSED, stream=sp)
+    lat["host_enqueue_us_per_call"] = (time.perf_counter() - t0) / L * 1e6
+    torch.cuda.synchronize()
+    ex["token_layer_latency"] = lat
+
+    # prompt layer (163.8 MB) stream-out: fused vs staged, and HBM pack
+    pbuf = torch.empty(PROMPT_LAYER_BYTES // 2, dtype=torch.int16, pin_memory=True)
+    pep = dv.endpoint_of(pbuf)
+    pd = torch.empty(PROMPT_LAYER_BYTES // 2, dtype=torch.int16, device="cuda")
+    pdep = dv.endpoint_of(pd)
+    lay = [0]
+
+    def prm(epx, xf):
+        def f():
+            lay[0] = (lay[0] + 1) % L
+            dv.dv_scatter(ctx, cache, dv.region(lay[0], lay[0] + 1, 0, B, 0, P), epx, 0, xfer=xf, stream=sp)
+        return f
+    for name, epx, xf in (("fused", pep, dv.DV_XFER_FUSED), ("staged", pep, dv.DV_XFER_STAGED)):
+        ms = _time(prm(epx, xf), stream, 5)
+        ex[f"prompt_layer_host_{name}_gbs"] = PROMPT_LAYER_BYTES / ms / 1e6
+    ms = _time(prm(pdep, dv.DV_XFER_FUSED), stream, 10)
+    ex["prompt_layer_pack_hbm_gbs_2R"] = 2 * PROMPT_LAYER_BYTES / ms / 1e6
+    ex["prompt_layer_pack_hbm_frac"] = ex["prompt_layer_pack_hbm_gbs_2R"] / HBM_PEAK
+    del pbuf, pd
+
+    # the paper's prior-art copy methods on the same token step (Fig. 11 "Baseline" and Opt (1))
+    out = torch.empty(STEP_BYTES // 2, dtype=torch.int16, pin_memory=True)
+    stg = torch.empty(STEP_BYTES // 2, dtype=torch.int16, device="cuda")
+    q = pos_of(1)
+    reg = dv.region(0, L, 0, B, q, q + 1)
+    ms = _time(lambda: dv.dvb_per_run_copy(cache, reg, out.data_ptr(), stream=sp), stream, 2, warm=1)
+    ex["baseline_per_run_memcpy_us"] = ms * 1e3
+    ms = _time(lambda: dv.dvb_buffered_copy(cache, reg, stg.data_ptr(), out.data_ptr(), stream=sp), stream, 10)
+    ex["baseline_buffered_2d_memcpy_us"] = ms * 1e3
+    ex["speedup_buffered_vs_per_run"] = ex["baseline_per_run_memcpy_us"] / ex["baseline_buffered_2d_memcpy_us"]
+    ex["speedup_ours_vs_buffered"] = ex["baseline_buffered_2d_memcpy_us"] / ex["token_step_host_fused_us"]
+    return ex
+
+
+# =====================================================================================================
+# CPU oracle arm (cpu_baseline and --impl reference)
+# =====================================================================================================
+class OracleStep:
+    """The oracle's token step on a host-resident C2 cache: route -> pack -> transfer into a host
+    log. Only the positions it streams are materialised (np.zeros is lazy), filled by kvgen."""
+
+    def __init__(self, n_pos=16):
+        import numpy as np
+
+        import kvgen
+        from oracle import kvstream as ok
+        self.ok, self.np = ok, np
+        self.K = np.zeros((L, B, H, S, D), np.uint16)
+        self.V = np.zeros((L, B, H, S, D), np.uint16)
+        self.n_pos = n_pos
+        for j in range(n_pos):
+            q = P + j
+            for kv, arr in ((0, self.K), (1, self.V)):
+                arr[:, :, :, q, :] = kvgen.logical_block("hash", kv, range(L), range(B), H, [q], D,
+                                                         20240305)[:, :, :, 0, :]
+        self.cache = ok.Cache(self.K, self.V, 0, 0, H, S, D)
+        self.setup = ok.Setup([0, L], [0, B], S)
+        self.log = np.empty(STEP_BYTES // 2 * 4, np.uint16)
+        self.t = 0
+
+    def step(self):
+        ok = self.ok
+        q = P + self.t % self.n_pos
+        reg = (0, L, 0, B, q, q + 1)
+        for p in ok.route(self.setup, self.setup, reg, H, D, E):
+            wire = ok.transfer(ok.pack(self.cache, p.region()))
+            o = (self.t % 4) * (STEP_BYTES // 2)
+            self.log[o:o + wire.size] = wire
+        self.t += 1
+
+
+def cpu_baseline(seconds=10.0):
+    o = OracleStep()
+    o.step()
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        o.step()
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n * STEP_BYTES / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} C2 token steps (route+pack+transfer of 6,553,600 B each) over "
+                      f"{o.n_pos} distinct positions of a lazily materialised 13.4 GB host cache, "
+                      f"{dt:.1f} s, numpy single-threaded"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    o = OracleStep()
+    for _ in range(args.warmup):
+        o.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.step()
+    dt = time.perf_counter() - t0
+    val = args.steps * STEP_BYTES / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16 (opaque fp16 words)", "data": "synthetic",
+            "config": dict(CONFIG, parallelism="1 stage (CPU oracle)"),
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} timed C2 token steps of the numpy oracle on host cores"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--xfer", default="auto", choices=["auto", "fused", "staged"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
+        args.cpu_baseline = False
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,8 @@ enum {
   DV_XFER_AUTO = 0,
   DV_XFER_FUSED = 1u << 0,  /* SM kernel reads/writes the endpoint memory directly (zero-copy / P2P) */
   DV_XFER_STAGED = 1u << 1, /* kernel <-> local staging, copy engine DMA for the contiguous chunk */
+  DV_PUBLISH_STREAMOP = 1u << 2, /* publish flags with a stream memory operation after the kernel
+                                    instead of the kernel's own fenced release store            */
   DV_NO_FLAG = 1u << 8      /* do not publish / wait on sequence flags                           */
 };
 
@@ -155,6 +157,9 @@ typedef struct dv_config {
 DV_API const char* dv_last_error(void);                 /* thread-local message of the last failure     */
 DV_API const char* dv_status_str(dv_status s);
 DV_API int32_t dv_abi_version(void);
+/* Counters since the library was loaded (benchmark evidence): kernels launched by the library and
+ * copy-engine DMA calls (cudaMemcpy*Async) it issued. Either pointer may be NULL. */
+DV_API dv_status dv_stats(uint64_t* kernel_launches, uint64_t* dma_calls);
 
 /* ---- pure host functions (no GPU needed) ------------------------------------------------- */
 /* Bytes of K and V in a region: 2*nL*nR*(pos_end-pos_begin)*n_heads*head_dim*elem_bytes

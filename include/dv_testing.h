@@ -20,9 +20,17 @@ enum { DVT_FILL_HASH = 0, DVT_FILL_UID = 1, DVT_FILL_CONST = 2 };
  *                  kv<<62 | l<<52 | r<<40 | h<<30 | s<<10 | d  (elem_bytes must be 2);
  *   DVT_FILL_UID   word = ((((kv*L + l)*R + r)*H + h)*S + s)*D + d with box = {L,R,H,S,D};
  *   DVT_FILL_CONST word = (uint16_t)seed.
+ * If t_end is non-NULL (device memory), the kernel atomically maxes %globaltimer (ns) into it after
+ * its stores -- "the new K/V is written" time for latency measurements. The kernel triggers
+ * programmatic dependent launch at its start, like a PDL-aware attention kernel would.
  * Stream-ordered; no synchronisation. */
 DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
-                   int32_t valid_begin, int32_t valid_end, const dv_region* region, void* stream);
+                   int32_t valid_begin, int32_t valid_end, const dv_region* region,
+                   uint64_t* t_end, void* stream);
+
+/* Latency tracing: while `ts` (device memory) is set, every fused flag publish of `ctx` writes
+ * %globaltimer (ns) to *ts right after its release store. NULL disables. */
+DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
 
 /* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */
 DV_API dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream);

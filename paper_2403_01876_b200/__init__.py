@@ -22,7 +22,7 @@ DV_OK, DV_EINVAL, DV_EMAP, DV_ERANGE, DV_EALIGN, DV_ENOMEM, DV_EPEER, DV_EBUSY, 
     DV_ENOTSUP = range(10)
 DV_LAYOUT_KV5D = 0
 DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
-DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_NO_FLAG = 0, 1, 2, 256
+DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_PUBLISH_STREAMOP, DV_NO_FLAG = 0, 1, 2, 4, 256
 DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
 
 
@@ -78,6 +78,7 @@ _SIGS = {
     "dv_last_error": (C.c_char_p, []),
     "dv_status_str": (C.c_char_p, [C.c_int]),
     "dv_abi_version": (C.c_int32, []),
+    "dv_stats": (C.c_int, [P(C.c_uint64), P(C.c_uint64)]),
     "dv_region_bytes": (C.c_int, [P(dv_region), C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64)]),
     "dv_route": (C.c_int, [P(dv_setup), P(dv_setup), P(dv_region), C.c_int32, C.c_int32, C.c_int32,
                            P(dv_piece), C.c_uint64, P(C.c_uint64)]),
@@ -114,7 +115,8 @@ _SIGS = {
     "dv_signal": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
     "dv_query": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, P(C.c_int32)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
-                           P(dv_region), C.c_void_p]),
+                           P(dv_region), C.c_void_p, C.c_void_p]),
+    "dvt_trace": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dvt_spin": (C.c_int, [C.c_uint64, C.c_int32, C.c_void_p]),
     "dvb_per_run_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, P(C.c_uint64)]),
     "dvb_buffered_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, C.c_void_p,
@@ -245,6 +247,13 @@ def dv_last_error() -> str:
 
 def dv_abi_version() -> int:
     return lib().dv_abi_version()
+
+
+def dv_stats():
+    """(kernel launches, DMA calls) issued by the library since it was loaded."""
+    a, b = C.c_uint64(), C.c_uint64()
+    _call("dv_stats", C.byref(a), C.byref(b))
+    return a.value, b.value
 
 
 def dv_region_bytes(reg: dv_region, n_heads, head_dim, elem_bytes) -> int:
@@ -395,9 +404,15 @@ def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
 
 
 # ---- test-only utilities (include/dv_testing.h) and baselines (include/dv_baselines.h) -----------
-def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_region = None, stream=None):
+def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_region = None, stream=None,
+             t_end_ptr=0):
     b = (C.c_int32 * 5)(*box) if box is not None else None
-    _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], _ref(reg), _stream(stream))
+    _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], _ref(reg), C.c_void_p(t_end_ptr),
+          _stream(stream))
+
+
+def dvt_trace(ctx, ts_ptr=0):
+    _call("dvt_trace", ctx.h, C.c_void_p(ts_ptr))
 
 
 def dvt_spin(ns, ctas, stream=None):

@@ -233,6 +233,7 @@ static Release ticket_release(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, 
     r.flag = (unsigned long long*)&ep->flags[slot];
     r.seq = seq;
     r.ticket = ctx->tickets + (ctx->next_ticket.fetch_add(1) % dv_ctx::kTickets);
+    r.ts = ctx->trace_ts;
   }
   return r;
 }
@@ -254,6 +255,18 @@ static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
   int r = d->streamWaitValue64(stream, (unsigned long long)(uintptr_t)&ep->flags[slot], seq,
                                CU_STREAM_WAIT_VALUE_GEQ);
   if (r) return drv_fail(r, "cuStreamWaitValue64");
+  return DV_OK;
+}
+
+// One fused kernel, then the flag: by the kernel itself (fenced st.release.sys from the last CTA)
+// or, with DV_PUBLISH_STREAMOP, by a stream memory operation after it.
+static dv_status launch_publish(dv_ctx* ctx, const CopyPlan& p, const dv_endpoint* ep, int32_t slot,
+                                uint64_t seq, bool use_flag, uint32_t xfer, cudaStream_t st) {
+  const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
+  const Release none{nullptr, 0, nullptr};
+  DV_TRY(launch_copy(p, 0, p.runs(), streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag),
+                     ctx->max_ctas, st));
+  if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
   return DV_OK;
 }
 
@@ -299,8 +312,7 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
   if (mode == DV_XFER_FUSED) {
     CopyPlan p = make_plan(cache_side(c, &op.reg), wire_side(wire, &op.reg, c->n_heads, run),
                            &op.reg, c->n_heads, run, ORDER_WIRE);
-    return launch_copy(p, 0, p.runs(), ticket_release(ctx, op.dst, op.slot, op.seq, use_flag),
-                       ctx->max_ctas, st);
+    return launch_publish(ctx, p, op.dst, op.slot, op.seq, use_flag, op.xfer, st);
   }
   // STAGED: pack chunks of runs into staging, copy engine moves each chunk.
   if (bytes) {
@@ -319,7 +331,7 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
       CopyPlan pc = p;
       pc.dst = stg - q0 * rb;  // run q lands at stg + (q - q0) * rb (wire side is dense)
       DV_TRY(launch_copy(pc, q0, q1, Release{nullptr, 0, nullptr}, ctx->max_ctas, st));
-      DV_CUDA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, st));
+      DV_DMA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, st));
       DV_TRY(ctx->staging.release(off, nb, st));
     }
   }
@@ -369,7 +381,7 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
     uint8_t* stg;
     uint64_t off;
     DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
-    DV_CUDA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, st));
+    DV_DMA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, st));
     CopyPlan pc = p;
     pc.src = stg - q0 * rb;
     DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
@@ -424,17 +436,16 @@ static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
           const uint8_t* sp = s.base + kv * s.s_kv + l * s.s_l + r * s.s_r;
           uint8_t* dp = (uint8_t*)d.base + kv * d.s_kv + l * d.s_l + r * d.s_r;
           if (flat || H == 1) {
-            DV_CUDA(cudaMemcpyAsync(dp, sp, (size_t)run * (flat ? H : 1), cudaMemcpyDefault, st));
+            DV_DMA(cudaMemcpyAsync(dp, sp, (size_t)run * (flat ? H : 1), cudaMemcpyDefault, st));
           } else {
-            DV_CUDA(cudaMemcpy2DAsync(dp, (size_t)d.s_h, sp, (size_t)s.s_h, (size_t)run, H,
+            DV_DMA(cudaMemcpy2DAsync(dp, (size_t)d.s_h, sp, (size_t)s.s_h, (size_t)run, H,
                                       cudaMemcpyDefault, st));
           }
         }
     if (use_flag) DV_TRY(stream_signal(op.signal, op.slot, op.seq, st));
     return DV_OK;
   }
-  return launch_copy(p, 0, p.runs(), ticket_release(ctx, op.signal, op.slot, op.seq, use_flag),
-                     ctx->max_ctas, st);
+  return launch_publish(ctx, p, op.signal, op.slot, op.seq, use_flag, op.xfer, st);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -596,6 +607,12 @@ dv_status dv_ipc_close(void* mapped) {
   return DV_OK;
 }
 
+dv_status dv_stats(uint64_t* kernel_launches, uint64_t* dma_calls) {
+  if (kernel_launches) *kernel_launches = g_kernel_launches.load();
+  if (dma_calls) *dma_calls = g_dma_calls.load();
+  return DV_OK;
+}
+
 // ---- level 3 --------------------------------------------------------------------------------
 dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoint* dst,
                    uint64_t dst_off, int32_t flag_slot, uint64_t seq, uint32_t xfer,
@@ -620,10 +637,9 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
       p.ss[3] = p.ds[3] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
-    return launch_copy(p, 0, p.runs(), ticket_release(ctx, dst, flag_slot, seq, use_flag),
-                       ctx->max_ctas, st);
+    return launch_publish(ctx, p, dst, flag_slot, seq, use_flag, xfer, st);
   }
-  if (bytes) DV_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st));
+  if (bytes) DV_DMA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st));
   if (use_flag) DV_TRY(stream_signal(dst, flag_slot, seq, st));
   return DV_OK;
 }
@@ -652,7 +668,7 @@ dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_
     }
     return launch_copy(p, 0, p.runs(), Release{nullptr, 0, nullptr}, ctx->max_ctas, st);
   }
-  if (bytes) DV_CUDA(cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDefault, st));
+  if (bytes) DV_DMA(cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDefault, st));
   return DV_OK;
 }
 

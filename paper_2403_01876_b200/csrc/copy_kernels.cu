@@ -20,11 +20,16 @@
 //   * optional fused publish: after its stores each CTA fences at system scope and bumps a
 //     ticket; the last CTA stores the 64-bit sequence flag with st.release.sys (peer / host
 //     observers then see the payload before the flag).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "dv_internal.h"
 
 namespace dv {
+
+std::atomic<uint64_t> g_kernel_launches{0};
+std::atomic<uint64_t> g_dma_calls{0};
 
 struct DevDiv {
   uint32_t d, mul, shr;
@@ -48,6 +53,7 @@ struct KParams {
   unsigned long long* flag;
   unsigned long long seq;
   unsigned int* ticket;
+  unsigned long long* ts;  // optional: %globaltimer right after the flag store (latency tracing)
 };
 
 template <int VEC>
@@ -103,12 +109,20 @@ __device__ __forceinline__ void publish(const KParams& p) {
       __threadfence_system();
       *p.ticket = 0u;  // ready for the next stream-ordered user of this ticket
       asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(p.seq) : "memory");
+      if (p.ts) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        *p.ts = t;
+      }
     }
   }
 }
 
 template <int VEC, int U, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
+  // Programmatic dependent launch: this grid may become resident while the kernel that wrote the
+  // K/V (e.g. attention) is still draining; wait here until that grid's memory is visible.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t chunk = THREADS * U;
   for (uint32_t base = blockIdx.x * chunk; base < p.n_vec; base += gridDim.x * chunk) {
     Vec<VEC> v[U];
@@ -133,11 +147,67 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
 
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
 
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int VEC, int U, int THREADS>
 static cudaError_t go(const KParams& kp, int blocks, cudaStream_t st) {
   (void)cudaGetLastError();  // clear stale non-sticky errors of unrelated earlier calls
-  k_run_copy<VEC, U, THREADS><<<blocks, THREADS, 0, st>>>(kp);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_run_copy<VEC, U, THREADS>, kp);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// Launch-shape tunables (environment, read once; for experiments -- DESIGN.md "Kernel tuning").
+struct Tune {
+  int u = 0;          // DV_U: vectors in flight per thread (1,2,4,8); 0 = automatic
+  int vec = 0;        // DV_VEC: force 16-byte vectors when 16
+  uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
+};
+static const Tune& tune() {
+  static Tune t = [] {
+    Tune x;
+    if (const char* e = getenv("DV_U")) x.u = atoi(e);
+    if (const char* e = getenv("DV_VEC")) x.vec = atoi(e);
+    if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
+    return x;
+  }();
+  return t;
+}
+
+template <int VEC>
+static cudaError_t launch_vec(const KParams& kp, int u, int max_ctas, cudaStream_t st) {
+  const int threads = u == 1 ? 128 : 256;
+  const uint64_t need = (kp.n_vec + (uint64_t)threads * u - 1) / ((uint64_t)threads * u);
+  const int blocks = (int)std::min<uint64_t>(need, (uint64_t)(u == 1 ? (1u << 30) : max_ctas));
+  switch (u) {
+    case 1: return go<VEC, 1, 128>(kp, blocks, st);
+    case 2: return go<VEC, 2, 256>(kp, blocks, st);
+    case 8: return go<VEC, 8, 256>(kp, blocks, st);
+    default: return go<VEC, 4, 256>(kp, blocks, st);
+  }
+}
+
+// Small copies (per-token updates): one vector per thread, 128-thread CTAs, as many CTAs as
+// needed -> lowest latency. Large copies: U vectors in flight per thread, grid capped at max_ctas.
+static cudaError_t launch_cfg(const KParams& kp, int vec, int max_ctas, cudaStream_t st) {
+  const Tune& t = tune();
+  int u = t.u ? t.u : (kp.n_vec <= t.small ? 1 : 4);
+  return vec == 32 ? launch_vec<32>(kp, u, max_ctas, st) : launch_vec<16>(kp, u, max_ctas, st);
 }
 
 dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, const Release& rel,
@@ -151,6 +221,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
       kp.flag = rel.flag;
       kp.seq = rel.seq;
       kp.ticket = rel.ticket;
+      kp.ts = rel.ts;
       cudaError_t e = go<16, 1, 32>(kp, 1, stream);
       if (e != cudaSuccess) return cuda_fail(e, "publish kernel launch");
     }
@@ -160,7 +231,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
   uint64_t orall = (uint64_t)(uintptr_t)p.src | (uint64_t)(uintptr_t)p.dst | p.run_bytes;
   for (int k = 0; k < 4; ++k) orall |= (uint64_t)p.ss[k] | (uint64_t)p.ds[k];
   if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
-  const int VEC = (orall % 32 == 0) ? 32 : 16;
+  const int VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
   const uint64_t vpr = p.run_bytes / VEC;
   if (vpr >= (1ull << 31)) return fail(DV_ENOTSUP, "run of %llu bytes too long", (unsigned long long)p.run_bytes);
   for (int k = 1; k < 4; ++k)
@@ -187,18 +258,8 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.flag = last ? rel.flag : nullptr;
     kp.seq = rel.seq;
     kp.ticket = rel.ticket;
-    cudaError_t e;
-    // Small copies (per-token updates): one vector per thread, 128-thread CTAs, as many CTAs as
-    // needed -> lowest latency. Large copies: 4 vectors in flight per thread, capped grid.
-    const uint64_t small_limit = 148ull * 128 * 4;
-    if (kp.n_vec <= small_limit) {
-      const int blocks = (int)((kp.n_vec + 127) / 128);
-      e = VEC == 32 ? go<32, 1, 128>(kp, blocks, stream) : go<16, 1, 128>(kp, blocks, stream);
-    } else {
-      const uint64_t need = (kp.n_vec + 256 * 4 - 1) / (256 * 4);
-      const int blocks = (int)std::min<uint64_t>(need, (uint64_t)max_ctas);
-      e = VEC == 32 ? go<32, 4, 256>(kp, blocks, stream) : go<16, 4, 256>(kp, blocks, stream);
-    }
+    kp.ts = last ? rel.ts : nullptr;
+    cudaError_t e = launch_cfg(kp, VEC, max_ctas, stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");
   }
   return DV_OK;

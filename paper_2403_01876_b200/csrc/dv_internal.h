@@ -59,6 +59,7 @@ struct Release {
   unsigned long long* flag;  // NULL = none
   unsigned long long seq;
   unsigned int* ticket;      // per-launch CTA counter (library-owned, zero between uses)
+  unsigned long long* ts = nullptr;  // optional publish timestamp (dvt_trace)
 };
 
 // Enqueue the copy kernel(s) for runs [q_first, q_last) of the (collapsed) plan `p` on `stream`;
@@ -77,6 +78,16 @@ struct Driver {
   int (*getErrorString)(int err, const char** str) = nullptr;
 };
 dv_status driver(const Driver** out);
+
+// ---- counters (dv_stats) ---------------------------------------------------------------------
+extern std::atomic<uint64_t> g_kernel_launches;
+extern std::atomic<uint64_t> g_dma_calls;
+// A copy-engine call, counted for dv_stats.
+#define DV_DMA(expr)                                         \
+  do {                                                       \
+    ::dv::g_dma_calls.fetch_add(1, std::memory_order_relaxed); \
+    DV_CUDA(expr);                                           \
+  } while (0)
 
 // ---- staging pool (device), stream-ordered reuse via events ---------------------------------
 class Staging {
@@ -112,6 +123,7 @@ struct dv_ctx {
   unsigned int* tickets;  // device array of kTickets counters
   std::atomic<uint32_t> next_ticket{0};
   cudaStream_t aux;       // private stream for dv_query on device flags
+  unsigned long long* trace_ts = nullptr;  // dvt_trace: publish timestamps land here
   static constexpr uint32_t kTickets = 4096;
 };
 

@@ -22,9 +22,13 @@ struct FillParams {
   uint64_t seedmix;
   int32_t box[5];
   int32_t vlo, vhi;
+  unsigned long long* t_end;  // optional: max over CTAs of %globaltimer after their stores
 };
 
 __global__ void k_fill(const FillParams p) {
+  // Behave like a PDL-aware producer (an attention kernel would do the same): let the dependent
+  // streaming kernel be scheduled now; it still waits (griddepcontrol.wait) for our memory.
+  asm volatile("griddepcontrol.launch_dependents;");
   // blockIdx.x = slab (l, r, h) of the region, blockIdx.y = kv
   uint32_t slab = blockIdx.x;
   const int h = slab % p.H;
@@ -55,6 +59,15 @@ __global__ void k_fill(const FillParams p) {
     }
     base[(int64_t)s * p.D + d] = w;
   }
+  if (p.t_end) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p.t_end, t);
+    }
+  }
 }
 
 __global__ void k_spin(uint64_t ns) {
@@ -71,7 +84,7 @@ using namespace dv;
 
 extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
                               int32_t valid_begin, int32_t valid_end, const dv_region* region,
-                              void* stream) {
+                              uint64_t* t_end, void* stream) {
   DV_TRY(check_cache(c, "cache"));
   if (c->elem_bytes != 2) return fail(DV_ENOTSUP, "dvt_fill supports 16-bit words only");
   dv_region whole{c->layer_begin, c->layer_begin + c->n_layers, c->req_begin,
@@ -101,17 +114,30 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
     for (int i = 0; i < 5; ++i) p.box[i] = box[i];
   p.vlo = valid_begin;
   p.vhi = valid_end;
+  p.t_end = (unsigned long long*)t_end;
   const uint64_t slabs = (uint64_t)(r->layer_end - r->layer_begin) * p.nR * p.H;
   if (!slabs || !p.n) return DV_OK;
   if (slabs >= (1ull << 31)) return fail(DV_ENOTSUP, "region too large for dvt_fill");
   const int threads = p.n * p.D >= 256 ? 256 : 128;
-  k_fill<<<dim3((unsigned)slabs, 2), threads, 0, (cudaStream_t)stream>>>(p);
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)slabs, 2);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = (cudaStream_t)stream;
+  DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill, p));
   DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts) {
+  if (!ctx) return fail(DV_EINVAL, "NULL context");
+  ctx->trace_ts = (unsigned long long*)ts;
   return DV_OK;
 }
 
 extern "C" dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream) {
   if (ctas < 1) return fail(DV_EINVAL, "ctas must be >= 1");
+  (void)cudaGetLastError();
   k_spin<<<ctas, 128, 0, (cudaStream_t)stream>>>(ns);
   DV_CUDA(cudaGetLastError());
   return DV_OK;
