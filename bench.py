@@ -245,6 +245,7 @@ def run_ours(args):
         "roofline": roof,
         "clocks": clk,
         "parity_spot_check": spot,
+        "us_per_token_layer": (extras.get("token_layer_latency", {}).get("host") or {}).get("p50_us"),
         "extras": extras,
     }
     if args.cpu_baseline:
@@ -338,33 +339,56 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["token_step_pack_hbm_frac"] = ex["token_step_pack_hbm_gbs_2R"] / HBM_PEAK
     ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else "staged"
 
-    # per-layer token latency: writer (fill of the layer's new position) -> stream_out done
+    # per-layer token latency: from "layer l's new K/V written" to "bytes resident at
+    # the destination and seq flag visible". The writer is dvt_fill of that layer's new position
+    # (a PDL-aware producer); times are %globaltimer stamps taken by the writer after its stores
+    # and by the stream-out kernel right after its st.release.sys of the flag.
     lat = {}
     fl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
     lep = dv.endpoint_of(log, fl)
-    for name, xf in (("fused", dv.DV_XFER_FUSED), ("staged", dv.DV_XFER_STAGED)):
-        samples = []
-        seq = 0
-        for t in range(1, 11):
-            q = pos_of(t)
-            for layer in range(L):
-                reg = dv.region(layer, layer + 1, 0, B, q, q + 1)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp)  # the writer
-                a.record(stream)
-                seq += 1
-                dv.dv_scatter(ctx, cache, reg, lep, layer * LAYER_BYTES, flag_slot=0, seq=seq, xfer=xf,
-                              stream=sp)
-                b.record(stream)
-                samples.append((a, b))
+    dlog = torch.empty(LAYER_BYTES // 2 * L, dtype=torch.int16, device="cuda")
+    dfl = torch.zeros(1, dtype=torch.int64, device="cuda")
+    n = 400
+    for name, epx in (("host", lep), ("hbm", dv.endpoint_of(dlog, dfl))):
+        te = torch.zeros(n, dtype=torch.int64, device="cuda")
+        ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
+        ts[:, 1:3] = 2 ** 63 - 1
+        # head start: the GPU must run behind the host (as it does in serving), so the stream-out
+        # launch is queued before its producer finishes and PDL can take effect
+        dv.dvt_spin(20_000_000, 1, stream=sp)
+        for i in range(n):
+            q = pos_of(1 + i // L)
+            layer = i % L
+            reg = dv.region(layer, layer + 1, 0, B, q, q + 1)
+            dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp, t_end_ptr=te[i].data_ptr())
+            dv.dvt_trace(ctx, ts[i].data_ptr())
+            dv.dv_scatter(ctx, cache, reg, epx, layer * LAYER_BYTES, flag_slot=0, seq=10 ** 8 + i,
+                          xfer=dv.DV_XFER_FUSED, stream=sp)
+        dv.dvt_trace(ctx, 0)
         torch.cuda.synchronize()
-        us = sorted(a.elapsed_time(b) * 1e3 for a, b in samples)
-        lat[name] = {"p50_us": us[len(us) // 2], "p99_us": us[int(len(us) * 0.99)], "n": len(us)}
-    # host enqueue cost of one per-layer call
+        d = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
+        lat[name] = {"p50_us": d[len(d) // 2], "p99_us": d[int(len(d) * 0.99)], "min_us": d[0], "n": len(d),
+                     "how": "writer-end -> flag-published, %globaltimer"}
+    # the same with a CUDA event between writer and stream-out (breaks PDL, adds the launch gap)
+    samples = []
+    for i in range(n):
+        q = pos_of(1 + i // L)
+        layer = i % L
+        reg = dv.region(layer, layer + 1, 0, B, q, q + 1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp)
+        a.record(stream)
+        dv.dv_scatter(ctx, cache, reg, lep, layer * LAYER_BYTES, flag_slot=0, seq=2 * 10 ** 8 + i,
+                      xfer=dv.DV_XFER_FUSED, stream=sp)
+        b.record(stream)
+        samples.append((a, b))
+    torch.cuda.synchronize()
+    us = sorted(a.elapsed_time(b) * 1e3 for a, b in samples)
+    lat["host_event_bracketed"] = {"p50_us": us[len(us) // 2], "p99_us": us[int(len(us) * 0.99)], "n": len(us)}
     t0 = time.perf_counter()
     for layer in range(L):
         dv.dv_scatter(ctx, cache, dv.region(layer, layer + 1, 0, B, P, P + 1), lep, layer * LAYER_BYTES,
-                      flag_slot=0, seq=10 ** 9 + layer, xfer=dv.DV_XFER_FUSED, stream=sp)
+                      flag_slot=0, seq=3 * 10 ** 8 + layer, xfer=dv.DV_XFER_FUSED, stream=sp)
     lat["host_enqueue_us_per_call"] = (time.perf_counter() - t0) / L * 1e6
     torch.cuda.synchronize()
     ex["token_layer_latency"] = lat

@@ -219,6 +219,17 @@ DV_API dv_status dv_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* r
 DV_API dv_status dv_gather(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_t flag_slot,
                     uint64_t wait_seq, const dv_cache* dst, const dv_region* region,
                     uint32_t xfer, void* stream);
+/* Batched gather of a LOG of chunks: n_chunks canonical wire chunks stored back to back at
+ * src->base + src_off; chunk k is the wire of `first` shifted by k*pos_step positions
+ * (pos_step >= first's position count). Typical use: swap-in of a microbatch from its host log,
+ * where every token step appended one chunk of one position (swap-out moves only the
+ * step's delta; swap-in moves the whole prefix). One copy-engine stream of the whole
+ * log (STAGED, the AUTO choice for host sources) or one kernel (FUSED) for all chunks. Waits for
+ * src->flags[flag_slot] >= wait_seq first when flag_slot >= 0. */
+DV_API dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off,
+                                  int32_t flag_slot, uint64_t wait_seq, const dv_cache* dst,
+                                  const dv_region* first, int32_t n_chunks, int32_t pos_step,
+                                  uint32_t xfer, void* stream);
 /* Direct layout-to-layout copy of `region` (pack and unpack fused, no wire buffer). Either cache
  * may live in local device memory, pinned host memory (mirror-form arena) or mapped peer memory.
  * If `signal` is non-NULL and flag_slot >= 0, publishes signal->flags[flag_slot] = seq after. */

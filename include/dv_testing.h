@@ -28,8 +28,11 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
                    int32_t valid_begin, int32_t valid_end, const dv_region* region,
                    uint64_t* t_end, void* stream);
 
-/* Latency tracing: while `ts` (device memory) is set, every fused flag publish of `ctx` writes
- * %globaltimer (ns) to *ts right after its release store. NULL disables. */
+/* Latency tracing: while `ts` (device memory, 4 x uint64) is set, every fused copy of `ctx` that
+ * publishes a flag records %globaltimer (ns): ts[0] = right after the release store of the flag,
+ * ts[1] = min over CTAs of "resident" (before the programmatic-dependency wait; initialise to
+ * UINT64_MAX), ts[2] = min over CTAs of "past the wait" (initialise to UINT64_MAX), ts[3] = max
+ * over CTAs of "stores issued". NULL disables. */
 DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
 
 /* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */

@@ -325,6 +325,22 @@ def unpack(dst: Cache, region, wire: np.ndarray, mode: str = "vector") -> None:
         dst.set_logical(kv, l0, l1, r0, r1, s0, s1, w[:, kv])
 
 
+def shifted(region, k):
+    """`region` moved k positions later."""
+    l0, l1, r0, r1, s0, s1 = region
+    return (l0, l1, r0, r1, s0 + k, s1 + k)
+
+
+def unpack_chunks(dst: Cache, first, log: np.ndarray, n_chunks: int, pos_step: int,
+                  mode: str = "vector") -> None:
+    """A log of chunks (host log form of a swap arena, reading of PAPER.md:270/572): chunk k is the
+    wire of `first` shifted by k*pos_step positions, stored back to back. Unpack them in order."""
+    e = dst.elem_bytes
+    w = region_bytes(*first, dst.n_heads, dst.head_dim, e) // e
+    for k in range(n_chunks):
+        unpack(dst, shifted(first, k * pos_step), log[k * w:(k + 1) * w], mode)
+
+
 def transfer(wire: np.ndarray) -> np.ndarray:
     """flush / fetch: copy one contiguous chunk. On the CPU: a byte copy."""
     return np.frombuffer(bytes(wire.tobytes()), dtype=wire.dtype).copy()

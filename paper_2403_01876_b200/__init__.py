@@ -99,6 +99,8 @@ _SIGS = {
                              C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
     "dv_gather": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_uint64, C.c_int32, C.c_uint64,
                             P(dv_cache), P(dv_region), C.c_uint32, C.c_void_p]),
+    "dv_gather_chunks": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_uint64, C.c_int32, C.c_uint64,
+                                   P(dv_cache), P(dv_region), C.c_int32, C.c_int32, C.c_uint32, C.c_void_p]),
     "dv_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint),
                            C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
     "dv_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
@@ -360,6 +362,12 @@ def dv_gather(ctx, src: dv_endpoint, src_off, dst: dv_cache, reg: dv_region, fla
               xfer=0, stream=None):
     _call("dv_gather", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), C.byref(reg),
           xfer, _stream(stream))
+
+
+def dv_gather_chunks(ctx, src: dv_endpoint, src_off, dst: dv_cache, first: dv_region, n_chunks, pos_step,
+                     flag_slot=-1, wait_seq=0, xfer=0, stream=None):
+    _call("dv_gather_chunks", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), C.byref(first),
+          n_chunks, pos_step, xfer, _stream(stream))
 
 
 def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpoint = None, flag_slot=-1,

@@ -2,6 +2,7 @@
 // (Table 1) on top of the run-copy kernel (copy_kernels.cu) and the route
 // planner (route.cpp).
 #include <cuda.h>
+#include <limits.h>
 #include <string.h>
 #include <unistd.h>
 
@@ -178,15 +179,16 @@ static CopyPlan make_plan(const Side& s, const Side& d, const dv_region* r, int3
   p.src = s.base;
   p.dst = (uint8_t*)d.base;
   const uint32_t nL = r->layer_end - r->layer_begin, nR = r->req_end - r->req_begin;
+  p.n[0] = 1;
   if (order == ORDER_WIRE) {
-    p.n[0] = nL; p.ss[0] = s.s_l;  p.ds[0] = d.s_l;
-    p.n[1] = 2;  p.ss[1] = s.s_kv; p.ds[1] = d.s_kv;
-  } else {
-    p.n[0] = 2;  p.ss[0] = s.s_kv; p.ds[0] = d.s_kv;
     p.n[1] = nL; p.ss[1] = s.s_l;  p.ds[1] = d.s_l;
+    p.n[2] = 2;  p.ss[2] = s.s_kv; p.ds[2] = d.s_kv;
+  } else {
+    p.n[1] = 2;  p.ss[1] = s.s_kv; p.ds[1] = d.s_kv;
+    p.n[2] = nL; p.ss[2] = s.s_l;  p.ds[2] = d.s_l;
   }
-  p.n[2] = nR; p.ss[2] = s.s_r; p.ds[2] = d.s_r;
-  p.n[3] = H;  p.ss[3] = s.s_h; p.ds[3] = d.s_h;
+  p.n[3] = nR; p.ss[3] = s.s_r; p.ds[3] = d.s_r;
+  p.n[4] = H;  p.ss[4] = s.s_h; p.ds[4] = d.s_h;
   p.run_bytes = (uint64_t)run;
   collapse(p);
   return p;
@@ -270,14 +272,18 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan& p, const dv_endpoin
   return DV_OK;
 }
 
-// Chooses FUSED or STAGED for a data call.
-static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes) {
+// Chooses FUSED or STAGED for a data call (measured in
+// profiles/r01_tune_host*.jsonl): writes to pinned host go through the kernel's own PCIe stores
+// (same throughput as pack+DMA, lower latency, no staging); reads from pinned host go through the
+// copy engine (SM zero-copy reads do not overlap with concurrent D2H traffic).
+static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes, bool reading) {
   uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   if (m == DV_XFER_FUSED || m == DV_XFER_STAGED) {
     if (m == DV_XFER_STAGED && ep->kind == DV_EP_DEVICE) return DV_XFER_FUSED;  // already local
     return m;
   }
-  if (ep->kind == DV_EP_HOST && bytes > (64ull << 20)) return DV_XFER_STAGED;
+  if (ep->kind == DV_EP_HOST && reading) return DV_XFER_STAGED;
+  (void)bytes;
   return DV_XFER_FUSED;
 }
 
@@ -307,7 +313,7 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
   const uint64_t bytes = region_bytes(&op.reg, c);
   const int64_t run = run_bytes(&op.reg, c);
   const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
-  const uint32_t mode = pick_xfer(op.xfer, op.dst, bytes);
+  const uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
   uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off;
   if (mode == DV_XFER_FUSED) {
     CopyPlan p = make_plan(cache_side(c, &op.reg), wire_side(wire, &op.reg, c->n_heads, run),
@@ -358,17 +364,11 @@ static dv_status gather_check(dv_ctx* ctx, const GatherOp& op) {
   return check_ep(op.src, op.src_off, region_bytes(&op.reg, op.dst), op.slot, use_flag, "source");
 }
 
-static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
-  const dv_cache* c = op.dst;
-  const uint64_t bytes = region_bytes(&op.reg, c);
-  const int64_t run = run_bytes(&op.reg, c);
-  if (!(op.xfer & DV_NO_FLAG) && op.slot >= 0 && op.wait_seq)
-    DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
-  if (!bytes) return DV_OK;
-  const uint32_t mode = pick_xfer(op.xfer, op.src, bytes);
-  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
-  CopyPlan p = make_plan(wire_side(wire, &op.reg, c->n_heads, run), cache_side(c, &op.reg),
-                         &op.reg, c->n_heads, run, ORDER_WIRE);
+// Runs an unpack plan whose source side is a dense wire chunk at `wire` (run q at wire + q*run):
+// FUSED = one kernel reading the endpoint memory directly; STAGED = the copy engine brings chunks
+// of runs into HBM staging, the kernel unpacks each chunk.
+static dv_status unpack_plan(dv_ctx* ctx, const CopyPlan& p, const uint8_t* wire, uint32_t mode,
+                             cudaStream_t st) {
   const Release none{nullptr, 0, nullptr};
   if (mode == DV_XFER_FUSED) return launch_copy(p, 0, p.runs(), none, ctx->max_ctas, st);
   const uint64_t rb = p.run_bytes, runs = p.runs();
@@ -388,6 +388,20 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
     DV_TRY(ctx->staging.release(off, nb, st));
   }
   return DV_OK;
+}
+
+static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
+  const dv_cache* c = op.dst;
+  const uint64_t bytes = region_bytes(&op.reg, c);
+  const int64_t run = run_bytes(&op.reg, c);
+  if (!(op.xfer & DV_NO_FLAG) && op.slot >= 0 && op.wait_seq)
+    DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
+  if (!bytes) return DV_OK;
+  const uint32_t mode = pick_xfer(op.xfer, op.src, bytes, true);
+  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
+  CopyPlan p = make_plan(wire_side(wire, &op.reg, c->n_heads, run), cache_side(c, &op.reg),
+                         &op.reg, c->n_heads, run, ORDER_WIRE);
+  return unpack_plan(ctx, p, wire, mode, st);
 }
 
 struct RemapOp {
@@ -421,7 +435,9 @@ static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
   const bool use_flag = op.signal && !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
   CopyPlan p = make_plan(cache_side(op.src, &op.reg), cache_side(op.dst, &op.reg), &op.reg,
                          c->n_heads, run, ORDER_KV_OUTER);
-  const uint32_t m = op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
+  uint32_t m = op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
+  if (m != DV_XFER_FUSED && m != DV_XFER_STAGED)  // AUTO (profiles/r01_configs*.jsonl, C4):
+    m = (op.src->device < 0 && op.dst->device >= 0) ? DV_XFER_STAGED : DV_XFER_FUSED;
   if (m == DV_XFER_STAGED && p.runs() && p.run_bytes) {
     // Copy-engine form (paper-style DMA, used for pinned-host mirror arenas): one
     // 2-D copy per (kv, layer, request) over the heads, or one 1-D copy when the heads are
@@ -629,12 +645,12 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
     CopyPlan p{};
     p.src = (const uint8_t*)src;
     p.dst = d;
-    p.n[0] = p.n[1] = p.n[2] = p.n[3] = 1;
+    for (int k = 0; k < kDims; ++k) p.n[k] = 1;
     p.run_bytes = bytes;
     // split one long run into 1 MiB runs so the kernel's 32-bit vector index suffices
     if (bytes > (1u << 20) && bytes % (1u << 20) == 0) {
-      p.n[3] = (uint32_t)(bytes >> 20);
-      p.ss[3] = p.ds[3] = 1 << 20;
+      p.n[kDims - 1] = (uint32_t)(bytes >> 20);
+      p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
     return launch_publish(ctx, p, dst, flag_slot, seq, use_flag, xfer, st);
@@ -659,11 +675,11 @@ dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_
     CopyPlan p{};
     p.src = s;
     p.dst = (uint8_t*)dst;
-    p.n[0] = p.n[1] = p.n[2] = p.n[3] = 1;
+    for (int k = 0; k < kDims; ++k) p.n[k] = 1;
     p.run_bytes = bytes;
     if (bytes > (1u << 20) && bytes % (1u << 20) == 0) {
-      p.n[3] = (uint32_t)(bytes >> 20);
-      p.ss[3] = p.ds[3] = 1 << 20;
+      p.n[kDims - 1] = (uint32_t)(bytes >> 20);
+      p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
     return launch_copy(p, 0, p.runs(), Release{nullptr, 0, nullptr}, ctx->max_ctas, st);
@@ -691,6 +707,53 @@ dv_status dv_gather(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32
   DV_TRY(gather_check(ctx, op));
   DV_ON_DEVICE(ctx->device);
   return gather_run(ctx, op, (cudaStream_t)stream);
+}
+
+dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_t flag_slot,
+                           uint64_t wait_seq, const dv_cache* dst, const dv_region* first,
+                           int32_t n_chunks, int32_t pos_step, uint32_t xfer, void* stream) {
+  DV_TRY(check_ctx(ctx));
+  if (!first) return fail(DV_EINVAL, "NULL region");
+  if (n_chunks < 0) return fail(DV_EINVAL, "negative n_chunks");
+  DV_TRY(check_cache(dst, "destination"));
+  DV_TRY(check_region_shape(first));
+  const int32_t n = first->pos_end - first->pos_begin;
+  if (n_chunks > 1 && pos_step < n)
+    return fail(DV_EINVAL, "pos_step %d smaller than the chunk's %d positions", pos_step, n);
+  dv_region last = *first;
+  if (n_chunks > 0) {
+    const int64_t shift = (int64_t)(n_chunks - 1) * pos_step;
+    if (first->pos_end + shift > INT32_MAX) return fail(DV_ERANGE, "chunk positions overflow");
+    last.pos_begin += (int32_t)shift;
+    last.pos_end += (int32_t)shift;
+  }
+  DV_TRY(check_cache_holds(dst, first, "destination"));
+  DV_TRY(check_cache_holds(dst, &last, "destination"));
+  const uint64_t chunk_bytes = region_bytes(first, dst);
+  const uint64_t total = chunk_bytes * (uint64_t)n_chunks;
+  DV_TRY(check_ep(src, src_off, total, flag_slot, !(xfer & DV_NO_FLAG), "source"));
+  DV_ON_DEVICE(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(xfer & DV_NO_FLAG) && flag_slot >= 0 && wait_seq)
+    DV_TRY(stream_wait(src, flag_slot, wait_seq, st));
+  if (!total) return DV_OK;
+  const int64_t run = run_bytes(first, dst);
+  const uint8_t* wire = (const uint8_t*)src->base + src_off;
+  // dims [chunk][l][kv][r][h]: the log side is dense in this order
+  const Side ws = wire_side(wire, first, dst->n_heads, run);
+  const Side cs = cache_side(dst, first);
+  CopyPlan p{};
+  p.src = ws.base;
+  p.dst = (uint8_t*)cs.base;
+  p.n[0] = (uint32_t)n_chunks; p.ss[0] = (int64_t)chunk_bytes;
+  p.ds[0] = (int64_t)pos_step * dst->head_dim * dst->elem_bytes;
+  p.n[1] = first->layer_end - first->layer_begin; p.ss[1] = ws.s_l; p.ds[1] = cs.s_l;
+  p.n[2] = 2; p.ss[2] = ws.s_kv; p.ds[2] = cs.s_kv;
+  p.n[3] = first->req_end - first->req_begin; p.ss[3] = ws.s_r; p.ds[3] = cs.s_r;
+  p.n[4] = dst->n_heads; p.ss[4] = ws.s_h; p.ds[4] = cs.s_h;
+  p.run_bytes = (uint64_t)run;
+  collapse(p);
+  return unpack_plan(ctx, p, wire, pick_xfer(xfer, src, total, true), st);
 }
 
 dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const dv_region* region,

@@ -42,14 +42,13 @@ struct DevDiv {
 struct KParams {
   const uint8_t* src;
   uint8_t* dst;
-  int64_t ss0, ss1, ss2, ss3;
-  int64_t ds0, ds1, ds2, ds3;
-  DevDiv fv;   // vectors per run
-  DevDiv f3;   // n[3]
-  DevDiv f2;   // n[2]
-  DevDiv f1;   // n[1]
+  int64_t ss[kDims];
+  int64_t ds[kDims];
+  DevDiv fv;          // vectors per run
+  DevDiv fd[kDims];   // n[k] (fd[0] unused: the outermost index is what remains)
   uint32_t q_begin;  // first run of this launch
   uint32_t n_vec;    // vectors in this launch (< 2^31)
+  int32_t per_cta_sys;  // publish variant (see publish())
   unsigned long long* flag;
   unsigned long long seq;
   unsigned int* ticket;
@@ -87,32 +86,46 @@ __device__ __forceinline__ void st_vec(uint8_t* p, const Vec<32>& v) {
 template <int VEC>
 __device__ __forceinline__ void locate(const KParams& p, uint32_t g, const uint8_t*& s,
                                        uint8_t*& d) {
-  uint32_t q, w, i3, i2, i1;
+  uint32_t q, w;
   p.fv.divmod(g, q, w);
   q += p.q_begin;
-  p.f3.divmod(q, q, i3);
-  p.f2.divmod(q, q, i2);
-  p.f1.divmod(q, q, i1);  // q is now i0
   const int64_t wo = (int64_t)w * VEC;
-  s = p.src + (int64_t)q * p.ss0 + (int64_t)i1 * p.ss1 + (int64_t)i2 * p.ss2 +
-      (int64_t)i3 * p.ss3 + wo;
-  d = p.dst + (int64_t)q * p.ds0 + (int64_t)i1 * p.ds1 + (int64_t)i2 * p.ds2 +
-      (int64_t)i3 * p.ds3 + wo;
+  int64_t so = wo, dof = wo;
+#pragma unroll
+  for (int k = kDims - 1; k >= 1; --k) {
+    uint32_t i;
+    p.fd[k].divmod(q, q, i);
+    so += (int64_t)i * p.ss[k];
+    dof += (int64_t)i * p.ds[k];
+  }
+  s = p.src + so + (int64_t)q * p.ss[0];
+  d = p.dst + dof + (int64_t)q * p.ds[0];
 }
 
-__device__ __forceinline__ void publish(const KParams& p) {
+// Publish protocol: every CTA orders its stores before a GPU-scope release
+// (bar.sync, then thread 0's fence.acq_rel.gpu + ticket atomic); the CTA that takes the last
+// ticket has, by the acquire on that atomic, every CTA's stores ordered before it, and makes them
+// visible to the system with ONE fence.sc.sys before the st.release.sys of the flag (PTX memory
+// model: causality order is transitive, fences are cumulative). DV_PUBLISH=0 selects the older,
+// more conservative variant with a system fence in every CTA.
+__device__ __forceinline__ void publish(const KParams& p, int per_cta_sys) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's payload (ordered before by the barrier) -> system scope
+    if (per_cta_sys) {
+      __threadfence_system();
+    } else {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
     unsigned int prev = atomicAdd(p.ticket, 1u);
     if (prev == gridDim.x - 1) {
-      __threadfence_system();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire side of the ticket chain
+      __threadfence_system();                          // fence.sc.sys: everything -> system scope
       *p.ticket = 0u;  // ready for the next stream-ordered user of this ticket
       asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(p.seq) : "memory");
       if (p.ts) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        *p.ts = t;
+        p.ts[0] = t;  // flag published
       }
     }
   }
@@ -122,7 +135,17 @@ template <int VEC, int U, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
   // Programmatic dependent launch: this grid may become resident while the kernel that wrote the
   // K/V (e.g. attention) is still draining; wait here until that grid's memory is visible.
+  if (p.ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.ts + 1, t);  // first CTA resident
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.ts + 2, t);  // first CTA past the dependency wait
+  }
   const uint32_t chunk = THREADS * U;
   for (uint32_t base = blockIdx.x * chunk; base < p.n_vec; base += gridDim.x * chunk) {
     Vec<VEC> v[U];
@@ -142,7 +165,65 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
       if (g < p.n_vec) st_vec(d[i], v[i]);
     }
   }
-  if (p.flag) publish(p);
+  if (p.ts) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p.ts + 3, t);  // last CTA done with its stores (issued)
+    }
+  }
+  if (p.flag) publish(p, p.per_cta_sys);
+}
+
+// Dense-destination variant: the destination of vectors [q_begin*vpr, ...) is one contiguous
+// range (packing into a wire chunk). Each CTA gathers THREADS*U vectors into shared memory and one
+// thread moves the whole chunk with a bulk async copy (cp.async.bulk, the TMA engine: UBLKCP),
+// double-buffered. Large, well-formed writes matter most over PCIe and NVLink.
+template <int VEC, int U, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t* dst0) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr uint32_t chunk = THREADS * U;
+  int stage = 0;
+  for (uint32_t base = blockIdx.x * chunk; base < p.n_vec; base += gridDim.x * chunk) {
+    uint8_t* buf = smem + stage * (chunk * VEC);
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    Vec<VEC> v[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t g = base + i * THREADS + threadIdx.x;
+      if (g < p.n_vec) {
+        const uint8_t* s;
+        uint8_t* d;
+        locate<VEC>(p, g, s, d);
+        ld_vec(v[i], s);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t g = base + i * THREADS + threadIdx.x;
+      if (g < p.n_vec) *reinterpret_cast<Vec<VEC>*>(buf + (i * THREADS + threadIdx.x) * VEC) = v[i];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t n = min(chunk, p.n_vec - base) * VEC;
+      uint8_t* d = dst0 + (uint64_t)base * VEC;
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(buf);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(sa),
+                   "r"(n)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    stage ^= 1;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  if (p.flag) publish(p, p.per_cta_sys);
 }
 
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
@@ -176,6 +257,8 @@ static cudaError_t go(const KParams& kp, int blocks, cudaStream_t st) {
 struct Tune {
   int u = 0;          // DV_U: vectors in flight per thread (1,2,4,8); 0 = automatic
   int vec = 0;        // DV_VEC: force 16-byte vectors when 16
+  int bulk = 0;       // DV_BULK: 1 = dense-destination copies use k_pack_bulk
+  int per_cta_sys = 0;  // DV_PUBLISH=0: system fence in every CTA before the ticket
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
 };
 static const Tune& tune() {
@@ -183,6 +266,8 @@ static const Tune& tune() {
     Tune x;
     if (const char* e = getenv("DV_U")) x.u = atoi(e);
     if (const char* e = getenv("DV_VEC")) x.vec = atoi(e);
+    if (const char* e = getenv("DV_BULK")) x.bulk = atoi(e);
+    if (const char* e = getenv("DV_PUBLISH")) x.per_cta_sys = (atoi(e) == 0);
     if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
     return x;
   }();
@@ -210,6 +295,50 @@ static cudaError_t launch_cfg(const KParams& kp, int vec, int max_ctas, cudaStre
   return vec == 32 ? launch_vec<32>(kp, u, max_ctas, st) : launch_vec<16>(kp, u, max_ctas, st);
 }
 
+// Is the destination of run q at dst + q*run_bytes (row-major dense over the loop dims)?
+static bool dense_dst(const CopyPlan& p) {
+  int64_t expect = (int64_t)p.run_bytes;
+  for (int k = kDims - 1; k >= 0; --k) {
+    if (p.n[k] == 1) continue;
+    if (p.ds[k] != expect) return false;
+    expect *= p.n[k];
+  }
+  return true;
+}
+
+template <int VEC>
+static cudaError_t launch_bulk_vec(const KParams& kp, uint8_t* dst0, int max_ctas, cudaStream_t st) {
+  constexpr int T = 256, U = 4;
+  const int smem = 2 * T * U * VEC;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pack_bulk<VEC, U, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const uint64_t need = (kp.n_vec + T * U - 1) / (T * U);
+  const int blocks = (int)std::min<uint64_t>(need, (uint64_t)max_ctas);
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_pack_bulk<VEC, U, T>, kp, dst0);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+static cudaError_t launch_bulk(const KParams& kp, int vec, uint8_t* dst0, int max_ctas,
+                               cudaStream_t st) {
+  return vec == 32 ? launch_bulk_vec<32>(kp, dst0, max_ctas, st)
+                   : launch_bulk_vec<16>(kp, dst0, max_ctas, st);
+}
+
 dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, const Release& rel,
                       int max_ctas, cudaStream_t stream) {
   if (q_last > p.runs()) q_last = p.runs();
@@ -217,11 +346,13 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
   if (q_last == q_first || p.run_bytes == 0) {
     if (rel.flag) {  // nothing to move: still publish in stream order
       KParams kp{};
-      kp.fv = kp.f1 = kp.f2 = kp.f3 = DevDiv{1, 0, 0};
+      kp.fv = DevDiv{1, 0, 0};
+      for (int k = 0; k < kDims; ++k) kp.fd[k] = DevDiv{1, 0, 0};
       kp.flag = rel.flag;
       kp.seq = rel.seq;
       kp.ticket = rel.ticket;
       kp.ts = rel.ts;
+      kp.per_cta_sys = tune().per_cta_sys;
       cudaError_t e = go<16, 1, 32>(kp, 1, stream);
       if (e != cudaSuccess) return cuda_fail(e, "publish kernel launch");
     }
@@ -229,24 +360,24 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
   }
   // 32-byte vectors when every address and stride allows it.
   uint64_t orall = (uint64_t)(uintptr_t)p.src | (uint64_t)(uintptr_t)p.dst | p.run_bytes;
-  for (int k = 0; k < 4; ++k) orall |= (uint64_t)p.ss[k] | (uint64_t)p.ds[k];
+  for (int k = 0; k < kDims; ++k) orall |= (uint64_t)p.ss[k] | (uint64_t)p.ds[k];
   if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
   const int VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
   const uint64_t vpr = p.run_bytes / VEC;
   if (vpr >= (1ull << 31)) return fail(DV_ENOTSUP, "run of %llu bytes too long", (unsigned long long)p.run_bytes);
-  for (int k = 1; k < 4; ++k)
+  for (int k = 1; k < kDims; ++k)
     if (p.n[k] >= (1u << 31)) return fail(DV_ENOTSUP, "copy extent too large");
   if (p.runs() >= (1ull << 31)) return fail(DV_ENOTSUP, "too many runs");
 
   KParams kp{};
   kp.src = p.src;
   kp.dst = p.dst;
-  kp.ss0 = p.ss[0]; kp.ss1 = p.ss[1]; kp.ss2 = p.ss[2]; kp.ss3 = p.ss[3];
-  kp.ds0 = p.ds[0]; kp.ds1 = p.ds[1]; kp.ds2 = p.ds[2]; kp.ds3 = p.ds[3];
+  for (int k = 0; k < kDims; ++k) {
+    kp.ss[k] = p.ss[k];
+    kp.ds[k] = p.ds[k];
+    kp.fd[k] = to_dev(make_fastdiv(p.n[k]));
+  }
   kp.fv = to_dev(make_fastdiv((uint32_t)vpr));
-  kp.f3 = to_dev(make_fastdiv(p.n[3]));
-  kp.f2 = to_dev(make_fastdiv(p.n[2]));
-  kp.f1 = to_dev(make_fastdiv(p.n[1]));
 
   // Split into launches of < 2^31 vectors at run boundaries.
   const uint64_t runs_per_launch = std::max<uint64_t>(1, ((1ull << 31) - 1) / vpr);
@@ -259,7 +390,10 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.seq = rel.seq;
     kp.ticket = rel.ticket;
     kp.ts = last ? rel.ts : nullptr;
-    cudaError_t e = launch_cfg(kp, VEC, max_ctas, stream);
+    kp.per_cta_sys = tune().per_cta_sys;
+    cudaError_t e = (tune().bulk && dense_dst(p))
+                        ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
+                        : launch_cfg(kp, VEC, max_ctas, stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");
   }
   return DV_OK;

@@ -37,17 +37,22 @@ struct FastDiv {
 };
 FastDiv make_fastdiv(uint32_t d);
 
-// ---- a batched strided copy: up to 4 loop dims of contiguous runs ---------------------------
-// Run q (row-major over n[0..3], n[3] innermost) starts at src + sum_k i_k*ss[k] and
+// ---- a batched strided copy: up to kDims loop dims of contiguous runs -----------------------
+// Run q (row-major over n[0..kDims-1], last innermost) starts at src + sum_k i_k*ss[k] and
 // dst + sum_k i_k*ds[k]; every run is run_bytes contiguous bytes on both sides.
+constexpr int kDims = 5;
 struct CopyPlan {
   const uint8_t* src;
   uint8_t* dst;
-  uint32_t n[4];
-  int64_t ss[4];
-  int64_t ds[4];
+  uint32_t n[kDims];
+  int64_t ss[kDims];
+  int64_t ds[kDims];
   uint64_t run_bytes;
-  uint64_t runs() const { return (uint64_t)n[0] * n[1] * n[2] * n[3]; }
+  uint64_t runs() const {
+    uint64_t r = 1;
+    for (int k = 0; k < kDims; ++k) r *= n[k];
+    return r;
+  }
   uint64_t bytes() const { return runs() * run_bytes; }
 };
 

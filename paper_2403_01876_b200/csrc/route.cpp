@@ -185,7 +185,7 @@ FastDiv make_fastdiv(uint32_t d) {
 
 void collapse(CopyPlan& p) {
   // 1) fold innermost dims into the run while both sides are contiguous across them
-  for (int k = 3; k >= 0; --k) {
+  for (int k = kDims - 1; k >= 0; --k) {
     if (p.n[k] == 1) continue;
     if (p.ss[k] == (int64_t)p.run_bytes && p.ds[k] == (int64_t)p.run_bytes) {
       p.run_bytes *= p.n[k];
@@ -197,10 +197,10 @@ void collapse(CopyPlan& p) {
   }
   // 2) drop unit dims, keep order; then merge adjacent dims (outer j, inner i) when
   //    stride_j == n_i * stride_i on both sides
-  uint32_t n[4];
-  int64_t ss[4], ds[4];
+  uint32_t n[kDims];
+  int64_t ss[kDims], ds[kDims];
   int m = 0;
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < kDims; ++k)
     if (p.n[k] != 1) {
       n[m] = p.n[k];
       ss[m] = p.ss[k];
@@ -221,9 +221,9 @@ void collapse(CopyPlan& p) {
       ++w;
     }
   }
-  // right-align into 4 slots (outer padding with unit dims)
-  for (int k = 0; k < 4; ++k) {
-    int src_k = k - (4 - w);
+  // right-align into kDims slots (outer padding with unit dims)
+  for (int k = 0; k < kDims; ++k) {
+    int src_k = k - (kDims - w);
     if (src_k < 0) {
       p.n[k] = 1;
       p.ss[k] = p.ds[k] = 0;

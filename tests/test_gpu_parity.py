@@ -476,3 +476,102 @@ def test_paper_baselines_produce_the_wire():
     calls = dv.dvb_buffered_copy(c, dv.region(*reg), stg.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
     assert calls == 2 * nL * nR + 1 and np.array_equal(to_np(out), exp)
+
+
+@pytest.mark.parametrize("xfer", [dv.DV_XFER_FUSED, dv.DV_XFER_FUSED | dv.DV_PUBLISH_STREAMOP, dv.DV_XFER_STAGED])
+def test_host_poller_never_sees_flag_before_payload(xfer):
+    """Release protocol (A5) observed from the CPU: a host thread spins on the pinned flag while
+    the GPU streams 300 per-layer chunks; whenever it sees seq k it immediately compares chunk k
+    with the oracle. A flag visible before its payload would show up as a mismatch."""
+    import threading
+    L, B, H, S, D = 4, 8, 8, 64, 128
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=12)
+    k, v, c = dev_cache(K, V, 0, 0)
+    osrc = oc(K, V, 0, 0, S)
+    n = 300
+    regs = [(i % L, i % L + 1, 0, B, i % S, i % S + 1) for i in range(n)]
+    chunk = ok.region_bytes(*regs[0], H, D, 2)
+    exp = [ok.pack(osrc, r) for r in regs]
+    log = pinned_u16(n * chunk // 2)
+    fl = flags(1, pinned=True)
+    ep = dv.endpoint_of(log, fl)
+    lnp = log.numpy().view(np.uint16)
+    fnp = fl.numpy()
+    bad, seen = [], []
+    stop = threading.Event()
+
+    def poll():
+        last = 0
+        while not stop.is_set() or last < n:
+            cur = int(fnp[0])
+            if cur > last:
+                i = cur - 1
+                if not np.array_equal(lnp[i * chunk // 2:(i + 1) * chunk // 2], exp[i]):
+                    bad.append(i)
+                seen.append(cur)
+                last = cur
+            if stop.is_set() and cur >= n:
+                break
+    th = threading.Thread(target=poll)
+    th.start()
+    cx = ctx()
+    for i, r in enumerate(regs):
+        dv.dvt_spin(3000, 1)   # spread the chunks out so the poller samples many of them
+        dv.dv_scatter(cx, c, dv.region(*r), ep, i * chunk, flag_slot=0, seq=i + 1, xfer=xfer)
+    torch.cuda.synchronize()
+    stop.set()
+    th.join(timeout=60)
+    assert not bad, f"flag seen before payload for chunks {bad[:10]}"
+    assert len(seen) > 10 and seen[-1] == n
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("xfer", XFERS)
+@pytest.mark.parametrize("host", [False, True])
+def test_gather_chunks_matches_oracle(seed, xfer, host):
+    """dv_gather_chunks (log of chunks -> cache in one go) == oracle.unpack_chunks."""
+    rng = random.Random(500 + seed)
+    H, D, nL, nR, S, lb, rb, reg = _rand_case(rng)
+    S = max(S, 8)
+    n = rng.randint(1, 3)
+    step = n + rng.randint(0, 2)
+    n_chunks = max(1, (S - n) // step)
+    first = (reg[0], reg[1], reg[2], reg[3], 0, n)
+    K, V = kvgen.kv5d_cache("hash", lb, nL, rb, nR, H, S, D, seed=seed)
+    osrc = oc(K, V, lb, rb, S)
+    log_np = np.concatenate([ok.pack(osrc, ok.shifted(first, k * step)) for k in range(n_chunks)])
+    log = to_pinned(log_np) if host else to_dev(log_np)
+    dk = sentinel_like((nL, nR, H, S, D)); dvv = sentinel_like((nL, nR, H, S, D))
+    dv.dv_gather_chunks(ctx(), dv.endpoint_of(log), 0, dv.cache(dk, dvv, lb, rb), dv.region(*first), n_chunks, step,
+                        xfer=xfer)
+    torch.cuda.synchronize()
+    o = oc(*kvgen.sentinel_cache(nL, nR, H, S, D), lb, rb, S)
+    ok.unpack_chunks(o, first, log_np, n_chunks, step)
+    assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)
+
+
+def test_swap_log_form_round_trip():
+    """C4 log form end to end: prompt chunk + per-token delta chunks appended to a pinned host
+    log by dv_scatter (swap-out), then one dv_gather_chunks + one dv_gather (swap-in) rebuild the
+    microbatch in an empty slot == the source on [0, p+T)."""
+    L, b, H, S, D, p, T = 3, 4, 8, 64, 128, 20, 30
+    K, V = kvgen.kv5d_cache("hash", 9, L, 8, b, H, S, D, seed=31)
+    k, v, c = dev_cache(K, V, 9, 8)
+    C = 2 * L * b * H * D * 2
+    log = pinned_u16((p + T) * C // 2)
+    fl = flags(1, pinned=True)
+    ep = dv.endpoint_of(log, fl)
+    cx = ctx()
+    dv.dv_scatter(cx, c, dv.region(9, 9 + L, 8, 8 + b, 0, p), ep, 0, flag_slot=0, seq=1)
+    for t in range(T):
+        dv.dv_scatter(cx, c, dv.region(9, 9 + L, 8, 8 + b, p + t, p + t + 1), ep, (p + t) * C, flag_slot=0,
+                      seq=2 + t)
+    sk = sentinel_like((L, b, H, S, D)); sv = sentinel_like((L, b, H, S, D))
+    sc = dv.cache(sk, sv, 9, 8)
+    dv.dv_gather(cx, ep, 0, sc, dv.region(9, 9 + L, 8, 8 + b, 0, p), flag_slot=0, wait_seq=1 + T)
+    dv.dv_gather_chunks(cx, ep, p * C, sc, dv.region(9, 9 + L, 8, 8 + b, p, p + 1), T, 1, flag_slot=0,
+                        wait_seq=1 + T)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(sk)[:, :, :, :p + T], K[:, :, :, :p + T])
+    assert np.array_equal(to_np(sv)[:, :, :, :p + T], V[:, :, :, :p + T])
+    assert np.all(to_np(sk)[:, :, :, p + T:] == kvgen.SENTINEL)

@@ -446,3 +446,26 @@ def test_kvgen_hash_is_splitmix64():
     got = kvgen.splitmix64(np.array([0, 0x9E3779B97F4A7C15], dtype=np.uint64))
     assert int(got[0]) == 0xE220A8397B1DCDAF
     assert int(got[1]) == 0x6E789E6AA1B965F4
+
+
+def test_log_form_swap_round_trip_equals_definition():
+    """Host log form (C4): the prompt as one chunk, then one chunk per token step
+    appended; unpacking the log rebuilds exactly kvgen's words on [0, p+T) and nothing else."""
+    L, B, H, S, D, p, T = 3, 2, 2, 24, 8, 7, 6
+    src = Cache(*kvgen.kv5d_cache("hash", 4, L, 2, B, H, S, D, seed=13), 4, 2, H, S, D)
+    prompt = pack(src, (4, 4 + L, 2, 2 + B, 0, p))
+    steps = [pack(src, (4, 4 + L, 2, 2 + B, p + t, p + t + 1)) for t in range(T)]
+    dst = Cache(*kvgen.sentinel_cache(L, B, H, S, D), 4, 2, H, S, D)
+    unpack(dst, (4, 4 + L, 2, 2 + B, 0, p), prompt)
+    from oracle.kvstream import unpack_chunks
+    unpack_chunks(dst, (4, 4 + L, 2, 2 + B, p, p + 1), np.concatenate(steps), T, 1)
+    exp = kvgen.kv5d_cache("hash", 4, L, 2, B, H, S, D, seed=13)
+    for kv in (0, 1):
+        assert np.array_equal(dst.arr(kv)[:, :, :, :p + T], exp[kv][:, :, :, :p + T])
+        assert np.all(dst.arr(kv)[:, :, :, p + T:] == kvgen.SENTINEL)
+    # chunks of 2 positions with pos_step 3 leave every third position untouched
+    dst2 = Cache(*kvgen.sentinel_cache(L, B, H, S, D), 4, 2, H, S, D)
+    log2 = np.concatenate([pack(src, (4, 4 + L, 2, 2 + B, 3 * k, 3 * k + 2)) for k in range(4)])
+    unpack_chunks(dst2, (4, 4 + L, 2, 2 + B, 0, 2), log2, 4, 3, mode="brute")
+    filled = ~np.all(dst2.K == kvgen.SENTINEL, axis=(0, 1, 2, 4))
+    assert np.flatnonzero(filled).tolist() == [0, 1, 3, 4, 6, 7, 9, 10]

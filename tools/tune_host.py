@@ -32,7 +32,7 @@ def child():
     fl = torch.zeros(2, dtype=torch.int64, pin_memory=True)
     dbuf = torch.empty(STEP * 8 // 2, dtype=torch.int16, device="cuda")
     dfl = torch.zeros(2, dtype=torch.int64, device="cuda")
-    out = {"env": {k_: os.environ.get(k_) for k_ in ("DV_U", "DV_VEC", "DV_PDL")}}
+    out = {"env": {k_: os.environ.get(k_) for k_ in ("DV_U", "DV_VEC", "DV_PDL", "DV_BULK")}}
     cnt = [0]
 
     def ev():
@@ -97,7 +97,9 @@ def child():
     def gt_lat(buf, flg, xf, n=400):
         ep = dv.endpoint_of(buf, flg)
         te = torch.zeros(n, dtype=torch.int64, device="cuda")
-        ts = torch.zeros(n, dtype=torch.int64, device="cuda")
+        ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
+        ts[:, 1:3] = 2 ** 63 - 1
+        dv.dvt_spin(20_000_000, 1, stream=sp)   # head start: GPU runs behind the host
         for i in range(n):
             q = P + i % 1000
             lay = i % L
@@ -107,8 +109,14 @@ def child():
             dv.dv_scatter(ctx, c, reg, ep, lay * LAYER, flag_slot=0, seq=10 ** 6 + i, xfer=xf, stream=sp)
         dv.dvt_trace(ctx, 0)
         torch.cuda.synchronize()
-        d = sorted(((ts - te).double() / 1e3).tolist()[20:])
-        return {"p50": d[len(d) // 2], "p99": d[int(len(d) * 0.99)], "min": d[0]}
+        res = {}
+        for nm, col in (("flag", 0), ("resident", 1), ("past_wait", 2), ("stores_issued", 3)):
+            d = sorted(((ts[:, col] - te).double() / 1e3).tolist()[20:])
+            res[nm + "_p50"] = d[len(d) // 2]
+            if col == 0:
+                res["flag_p99"] = d[int(len(d) * 0.99)]
+                res["flag_min"] = d[0]
+        return res
     out["gt_layer_host_fused"] = gt_lat(log, fl, F)
     out["gt_layer_hbm_fused"] = gt_lat(dbuf, dfl, F)
     tres = torch.zeros(64, dtype=torch.int64, device="cuda")
@@ -116,6 +124,37 @@ def child():
         dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=1, reg=dv.region(0, 1, 0, 1, 5, 6), stream=sp, t_end_ptr=tres[i].data_ptr())
     torch.cuda.synchronize()
     out["globaltimer_samples_ns"] = sorted(set((tres % 1000).tolist()))[:16]
+    # e2e: H2D of the token's K/V (side stream) -> cache, then stream-out (main stream)
+    s_in = torch.cuda.Stream()
+    dl = torch.empty(STEP * 8 // 2, dtype=torch.int16, pin_memory=True)
+    dep_ = dv.endpoint_of(dl)
+    evs = [torch.cuda.Event() for _ in range(8)]
+    lep = dv.endpoint_of(log, fl)
+
+    def e2e(gx, sx, n=200):
+        def one(t):
+            q = P + t % 1000
+            dv.dv_gather(ctx, dep_, (t % 8) * STEP, c, dv.region(0, L, 0, B, q, q + 1), xfer=gx, stream=s_in)
+            e = evs[t % 8]
+            e.record(s_in)
+            st.wait_event(e)
+            dv.dv_scatter(ctx, c, dv.region(0, L, 0, B, q, q + 1), lep, (t % 8) * STEP, flag_slot=0, seq=t,
+                          xfer=sx, stream=sp)
+        for t in range(5):
+            one(t)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(st)
+        s_in.wait_event(a)
+        for t in range(n):
+            one(t)
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n * 1e3
+    for gn, gx in (("fused", F), ("staged", G)):
+        for sn, sx in (("fused", F), ("staged", G)):
+            out[f"e2e_gather_{gn}_scatter_{sn}_us"] = e2e(gx, sx)
+
     # prompt layer 163.8 MB
     pb = torch.empty(LAYER * P // 2, dtype=torch.int16, pin_memory=True)
     pd = torch.empty(LAYER * P // 2, dtype=torch.int16, device="cuda")
@@ -138,8 +177,7 @@ def child():
 
 
 def main():
-    variants = [{}, {"DV_PDL": "0"}, {"DV_U": "1"}, {"DV_U": "2"}, {"DV_U": "8"}, {"DV_VEC": "16"},
-                {"DV_VEC": "16", "DV_U": "1"}, {"DV_VEC": "16", "DV_U": "8"}]
+    variants = [{}, {"DV_PDL": "0"}]
     for var in variants:
         env = dict(os.environ)
         env.update(var)
