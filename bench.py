@@ -99,10 +99,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DV_BENCH_SAME_DEVICE") == "1":   # test hook: all ranks on cuda:0 (gloo)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = args.dist_backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     xfer = {"auto": dv.DV_XFER_AUTO, "fused": dv.DV_XFER_FUSED, "staged": dv.DV_XFER_STAGED}[args.xfer]
     ctx = dv.dv_create(local)
@@ -158,9 +169,7 @@ def run_ours(args):
     assert int(fl[0]) == t_, "flag not published"
     spot = _spot_check(wire, last_q, seed)
     if world > 1:
-        tt = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
+        elapsed_ms = max_over_ranks(elapsed_ms)
 
     # ---- e2e: host buffers through the public API (H2D of the step's new K/V -> cache, stream-out)
     delta = torch.empty(RING * STEP_BYTES // 2, dtype=torch.int16, pin_memory=True)
@@ -200,9 +209,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        e2e_ms = max_over_ranks(e2e_ms)
 
     extras = {}
     if not args.no_extras and rank == 0:
@@ -512,6 +519,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:

@@ -33,8 +33,9 @@
  *   byte ((((l*n_reqs + r)*n_heads + h)*max_seq + s)*head_dim + d)*elem_bytes.
  *   Words are opaque (fp16/bf16 bit patterns are moved, never converted; NaN payloads survive).
  *
- * Wire format (reading Q3): a region [l0,l1)x[r0,r1)x[s0,s1) packs to the dense array
- *   [l-l0][kv][r-r0][h][s-s0][d]  (kv: 0 = K, 1 = V), i.e. 2*nL*nR*H*n*D*e bytes, d fastest.
+ * Wire format (reading Q3): a region [l0,l1)x[r0,r1)x[s0,s1)x[h0,h1) packs to the dense array
+ *   [l-l0][kv][r-r0][h-h0][s-s0][d]  (kv: 0 = K, 1 = V), 2*nL*nR*nH*n*D*e bytes, d fastest,
+ *   whatever the cache layout (KV5D or FT6D) on either side.
  *
  * Alignment: cache bases, endpoint bases/offsets and head_dim*elem_bytes must be multiples of
  * 16 bytes (else DV_EALIGN).
@@ -49,7 +50,7 @@
 extern "C" {
 #endif
 
-#define DV_ABI_VERSION 1
+#define DV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define DV_API __attribute__((visibility("default")))
@@ -70,7 +71,13 @@ typedef enum dv_status {
   DV_ENOTSUP = 9  /* valid request this build does not implement                              */
 } dv_status;
 
-enum { DV_LAYOUT_KV5D = 0 };
+/* Cache layouts (reading Q1; PAPER.md:131 fn 5 "the key cache is a 6D tensor, and the value cache
+ * is a 5D tensor"):
+ *   DV_LAYOUT_KV5D  K and V both [n_layers][n_reqs][n_heads][max_seq][head_dim].
+ *   DV_LAYOUT_FT6D  K [n_layers][n_reqs][n_heads][head_dim/x][max_seq][x] with x = 16/elem_bytes
+ *                   (FasterTransformer's key layout: 16-byte packets of d, position-major inside
+ *                   each packet column), V as in KV5D. */
+enum { DV_LAYOUT_KV5D = 0, DV_LAYOUT_FT6D = 1 };
 
 /* A worker's K and V cache, preallocated to max_seq. Descriptor only: the library
  * never allocates or frees caches. */
@@ -84,38 +91,50 @@ typedef struct dv_cache {
   int32_t n_layers;
   int32_t req_begin;   /* global id of the first request held (a microbatch's requests)         */
   int32_t n_reqs;
-  int32_t n_heads;
+  int32_t n_heads;     /* heads held (a tensor-parallel shard holds a head range)                */
   int32_t max_seq;     /* preallocated positions S                                              */
   int32_t head_dim;
+  int32_t head_begin;  /* global id of the first head held (0 without tensor parallelism)        */
 } dv_cache;
 
-/* Half-open box of GLOBAL layer ids x GLOBAL request ids x absolute positions (reading Q5). */
+/* Half-open box of GLOBAL layer ids x GLOBAL request ids x absolute positions (reading Q5) x
+ * GLOBAL head ids. head_begin == head_end == 0 means "all heads": the heads of the cache in the
+ * level-2 calls (the source cache's for dv_remap), the heads covered by the setups in the route. */
 typedef struct dv_region {
   int32_t layer_begin, layer_end;
   int32_t req_begin, req_end;
   int32_t pos_begin, pos_end;
+  int32_t head_begin, head_end;
 } dv_region;
 
-/* A pipeline configuration: layers partitioned over n_stages stages,
- * requests split into n_micro microbatches; bounds are global ids, strictly increasing. */
+/* A pipeline configuration: layers partitioned over n_stages stages (PP),
+ * requests split into n_micro microbatches, and -- optionally -- heads split over n_tp tensor-
+ * parallel ranks inside a stage. Bounds are global ids, strictly
+ * increasing. n_tp = 0 (head_bounds NULL): no head split, every block holds all heads.
+ * A block is (stage, micro, tp); its flat index is (stage*n_micro + micro)*max(n_tp,1) + tp. */
 typedef struct dv_setup {
   int32_t n_stages;
   const int32_t* layer_bounds; /* n_stages + 1 entries */
   int32_t n_micro;
   const int32_t* req_bounds;   /* n_micro + 1 entries  */
   int32_t max_seq;
+  int32_t n_tp;                /* 0 = no head split                    */
+  const int32_t* head_bounds;  /* n_tp + 1 entries, or NULL            */
 } dv_setup;
 
-/* One route piece = region x source block (stage, micro) x destination block (stage, micro).
- * Pieces come in lexicographic order of (src_stage, src_micro, dst_stage, dst_micro).
+/* One route piece = region x source block x destination block (all non-empty).
+ * Pieces come in lexicographic order of (src block flat index, dst block flat index).
  * src_wire_off / dst_wire_off: byte offset of this piece's wire chunk among the pieces leaving
- * the source block / entering the destination block, cumulative in piece order. */
+ * the source block / entering the destination block, cumulative in piece order. head range
+ * [0,0) means all heads (neither setup splits heads). */
 typedef struct dv_piece {
   int32_t src_stage, src_micro, dst_stage, dst_micro;
   int32_t layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end;
   uint64_t bytes;
   uint64_t src_wire_off;
   uint64_t dst_wire_off;
+  int32_t src_tp, dst_tp;
+  int32_t head_begin, head_end;
 } dv_piece;
 
 /* Where contiguous chunks go / come from (the paper's flush/fetch targets). */
@@ -162,16 +181,18 @@ DV_API int32_t dv_abi_version(void);
 DV_API dv_status dv_stats(uint64_t* kernel_launches, uint64_t* dma_calls);
 
 /* ---- pure host functions (no GPU needed) ------------------------------------------------- */
-/* Bytes of K and V in a region: 2*nL*nR*(pos_end-pos_begin)*n_heads*head_dim*elem_bytes
- * ("2*L*hidden*element_bytes*batch*seq"). */
+/* Bytes of K and V in a region: 2*nL*nR*(pos_end-pos_begin)*nH*head_dim*elem_bytes, nH = the
+ * region's head count, or n_heads when its head range is [0,0) (SPEC.md:38
+ * "2*L*hidden*element_bytes*batch*seq"). */
 DV_API dv_status dv_region_bytes(const dv_region* region, int32_t n_heads, int32_t head_dim,
                           int32_t elem_bytes, uint64_t* out_bytes);
 
 /* Route a region from src setup to dst setup (Table 1 stream_out/stream_in).
  * Writes up to `cap` pieces to `out` and the total count to *n (call with cap=0 to size).
- * Errors in order: DV_EINVAL (malformed setup/region), DV_EMAP (a setup does not hold the
- * region's layers/requests), DV_ERANGE (pos_end > max_seq on either side). An empty region
- * (any zero extent) yields 0 pieces. */
+ * n_heads is the model's head count used for byte sizes when neither setup splits heads.
+ * Errors in order: DV_EINVAL (malformed setup/region; one setup splits heads and the other does
+ * not), DV_EMAP (a setup does not hold the region's layers/requests/heads), DV_ERANGE (pos_end >
+ * max_seq on either side). An empty region (any zero extent) yields 0 pieces. */
 DV_API dv_status dv_route(const dv_setup* src, const dv_setup* dst, const dv_region* region,
                    int32_t n_heads, int32_t head_dim, int32_t elem_bytes, dv_piece* out,
                    uint64_t cap, uint64_t* n);
@@ -239,27 +260,27 @@ DV_API dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
 
 /* ---- level 1: stream_out / stream_in ------------------------------ */
 /* Sender side. `src` is the cache of source block (my_stage, my_micro) of `src_setup`. Routes
- * `region`; for every piece leaving this block, scatters it into inboxes[dst_stage*n_micro_dst +
- * dst_micro] at the piece's dst_wire_off and publishes flag slot (my_stage*n_micro_src +
- * my_micro) = seq in that inbox. `inboxes` has dst_setup->n_stages*dst_setup->n_micro entries
- * (entries never addressed may be zeroed). */
+ * `region`; for every piece leaving this block, scatters it into inboxes[dst block flat index] at
+ * the piece's dst_wire_off and publishes flag slot (this block's flat index) = seq in that inbox.
+ * `inboxes` has one entry per destination block (entries never addressed may be zeroed). With
+ * tensor parallelism (setups with n_tp > 0) my_tp selects this block's head group. */
 DV_API dv_status dv_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                         const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
-                        const dv_setup* dst_setup, const dv_endpoint* inboxes, int32_t n_inboxes,
-                        uint64_t seq, uint32_t xfer, void* stream);
-/* Receiver side. For every piece entering block (my_stage, my_micro) of `dst_setup`: wait for
- * inbox->flags[src_stage*n_micro_src + src_micro] >= wait_seq, then gather the piece from
- * inbox at its dst_wire_off into `dst`. */
+                        int32_t my_tp, const dv_setup* dst_setup, const dv_endpoint* inboxes,
+                        int32_t n_inboxes, uint64_t seq, uint32_t xfer, void* stream);
+/* Receiver side. For every piece entering block (my_stage, my_micro, my_tp) of `dst_setup`: wait
+ * for inbox->flags[source block flat index] >= wait_seq, then gather the piece from inbox at its
+ * dst_wire_off into `dst`. */
 DV_API dv_status dv_stream_in(dv_ctx* ctx, const dv_cache* dst, const dv_region* region,
                        const dv_setup* src_setup, const dv_setup* dst_setup, int32_t my_stage,
-                       int32_t my_micro, const dv_endpoint* inbox, uint64_t wait_seq,
-                       uint32_t xfer, void* stream);
-/* Sender side, direct form: every piece leaving (my_stage, my_micro) is remapped straight into
- * dst_caches[dst block] (mapped peer, host or local memory), then flag slot
- * (my_stage*n_micro_src + my_micro) of signals[dst block] (if non-NULL) is set to seq. */
+                       int32_t my_micro, int32_t my_tp, const dv_endpoint* inbox,
+                       uint64_t wait_seq, uint32_t xfer, void* stream);
+/* Sender side, direct form: every piece leaving (my_stage, my_micro, my_tp) is remapped straight
+ * into dst_caches[dst block flat index] (mapped peer, host or local memory), then flag slot
+ * (this block's flat index) of signals[dst block] (if non-NULL) is set to seq. */
 DV_API dv_status dv_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                                const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
-                               const dv_setup* dst_setup, const dv_cache* dst_caches,
+                               int32_t my_tp, const dv_setup* dst_setup, const dv_cache* dst_caches,
                                const dv_endpoint* signals, int32_t n_dst, uint64_t seq,
                                uint32_t xfer, void* stream);
 

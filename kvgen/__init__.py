@@ -1,8 +1,9 @@
 """Seeded synthetic KV-cache inputs shared by the oracle side and the CUDA side of the tests.
 
-This module holds NO arithmetic of the streaming method (no routing, no offsets of any layout, no
-packing). It only answers "what 16-bit word does the writer put at LOGICAL coordinate
-(kv, layer, request, head, position, d)", plus materialising a logical block as a numpy array.
+This module holds NO arithmetic of the streaming method (no routing, no offsets, no packing). It
+only answers "what 16-bit word does the writer put at LOGICAL coordinate (kv, layer, request,
+head, position, d)", plus materialising a logical block as a numpy array (and, for the
+FasterTransformer 6-D key structure, as that array's plain transpose).
 
 Generators (SURVEY §8(c) C-3 and §8(d) "Synthetic inputs"):
 
@@ -86,15 +87,16 @@ def uid_decode(w: np.ndarray, box):
 
 
 def logical_block(kind: str, kv: int, layers, reqs, n_heads: int, positions, head_dim: int,
-                  seed: int = 0, box=None, valid_pos=None) -> np.ndarray:
+                  seed: int = 0, box=None, valid_pos=None, head_begin: int = 0) -> np.ndarray:
     """Logical array [nL][nR][H][nS][D] (uint16) of the writer's words.
 
-    layers/reqs/positions are iterables of GLOBAL ids. Positions outside ``valid_pos`` (a half-open
-    (lo, hi) pair, default: all) hold POISON -- the writer never produced them.
+    layers/reqs/positions are iterables of GLOBAL ids; heads are the global ids
+    [head_begin, head_begin + n_heads) (a tensor-parallel shard). Positions outside ``valid_pos``
+    (a half-open (lo, hi) pair, default: all) hold POISON -- the writer never produced them.
     """
     L = np.asarray(list(layers), dtype=np.int64)[:, None, None, None, None]
     R = np.asarray(list(reqs), dtype=np.int64)[None, :, None, None, None]
-    Hh = np.arange(n_heads, dtype=np.int64)[None, None, :, None, None]
+    Hh = np.arange(head_begin, head_begin + n_heads, dtype=np.int64)[None, None, :, None, None]
     P = np.asarray(list(positions), dtype=np.int64)[None, None, None, :, None]
     Dd = np.arange(head_dim, dtype=np.int64)[None, None, None, None, :]
     if kind == "hash":
@@ -113,7 +115,7 @@ def logical_block(kind: str, kv: int, layers, reqs, n_heads: int, positions, hea
 
 def kv5d_cache(kind: str, layer_begin: int, n_layers: int, req_begin: int, n_reqs: int,
                n_heads: int, max_seq: int, head_dim: int, seed: int = 0, box=None,
-               valid_pos=None):
+               valid_pos=None, head_begin: int = 0):
     """(K, V) arrays in the [L][B][H][S][D] order the writer (FasterTransformer-style) fills.
 
     For this order the logical block IS the physical array, so no layout arithmetic is involved.
@@ -121,8 +123,16 @@ def kv5d_cache(kind: str, layer_begin: int, n_layers: int, req_begin: int, n_req
     layers = range(layer_begin, layer_begin + n_layers)
     reqs = range(req_begin, req_begin + n_reqs)
     pos = range(max_seq)
-    return tuple(logical_block(kind, kv, layers, reqs, n_heads, pos, head_dim, seed, box, valid_pos)
-                 for kv in (0, 1))
+    return tuple(logical_block(kind, kv, layers, reqs, n_heads, pos, head_dim, seed, box, valid_pos,
+                               head_begin) for kv in (0, 1))
+
+
+def as_ft6d_key(K: np.ndarray, elem_bytes: int = 2) -> np.ndarray:
+    """Materialise a logical [L][B][H][S][D] key block in FasterTransformer's 6-D key structure
+    [L][B][H][D/x][S][x], x = 16/elem_bytes (input STRUCTURE of NEXT-1; a plain transpose)."""
+    x = 16 // elem_bytes
+    nL, nR, H, S, D = K.shape
+    return np.ascontiguousarray(K.reshape(nL, nR, H, S, D // x, x).transpose(0, 1, 2, 4, 3, 5))
 
 
 def sentinel_cache(n_layers: int, n_reqs: int, n_heads: int, max_seq: int, head_dim: int):

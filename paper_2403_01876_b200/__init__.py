@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libdvstream.so")
 # ---- constants mirrored from include/dv.h --------------------------------------------------------
 DV_OK, DV_EINVAL, DV_EMAP, DV_ERANGE, DV_EALIGN, DV_ENOMEM, DV_EPEER, DV_EBUSY, DV_ECUDA, \
     DV_ENOTSUP = range(10)
-DV_LAYOUT_KV5D = 0
+DV_LAYOUT_KV5D, DV_LAYOUT_FT6D = 0, 1
 DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
 DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_PUBLISH_STREAMOP, DV_NO_FLAG = 0, 1, 2, 4, 256
 DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
@@ -30,24 +30,27 @@ class dv_cache(C.Structure):
     _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("device", C.c_int32), ("layout", C.c_int32),
                 ("elem_bytes", C.c_int32), ("layer_begin", C.c_int32), ("n_layers", C.c_int32),
                 ("req_begin", C.c_int32), ("n_reqs", C.c_int32), ("n_heads", C.c_int32),
-                ("max_seq", C.c_int32), ("head_dim", C.c_int32)]
+                ("max_seq", C.c_int32), ("head_dim", C.c_int32), ("head_begin", C.c_int32)]
 
 
 class dv_region(C.Structure):
     _fields_ = [("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("req_begin", C.c_int32),
-                ("req_end", C.c_int32), ("pos_begin", C.c_int32), ("pos_end", C.c_int32)]
+                ("req_end", C.c_int32), ("pos_begin", C.c_int32), ("pos_end", C.c_int32),
+                ("head_begin", C.c_int32), ("head_end", C.c_int32)]
 
 
 class dv_setup(C.Structure):
     _fields_ = [("n_stages", C.c_int32), ("layer_bounds", C.POINTER(C.c_int32)),
-                ("n_micro", C.c_int32), ("req_bounds", C.POINTER(C.c_int32)), ("max_seq", C.c_int32)]
+                ("n_micro", C.c_int32), ("req_bounds", C.POINTER(C.c_int32)), ("max_seq", C.c_int32),
+                ("n_tp", C.c_int32), ("head_bounds", C.POINTER(C.c_int32))]
 
 
 class dv_piece(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("src_stage", "src_micro", "dst_stage", "dst_micro",
                                          "layer_begin", "layer_end", "req_begin", "req_end",
                                          "pos_begin", "pos_end")] + \
-               [("bytes", C.c_uint64), ("src_wire_off", C.c_uint64), ("dst_wire_off", C.c_uint64)]
+               [("bytes", C.c_uint64), ("src_wire_off", C.c_uint64), ("dst_wire_off", C.c_uint64)] + \
+               [(n, C.c_int32) for n in ("src_tp", "dst_tp", "head_begin", "head_end")]
 
 
 class dv_endpoint(C.Structure):
@@ -104,13 +107,13 @@ _SIGS = {
     "dv_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint),
                            C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
     "dv_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
-                                C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32, C.c_uint64,
-                                C.c_uint32, C.c_void_p]),
+                                C.c_int32, C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32,
+                                C.c_uint64, C.c_uint32, C.c_void_p]),
     "dv_stream_in": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), P(dv_setup),
-                               C.c_int32, C.c_int32, P(dv_endpoint), C.c_uint64, C.c_uint32,
-                               C.c_void_p]),
+                               C.c_int32, C.c_int32, C.c_int32, P(dv_endpoint), C.c_uint64,
+                               C.c_uint32, C.c_void_p]),
     "dv_stream_out_direct": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup),
-                                       C.c_int32, C.c_int32, P(dv_setup), P(dv_cache),
+                                       C.c_int32, C.c_int32, C.c_int32, P(dv_setup), P(dv_cache),
                                        P(dv_endpoint), C.c_int32, C.c_uint64, C.c_uint32,
                                        C.c_void_p]),
     "dv_wait": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
@@ -171,18 +174,33 @@ def _ref(x):
 
 
 # ---- descriptor helpers --------------------------------------------------------------------------
-def region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end) -> dv_region:
-    return dv_region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end)
+def region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end, head_begin=0,
+           head_end=0) -> dv_region:
+    """Region of global ids; heads (0, 0) = all heads (see include/dv.h)."""
+    return dv_region(layer_begin, layer_end, req_begin, req_end, pos_begin, pos_end, head_begin, head_end)
 
 
 class Setup:
-    """Owns the bound arrays of a dv_setup."""
+    """Owns the bound arrays of a dv_setup (head_bounds None = no tensor-parallel head split)."""
 
-    def __init__(self, layer_bounds, req_bounds, max_seq):
+    def __init__(self, layer_bounds, req_bounds, max_seq, head_bounds=None):
         self.lb = (C.c_int32 * len(layer_bounds))(*layer_bounds)
         self.rb = (C.c_int32 * len(req_bounds))(*req_bounds)
-        self.c = dv_setup(len(layer_bounds) - 1, self.lb, len(req_bounds) - 1, self.rb, max_seq)
+        if head_bounds is not None:
+            self.hb = (C.c_int32 * len(head_bounds))(*head_bounds)
+            ntp, hbp = len(head_bounds) - 1, self.hb
+        else:
+            self.hb, ntp, hbp = None, 0, None
+        self.c = dv_setup(len(layer_bounds) - 1, self.lb, len(req_bounds) - 1, self.rb, max_seq, ntp, hbp)
         self.layer_bounds, self.req_bounds, self.max_seq = list(layer_bounds), list(req_bounds), max_seq
+        self.head_bounds = None if head_bounds is None else list(head_bounds)
+
+    @property
+    def n_tp(self):
+        return 1 if self.head_bounds is None else len(self.head_bounds) - 1
+
+    def flat(self, stage, micro, tp=0):
+        return (stage * self.n_micro + micro) * self.n_tp + tp
 
     @property
     def n_stages(self):
@@ -193,22 +211,29 @@ class Setup:
         return self.c.n_micro
 
 
-def cache(k, v, layer_begin=0, req_begin=0, device=None) -> dv_cache:
-    """Descriptor of a KV5D cache held in two tensors (or raw pointers with explicit shapes via
-    cache_raw). Tensors must be [n_layers][n_reqs][n_heads][max_seq][head_dim], contiguous."""
-    assert k.shape == v.shape and k.dtype == v.dtype and k.dim() == 5
-    assert k.is_contiguous() and v.is_contiguous()
-    nL, nR, H, S, D = k.shape
+def cache(k, v, layer_begin=0, req_begin=0, device=None, head_begin=0) -> dv_cache:
+    """Descriptor of a cache held in two contiguous tensors. V is [n_layers][n_reqs][n_heads]
+    [max_seq][head_dim]; K has the same shape (KV5D) or is 6-D [n_layers][n_reqs][n_heads]
+    [head_dim/x][max_seq][x], x = 16/elem_bytes (FT6D). head_begin = first global head held."""
+    assert k.dtype == v.dtype and v.dim() == 5 and k.is_contiguous() and v.is_contiguous()
+    nL, nR, H, S, D = v.shape
+    if k.dim() == 6:
+        x = 16 // k.element_size()
+        assert tuple(k.shape) == (nL, nR, H, D // x, S, x)
+        layout = DV_LAYOUT_FT6D
+    else:
+        assert k.shape == v.shape
+        layout = DV_LAYOUT_KV5D
     if device is None:
         device = k.device.index if k.is_cuda else -1
-    return dv_cache(k.data_ptr(), v.data_ptr(), device, DV_LAYOUT_KV5D, k.element_size(),
-                    layer_begin, nL, req_begin, nR, H, S, D)
+    return dv_cache(k.data_ptr(), v.data_ptr(), device, layout, k.element_size(),
+                    layer_begin, nL, req_begin, nR, H, S, D, head_begin)
 
 
 def cache_raw(k_ptr, v_ptr, device, elem_bytes, layer_begin, n_layers, req_begin, n_reqs, n_heads,
-              max_seq, head_dim) -> dv_cache:
-    return dv_cache(k_ptr, v_ptr, device, DV_LAYOUT_KV5D, elem_bytes, layer_begin, n_layers,
-                    req_begin, n_reqs, n_heads, max_seq, head_dim)
+              max_seq, head_dim, head_begin=0, layout=DV_LAYOUT_KV5D) -> dv_cache:
+    return dv_cache(k_ptr, v_ptr, device, layout, elem_bytes, layer_begin, n_layers,
+                    req_begin, n_reqs, n_heads, max_seq, head_dim, head_begin)
 
 
 def endpoint(kind, base_ptr, nbytes, flags_ptr=0, n_flags=0, device=-1) -> dv_endpoint:
@@ -376,25 +401,26 @@ def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpo
           xfer, _stream(stream))
 
 
+# The level-1 wrappers take my_tp as a keyword (default 0) after the C positional arguments.
 def dv_stream_out(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
-                  dst_setup: Setup, inboxes, seq, xfer=0, stream=None):
+                  dst_setup: Setup, inboxes, seq, xfer=0, stream=None, my_tp=0):
     arr = endpoint_array(inboxes)
     _call("dv_stream_out", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage, my_micro,
-          C.byref(dst_setup.c), arr, len(inboxes), seq, xfer, _stream(stream))
+          my_tp, C.byref(dst_setup.c), arr, len(inboxes), seq, xfer, _stream(stream))
 
 
 def dv_stream_in(ctx, dst: dv_cache, reg: dv_region, src_setup: Setup, dst_setup: Setup, my_stage,
-                 my_micro, inbox: dv_endpoint, wait_seq, xfer=0, stream=None):
+                 my_micro, inbox: dv_endpoint, wait_seq, xfer=0, stream=None, my_tp=0):
     _call("dv_stream_in", ctx.h, C.byref(dst), C.byref(reg), C.byref(src_setup.c), C.byref(dst_setup.c),
-          my_stage, my_micro, C.byref(inbox), wait_seq, xfer, _stream(stream))
+          my_stage, my_micro, my_tp, C.byref(inbox), wait_seq, xfer, _stream(stream))
 
 
 def dv_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
-                         dst_setup: Setup, dst_caches, signals=None, seq=0, xfer=0, stream=None):
+                         dst_setup: Setup, dst_caches, signals=None, seq=0, xfer=0, stream=None, my_tp=0):
     carr = cache_array(dst_caches)
     sarr = endpoint_array(signals) if signals is not None else None
     _call("dv_stream_out_direct", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage,
-          my_micro, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, xfer, _stream(stream))
+          my_micro, my_tp, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, xfer, _stream(stream))
 
 
 def dv_wait(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):

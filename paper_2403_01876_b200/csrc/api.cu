@@ -137,72 +137,140 @@ dv_status Staging::release(uint64_t off, uint64_t n, cudaStream_t stream) {
 // ---------------------------------------------------------------------------------------------
 // descriptors -> copy plans
 // ---------------------------------------------------------------------------------------------
-// One side of a copy: address of word (l0, r0, h=0, s0, d=0) of K, and byte strides.
-struct Side {
+// One tensor (K or V) of one side of a copy: the address of word (l0, r0, h0, s0, d=0) and the
+// byte strides of the dims (layer, request, head, position, 16-byte packet of d). The packet
+// granularity expresses both cache layouts and the wire:
+//   KV5D (and V of FT6D): position stride D*e, packet stride 16       (d contiguous)
+//   FT6D K:               position stride 16,  packet stride S*16     (x = 16/e words per packet)
+//   wire [l][kv][r][h][s][d]: position stride D*e, packet stride 16
+enum { DL = 0, DR, DH, DS, DU, NDIM };
+struct TView {
   const uint8_t* base;
-  int64_t s_kv, s_l, s_r, s_h;
+  int64_t st[NDIM];
 };
 
-static Side cache_side(const dv_cache* c, const dv_region* r) {
+// `r` must have its heads resolved (explicit head range).
+static TView cache_view(const dv_cache* c, int kv, const dv_region* r) {
   const int64_t row = (int64_t)c->head_dim * c->elem_bytes;
-  const int64_t sh = (int64_t)c->max_seq * row;
+  const int64_t sh = (int64_t)c->max_seq * row;  // a head's [S][D] (or [D/x][S][x]) block
   const int64_t sr = (int64_t)c->n_heads * sh;
   const int64_t sl = (int64_t)c->n_reqs * sr;
+  const bool ft = c->layout == DV_LAYOUT_FT6D && kv == 0;
+  TView t;
+  t.st[DL] = sl;
+  t.st[DR] = sr;
+  t.st[DH] = sh;
+  t.st[DS] = ft ? 16 : row;
+  t.st[DU] = ft ? (int64_t)c->max_seq * 16 : 16;
   const int64_t off = (int64_t)(r->layer_begin - c->layer_begin) * sl +
-                      (int64_t)(r->req_begin - c->req_begin) * sr + (int64_t)r->pos_begin * row;
-  Side s;
-  s.base = (const uint8_t*)c->k + off;
-  s.s_kv = (int64_t)((const uint8_t*)c->v - (const uint8_t*)c->k);
-  s.s_l = sl;
-  s.s_r = sr;
-  s.s_h = sh;
-  return s;
+                      (int64_t)(r->req_begin - c->req_begin) * sr +
+                      (int64_t)(r->head_begin - c->head_begin) * sh +
+                      (int64_t)r->pos_begin * t.st[DS];
+  t.base = (const uint8_t*)(kv ? c->v : c->k) + off;
+  return t;
 }
 
-// Canonical wire chunk [l][kv][r][h][s][d] of a region (reading Q3).
-static Side wire_side(const uint8_t* w, const dv_region* r, int32_t H, int64_t run) {
-  const int64_t nR = r->req_end - r->req_begin;
-  Side s;
-  s.base = w;
-  s.s_h = run;
-  s.s_r = (int64_t)H * run;
-  s.s_kv = nR * s.s_r;
-  s.s_l = 2 * s.s_kv;
-  return s;
+// Canonical wire chunk [l][kv][r][h][s][d] of a region (reading Q3), heads resolved.
+static TView wire_view(const uint8_t* w, int kv, const dv_region* r, int64_t row) {
+  const int64_t run = (int64_t)(r->pos_end - r->pos_begin) * row;
+  const int64_t nH = r->head_end - r->head_begin, nR = r->req_end - r->req_begin;
+  TView t;
+  t.st[DH] = run;
+  t.st[DR] = nH * run;
+  const int64_t kvs = nR * nH * run;
+  t.st[DL] = 2 * kvs;
+  t.st[DS] = row;
+  t.st[DU] = 16;
+  t.base = w + kv * kvs;
+  return t;
+}
+
+static bool same_strides(const TView& a, const TView& b) {
+  for (int k = 0; k < NDIM; ++k)
+    if (a.st[k] != b.st[k]) return false;
+  return true;
 }
 
 enum Order { ORDER_WIRE /* [l][kv][r][h] */, ORDER_KV_OUTER /* [kv][l][r][h] */ };
 
-static CopyPlan make_plan(const Side& s, const Side& d, const dv_region* r, int32_t H, int64_t run,
-                          Order order) {
-  CopyPlan p{};
-  p.src = s.base;
-  p.dst = (uint8_t*)d.base;
-  const uint32_t nL = r->layer_end - r->layer_begin, nR = r->req_end - r->req_begin;
-  p.n[0] = 1;
-  if (order == ORDER_WIRE) {
-    p.n[1] = nL; p.ss[1] = s.s_l;  p.ds[1] = d.s_l;
-    p.n[2] = 2;  p.ss[2] = s.s_kv; p.ds[2] = d.s_kv;
-  } else {
-    p.n[1] = 2;  p.ss[1] = s.s_kv; p.ds[1] = d.s_kv;
-    p.n[2] = nL; p.ss[2] = s.s_l;  p.ds[2] = d.s_l;
+// An optional outer dim in front of everything (the chunk index of a log).
+struct Outer {
+  uint32_t n = 1;
+  int64_t ss = 0, ds = 0;
+};
+
+// Copy plans moving K and V of a (heads-resolved) region from views `sv` to views `dv_`: one plan
+// with kv as a loop dim when K and V have the same strides on both sides, else one per tensor.
+// The (position, packet) dims are pre-merged into the run when contiguous on both sides.
+// only = 0 / 1: a single plan for that tensor alone.
+static int build_plans(const TView sv[2], const TView dv_[2], const dv_region* r, int64_t row,
+                       Order order, const Outer& outer, CopyPlan out[2], int only = -1) {
+  const uint32_t ext[NDIM] = {(uint32_t)(r->layer_end - r->layer_begin),
+                              (uint32_t)(r->req_end - r->req_begin),
+                              (uint32_t)(r->head_end - r->head_begin),
+                              (uint32_t)(r->pos_end - r->pos_begin), (uint32_t)(row / 16)};
+  const bool one = only < 0 && same_strides(sv[0], sv[1]) && same_strides(dv_[0], dv_[1]);
+  const int nplans = (one || only >= 0) ? 1 : 2;
+  for (int q = 0; q < nplans; ++q) {
+    const TView& a = sv[only >= 0 ? only : q];
+    const TView& b = dv_[only >= 0 ? only : q];
+    // dims outer -> inner, before collapsing
+    uint32_t n[8];
+    int64_t ss[8], ds[8];
+    int m = 0;
+    auto push = [&](uint32_t e, int64_t x, int64_t y) {
+      n[m] = e;
+      ss[m] = x;
+      ds[m] = y;
+      ++m;
+    };
+    push(outer.n, outer.ss, outer.ds);
+    if (one && order == ORDER_KV_OUTER) push(2, sv[1].base - sv[0].base, dv_[1].base - dv_[0].base);
+    push(ext[DL], a.st[DL], b.st[DL]);
+    if (one && order == ORDER_WIRE) push(2, sv[1].base - sv[0].base, dv_[1].base - dv_[0].base);
+    push(ext[DR], a.st[DR], b.st[DR]);
+    push(ext[DH], a.st[DH], b.st[DH]);
+    uint64_t run = 16;
+    if (a.st[DU] == 16 && b.st[DU] == 16 && a.st[DS] == row && b.st[DS] == row) {
+      run = (uint64_t)ext[DS] * row;  // positions x packets are one contiguous run on both sides
+    } else {
+      push(ext[DS], a.st[DS], b.st[DS]);
+      push(ext[DU], a.st[DU], b.st[DU]);
+    }
+    // drop unit dims; keep at most kDims (merging happens in collapse())
+    CopyPlan p{};
+    p.src = a.base;
+    p.dst = (uint8_t*)b.base;
+    p.run_bytes = run;
+    int w = 0;
+    uint32_t nn[8];
+    int64_t s2[8], d2[8];
+    for (int k = 0; k < m; ++k)
+      if (n[k] != 1) {
+        nn[w] = n[k];
+        s2[w] = ss[k];
+        d2[w] = ds[k];
+        ++w;
+      }
+    if (w > kDims) return -1;  // not expressible (cannot happen for the layouts above)
+    for (int k = 0; k < kDims; ++k) {
+      const int j = k - (kDims - w);
+      p.n[k] = j < 0 ? 1 : nn[j];
+      p.ss[k] = j < 0 ? 0 : s2[j];
+      p.ds[k] = j < 0 ? 0 : d2[j];
+    }
+    collapse(p);
+    out[q] = p;
   }
-  p.n[3] = nR; p.ss[3] = s.s_r; p.ds[3] = d.s_r;
-  p.n[4] = H;  p.ss[4] = s.s_h; p.ds[4] = d.s_h;
-  p.run_bytes = (uint64_t)run;
-  collapse(p);
-  return p;
+  return nplans;
 }
 
 static uint64_t region_bytes(const dv_region* r, const dv_cache* c) {
-  return 2ull * (uint64_t)(r->layer_end - r->layer_begin) * (uint64_t)(r->req_end - r->req_begin) *
-         (uint64_t)(r->pos_end - r->pos_begin) * (uint64_t)c->n_heads * (uint64_t)c->head_dim *
-         (uint64_t)c->elem_bytes;
+  const dv_region x = resolve_heads(r, c);
+  return region_bytes_h(&x, c->n_heads, c->head_dim, c->elem_bytes);
 }
 
-static int64_t run_bytes(const dv_region* r, const dv_cache* c) {
-  return (int64_t)(r->pos_end - r->pos_begin) * c->head_dim * c->elem_bytes;
-}
+static int64_t row_bytes(const dv_cache* c) { return (int64_t)c->head_dim * c->elem_bytes; }
 
 static dv_status check_ep(const dv_endpoint* ep, uint64_t off, uint64_t bytes, int32_t slot,
                           bool use_flag, const char* name) {
@@ -260,14 +328,19 @@ static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
   return DV_OK;
 }
 
-// One fused kernel, then the flag: by the kernel itself (fenced st.release.sys from the last CTA)
-// or, with DV_PUBLISH_STREAMOP, by a stream memory operation after it.
-static dv_status launch_publish(dv_ctx* ctx, const CopyPlan& p, const dv_endpoint* ep, int32_t slot,
-                                uint64_t seq, bool use_flag, uint32_t xfer, cudaStream_t st) {
+// The fused kernels of 1-2 plans, then the flag: by the last kernel itself (fenced st.release.sys
+// from its last CTA) or, with DV_PUBLISH_STREAMOP, by a stream memory operation after it.
+static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv_endpoint* ep,
+                                int32_t slot, uint64_t seq, bool use_flag, uint32_t xfer,
+                                cudaStream_t st) {
   const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
   const Release none{nullptr, 0, nullptr};
-  DV_TRY(launch_copy(p, 0, p.runs(), streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag),
-                     ctx->max_ctas, st));
+  for (int q = 0; q < np; ++q) {
+    const bool last = q == np - 1;
+    DV_TRY(launch_copy(p[q], 0, p[q].runs(),
+                       (last && !streamop) ? ticket_release(ctx, ep, slot, seq, use_flag) : none,
+                       ctx->max_ctas, st));
+  }
   if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
   return DV_OK;
 }
@@ -308,39 +381,141 @@ static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
                   "destination");
 }
 
-static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) {
-  const dv_cache* c = op.src;
-  const uint64_t bytes = region_bytes(&op.reg, c);
-  const int64_t run = run_bytes(&op.reg, c);
-  const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
-  const uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
-  uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off;
-  if (mode == DV_XFER_FUSED) {
-    CopyPlan p = make_plan(cache_side(c, &op.reg), wire_side(wire, &op.reg, c->n_heads, run),
-                           &op.reg, c->n_heads, run, ORDER_WIRE);
-    return launch_publish(ctx, p, op.dst, op.slot, op.seq, use_flag, op.xfer, st);
-  }
-  // STAGED: pack chunks of runs into staging, copy engine moves each chunk.
-  if (bytes) {
-    CopyPlan p = make_plan(cache_side(c, &op.reg), wire_side(wire, &op.reg, c->n_heads, run),
-                           &op.reg, c->n_heads, run, ORDER_WIRE);
-    const uint64_t rb = p.run_bytes, runs = p.runs();
-    const uint64_t chunk = std::max<uint64_t>(1, (ctx->staging.capacity() / 2) / rb);
-    if (rb > ctx->staging.capacity() / 2)
-      return fail(DV_ENOMEM, "run of %llu bytes exceeds half the staging pool",
-                  (unsigned long long)rb);
+// Layer slabs of a region's wire: [l][...] -- slab l starts at (l - l0) * slab bytes.
+static uint64_t layer_slab_bytes(const dv_region* r, int64_t row) {
+  return 2ull * (uint64_t)(r->req_end - r->req_begin) * (uint64_t)(r->head_end - r->head_begin) *
+         (uint64_t)(r->pos_end - r->pos_begin) * (uint64_t)row;
+}
+
+// Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
+// the kernel packs a group of layer slabs (or, with one plan, a range of runs) into staging, the
+// copy engine moves that contiguous piece to its place in the wire.
+static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, uint8_t* wire,
+                             cudaStream_t st) {
+  const int64_t row = row_bytes(c);
+  const uint64_t half = ctx->staging.capacity() / 2;
+  const Release none{nullptr, 0, nullptr};
+  TView sv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  CopyPlan p[2];
+  const int np = build_plans(sv, wv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  if (np == 1 && p[0].run_bytes <= half) {  // dense wire in run order: chunk by runs
+    const uint64_t rb = p[0].run_bytes, runs = p[0].runs();
+    const uint64_t chunk = std::max<uint64_t>(1, half / rb);
     for (uint64_t q0 = 0; q0 < runs; q0 += chunk) {
       const uint64_t q1 = std::min(runs, q0 + chunk), nb = (q1 - q0) * rb;
       uint8_t* stg;
       uint64_t off;
       DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
-      CopyPlan pc = p;
+      CopyPlan pc = p[0];
       pc.dst = stg - q0 * rb;  // run q lands at stg + (q - q0) * rb (wire side is dense)
-      DV_TRY(launch_copy(pc, q0, q1, Release{nullptr, 0, nullptr}, ctx->max_ctas, st));
+      DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
       DV_DMA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, st));
       DV_TRY(ctx->staging.release(off, nb, st));
     }
+    return DV_OK;
   }
+  const uint64_t slab = layer_slab_bytes(&reg, row);
+  if (slab > half)
+    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+                "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
+  const int32_t per = (int32_t)std::max<uint64_t>(1, half / slab);
+  for (int32_t la = reg.layer_begin; la < reg.layer_end; la += per) {
+    dv_region sub = reg;
+    sub.layer_begin = la;
+    sub.layer_end = std::min(reg.layer_end, la + per);
+    const uint64_t nb = (uint64_t)(sub.layer_end - la) * slab;
+    uint8_t* stg;
+    uint64_t off;
+    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
+    TView s2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
+    TView w2[2] = {wire_view(stg, 0, &sub, row), wire_view(stg, 1, &sub, row)};
+    CopyPlan ps[2];
+    const int n2 = build_plans(s2, w2, &sub, row, ORDER_WIRE, Outer{}, ps);
+    for (int q = 0; q < n2; ++q) DV_TRY(launch_copy(ps[q], 0, ps[q].runs(), none, ctx->max_ctas, st));
+    DV_DMA(cudaMemcpyAsync(wire + (uint64_t)(la - reg.layer_begin) * slab, stg, nb,
+                           cudaMemcpyDefault, st));
+    DV_TRY(ctx->staging.release(off, nb, st));
+  }
+  return DV_OK;
+}
+
+// Unpack a wire chunk at `wire` (any memory) into `reg` of cache `c` through HBM staging.
+static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache* c,
+                               const dv_region& reg, cudaStream_t st) {
+  const int64_t row = row_bytes(c);
+  const uint64_t half = ctx->staging.capacity() / 2;
+  const Release none{nullptr, 0, nullptr};
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  TView cv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
+  CopyPlan p[2];
+  const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  if (np == 1 && p[0].run_bytes <= half) {
+    const uint64_t rb = p[0].run_bytes, runs = p[0].runs();
+    const uint64_t chunk = std::max<uint64_t>(1, half / rb);
+    for (uint64_t q0 = 0; q0 < runs; q0 += chunk) {
+      const uint64_t q1 = std::min(runs, q0 + chunk), nb = (q1 - q0) * rb;
+      uint8_t* stg;
+      uint64_t off;
+      DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
+      DV_DMA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, st));
+      CopyPlan pc = p[0];
+      pc.src = stg - q0 * rb;
+      DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
+      DV_TRY(ctx->staging.release(off, nb, st));
+    }
+    return DV_OK;
+  }
+  const uint64_t slab = layer_slab_bytes(&reg, row);
+  if (slab > half)
+    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+                "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
+  const int32_t per = (int32_t)std::max<uint64_t>(1, half / slab);
+  for (int32_t la = reg.layer_begin; la < reg.layer_end; la += per) {
+    dv_region sub = reg;
+    sub.layer_begin = la;
+    sub.layer_end = std::min(reg.layer_end, la + per);
+    const uint64_t nb = (uint64_t)(sub.layer_end - la) * slab;
+    uint8_t* stg;
+    uint64_t off;
+    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
+    DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)(la - reg.layer_begin) * slab, nb,
+                           cudaMemcpyDefault, st));
+    TView w2[2] = {wire_view(stg, 0, &sub, row), wire_view(stg, 1, &sub, row)};
+    TView c2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
+    CopyPlan ps[2];
+    const int n2 = build_plans(w2, c2, &sub, row, ORDER_WIRE, Outer{}, ps);
+    for (int q = 0; q < n2; ++q) DV_TRY(launch_copy(ps[q], 0, ps[q].runs(), none, ctx->max_ctas, st));
+    DV_TRY(ctx->staging.release(off, nb, st));
+  }
+  return DV_OK;
+}
+
+static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) {
+  const dv_cache* c = op.src;
+  const dv_region reg = resolve_heads(&op.reg, c);
+  const uint64_t bytes = region_bytes(&reg, c);
+  const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
+  const uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
+  uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off;
+  const int64_t row = row_bytes(c);
+  if (mode == DV_XFER_FUSED || region_empty(&reg)) {
+    CopyPlan p[2];
+    int np = 0;
+    if (!region_empty(&reg)) {
+      TView sv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
+      TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+      np = build_plans(sv, wv, &reg, row, ORDER_WIRE, Outer{}, p);
+      if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+    } else {
+      p[0] = CopyPlan{};
+      np = 1;  // empty plan: still publishes the flag in stream order
+    }
+    return launch_publish(ctx, p, np, op.dst, op.slot, op.seq, use_flag, op.xfer, st);
+  }
+  DV_TRY(staged_pack(ctx, c, reg, wire, st));
   if (use_flag) DV_TRY(stream_signal(op.dst, op.slot, op.seq, st));
   return DV_OK;
 }
@@ -364,44 +539,25 @@ static dv_status gather_check(dv_ctx* ctx, const GatherOp& op) {
   return check_ep(op.src, op.src_off, region_bytes(&op.reg, op.dst), op.slot, use_flag, "source");
 }
 
-// Runs an unpack plan whose source side is a dense wire chunk at `wire` (run q at wire + q*run):
-// FUSED = one kernel reading the endpoint memory directly; STAGED = the copy engine brings chunks
-// of runs into HBM staging, the kernel unpacks each chunk.
-static dv_status unpack_plan(dv_ctx* ctx, const CopyPlan& p, const uint8_t* wire, uint32_t mode,
-                             cudaStream_t st) {
-  const Release none{nullptr, 0, nullptr};
-  if (mode == DV_XFER_FUSED) return launch_copy(p, 0, p.runs(), none, ctx->max_ctas, st);
-  const uint64_t rb = p.run_bytes, runs = p.runs();
-  if (rb > ctx->staging.capacity() / 2)
-    return fail(DV_ENOMEM, "run of %llu bytes exceeds half the staging pool",
-                (unsigned long long)rb);
-  const uint64_t chunk = std::max<uint64_t>(1, (ctx->staging.capacity() / 2) / rb);
-  for (uint64_t q0 = 0; q0 < runs; q0 += chunk) {
-    const uint64_t q1 = std::min(runs, q0 + chunk), nb = (q1 - q0) * rb;
-    uint8_t* stg;
-    uint64_t off;
-    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
-    DV_DMA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, st));
-    CopyPlan pc = p;
-    pc.src = stg - q0 * rb;
-    DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
-    DV_TRY(ctx->staging.release(off, nb, st));
-  }
-  return DV_OK;
-}
-
 static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   const dv_cache* c = op.dst;
-  const uint64_t bytes = region_bytes(&op.reg, c);
-  const int64_t run = run_bytes(&op.reg, c);
+  const dv_region reg = resolve_heads(&op.reg, c);
+  const uint64_t bytes = region_bytes(&reg, c);
   if (!(op.xfer & DV_NO_FLAG) && op.slot >= 0 && op.wait_seq)
     DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
   if (!bytes) return DV_OK;
   const uint32_t mode = pick_xfer(op.xfer, op.src, bytes, true);
   const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
-  CopyPlan p = make_plan(wire_side(wire, &op.reg, c->n_heads, run), cache_side(c, &op.reg),
-                         &op.reg, c->n_heads, run, ORDER_WIRE);
-  return unpack_plan(ctx, p, wire, mode, st);
+  if (mode == DV_XFER_STAGED) return staged_unpack(ctx, wire, c, reg, st);
+  const int64_t row = row_bytes(c);
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  TView cv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
+  CopyPlan p[2];
+  const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  for (int q = 0; q < np; ++q)
+    DV_TRY(launch_copy(p[q], 0, p[q].runs(), Release{nullptr, 0, nullptr}, ctx->max_ctas, st));
+  return DV_OK;
 }
 
 struct RemapOp {
@@ -419,49 +575,59 @@ static dv_status remap_check(dv_ctx* ctx, const RemapOp& op) {
   DV_TRY(check_cache(op.src, "source"));
   DV_TRY(check_cache(op.dst, "destination"));
   DV_TRY(check_region_shape(&op.reg));
-  DV_TRY(check_cache_holds(op.src, &op.reg, "source"));
-  DV_TRY(check_cache_holds(op.dst, &op.reg, "destination"));
-  if (op.src->n_heads != op.dst->n_heads || op.src->head_dim != op.dst->head_dim ||
-      op.src->elem_bytes != op.dst->elem_bytes)
-    return fail(DV_EMAP, "source and destination caches differ in heads/head_dim/elem_bytes");
+  const dv_region reg = resolve_heads(&op.reg, op.src);
+  DV_TRY(check_cache_holds(op.src, &reg, "source"));
+  DV_TRY(check_cache_holds(op.dst, &reg, "destination"));
+  if (op.src->head_dim != op.dst->head_dim || op.src->elem_bytes != op.dst->elem_bytes)
+    return fail(DV_EMAP, "source and destination caches differ in head_dim/elem_bytes");
   if (op.signal && !(op.xfer & DV_NO_FLAG) && op.slot >= 0)
     DV_TRY(check_ep(op.signal, 0, 0, op.slot, true, "signal"));
   return DV_OK;
 }
 
 static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
-  const dv_cache* c = op.src;
-  const int64_t run = run_bytes(&op.reg, c);
+  const dv_region reg = resolve_heads(&op.reg, op.src);
+  const int64_t row = row_bytes(op.src);
   const bool use_flag = op.signal && !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
-  CopyPlan p = make_plan(cache_side(op.src, &op.reg), cache_side(op.dst, &op.reg), &op.reg,
-                         c->n_heads, run, ORDER_KV_OUTER);
   uint32_t m = op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   if (m != DV_XFER_FUSED && m != DV_XFER_STAGED)  // AUTO (profiles/r01_configs*.jsonl, C4):
     m = (op.src->device < 0 && op.dst->device >= 0) ? DV_XFER_STAGED : DV_XFER_FUSED;
-  if (m == DV_XFER_STAGED && p.runs() && p.run_bytes) {
+  const bool both5 = op.src->layout == DV_LAYOUT_KV5D && op.dst->layout == DV_LAYOUT_KV5D;
+  if (m == DV_XFER_STAGED && both5 && !region_empty(&reg)) {
     // Copy-engine form (paper-style DMA, used for pinned-host mirror arenas): one
     // 2-D copy per (kv, layer, request) over the heads, or one 1-D copy when the heads are
     // contiguous on both sides.
-    const Side s = cache_side(op.src, &op.reg), d = cache_side(op.dst, &op.reg);
-    const int nL = op.reg.layer_end - op.reg.layer_begin, nR = op.reg.req_end - op.reg.req_begin;
-    const int H = c->n_heads;
-    const bool flat = s.s_h == run && d.s_h == run;
-    for (int kv = 0; kv < 2; ++kv)
+    const int64_t run = (int64_t)(reg.pos_end - reg.pos_begin) * row;
+    const int nL = reg.layer_end - reg.layer_begin, nR = reg.req_end - reg.req_begin;
+    const int H = reg.head_end - reg.head_begin;
+    for (int kv = 0; kv < 2; ++kv) {
+      const TView s = cache_view(op.src, kv, &reg), d = cache_view(op.dst, kv, &reg);
+      const bool flat = s.st[DH] == run && d.st[DH] == run;
       for (int l = 0; l < nL; ++l)
         for (int r = 0; r < nR; ++r) {
-          const uint8_t* sp = s.base + kv * s.s_kv + l * s.s_l + r * s.s_r;
-          uint8_t* dp = (uint8_t*)d.base + kv * d.s_kv + l * d.s_l + r * d.s_r;
+          const uint8_t* sp = s.base + l * s.st[DL] + r * s.st[DR];
+          uint8_t* dp = (uint8_t*)d.base + l * d.st[DL] + r * d.st[DR];
           if (flat || H == 1) {
             DV_DMA(cudaMemcpyAsync(dp, sp, (size_t)run * (flat ? H : 1), cudaMemcpyDefault, st));
           } else {
-            DV_DMA(cudaMemcpy2DAsync(dp, (size_t)d.s_h, sp, (size_t)s.s_h, (size_t)run, H,
-                                      cudaMemcpyDefault, st));
+            DV_DMA(cudaMemcpy2DAsync(dp, (size_t)d.st[DH], sp, (size_t)s.st[DH], (size_t)run, H,
+                                     cudaMemcpyDefault, st));
           }
         }
+    }
     if (use_flag) DV_TRY(stream_signal(op.signal, op.slot, op.seq, st));
     return DV_OK;
   }
-  return launch_publish(ctx, p, op.signal, op.slot, op.seq, use_flag, op.xfer, st);
+  CopyPlan p[2];
+  int np = 1;
+  p[0] = CopyPlan{};
+  if (!region_empty(&reg)) {
+    TView sv[2] = {cache_view(op.src, 0, &reg), cache_view(op.src, 1, &reg)};
+    TView dv_[2] = {cache_view(op.dst, 0, &reg), cache_view(op.dst, 1, &reg)};
+    np = build_plans(sv, dv_, &reg, row, ORDER_KV_OUTER, Outer{}, p);
+    if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  }
+  return launch_publish(ctx, p, np, op.signal, op.slot, op.seq, use_flag, op.xfer, st);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -653,7 +819,7 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
       p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
-    return launch_publish(ctx, p, dst, flag_slot, seq, use_flag, xfer, st);
+    return launch_publish(ctx, &p, 1, dst, flag_slot, seq, use_flag, xfer, st);
   }
   if (bytes) DV_DMA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st));
   if (use_flag) DV_TRY(stream_signal(dst, flag_slot, seq, st));
@@ -710,26 +876,27 @@ dv_status dv_gather(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32
 }
 
 dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_t flag_slot,
-                           uint64_t wait_seq, const dv_cache* dst, const dv_region* first,
+                           uint64_t wait_seq, const dv_cache* dst, const dv_region* first0,
                            int32_t n_chunks, int32_t pos_step, uint32_t xfer, void* stream) {
   DV_TRY(check_ctx(ctx));
-  if (!first) return fail(DV_EINVAL, "NULL region");
+  if (!first0) return fail(DV_EINVAL, "NULL region");
   if (n_chunks < 0) return fail(DV_EINVAL, "negative n_chunks");
   DV_TRY(check_cache(dst, "destination"));
-  DV_TRY(check_region_shape(first));
-  const int32_t n = first->pos_end - first->pos_begin;
+  DV_TRY(check_region_shape(first0));
+  const dv_region first = resolve_heads(first0, dst);
+  const int32_t n = first.pos_end - first.pos_begin;
   if (n_chunks > 1 && pos_step < n)
     return fail(DV_EINVAL, "pos_step %d smaller than the chunk's %d positions", pos_step, n);
-  dv_region last = *first;
+  dv_region last = first;
   if (n_chunks > 0) {
     const int64_t shift = (int64_t)(n_chunks - 1) * pos_step;
-    if (first->pos_end + shift > INT32_MAX) return fail(DV_ERANGE, "chunk positions overflow");
+    if (first.pos_end + shift > INT32_MAX) return fail(DV_ERANGE, "chunk positions overflow");
     last.pos_begin += (int32_t)shift;
     last.pos_end += (int32_t)shift;
   }
-  DV_TRY(check_cache_holds(dst, first, "destination"));
+  DV_TRY(check_cache_holds(dst, &first, "destination"));
   DV_TRY(check_cache_holds(dst, &last, "destination"));
-  const uint64_t chunk_bytes = region_bytes(first, dst);
+  const uint64_t chunk_bytes = region_bytes(&first, dst);
   const uint64_t total = chunk_bytes * (uint64_t)n_chunks;
   DV_TRY(check_ep(src, src_off, total, flag_slot, !(xfer & DV_NO_FLAG), "source"));
   DV_ON_DEVICE(ctx->device);
@@ -737,23 +904,57 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
   if (!(xfer & DV_NO_FLAG) && flag_slot >= 0 && wait_seq)
     DV_TRY(stream_wait(src, flag_slot, wait_seq, st));
   if (!total) return DV_OK;
-  const int64_t run = run_bytes(first, dst);
+  const int64_t row = row_bytes(dst);
   const uint8_t* wire = (const uint8_t*)src->base + src_off;
-  // dims [chunk][l][kv][r][h]: the log side is dense in this order
-  const Side ws = wire_side(wire, first, dst->n_heads, run);
-  const Side cs = cache_side(dst, first);
-  CopyPlan p{};
-  p.src = ws.base;
-  p.dst = (uint8_t*)cs.base;
-  p.n[0] = (uint32_t)n_chunks; p.ss[0] = (int64_t)chunk_bytes;
-  p.ds[0] = (int64_t)pos_step * dst->head_dim * dst->elem_bytes;
-  p.n[1] = first->layer_end - first->layer_begin; p.ss[1] = ws.s_l; p.ds[1] = cs.s_l;
-  p.n[2] = 2; p.ss[2] = ws.s_kv; p.ds[2] = cs.s_kv;
-  p.n[3] = first->req_end - first->req_begin; p.ss[3] = ws.s_r; p.ds[3] = cs.s_r;
-  p.n[4] = dst->n_heads; p.ss[4] = ws.s_h; p.ds[4] = cs.s_h;
-  p.run_bytes = (uint64_t)run;
-  collapse(p);
-  return unpack_plan(ctx, p, wire, pick_xfer(xfer, src, total, true), st);
+  const uint32_t mode = pick_xfer(xfer, src, total, true);
+  const Release none{nullptr, 0, nullptr};
+  // groups of chunks [k0, k1): the log side is dense over [chunk][l][kv][r][h][s][d]
+  auto unpack_group = [&](const uint8_t* base, int32_t k0, int32_t k1) -> dv_status {
+    dv_region f = first;
+    f.pos_begin += k0 * pos_step;
+    f.pos_end += k0 * pos_step;
+    TView wv[2] = {wire_view(base, 0, &f, row), wire_view(base, 1, &f, row)};
+    TView cv[2] = {cache_view(dst, 0, &f), cache_view(dst, 1, &f)};
+    // chunk dim: log stride = chunk bytes; cache stride = pos_step positions (per tensor; equal
+    // for K and V unless K is FT6D, whose position stride is 16 B -- then two plans anyway)
+    CopyPlan p[2];
+    const bool one = same_strides(wv[0], wv[1]) && same_strides(cv[0], cv[1]);
+    int np = 0;
+    for (int q = 0; q < (one ? 1 : 2); ++q) {
+      Outer o;
+      o.n = (uint32_t)(k1 - k0);
+      o.ss = (int64_t)chunk_bytes;
+      o.ds = (int64_t)pos_step * cv[q].st[DS];
+      const int r = build_plans(wv, cv, &f, row, ORDER_WIRE, o, &p[np], one ? -1 : q);
+      if (r < 0) return fail(DV_ENOTSUP, "copy not expressible");
+      np += 1;
+    }
+    for (int q = 0; q < np; ++q) DV_TRY(launch_copy(p[q], 0, p[q].runs(), none, ctx->max_ctas, st));
+    return DV_OK;
+  };
+  if (mode == DV_XFER_FUSED) return unpack_group(wire, 0, n_chunks);
+  const uint64_t half = ctx->staging.capacity() / 2;
+  if (chunk_bytes > half) {  // big chunks: one staged gather per chunk
+    for (int32_t k = 0; k < n_chunks; ++k) {
+      dv_region f = first;
+      f.pos_begin += k * pos_step;
+      f.pos_end += k * pos_step;
+      DV_TRY(staged_unpack(ctx, wire + (uint64_t)k * chunk_bytes, dst, f, st));
+    }
+    return DV_OK;
+  }
+  const int32_t per = (int32_t)std::max<uint64_t>(1, half / chunk_bytes);
+  for (int32_t k0 = 0; k0 < n_chunks; k0 += per) {
+    const int32_t k1 = std::min(n_chunks, k0 + per);
+    const uint64_t nb = (uint64_t)(k1 - k0) * chunk_bytes;
+    uint8_t* stg;
+    uint64_t off;
+    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
+    DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)k0 * chunk_bytes, nb, cudaMemcpyDefault, st));
+    DV_TRY(unpack_group(stg, k0, k1));
+    DV_TRY(ctx->staging.release(off, nb, st));
+  }
+  return DV_OK;
 }
 
 dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const dv_region* region,
@@ -767,39 +968,49 @@ dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const 
 }
 
 // ---- level 1 --------------------------------------------------------------------------------
+static int32_t flat_block(const dv_setup* s, int32_t stage, int32_t micro, int32_t tp) {
+  return (stage * s->n_micro + micro) * std::max(s->n_tp, 1) + tp;
+}
+
 static dv_status my_pieces(const dv_setup* src_setup, const dv_setup* dst_setup,
                            const dv_region* region, const dv_cache* c, int32_t stage,
-                           int32_t micro, bool sender, std::vector<dv_piece>* out) {
+                           int32_t micro, int32_t tp, bool sender, std::vector<dv_piece>* out) {
   DV_TRY(check_cache(c, sender ? "source" : "destination"));
+  if (!region) return fail(DV_EINVAL, "NULL region");
   std::vector<dv_piece> all;
   DV_TRY(route(src_setup, dst_setup, region, c->n_heads, c->head_dim, c->elem_bytes, &all));
   const dv_setup* mine = sender ? src_setup : dst_setup;
-  if (stage < 0 || stage >= mine->n_stages || micro < 0 || micro >= mine->n_micro)
-    return fail(DV_EINVAL, "block (%d,%d) not in the %s setup", stage, micro,
+  if (stage < 0 || stage >= mine->n_stages || micro < 0 || micro >= mine->n_micro || tp < 0 ||
+      tp >= std::max(mine->n_tp, 1))
+    return fail(DV_EINVAL, "block (%d,%d,%d) not in the %s setup", stage, micro, tp,
                 sender ? "source" : "destination");
   out->clear();
   for (auto& p : all)
-    if (sender ? (p.src_stage == stage && p.src_micro == micro)
-               : (p.dst_stage == stage && p.dst_micro == micro))
+    if (sender ? (p.src_stage == stage && p.src_micro == micro && p.src_tp == tp)
+               : (p.dst_stage == stage && p.dst_micro == micro && p.dst_tp == tp))
       out->push_back(p);
   return DV_OK;
 }
 
+static dv_region piece_region(const dv_piece& p) {
+  return dv_region{p.layer_begin, p.layer_end, p.req_begin, p.req_end,
+                   p.pos_begin,   p.pos_end,   p.head_begin, p.head_end};
+}
+
 dv_status dv_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                         const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
-                        const dv_setup* dst_setup, const dv_endpoint* inboxes, int32_t n_inboxes,
-                        uint64_t seq, uint32_t xfer, void* stream) {
+                        int32_t my_tp, const dv_setup* dst_setup, const dv_endpoint* inboxes,
+                        int32_t n_inboxes, uint64_t seq, uint32_t xfer, void* stream) {
   DV_TRY(check_ctx(ctx));
   std::vector<dv_piece> ps;
-  DV_TRY(my_pieces(src_setup, dst_setup, region, src, my_stage, my_micro, true, &ps));
+  DV_TRY(my_pieces(src_setup, dst_setup, region, src, my_stage, my_micro, my_tp, true, &ps));
   if (!inboxes && !ps.empty()) return fail(DV_EINVAL, "NULL inboxes");
-  const int32_t slot = my_stage * src_setup->n_micro + my_micro;
+  const int32_t slot = flat_block(src_setup, my_stage, my_micro, my_tp);
   std::vector<ScatterOp> ops;
   for (auto& p : ps) {
-    const int32_t k = p.dst_stage * dst_setup->n_micro + p.dst_micro;
+    const int32_t k = flat_block(dst_setup, p.dst_stage, p.dst_micro, p.dst_tp);
     if (k >= n_inboxes) return fail(DV_EINVAL, "inbox %d missing (n_inboxes %d)", k, n_inboxes);
-    dv_region r{p.layer_begin, p.layer_end, p.req_begin, p.req_end, p.pos_begin, p.pos_end};
-    ScatterOp op{src, r, &inboxes[k], p.dst_wire_off, slot, seq, xfer};
+    ScatterOp op{src, piece_region(p), &inboxes[k], p.dst_wire_off, slot, seq, xfer};
     DV_TRY(scatter_check(ctx, op));  // validate every piece before enqueueing any
     ops.push_back(op);
   }
@@ -810,16 +1021,15 @@ dv_status dv_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* regio
 
 dv_status dv_stream_in(dv_ctx* ctx, const dv_cache* dst, const dv_region* region,
                        const dv_setup* src_setup, const dv_setup* dst_setup, int32_t my_stage,
-                       int32_t my_micro, const dv_endpoint* inbox, uint64_t wait_seq,
-                       uint32_t xfer, void* stream) {
+                       int32_t my_micro, int32_t my_tp, const dv_endpoint* inbox,
+                       uint64_t wait_seq, uint32_t xfer, void* stream) {
   DV_TRY(check_ctx(ctx));
   std::vector<dv_piece> ps;
-  DV_TRY(my_pieces(src_setup, dst_setup, region, dst, my_stage, my_micro, false, &ps));
+  DV_TRY(my_pieces(src_setup, dst_setup, region, dst, my_stage, my_micro, my_tp, false, &ps));
   std::vector<GatherOp> ops;
   for (auto& p : ps) {
-    dv_region r{p.layer_begin, p.layer_end, p.req_begin, p.req_end, p.pos_begin, p.pos_end};
-    const int32_t slot = p.src_stage * src_setup->n_micro + p.src_micro;
-    GatherOp op{inbox, p.dst_wire_off, slot, wait_seq, dst, r, xfer};
+    const int32_t slot = flat_block(src_setup, p.src_stage, p.src_micro, p.src_tp);
+    GatherOp op{inbox, p.dst_wire_off, slot, wait_seq, dst, piece_region(p), xfer};
     DV_TRY(gather_check(ctx, op));
     ops.push_back(op);
   }
@@ -830,20 +1040,20 @@ dv_status dv_stream_in(dv_ctx* ctx, const dv_cache* dst, const dv_region* region
 
 dv_status dv_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                                const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
-                               const dv_setup* dst_setup, const dv_cache* dst_caches,
+                               int32_t my_tp, const dv_setup* dst_setup, const dv_cache* dst_caches,
                                const dv_endpoint* signals, int32_t n_dst, uint64_t seq,
                                uint32_t xfer, void* stream) {
   DV_TRY(check_ctx(ctx));
   std::vector<dv_piece> ps;
-  DV_TRY(my_pieces(src_setup, dst_setup, region, src, my_stage, my_micro, true, &ps));
+  DV_TRY(my_pieces(src_setup, dst_setup, region, src, my_stage, my_micro, my_tp, true, &ps));
   if (!dst_caches && !ps.empty()) return fail(DV_EINVAL, "NULL dst_caches");
-  const int32_t slot = my_stage * src_setup->n_micro + my_micro;
+  const int32_t slot = flat_block(src_setup, my_stage, my_micro, my_tp);
   std::vector<RemapOp> ops;
   for (auto& p : ps) {
-    const int32_t k = p.dst_stage * dst_setup->n_micro + p.dst_micro;
+    const int32_t k = flat_block(dst_setup, p.dst_stage, p.dst_micro, p.dst_tp);
     if (k >= n_dst) return fail(DV_EINVAL, "destination %d missing (n_dst %d)", k, n_dst);
-    dv_region r{p.layer_begin, p.layer_end, p.req_begin, p.req_end, p.pos_begin, p.pos_end};
-    RemapOp op{src, &dst_caches[k], r, signals ? &signals[k] : nullptr, slot, seq, xfer};
+    RemapOp op{src, &dst_caches[k], piece_region(p), signals ? &signals[k] : nullptr, slot, seq,
+               xfer};
     DV_TRY(remap_check(ctx, op));
     ops.push_back(op);
   }

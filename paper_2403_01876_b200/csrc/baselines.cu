@@ -12,22 +12,26 @@ struct Geo {
   int64_t row, sh, sr, sl, run;
   int nL, nR, H;
 };
-dv_status geo(const dv_cache* c, const dv_region* r, Geo* g) {
+dv_status geo(const dv_cache* c, const dv_region* r0, Geo* g) {
   DV_TRY(check_cache(c, "source"));
-  DV_TRY(check_region_shape(r));
-  DV_TRY(check_cache_holds(c, r, "source"));
+  if (c->layout != DV_LAYOUT_KV5D) return fail(DV_ENOTSUP, "baselines support KV5D only");
+  DV_TRY(check_region_shape(r0));
+  DV_TRY(check_cache_holds(c, r0, "source"));
+  const dv_region rr = resolve_heads(r0, c);
+  const dv_region* r = &rr;
   g->row = (int64_t)c->head_dim * c->elem_bytes;
   g->sh = (int64_t)c->max_seq * g->row;
   g->sr = g->sh * c->n_heads;
   g->sl = g->sr * c->n_reqs;
   const int64_t off = (int64_t)(r->layer_begin - c->layer_begin) * g->sl +
-                      (int64_t)(r->req_begin - c->req_begin) * g->sr + (int64_t)r->pos_begin * g->row;
+                      (int64_t)(r->req_begin - c->req_begin) * g->sr +
+                      (int64_t)(r->head_begin - c->head_begin) * g->sh + (int64_t)r->pos_begin * g->row;
   g->k = (const uint8_t*)c->k + off;
   g->v = (const uint8_t*)c->v + off;
   g->run = (int64_t)(r->pos_end - r->pos_begin) * g->row;
   g->nL = r->layer_end - r->layer_begin;
   g->nR = r->req_end - r->req_begin;
-  g->H = c->n_heads;
+  g->H = r->head_end - r->head_begin;
   return DV_OK;
 }
 }  // namespace

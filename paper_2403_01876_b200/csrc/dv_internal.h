@@ -40,7 +40,7 @@ FastDiv make_fastdiv(uint32_t d);
 // ---- a batched strided copy: up to kDims loop dims of contiguous runs -----------------------
 // Run q (row-major over n[0..kDims-1], last innermost) starts at src + sum_k i_k*ss[k] and
 // dst + sum_k i_k*ds[k]; every run is run_bytes contiguous bytes on both sides.
-constexpr int kDims = 5;
+constexpr int kDims = 6;
 struct CopyPlan {
   const uint8_t* src;
   uint8_t* dst;
@@ -136,6 +136,10 @@ namespace dv {
 // Validation + descriptor helpers shared by the API translation units (route.cpp, api.cu).
 dv_status check_setup(const dv_setup* s, const char* name);
 dv_status check_region_shape(const dv_region* r);
+bool all_heads(const dv_region* r);
+bool region_empty(const dv_region* r);
+dv_region resolve_heads(const dv_region* r, const dv_cache* c);  // "all heads" -> the cache's
+uint64_t region_bytes_h(const dv_region* r, int32_t H, int32_t D, int32_t e);
 dv_status check_cache(const dv_cache* c, const char* name);
 dv_status check_cache_holds(const dv_cache* c, const dv_region* r, const char* name);
 dv_status route(const dv_setup* src, const dv_setup* dst, const dv_region* region,

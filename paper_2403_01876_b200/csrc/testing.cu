@@ -15,9 +15,11 @@ struct FillParams {
   uint16_t* k;
   uint16_t* v;
   int64_t s_l, s_r, s_h;  // element strides of the cache
-  int32_t lb, rb;         // cache layer_begin / req_begin
-  int32_t l0, r0, s0;     // region origin
-  int32_t nR, H, n, D;    // region extents
+  int32_t lb, rb, hb;     // cache layer_begin / req_begin / head_begin
+  int32_t l0, r0, s0, h0; // region origin (global ids)
+  int32_t nR, H, n, D;    // region extents (H = heads in the region)
+  int32_t S;              // cache max_seq
+  int32_t ft6d;           // K in FasterTransformer 6-D layout [..][D/x][S][x]
   int32_t kind;
   uint64_t seedmix;
   int32_t box[5];
@@ -31,13 +33,14 @@ __global__ void k_fill(const FillParams p) {
   asm volatile("griddepcontrol.launch_dependents;");
   // blockIdx.x = slab (l, r, h) of the region, blockIdx.y = kv
   uint32_t slab = blockIdx.x;
-  const int h = slab % p.H;
+  const int h = p.h0 + (int)(slab % p.H);  // global head id
   slab /= p.H;
   const int r = p.r0 + (int)(slab % p.nR);
   const int l = p.l0 + (int)(slab / p.nR);
   const int kv = blockIdx.y;
   uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
-                   (int64_t)h * p.s_h;
+                   (int64_t)(h - p.hb) * p.s_h;
+  const bool ft = p.ft6d && kv == 0;
   const int64_t words = (int64_t)p.n * p.D;
   for (int64_t i = threadIdx.x; i < words; i += blockDim.x) {
     const int s = p.s0 + (int)(i / p.D);
@@ -57,7 +60,10 @@ __global__ void k_fill(const FillParams p) {
     } else {
       w = (uint16_t)p.seedmix;
     }
-    base[(int64_t)s * p.D + d] = w;
+    if (ft)  // x = 8 16-bit words per 16-byte packet
+      base[((int64_t)(d >> 3) * p.S + s) * 8 + (d & 7)] = w;
+    else
+      base[(int64_t)s * p.D + d] = w;
   }
   if (p.t_end) {
     __syncthreads();
@@ -88,8 +94,9 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
   DV_TRY(check_cache(c, "cache"));
   if (c->elem_bytes != 2) return fail(DV_ENOTSUP, "dvt_fill supports 16-bit words only");
   dv_region whole{c->layer_begin, c->layer_begin + c->n_layers, c->req_begin,
-                  c->req_begin + c->n_reqs, 0, c->max_seq};
-  const dv_region* r = region ? region : &whole;
+                  c->req_begin + c->n_reqs, 0, c->max_seq, 0, 0};
+  const dv_region rr = resolve_heads(region ? region : &whole, c);
+  const dv_region* r = &rr;
   DV_TRY(check_region_shape(r));
   DV_TRY(check_cache_holds(c, r, "cache"));
   if (kind == DVT_FILL_UID && !box) return fail(DV_EINVAL, "uid fill needs a box");
@@ -101,11 +108,15 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
   p.s_l = p.s_r * c->n_reqs;
   p.lb = c->layer_begin;
   p.rb = c->req_begin;
+  p.hb = c->head_begin;
   p.l0 = r->layer_begin;
   p.r0 = r->req_begin;
+  p.h0 = r->head_begin;
   p.s0 = r->pos_begin;
   p.nR = r->req_end - r->req_begin;
-  p.H = c->n_heads;
+  p.H = r->head_end - r->head_begin;
+  p.S = c->max_seq;
+  p.ft6d = c->layout == DV_LAYOUT_FT6D;
   p.n = r->pos_end - r->pos_begin;
   p.D = c->head_dim;
   p.kind = kind;

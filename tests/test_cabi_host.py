@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
     assert set(dv.exported_symbols()) == syms
-    assert dv.dv_abi_version() == 1
+    assert dv.dv_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu():
@@ -118,3 +118,21 @@ def test_route_c3_and_errors_match_golden(golden):
     with pytest.raises(dv.DVError, match="max_seq 16"):
         dv.dv_route(s, dv.Setup([0, 8], [0, 4], 16), dv.region(0, 8, 0, 4, 0, 17), 2, 8, 2)
     assert dv.dv_route(s, s, dv.region(0, 8, 0, 4, 5, 5), 2, 8, 2) == []
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_route_with_tp_matches_oracle(seed):
+    rng = random.Random(4000 + seed)
+    L, R, Hn = rng.randint(1, 30), rng.randint(1, 12), rng.randint(1, 16)
+    sl = _bounds(rng, 0, L, rng.randint(1, min(L, 4)))
+    dl = _bounds(rng, 0, L, rng.randint(1, min(L, 4)))
+    sr = _bounds(rng, 0, R, rng.randint(1, min(R, 3)))
+    dr = _bounds(rng, 0, R, rng.randint(1, min(R, 3)))
+    sh = _bounds(rng, 0, Hn, rng.randint(1, min(Hn, 4)))
+    dh = _bounds(rng, 0, Hn, rng.randint(1, min(Hn, 4)))
+    h0 = rng.randint(0, Hn - 1); h1 = rng.randint(h0 + 1, Hn)
+    reg = (0, L, 0, R, 2, 9) + ((h0, h1) if rng.random() < 0.5 else (0, 0))
+    exp = ok.route(ok.Setup(sl, sr, 16, sh), ok.Setup(dl, dr, 16, dh), reg, Hn, 64, 2)
+    got = dv.dv_route(dv.Setup(sl, sr, 16, sh), dv.Setup(dl, dr, 16, dh), dv.region(*reg), Hn, 64, 2)
+    F = FIELDS + ["src_tp", "dst_tp", "head_begin", "head_end"]
+    assert [[getattr(p, f) for f in F] for p in got] == [[getattr(p, f) for f in F] for p in exp]

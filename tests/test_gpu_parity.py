@@ -575,3 +575,110 @@ def test_swap_log_form_round_trip():
     assert np.array_equal(to_np(sk)[:, :, :, :p + T], K[:, :, :, :p + T])
     assert np.array_equal(to_np(sv)[:, :, :, :p + T], V[:, :, :, :p + T])
     assert np.all(to_np(sk)[:, :, :, p + T:] == kvgen.SENTINEL)
+
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-1: FasterTransformer 6-D key layout;  NEXT-4: tensor-parallel head re-split
+# ------------------------------------------------------------------------------------------------
+def _mk(K, V, lb, rb, layout, pinned=False, hb=0):
+    """Device (or pinned) cache from logical K, V in the requested layout + its oracle twin."""
+    S, D = K.shape[3], K.shape[4]
+    Kp = kvgen.as_ft6d_key(K) if layout == ok.LAYOUT_FT6D else K
+    k = to_pinned(Kp) if pinned else to_dev(Kp)
+    v = to_pinned(V) if pinned else to_dev(V)
+    o = ok.Cache(Kp.copy(), V.copy(), lb, rb, K.shape[2], S, D, layout, hb)
+    return k, v, dv.cache(k, v, lb, rb, head_begin=hb), o
+
+
+def test_device_fill_ft6d_with_head_offset():
+    L, B, H, S, D, hb = 2, 3, 4, 12, 64, 5
+    K, V = kvgen.kv5d_cache("hash", 3, L, 1, B, H, S, D, seed=17, head_begin=hb, valid_pos=(1, 10))
+    k = torch.empty(kvgen.as_ft6d_key(K).shape, dtype=torch.int16, device="cuda")
+    v = torch.empty(V.shape, dtype=torch.int16, device="cuda")
+    dv.dvt_fill(dv.cache(k, v, 3, 1, head_begin=hb), dv.DVT_FILL_HASH, seed=17, valid=(1, 10))
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(k), kvgen.as_ft6d_key(K)) and np.array_equal(to_np(v), V)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("layouts", [(ok.LAYOUT_FT6D, ok.LAYOUT_KV5D), (ok.LAYOUT_KV5D, ok.LAYOUT_FT6D),
+                                     (ok.LAYOUT_FT6D, ok.LAYOUT_FT6D)])
+@pytest.mark.parametrize("xfer", XFERS)
+def test_ft6d_pack_unpack_remap(seed, layouts, xfer):
+    """Pack from a cache in one layout, unpack into a cache in the other (and remap directly),
+    with head sub-ranges; == the oracle (whose FT6D offset function is pinned on CPU)."""
+    rng = random.Random(900 + seed)
+    H, D = rng.choice([2, 3, 5]), rng.choice([16, 64, 128])
+    nL, nR, S = rng.randint(1, 3), rng.randint(1, 3), rng.randint(2, 40)
+    hb = rng.randint(0, 4)
+    s0 = rng.randint(0, S - 1); s1 = rng.randint(s0 + 1, S)
+    h0 = hb + rng.randint(0, H - 1); h1 = rng.randint(h0 + 1, hb + H)
+    reg = (0, nL, 0, nR, s0, s1, h0, h1)
+    K, V = kvgen.kv5d_cache("hash", 0, nL, 0, nR, H, S, D, seed=seed, head_begin=hb)
+    k, v, c, o = _mk(K, V, 0, 0, layouts[0], hb=hb)
+    exp = ok.pack(o, reg)
+    buf = sentinel_like((exp.size,), pinned=(xfer == dv.DV_XFER_STAGED))
+    dv.dv_scatter(ctx(), c, dv.region(*reg), dv.endpoint_of(buf), xfer=xfer)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(buf), exp)
+    S2 = s1 + rng.randint(0, 5)
+    Ks, Vs = kvgen.sentinel_cache(nL, nR, H, S2, D)
+    dk, dvv, dc, do = _mk(Ks, Vs, 0, 0, layouts[1], hb=hb)
+    dv.dv_gather(ctx(), dv.endpoint_of(buf), 0, dc, dv.region(*reg), xfer=xfer)
+    torch.cuda.synchronize()
+    ok.unpack(do, reg, exp)
+    assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
+    ek, ev, ec, eo = _mk(Ks, Vs, 0, 0, layouts[1], hb=hb)
+    dv.dv_remap(ctx(), c, ec, dv.region(*reg))
+    torch.cuda.synchronize()
+    ok.remap(o, eo, reg)
+    assert np.array_equal(to_np(ek), eo.K) and np.array_equal(to_np(ev), eo.V)
+
+
+@pytest.mark.parametrize("sh,th", [([0, 6], [0, 3, 6]), ([0, 2, 4, 6], [0, 3, 6]), ([0, 3, 6], [0, 1, 2, 3, 4, 5, 6])])
+@pytest.mark.parametrize("direct", [False, True])
+def test_tp_resplit_stream_out_in(sh, th, direct):
+    """NEXT-4: prompt and token pipelines with different TP degrees (and layer splits): every
+    prompt block (stage, micro, tp) streams out, every token block streams in; == oracle.stream."""
+    H, D, p, S, seed = 6, 16, 7, 12, 43
+    ps, ts = ok.Setup([0, 2, 4], [0, 2], S, sh), ok.Setup([0, 3, 4], [0, 2], S, th)
+    dps, dts = dv.Setup([0, 2, 4], [0, 2], S, sh), dv.Setup([0, 3, 4], [0, 2], S, th)
+    prompt, oprompt, token, otoken = {}, {}, {}, {}
+    for i in range(ps.n_stages):
+        for t in range(ps.n_tp):
+            a, b, h0, h1 = ps.layer_bounds[i], ps.layer_bounds[i + 1], sh[t], sh[t + 1]
+            K, V = kvgen.kv5d_cache("hash", a, b - a, 0, 2, h1 - h0, S, D, seed=seed, head_begin=h0)
+            k, v, c, o = _mk(K, V, a, 0, ok.LAYOUT_KV5D, hb=h0)
+            prompt[(i, 0, t)] = (k, v, c)
+            oprompt[(i, 0, t)] = o
+    for j in range(ts.n_stages):
+        for t in range(ts.n_tp):
+            a, b, h0, h1 = ts.layer_bounds[j], ts.layer_bounds[j + 1], th[t], th[t + 1]
+            Ks, Vs = kvgen.sentinel_cache(b - a, 2, h1 - h0, S, D)
+            k, v, c, o = _mk(Ks, Vs, a, 0, ok.LAYOUT_KV5D, hb=h0)
+            token[(j, 0, t)] = (k, v, c)
+            otoken[(j, 0, t)] = o
+    reg = dv.region(0, 4, 0, 2, 0, p)
+    cx = ctx()
+    keys_t = sorted(token, key=lambda x: dts.flat(*x))
+    if direct:
+        dcs = [token[kk][2] for kk in keys_t]
+        for (i, u, t), (_, _, c) in prompt.items():
+            dv.dv_stream_out_direct(cx, c, reg, dps, i, u, dts, dcs, None, seq=1, my_tp=t)
+    else:
+        eps, keep = [], []
+        for kk in keys_t:
+            c = token[kk][2]
+            buf = sentinel_like((c.n_layers * 2 * c.n_heads * p * D * 2,))
+            fl = flags(ps.n_stages * ps.n_micro * ps.n_tp)
+            keep += [buf, fl]          # endpoints hold raw pointers: keep the tensors alive
+            eps.append(dv.endpoint_of(buf, fl))
+        for (i, u, t), (_, _, c) in prompt.items():
+            dv.dv_stream_out(cx, c, reg, dps, i, u, dts, eps, seq=1, my_tp=t)
+        for n_, kk in enumerate(keys_t):
+            dv.dv_stream_in(cx, token[kk][2], reg, dps, dts, kk[0], kk[1], eps[n_], 1, my_tp=kk[2])
+    torch.cuda.synchronize()
+    ok.stream(oprompt, ps, otoken, ts, (0, 4, 0, 2, 0, p))
+    for kk, (k, v, _) in token.items():
+        assert np.array_equal(to_np(k), otoken[kk].K) and np.array_equal(to_np(v), otoken[kk].V), kk

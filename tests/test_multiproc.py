@@ -1,0 +1,75 @@
+"""Multi-process paths (one process per rank, torch.distributed plumbing).
+
+* `-m "not gpu"`: world_size 2 over gloo on CPU -- ranks route independently and must agree.
+* `-m gpu`: 5 processes on ONE GPU (the only one available to this build): prompt ranks map the
+  token ranks' inboxes/caches through real cross-process CUDA IPC (dv_ipc_export/open) and stream
+  into them with seq flags; token ranks wait/unpack; results equal kvgen's single-machine KV.
+  On an 8-GPU box the same code path crosses NVLink instead of HBM.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(mode, world, timeout=240):
+    port = _free_port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), LOCAL_RANK="0")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), mode], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    outs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=timeout)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        outs.append((p.returncode, out))
+    for r, (rc, out) in enumerate(outs):
+        assert rc == 0 and f"OK {r}" in out, f"rank {r} rc={rc}\n{out[-3000:]}"
+
+
+def test_route_agreement_gloo_world2():
+    _run("route", 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["ipc", "direct"])
+def test_cross_process_ipc_stream(mode):
+    # 2 prompt blocks (stages [0,6),[6,12) x 1 microbatch) + 3x2 token blocks -> 8 ranks
+    _run(mode, 2 + 6)
+
+
+@pytest.mark.gpu
+def test_bench_multirank_launch_path():
+    """bench.py under torchrun with 2 ranks (both on the one available GPU, gloo plumbing): the
+    weak-scaling path runs, takes the max over ranks and rank 0 prints one JSON line."""
+    import json
+    port = _free_port()
+    env = dict(os.environ, DV_BENCH_SAME_DEVICE="1")
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+                        "--gpus", "2", "--steps", "20", "--warmup", "3", "--no-extras", "--no-cpu-baseline",
+                        "--dist-backend", "gloo"], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] == 20

@@ -469,3 +469,82 @@ def test_log_form_swap_round_trip_equals_definition():
     unpack_chunks(dst2, (4, 4 + L, 2, 2 + B, 0, 2), log2, 4, 3, mode="brute")
     filled = ~np.all(dst2.K == kvgen.SENTINEL, axis=(0, 1, 2, 4))
     assert np.flatnonzero(filled).tolist() == [0, 1, 3, 4, 6, 7, 9, 10]
+
+
+# ---------------------------------------------------------------------------------------------
+# tensor-parallel head split (NEXT-4; "tensor parallelism inside a stage")
+# ---------------------------------------------------------------------------------------------
+def test_route_tp_2_to_4_splits_each_head_group_in_two():
+    """Same stages, TP 2 -> 4 over 8 heads: each source head group [0,4), [4,8) splits into two
+    destination groups (the head analogue of SPEC.md:376's depth split)."""
+    src = Setup([0, 4], [0, 2], 16, head_bounds=[0, 4, 8])
+    dst = Setup([0, 4], [0, 2], 16, head_bounds=[0, 2, 4, 6, 8])
+    ps = route(src, dst, (0, 4, 0, 2, 0, 5), 8, 16, 2)
+    assert [(p.src_tp, p.dst_tp, p.head_begin, p.head_end) for p in ps] == \
+        [(0, 0, 0, 2), (0, 1, 2, 4), (1, 2, 4, 6), (1, 3, 6, 8)]
+    assert all(p.bytes == 2 * 4 * 2 * 5 * 2 * 16 * 2 for p in ps)
+    assert [p.src_wire_off for p in ps] == [0, ps[0].bytes, 0, ps[2].bytes]
+    with pytest.raises(ValueError):                       # one side split, the other not
+        route(src, Setup([0, 4], [0, 2], 16), (0, 4, 0, 2, 0, 5), 8, 16, 2)
+    with pytest.raises(MappingError):                     # heads not held
+        route(src, dst, (0, 4, 0, 2, 0, 5, 0, 9), 8, 16, 2)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_route_tp_brute_force_coverage(seed):
+    rng = random.Random(700 + seed)
+    L, R, Hn = rng.randint(1, 6), rng.randint(1, 5), rng.randint(1, 9)
+    mk = lambda n, k: _random_bounds(rng, 0, n, rng.randint(1, min(n, k)))
+    src = Setup(mk(L, 3), mk(R, 2), 32, head_bounds=mk(Hn, 4))
+    dst = Setup(mk(L, 3), mk(R, 2), 32, head_bounds=mk(Hn, 4))
+    ps = route(src, dst, (0, L, 0, R, 3, 7), Hn, 8, 2)
+    for l in range(L):
+        for r in range(R):
+            for h in range(Hn):
+                cov = [p for p in ps if p.layer_begin <= l < p.layer_end and p.req_begin <= r < p.req_end
+                       and p.head_begin <= h < p.head_end]
+                assert len(cov) == 1
+                p = cov[0]
+                assert src.head_bounds[p.src_tp] <= h < src.head_bounds[p.src_tp + 1]
+                assert dst.head_bounds[p.dst_tp] <= h < dst.head_bounds[p.dst_tp + 1]
+    assert sum(p.bytes for p in ps) == 2 * L * R * 4 * Hn * 8 * 2
+
+
+@pytest.mark.parametrize("sh,th", [([0, 6], [0, 3, 6]), ([0, 2, 4, 6], [0, 3, 6]), ([0, 3, 6], [0, 1, 2, 3, 4, 5, 6])])
+def test_disaggregation_with_tp_resplit_equals_definition(sh, th):
+    """Prompt pipeline TP degree != token pipeline TP degree (NEXT-4): every token shard equals
+    kvgen's words for its own layers, requests and HEADS."""
+    H, D, p, S, seed = 6, 8, 5, 9, 41
+    ps_, ts_ = Setup([0, 2, 4], [0, 2], S, head_bounds=sh), Setup([0, 3, 4], [0, 2], S, head_bounds=th)
+    prompt, token = {}, {}
+    for i in range(ps_.n_stages):
+        for t in range(ps_.n_tp):
+            a, b, h0, h1 = ps_.layer_bounds[i], ps_.layer_bounds[i + 1], sh[t], sh[t + 1]
+            K, V = kvgen.kv5d_cache("hash", a, b - a, 0, 2, h1 - h0, S, D, seed=seed, head_begin=h0)
+            prompt[(i, 0, t)] = Cache(K, V, a, 0, h1 - h0, S, D, head_begin=h0)
+    for j in range(ts_.n_stages):
+        for t in range(ts_.n_tp):
+            a, b, h0, h1 = ts_.layer_bounds[j], ts_.layer_bounds[j + 1], th[t], th[t + 1]
+            token[(j, 0, t)] = Cache(*kvgen.sentinel_cache(b - a, 2, h1 - h0, S, D), a, 0, h1 - h0, S, D,
+                                     head_begin=h0)
+    stream(prompt, ps_, token, ts_, (0, 4, 0, 2, 0, p))
+    for (j, _, t), c in token.items():
+        exp = kvgen.kv5d_cache("hash", c.layer_begin, c.n_layers, 0, 2, c.n_heads, S, D, seed=seed,
+                               head_begin=c.head_begin)
+        for kv in (0, 1):
+            assert np.array_equal(c.arr(kv)[:, :, :, :p], exp[kv][:, :, :, :p])
+            assert np.all(c.arr(kv)[:, :, :, p:] == kvgen.SENTINEL)
+
+
+def test_ft6d_key_layout_matches_fastertransformer_indexing():
+    """NEXT-1: in the 6-D key layout word (l,r,h,s,d) sits at [l][r][h][d//x][s][d%x], x = 16/e
+    (16-byte packets); the oracle's FT6D cache agrees element by element with that formula."""
+    L, B, H, S, D = 2, 2, 3, 6, 16
+    K, V = kvgen.kv5d_cache("uid", 0, L, 0, B, H, S, D, box=(L, B, H, S, D))
+    K6 = kvgen.as_ft6d_key(K)
+    c = Cache(K6, V, 0, 0, H, S, D, layout=LAYOUT_FT6D)
+    for l, r, h, s_, d in itertools.product(range(L), range(B), range(H), range(S), range(D)):
+        assert K6[l, r, h, d // 8, s_, d % 8] == K[l, r, h, s_, d]
+        assert c.K[c.word_index(0, l, r, h, s_, d)] == K[l, r, h, s_, d]
+    assert np.array_equal(pack(c, (0, L, 0, B, 1, 5), "brute"),
+                          pack(Cache(K, V, 0, 0, H, S, D), (0, L, 0, B, 1, 5), "vector"))
