@@ -169,7 +169,8 @@ typedef struct dv_ctx dv_ctx;
 typedef struct dv_config {
   uint64_t staging_bytes; /* device staging pool for DV_XFER_STAGED (0 = 256 MiB)                */
   int32_t max_ctas;       /* cap on CTAs per copy kernel (0 = 148 * 8)                           */
-  int32_t reserved;
+  int32_t host_ctas;      /* cap when the copy reads or writes pinned host memory (0 = 16): PCIe is
+                             saturated by 8 SMs, the rest stay free for compute (DESIGN.md NEXT-2) */
 } dv_config;
 
 /* ---- errors ------------------------------------------------------------------------------ */

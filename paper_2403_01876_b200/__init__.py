@@ -60,7 +60,7 @@ class dv_endpoint(C.Structure):
 
 
 class dv_config(C.Structure):
-    _fields_ = [("staging_bytes", C.c_uint64), ("max_ctas", C.c_int32), ("reserved", C.c_int32)]
+    _fields_ = [("staging_bytes", C.c_uint64), ("max_ctas", C.c_int32), ("host_ctas", C.c_int32)]
 
 
 class dv_ipc_blob(C.Structure):
@@ -302,9 +302,9 @@ def dv_route(src: Setup, dst: Setup, reg: dv_region, n_heads, head_dim, elem_byt
 class Context:
     """Owns a dv_ctx* (one per process and device)."""
 
-    def __init__(self, device: int = 0, staging_bytes: int = 0, max_ctas: int = 0):
+    def __init__(self, device: int = 0, staging_bytes: int = 0, max_ctas: int = 0, host_ctas: int = 0):
         h = C.c_void_p()
-        cfg = dv_config(staging_bytes, max_ctas, 0)
+        cfg = dv_config(staging_bytes, max_ctas, host_ctas)
         _call("dv_create", device, C.byref(cfg), C.byref(h))
         self.h = h
         self.device = device
@@ -321,8 +321,8 @@ class Context:
             pass
 
 
-def dv_create(device=0, staging_bytes=0, max_ctas=0) -> Context:
-    return Context(device, staging_bytes, max_ctas)
+def dv_create(device=0, staging_bytes=0, max_ctas=0, host_ctas=0) -> Context:
+    return Context(device, staging_bytes, max_ctas, host_ctas)
 
 
 def dv_destroy(ctx: Context):

@@ -332,14 +332,14 @@ static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
 // from its last CTA) or, with DV_PUBLISH_STREAMOP, by a stream memory operation after it.
 static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv_endpoint* ep,
                                 int32_t slot, uint64_t seq, bool use_flag, uint32_t xfer,
-                                cudaStream_t st) {
+                                cudaStream_t st, int ctas) {
   const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
   const Release none{nullptr, 0, nullptr};
   for (int q = 0; q < np; ++q) {
     const bool last = q == np - 1;
     DV_TRY(launch_copy(p[q], 0, p[q].runs(),
                        (last && !streamop) ? ticket_release(ctx, ep, slot, seq, use_flag) : none,
-                       ctx->max_ctas, st));
+                       ctas, st));
   }
   if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
   return DV_OK;
@@ -513,7 +513,9 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
       p[0] = CopyPlan{};
       np = 1;  // empty plan: still publishes the flag in stream order
     }
-    return launch_publish(ctx, p, np, op.dst, op.slot, op.seq, use_flag, op.xfer, st);
+    return launch_publish(ctx, p, np, op.dst, op.slot, op.seq, use_flag, op.xfer, st,
+                          (op.dst->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas
+                                                                         : ctx->max_ctas);
   }
   DV_TRY(staged_pack(ctx, c, reg, wire, st));
   if (use_flag) DV_TRY(stream_signal(op.dst, op.slot, op.seq, st));
@@ -555,8 +557,9 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   CopyPlan p[2];
   const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  const int ctas = (op.src->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas : ctx->max_ctas;
   for (int q = 0; q < np; ++q)
-    DV_TRY(launch_copy(p[q], 0, p[q].runs(), Release{nullptr, 0, nullptr}, ctx->max_ctas, st));
+    DV_TRY(launch_copy(p[q], 0, p[q].runs(), Release{nullptr, 0, nullptr}, ctas, st));
   return DV_OK;
 }
 
@@ -627,7 +630,9 @@ static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
     np = build_plans(sv, dv_, &reg, row, ORDER_KV_OUTER, Outer{}, p);
     if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
   }
-  return launch_publish(ctx, p, np, op.signal, op.slot, op.seq, use_flag, op.xfer, st);
+  return launch_publish(ctx, p, np, op.signal, op.slot, op.seq, use_flag, op.xfer, st,
+                        (op.src->device < 0 || op.dst->device < 0) ? ctx->host_ctas
+                                                                   : ctx->max_ctas);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -672,6 +677,7 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
   c->device = device;
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   c->max_ctas = (cfg && cfg->max_ctas > 0) ? cfg->max_ctas : c->sm_count * 8;
+  c->host_ctas = std::min(c->max_ctas, (cfg && cfg->host_ctas > 0) ? cfg->host_ctas : 16);
   uint64_t stg = (cfg && cfg->staging_bytes) ? cfg->staging_bytes : (256ull << 20);
   dv_status s = c->staging.init(device, stg);
   if (s != DV_OK) {
@@ -819,7 +825,8 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
       p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
-    return launch_publish(ctx, &p, 1, dst, flag_slot, seq, use_flag, xfer, st);
+    return launch_publish(ctx, &p, 1, dst, flag_slot, seq, use_flag, xfer, st,
+                          dst->kind == DV_EP_HOST ? ctx->host_ctas : ctx->max_ctas);
   }
   if (bytes) DV_DMA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st));
   if (use_flag) DV_TRY(stream_signal(dst, flag_slot, seq, st));
@@ -848,7 +855,8 @@ dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_
       p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
-    return launch_copy(p, 0, p.runs(), Release{nullptr, 0, nullptr}, ctx->max_ctas, st);
+    return launch_copy(p, 0, p.runs(), Release{nullptr, 0, nullptr},
+                       src->kind == DV_EP_HOST ? ctx->host_ctas : ctx->max_ctas, st);
   }
   if (bytes) DV_DMA(cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDefault, st));
   return DV_OK;
@@ -929,7 +937,8 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
       if (r < 0) return fail(DV_ENOTSUP, "copy not expressible");
       np += 1;
     }
-    for (int q = 0; q < np; ++q) DV_TRY(launch_copy(p[q], 0, p[q].runs(), none, ctx->max_ctas, st));
+    const int ctas = (base == wire && src->kind == DV_EP_HOST) ? ctx->host_ctas : ctx->max_ctas;
+    for (int q = 0; q < np; ++q) DV_TRY(launch_copy(p[q], 0, p[q].runs(), none, ctas, st));
     return DV_OK;
   };
   if (mode == DV_XFER_FUSED) return unpack_group(wire, 0, n_chunks);

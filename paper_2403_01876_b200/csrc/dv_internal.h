@@ -123,6 +123,7 @@ class Staging {
 struct dv_ctx {
   int device;
   int max_ctas;
+  int host_ctas;  // CTA cap for copies touching pinned host memory
   int sm_count;
   dv::Staging staging;
   unsigned int* tickets;  // device array of kTickets counters

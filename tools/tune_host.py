@@ -80,6 +80,31 @@ def child():
         return f
 
     F, G = dv.DV_XFER_FUSED, dv.DV_XFER_STAGED
+    if os.environ.get("DV_SWEEP_CTAS"):
+        pb = torch.empty(LAYER * P // 2, dtype=torch.int16, pin_memory=True)
+        pep = dv.endpoint_of(pb)
+        for mc in (8, 16, 32, 64, 148, 296, 1184):
+            cx = dv.dv_create(0, max_ctas=mc)
+            def f(cx=cx):
+                cnt[0] += 1
+                q = P + cnt[0] % 1000
+                dv.dv_scatter(cx, c, dv.region(0, L, 0, B, q, q + 1), dv.endpoint_of(log, fl), (cnt[0] % 8) * STEP,
+                              flag_slot=0, seq=cnt[0], xfer=F, stream=sp)
+            out[f"ctas{mc}_step_host_us"] = loop(f, 200)
+            def g(cx=cx):
+                cnt[0] += 1
+                l_ = cnt[0] % L
+                dv.dv_scatter(cx, c, dv.region(l_, l_ + 1, 0, B, 0, P), pep, 0, xfer=F, stream=sp)
+            out[f"ctas{mc}_prompt_host_gbs"] = LAYER * P / loop(g, 5) / 1e3
+            def h(cx=cx):
+                cnt[0] += 1
+                q = P + cnt[0] % 1000
+                dv.dv_gather(cx, dv.endpoint_of(log, fl), (cnt[0] % 8) * STEP, c, dv.region(0, L, 0, B, q, q + 1),
+                             xfer=F, stream=sp)
+            out[f"ctas{mc}_gather_host_fused_us"] = loop(h, 200)
+            cx.close()
+        print(json.dumps(out), flush=True)
+        return
     out["step_host_fused_noflag_us"] = loop(tok(log, None, F), 300)
     out["step_host_fused_flag_us"] = loop(tok(log, fl, F), 300)
     out["step_host_fused_flag_events_us"] = loop(tok(log, fl, F), 300, per_event=True)
