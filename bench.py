@@ -284,6 +284,25 @@ def _spot_check(wire, q, seed):
     return {"samples": n, "mismatches": bad}
 
 
+def sample_region(k, v, layer_begin, req_begin, n_heads, max_seq, head_dim, region, seed, n=20000):
+    """Sampled parity of a KV5D cache region against kvgen's definition (words at global coords)."""
+    import numpy as np
+    import torch
+
+    import kvgen
+    rng = np.random.default_rng(7)
+    l0, l1, r0, r1, s0, s1 = region
+    nR = k.shape[1]
+    l = rng.integers(l0, l1, n); r = rng.integers(r0, r1, n); s = rng.integers(s0, s1, n)
+    h = rng.integers(0, n_heads, n); d = rng.integers(0, head_dim, n); kv = rng.integers(0, 2, n)
+    exp = kvgen.hash_words(kv, l, r, h, s, d, seed)
+    idx = ((((l - layer_begin) * nR + (r - req_begin)) * n_heads + h) * max_seq + s) * head_dim + d
+    it = torch.from_numpy(idx.astype(np.int64)).to(k.device)
+    gk = k.view(-1)[it].cpu().numpy().view(np.uint16)
+    gv = v.view(-1)[it].cpu().numpy().view(np.uint16)
+    return int(np.sum(np.where(kv == 0, gk, gv) != exp))
+
+
 def _time(fn, stream, reps, warm=2):
     import torch
     for _ in range(warm):
@@ -520,14 +539,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+                    help="c2 (default, BASELINE configs[1]): token steps -> pinned host; "
+                         "c3: prompt->token disaggregation over NVLink; c5: ring replication over NVLink")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
         args.cpu_baseline = False
     if args.impl == "reference":
         run_reference(args)
-    else:
+    elif args.workload == "c2":
         run_ours(args)
+    else:
+        from tools import bench_peer
+        (bench_peer.run_c3 if args.workload == "c3" else bench_peer.run_c5)(args, sys.modules[__name__])
 
 
 if __name__ == "__main__":

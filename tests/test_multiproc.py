@@ -73,3 +73,26 @@ def test_bench_multirank_launch_path():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] == 20
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload,world", [("c5", 1), ("c5", 2), ("c3", 1), ("c3", 2)])
+def test_bench_peer_workloads(workload, world):
+    """bench.py --workload c3/c5 (the NVLink peer paths: CUDA-IPC-mapped destinations, seq flags):
+    loopback at N=1, and 2 ranks (both on the one available GPU, gloo plumbing) at N=2; the
+    sampled parity of the delivered KV must be clean."""
+    import json
+    root = os.path.dirname(HERE)
+    env = dict(os.environ, DV_BENCH_SAME_DEVICE="1")
+    args = ["--workload", workload, "--steps", "3", "--warmup", "3", "--dist-backend", "gloo", "--gpus", str(world)]
+    if world == 1:
+        cmd = [sys.executable, os.path.join(root, "bench.py")] + args
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py")] + args
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["value"] > 0 and d["parity_spot_check"]["mismatches"] == 0
