@@ -419,6 +419,36 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     torch.cuda.synchronize()
     ex["token_layer_latency"] = lat
 
+    # CUDA graph of one token step's 40 per-layer stream-outs (captured once, replayed per token
+    # with a device-side step counter): host cost per step and device time per step
+    d_step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        with torch.cuda.graph(g, stream=gs):
+            for layer in range(L):
+                dv.dv_scatter_dyn(ctx, cache, dv.region(layer, layer + 1, 0, B, P, P + 1), lep, layer * LAYER_BYTES,
+                                  0, d_step.data_ptr(), S - P - 1, flag_slot=0, seq=4 * 10 ** 8)
+    torch.cuda.synchronize()
+    reps = 200
+    with torch.cuda.stream(gs):
+        for i in range(5):
+            d_step.fill_(i)
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(gs)
+        for i in range(reps):
+            d_step.fill_(i % (S - P))
+            g.replay()
+        b.record(gs)
+        t_host = time.perf_counter() - t0
+        torch.cuda.synchronize()
+    ex["graph_token_step_40_layer_calls"] = {
+        "host_us_per_step": t_host / reps * 1e6, "gpu_us_per_step": a.elapsed_time(b) / reps * 1e3,
+        "eager_host_us_per_step": lat["host_enqueue_us_per_call"] * L}
+
     # prompt layer (163.8 MB) stream-out: fused vs staged, and HBM pack
     pbuf = torch.empty(PROMPT_LAYER_BYTES // 2, dtype=torch.int16, pin_memory=True)
     pep = dv.endpoint_of(pbuf)

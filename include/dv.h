@@ -259,6 +259,21 @@ DV_API dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
                    const dv_endpoint* signal, int32_t flag_slot, uint64_t seq, uint32_t xfer,
                    void* stream);
 
+/* ---- CUDA-graph forms (capture the per-token path once, replay per token) ----
+ * The kernel reads a step k from device memory `d_step` when it runs, shifts the region's
+ * positions by k (the token step t writes position p+t-1, reading Q4), the destination by k
+ * positions (remap) or k*dst_step_bytes (scatter into a log), and publishes seq + k. Everything
+ * is validated for every k in [0, max_step] at enqueue; at run time a k outside that range makes
+ * the launch a no-op (nothing moves, nothing is published). Always the FUSED transfer. */
+DV_API dv_status dv_scatter_dyn(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                                const dv_endpoint* dst, uint64_t dst_off, uint64_t dst_step_bytes,
+                                int32_t flag_slot, uint64_t seq, const int32_t* d_step,
+                                int32_t max_step, void* stream);
+DV_API dv_status dv_remap_dyn(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
+                              const dv_region* region, const dv_endpoint* signal,
+                              int32_t flag_slot, uint64_t seq, const int32_t* d_step,
+                              int32_t max_step, void* stream);
+
 /* ---- level 1: stream_out / stream_in ------------------------------ */
 /* Sender side. `src` is the cache of source block (my_stage, my_micro) of `src_setup`. Routes
  * `region`; for every piece leaving this block, scatters it into inboxes[dst block flat index] at

@@ -106,6 +106,10 @@ _SIGS = {
                                    P(dv_cache), P(dv_region), C.c_int32, C.c_int32, C.c_uint32, C.c_void_p]),
     "dv_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint),
                            C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
+    "dv_scatter_dyn": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_endpoint), C.c_uint64, C.c_uint64,
+                                 C.c_int32, C.c_uint64, C.c_void_p, C.c_int32, C.c_void_p]),
+    "dv_remap_dyn": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint), C.c_int32,
+                               C.c_uint64, C.c_void_p, C.c_int32, C.c_void_p]),
     "dv_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
                                 C.c_int32, C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32,
                                 C.c_uint64, C.c_uint32, C.c_void_p]),
@@ -399,6 +403,18 @@ def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpo
              seq=0, xfer=0, stream=None):
     _call("dv_remap", ctx.h, C.byref(src), C.byref(dst), C.byref(reg), _ref(signal), flag_slot, seq,
           xfer, _stream(stream))
+
+
+def dv_scatter_dyn(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off, dst_step_bytes, d_step_ptr,
+                   max_step, flag_slot=-1, seq=0, stream=None):
+    _call("dv_scatter_dyn", ctx.h, C.byref(src), C.byref(reg), C.byref(dst), dst_off, dst_step_bytes, flag_slot,
+          seq, C.c_void_p(d_step_ptr), max_step, _stream(stream))
+
+
+def dv_remap_dyn(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, d_step_ptr, max_step, signal: dv_endpoint = None,
+                 flag_slot=-1, seq=0, stream=None):
+    _call("dv_remap_dyn", ctx.h, C.byref(src), C.byref(dst), C.byref(reg), _ref(signal), flag_slot, seq,
+          C.c_void_p(d_step_ptr), max_step, _stream(stream))
 
 
 # The level-1 wrappers take my_tp as a keyword (default 0) after the C positional arguments.

@@ -976,6 +976,85 @@ dv_status dv_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const 
   return remap_run(ctx, op, (cudaStream_t)stream);
 }
 
+// ---- CUDA-graph forms --------------------------------------------------------------------------
+// dst_step < 0: the destination is a cache and moves by k positions; else by k*dst_step bytes.
+static void set_dyn(CopyPlan* p, int np, const TView* sv, const TView* dv_, int64_t dst_step,
+                    const int32_t* d, int32_t max_step) {
+  for (int q = 0; q < np; ++q) {
+    p[q].dyn = d;
+    p[q].dyn_max = max_step;
+    p[q].dyn_ss = sv[np == 1 ? 0 : q].st[DS];
+    p[q].dyn_ds = dst_step >= 0 ? dst_step : dv_[np == 1 ? 0 : q].st[DS];
+  }
+}
+
+static dv_region shift_pos(const dv_region& r, int32_t k) {
+  dv_region x = r;
+  x.pos_begin += k;
+  x.pos_end += k;
+  return x;
+}
+
+dv_status dv_scatter_dyn(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                         const dv_endpoint* dst, uint64_t dst_off, uint64_t dst_step_bytes,
+                         int32_t flag_slot, uint64_t seq, const int32_t* d_step, int32_t max_step,
+                         void* stream) {
+  DV_TRY(check_ctx(ctx));
+  if (!region || !d_step) return fail(DV_EINVAL, "NULL region or d_step");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  if (dst_step_bytes % 16) return fail(DV_EALIGN, "dst_step_bytes not a multiple of 16");
+  DV_TRY(check_cache(src, "source"));
+  DV_TRY(check_region_shape(region));
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  DV_TRY(check_cache_holds(src, &reg, "source"));
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  const uint64_t bytes = region_bytes(&reg, src);
+  DV_TRY(check_ep(dst, dst_off, bytes + (uint64_t)max_step * dst_step_bytes, flag_slot, true,
+                  "destination"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  DV_ON_DEVICE(ctx->device);
+  const int64_t row = row_bytes(src);
+  uint8_t* wire = (uint8_t*)dst->base + dst_off;
+  TView sv[2] = {cache_view(src, 0, &reg), cache_view(src, 1, &reg)};
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  CopyPlan p[2];
+  const int np = build_plans(sv, wv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  set_dyn(p, np, sv, wv, (int64_t)dst_step_bytes, d_step, max_step);
+  return launch_publish(ctx, p, np, dst, flag_slot, seq, flag_slot >= 0, DV_XFER_FUSED,
+                        (cudaStream_t)stream,
+                        (dst->kind == DV_EP_HOST || src->device < 0) ? ctx->host_ctas : ctx->max_ctas);
+}
+
+dv_status dv_remap_dyn(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
+                       const dv_region* region, const dv_endpoint* signal, int32_t flag_slot,
+                       uint64_t seq, const int32_t* d_step, int32_t max_step, void* stream) {
+  if (!region || !d_step) return fail(DV_EINVAL, "NULL region or d_step");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  RemapOp op{src, dst, *region, signal, flag_slot, seq, DV_XFER_FUSED};
+  DV_TRY(remap_check(ctx, op));
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  DV_TRY(check_cache_holds(dst, &last, "destination"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  DV_ON_DEVICE(ctx->device);
+  const int64_t row = row_bytes(src);
+  TView sv[2] = {cache_view(src, 0, &reg), cache_view(src, 1, &reg)};
+  TView dv_[2] = {cache_view(dst, 0, &reg), cache_view(dst, 1, &reg)};
+  CopyPlan p[2];
+  const int np = build_plans(sv, dv_, &reg, row, ORDER_KV_OUTER, Outer{}, p);
+  if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  set_dyn(p, np, sv, dv_, -1, d_step, max_step);
+  const bool use_flag = signal && flag_slot >= 0;
+  return launch_publish(ctx, p, np, signal, flag_slot, seq, use_flag, DV_XFER_FUSED,
+                        (cudaStream_t)stream,
+                        (src->device < 0 || dst->device < 0) ? ctx->host_ctas : ctx->max_ctas);
+}
+
 // ---- level 1 --------------------------------------------------------------------------------
 static int32_t flat_block(const dv_setup* s, int32_t stage, int32_t micro, int32_t tp) {
   return (stage * s->n_micro + micro) * std::max(s->n_tp, 1) + tp;

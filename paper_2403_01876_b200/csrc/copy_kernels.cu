@@ -53,6 +53,9 @@ struct KParams {
   unsigned long long seq;
   unsigned int* ticket;
   unsigned long long* ts;  // optional: %globaltimer right after the flag store (latency tracing)
+  const int32_t* dyn;      // optional device step counter (see CopyPlan::dyn)
+  int64_t dyn_ss, dyn_ds;
+  int32_t dyn_max;
 };
 
 template <int VEC>
@@ -84,8 +87,8 @@ __device__ __forceinline__ void st_vec(uint8_t* p, const Vec<32>& v) {
 }
 
 template <int VEC>
-__device__ __forceinline__ void locate(const KParams& p, uint32_t g, const uint8_t*& s,
-                                       uint8_t*& d) {
+__device__ __forceinline__ void locate(const KParams& p, const uint8_t* src, uint8_t* dst,
+                                       uint32_t g, const uint8_t*& s, uint8_t*& d) {
   uint32_t q, w;
   p.fv.divmod(g, q, w);
   q += p.q_begin;
@@ -98,8 +101,8 @@ __device__ __forceinline__ void locate(const KParams& p, uint32_t g, const uint8
     so += (int64_t)i * p.ss[k];
     dof += (int64_t)i * p.ds[k];
   }
-  s = p.src + so + (int64_t)q * p.ss[0];
-  d = p.dst + dof + (int64_t)q * p.ds[0];
+  s = src + so + (int64_t)q * p.ss[0];
+  d = dst + dof + (int64_t)q * p.ds[0];
 }
 
 // Publish protocol: every CTA orders its stores before a GPU-scope release
@@ -108,7 +111,7 @@ __device__ __forceinline__ void locate(const KParams& p, uint32_t g, const uint8
 // visible to the system with ONE fence.sc.sys before the st.release.sys of the flag (PTX memory
 // model: causality order is transitive, fences are cumulative). DV_PUBLISH=0 selects the older,
 // more conservative variant with a system fence in every CTA.
-__device__ __forceinline__ void publish(const KParams& p, int per_cta_sys) {
+__device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsigned long long seq) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (per_cta_sys) {
@@ -121,7 +124,7 @@ __device__ __forceinline__ void publish(const KParams& p, int per_cta_sys) {
       asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire side of the ticket chain
       __threadfence_system();                          // fence.sc.sys: everything -> system scope
       *p.ticket = 0u;  // ready for the next stream-ordered user of this ticket
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(p.seq) : "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
       if (p.ts) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -146,6 +149,13 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(p.ts + 2, t);  // first CTA past the dependency wait
   }
+  int32_t k = 0;
+  if (p.dyn) {
+    k = *p.dyn;
+    if (k < 0 || k > p.dyn_max) return;  // uniform across the grid: nothing moves, nothing published
+  }
+  const uint8_t* src = p.src + (int64_t)k * p.dyn_ss;
+  uint8_t* dst = p.dst + (int64_t)k * p.dyn_ds;
   const uint32_t chunk = THREADS * U;
   for (uint32_t base = blockIdx.x * chunk; base < p.n_vec; base += gridDim.x * chunk) {
     Vec<VEC> v[U];
@@ -155,7 +165,7 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
       const uint32_t g = base + i * THREADS + threadIdx.x;
       if (g < p.n_vec) {
         const uint8_t* s;
-        locate<VEC>(p, g, s, d[i]);
+        locate<VEC>(p, src, dst, g, s, d[i]);
         ld_vec(v[i], s);
       }
     }
@@ -173,7 +183,7 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
       atomicMax(p.ts + 3, t);  // last CTA done with its stores (issued)
     }
   }
-  if (p.flag) publish(p, p.per_cta_sys);
+  if (p.flag) publish(p, p.per_cta_sys, p.seq + (unsigned long long)k);
 }
 
 // Dense-destination variant: the destination of vectors [q_begin*vpr, ...) is one contiguous
@@ -197,7 +207,7 @@ __global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t*
       if (g < p.n_vec) {
         const uint8_t* s;
         uint8_t* d;
-        locate<VEC>(p, g, s, d);
+        locate<VEC>(p, p.src, p.dst, g, s, d);
         ld_vec(v[i], s);
       }
     }
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t*
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
-  if (p.flag) publish(p, p.per_cta_sys);
+  if (p.flag) publish(p, p.per_cta_sys, p.seq);
 }
 
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
@@ -353,6 +363,8 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
       kp.ticket = rel.ticket;
       kp.ts = rel.ts;
       kp.per_cta_sys = tune().per_cta_sys;
+      kp.dyn = p.dyn;
+      kp.dyn_max = p.dyn_max;
       cudaError_t e = go<16, 1, 32>(kp, 1, stream);
       if (e != cudaSuccess) return cuda_fail(e, "publish kernel launch");
     }
@@ -361,6 +373,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
   // 32-byte vectors when every address and stride allows it.
   uint64_t orall = (uint64_t)(uintptr_t)p.src | (uint64_t)(uintptr_t)p.dst | p.run_bytes;
   for (int k = 0; k < kDims; ++k) orall |= (uint64_t)p.ss[k] | (uint64_t)p.ds[k];
+  orall |= (uint64_t)p.dyn_ss | (uint64_t)p.dyn_ds;
   if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
   const int VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
   const uint64_t vpr = p.run_bytes / VEC;
@@ -378,6 +391,10 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.fd[k] = to_dev(make_fastdiv(p.n[k]));
   }
   kp.fv = to_dev(make_fastdiv((uint32_t)vpr));
+  kp.dyn = p.dyn;
+  kp.dyn_ss = p.dyn_ss;
+  kp.dyn_ds = p.dyn_ds;
+  kp.dyn_max = p.dyn_max;
 
   // Split into launches of < 2^31 vectors at run boundaries.
   const uint64_t runs_per_launch = std::max<uint64_t>(1, ((1ull << 31) - 1) / vpr);
@@ -391,7 +408,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.ticket = rel.ticket;
     kp.ts = last ? rel.ts : nullptr;
     kp.per_cta_sys = tune().per_cta_sys;
-    cudaError_t e = (tune().bulk && dense_dst(p))
+    cudaError_t e = (tune().bulk && dense_dst(p) && !p.dyn)
                         ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
                         : launch_cfg(kp, VEC, max_ctas, stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");

@@ -48,6 +48,12 @@ struct CopyPlan {
   int64_t ss[kDims];
   int64_t ds[kDims];
   uint64_t run_bytes;
+  // Optional run-time shift (CUDA-graph replay with a device-side step counter): the kernel reads
+  // k = *dyn and, if 0 <= k <= dyn_max, moves src by k*dyn_ss and dst by k*dyn_ds (and publishes
+  // seq + k); any other k makes the launch a no-op.
+  const int32_t* dyn = nullptr;
+  int64_t dyn_ss = 0, dyn_ds = 0;
+  int32_t dyn_max = 0;
   uint64_t runs() const {
     uint64_t r = 1;
     for (int k = 0; k < kDims; ++k) r *= n[k];

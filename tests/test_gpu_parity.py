@@ -682,3 +682,77 @@ def test_tp_resplit_stream_out_in(sh, th, direct):
     ok.stream(oprompt, ps, otoken, ts, (0, 4, 0, 2, 0, p))
     for kk, (k, v, _) in token.items():
         assert np.array_equal(to_np(k), otoken[kk].K) and np.array_equal(to_np(v), otoken[kk].V), kk
+
+
+# ------------------------------------------------------------------------------------------------
+# CUDA graphs: capture the per-token stream-out once, replay it with a device-side step counter
+# ------------------------------------------------------------------------------------------------
+def test_scatter_dyn_graph_replay_matches_oracle():
+    L, B, H, S, D, p, T = 3, 2, 4, 24, 64, 10, 8
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=61)
+    k, v, c = dev_cache(K, V, 0, 0)
+    osrc = oc(K, V, 0, 0, S)
+    chunk = ok.region_bytes(0, L, 0, B, p, p + 1, H, D, 2)
+    log = pinned_u16((T + 2) * chunk // 2)
+    fl = flags(1, pinned=True)
+    ep = dv.endpoint_of(log, fl)
+    d_step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cx = ctx()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            dv.dv_scatter_dyn(cx, c, dv.region(0, L, 0, B, p, p + 1), ep, chunk, chunk, d_step.data_ptr(), T - 1,
+                              flag_slot=0, seq=100)
+    torch.cuda.synchronize()
+    for t in range(T):
+        with torch.cuda.stream(s):
+            d_step.fill_(t)
+            g.replay()
+        torch.cuda.synchronize()
+        assert int(fl[0]) == 100 + t
+    got = to_np(log)
+    for t in range(T):
+        exp = ok.pack(osrc, (0, L, 0, B, p + t, p + t + 1))
+        assert np.array_equal(got[(1 + t) * chunk // 2:(2 + t) * chunk // 2], exp)
+    assert np.all(got[:chunk // 2] == kvgen.SENTINEL)
+    # a step outside [0, max_step] is a no-op: nothing moves, nothing is published
+    with torch.cuda.stream(s):
+        d_step.fill_(T)
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(fl[0]) == 100 + T - 1
+    assert np.all(to_np(log)[(1 + T) * chunk // 2:] == kvgen.SENTINEL)
+    with pytest.raises(dv.DVError) as ei:   # validated for every step up to max_step
+        dv.dv_scatter_dyn(cx, c, dv.region(0, L, 0, B, p, p + 1), ep, chunk, chunk, d_step.data_ptr(), S - p)
+    assert ei.value.status == dv.DV_ERANGE
+
+
+@pytest.mark.parametrize("dst_layout", [ok.LAYOUT_KV5D, ok.LAYOUT_FT6D])
+def test_remap_dyn_graph_ring_step(dst_layout):
+    """Per-token ring replication (C5) as one captured graph: remap position p+k of every layer into
+    the replica store (another layout allowed) and publish seq+k."""
+    L, B, H, S, D, p, T = 2, 3, 2, 20, 16, 5, 6
+    K, V = kvgen.kv5d_cache("hash", 4, L, 0, B, H, S, D, seed=62)
+    k, v, c = dev_cache(K, V, 4, 0)
+    Ks, Vs = kvgen.sentinel_cache(L, B, H, S, D)
+    rk, rv, rc, ro = _mk(Ks, Vs, 4, 0, dst_layout)
+    sig = flags(2)
+    sep = dv.endpoint_of(sig[:1], sig)
+    d_step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            dv.dv_remap_dyn(ctx(), c, rc, dv.region(4, 4 + L, 0, B, p, p + 1), d_step.data_ptr(), T - 1, sep,
+                            flag_slot=1, seq=7)
+    torch.cuda.synchronize()
+    for t in range(T):
+        with torch.cuda.stream(s):
+            d_step.fill_(t)
+            g.replay()
+    torch.cuda.synchronize()
+    assert int(sig[1]) == 7 + T - 1
+    osrc = oc(K, V, 4, 0, S)
+    ok.remap(osrc, ro, (4, 4 + L, 0, B, p, p + T))
+    assert np.array_equal(to_np(rk), ro.K) and np.array_equal(to_np(rv), ro.V)
