@@ -165,6 +165,22 @@ def c3():
     emit(config="C3", op="prompt_gpu_16_layers_inbox_pack+unpack (loopback)", bytes=16 * layer_bytes, us=us,
          gbs_2x2R=4 * 16 * layer_bytes / us / 1e3, bound="hbm", frac=4 * 16 * layer_bytes / us / 1e3 / HBM,
          parity_mismatches=bad)
+    # the paper's own route: prompt GPU -> local CPU -> (network) -> token GPU's CPU ->
+    # token GPU; on one box: pack to pinned host (D2H), then unpack from it (H2D)
+    hostbuf = torch.empty(13 * layer_bytes // 2, dtype=torch.int16, pin_memory=True)
+    hep = dv.endpoint_of(hostbuf)
+    t0[0].fill_(-1); t0[1].fill_(-1)
+    reg13 = dv.region(0, 13, 0, b, 0, p)
+
+    def via_host():
+        dv.dv_scatter(ctx, pc, reg13, hep, 0, stream=sp)
+        dv.dv_gather(ctx, hep, 0, t0[2], reg13, stream=sp)
+    us = timed(via_host, reps=2, warm=1)
+    bad = sample_check(t0[0], t0[1], t0[2], (0, 13, 0, b, 0, p), SEED + 2)
+    emit(config="C3", op="paper_route_via_pinned_host_13_layers (baseline, PAPER.md:266)", bytes=13 * layer_bytes,
+         us=us, gbs=13 * layer_bytes / us / 1e3, bound="pcie (D2H then H2D)",
+         vs_direct_loopback=us / (us_all * 13 / 16), parity_mismatches=bad)
+    del hostbuf
     del pk, pv, t0, t1, inb0, inb1
     torch.cuda.empty_cache()
 
@@ -290,7 +306,24 @@ def c5():
     emit(config="C5", op="token_layer_put_latency (loopback, writer end -> flag)", bytes=2 * b * H * D * 2,
          p50_us=d[len(d) // 2], p99_us=d[int(len(d) * 0.99)], bound="latency", target_us=10,
          parity_mismatches=bad)
-    del ok_, ov_, rk, rv
+    # NEXT-3 recovery: worker x lost its cache and the replica it hosted; (1) the
+    # successor sends x's replica back, (2) the predecessor re-sends its own cache; both full
+    # prefixes [0, n). Loopback: the two bulk remaps on one GPU.
+    n_pos = p + 100 + n // Ls
+    lost_k, lost_v, lost_c = new_cache(Ls, b, H, S, D, 0, 0)
+    rep2_k, rep2_v, rep2_c = new_cache(Ls, b, H, S, D, 0, 0)
+
+    def recover():
+        dv.dv_remap(ctx, rc, lost_c, dv.region(0, Ls, 0, b, 0, n_pos), stream=sp)       # replica -> own
+        dv.dv_remap(ctx, oc_, rep2_c, dv.region(0, Ls, 0, b, 0, n_pos), stream=sp)      # own(x-1) -> replica at x
+    us = timed(recover, reps=3, warm=1)
+    rb = 2 * 2 * Ls * b * H * n_pos * D * 2
+    bad = sample_check(lost_k, lost_v, lost_c, (0, Ls, 0, b, 0, n_pos), SEED + 5) + \
+        sample_check(rep2_k, rep2_v, rep2_c, (0, Ls, 0, b, 0, n_pos), SEED + 5)
+    emit(config="C5", op=f"recovery_two_bulk_copies_{n_pos}_positions (NEXT-3, loopback)", bytes=rb, us=us,
+         gbs_2R=2 * rb / us / 1e3, bound="hbm", frac=2 * rb / us / 1e3 / HBM,
+         ideal_nvlink_ms_at_770=rb / 770e6, parity_mismatches=bad)
+    del ok_, ov_, rk, rv, lost_k, lost_v, rep2_k, rep2_v
     torch.cuda.empty_cache()
 
 

@@ -85,13 +85,33 @@ def run_c5(args, bench):
     st = torch.cuda.current_stream()
     sp = st.cuda_stream
 
+    step_bytes = 2 * Ls * b * H * D * 2
+    nccl = getattr(args, "peer_baseline", "none") == "nccl"
+    if nccl:
+        # BASELINE (north_star: "NCCL send/recv kept only as the baseline"): pack the step into a
+        # device buffer, ncclSend it to the successor / ncclRecv the predecessor's, unpack it into
+        # the replica store. Needs >= 2 GPUs and the nccl backend.
+        assert world > 1 and args.dist_backend == "nccl", "--peer-baseline nccl needs >= 2 GPUs"
+        sbuf = torch.empty(step_bytes // 2, dtype=torch.int16, device=dev)
+        rbuf = torch.empty_like(sbuf)
+        rep_local = dv.cache(rep_k, rep_v, pred * Ls, 0)
+
     def step(t):
         q = p + (t - 1) % (S - p)
-        dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
-                                [rep_at_succ], [sig], seq=t, stream=sp)
+        if not nccl:
+            dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
+                                    [rep_at_succ], [sig], seq=t, stream=sp)
+            return
+        dv.dv_scatter(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), dv.endpoint_of(sbuf), 0, stream=sp)
+        ops = [dist.P2POp(dist.isend, sbuf, succ), dist.P2POp(dist.irecv, rbuf, pred)]
+        for r_ in dist.batch_isend_irecv(ops):
+            r_.wait()
+        dv.dv_gather(ctx, dv.endpoint_of(rbuf), 0, rep_local, dv.region(pred * Ls, pred * Ls + Ls, 0, b, q, q + 1),
+                     stream=sp)
     # prompt replica first (bulk, Q13), then token steps
-    dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, 0, p), setup, 0, 0, setup, [rep_at_succ],
-                            [sig], seq=1, stream=sp)
+    if not nccl:   # the NCCL baseline times the token steps only
+        dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, 0, p), setup, 0, 0, setup, [rep_at_succ],
+                                [sig], seq=1, stream=sp)
     t = 1
     for _ in range(args.warmup):
         t += 1
@@ -115,11 +135,12 @@ def run_c5(args, bench):
     q = p + (t - 1) % (S - p)
     bad = bench.sample_region(rep_k, rep_v, pred * Ls, 0, H, S, D, (pred * Ls, pred * Ls + Ls, 0, b, q, q + 1),
                               20240309)
-    step_bytes = 2 * Ls * b * H * D * 2
+    bad = int(_max(bad, world, dev, args.dist_backend))
     value = P * args.steps * step_bytes / (ms * 1e-3) / 1e9
     if rank == 0:
         print(json.dumps({
             "metric": "KV stream GB/s (ring replication, token step per stage)", "value": value, "unit": "GB/s",
+            "impl": "nccl-baseline" if nccl else "dvstream",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
             "data": "synthetic (splitmix64 coordinate-hash fill)",
