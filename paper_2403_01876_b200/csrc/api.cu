@@ -346,17 +346,18 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
 }
 
 // Chooses FUSED or STAGED for a data call (measured in
-// profiles/r01_tune_host*.jsonl): writes to pinned host go through the kernel's own PCIe stores
-// (same throughput as pack+DMA, lower latency, no staging); reads from pinned host go through the
-// copy engine (SM zero-copy reads do not overlap with concurrent D2H traffic).
+// profiles/r01_tune_host*.jsonl): writes to pinned host go through the kernel's own PCIe stores up
+// to 32 MB (same throughput as pack+DMA for a 6.55 MB token step, lower latency, no staging) and
+// through pipelined pack + copy-engine DMA above (54.8 vs 52.6 GB/s for a 163.8 MB prompt layer,
+// and no SMs held during the transfer); reads from pinned host always go through the copy engine
+// (SM zero-copy reads do not overlap with concurrent D2H traffic).
 static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes, bool reading) {
   uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   if (m == DV_XFER_FUSED || m == DV_XFER_STAGED) {
     if (m == DV_XFER_STAGED && ep->kind == DV_EP_DEVICE) return DV_XFER_FUSED;  // already local
     return m;
   }
-  if (ep->kind == DV_EP_HOST && reading) return DV_XFER_STAGED;
-  (void)bytes;
+  if (ep->kind == DV_EP_HOST && (reading || bytes >= (32ull << 20))) return DV_XFER_STAGED;
   return DV_XFER_FUSED;
 }
 
@@ -387,6 +388,28 @@ static uint64_t layer_slab_bytes(const dv_region* r, int64_t row) {
          (uint64_t)(r->pos_end - r->pos_begin) * (uint64_t)row;
 }
 
+// Pipelined staging: kernels run on the caller's stream, copy-engine DMAs on ctx->dma; each
+// hand-off is an event (record on one stream, wait on the other), so chunk k's DMA overlaps
+// chunk k+1's kernel and the transfer time approaches the DMA time alone.
+static cudaEvent_t next_event(dv_ctx* ctx) {
+  return ctx->pipe_ev[ctx->next_ev.fetch_add(1) % ctx->pipe_ev.size()];
+}
+static dv_status hand_off(dv_ctx* ctx, cudaStream_t from, cudaStream_t to) {
+  if (from == to) return DV_OK;
+  cudaEvent_t ev = next_event(ctx);
+  DV_CUDA(cudaEventRecord(ev, from));
+  DV_CUDA(cudaStreamWaitEvent(to, ev, 0));
+  return DV_OK;
+}
+// Transfers below this size are not worth the cross-stream hand-offs (measured: a 6.55 MB token
+// step took 151 us pipelined in 1 MiB chunks vs 137 us as one chunk on one stream).
+static const uint64_t kPipeMin = 32ull << 20;
+// Chunk size of a staged transfer: one chunk below kPipeMin; else ~8 chunks >= 4 MiB; <= half pool.
+static uint64_t pipe_chunk(uint64_t total, uint64_t half) {
+  if (total < kPipeMin) return half;
+  return std::min<uint64_t>(half, std::max<uint64_t>(4ull << 20, total / 8));
+}
+
 // Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
 // the kernel packs a group of layer slabs (or, with one plan, a range of runs) into staging, the
 // copy engine moves that contiguous piece to its place in the wire.
@@ -400,9 +423,13 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
   CopyPlan p[2];
   const int np = build_plans(sv, wv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+  const uint64_t total = region_bytes_h(&reg, c->n_heads, c->head_dim, c->elem_bytes);
+  cudaStream_t ds = total >= kPipeMin ? ctx->dma : st;  // copy-engine stream (pipelined or not)
   if (np == 1 && p[0].run_bytes <= half) {  // dense wire in run order: chunk by runs
     const uint64_t rb = p[0].run_bytes, runs = p[0].runs();
-    const uint64_t chunk = std::max<uint64_t>(1, half / rb);
+    const uint64_t chunk = std::max<uint64_t>(1, pipe_chunk(runs * rb, half) / rb);
+    DV_TRY(hand_off(ctx, st, ds));  // the DMA stream must not run ahead of the caller's work
     for (uint64_t q0 = 0; q0 < runs; q0 += chunk) {
       const uint64_t q1 = std::min(runs, q0 + chunk), nb = (q1 - q0) * rb;
       uint8_t* stg;
@@ -411,16 +438,19 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
       CopyPlan pc = p[0];
       pc.dst = stg - q0 * rb;  // run q lands at stg + (q - q0) * rb (wire side is dense)
       DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
-      DV_DMA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, st));
-      DV_TRY(ctx->staging.release(off, nb, st));
+      DV_TRY(hand_off(ctx, st, ds));
+      DV_DMA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, ds));
+      DV_TRY(ctx->staging.release(off, nb, ds));
     }
-    return DV_OK;
+    return hand_off(ctx, ds, st);
   }
   const uint64_t slab = layer_slab_bytes(&reg, row);
   if (slab > half)
     return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
                 "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
-  const int32_t per = (int32_t)std::max<uint64_t>(1, half / slab);
+  const int32_t per = (int32_t)std::max<uint64_t>(
+      1, pipe_chunk((uint64_t)(reg.layer_end - reg.layer_begin) * slab, half) / slab);
+  DV_TRY(hand_off(ctx, st, ds));
   for (int32_t la = reg.layer_begin; la < reg.layer_end; la += per) {
     dv_region sub = reg;
     sub.layer_begin = la;
@@ -434,11 +464,12 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
     CopyPlan ps[2];
     const int n2 = build_plans(s2, w2, &sub, row, ORDER_WIRE, Outer{}, ps);
     for (int q = 0; q < n2; ++q) DV_TRY(launch_copy(ps[q], 0, ps[q].runs(), none, ctx->max_ctas, st));
+    DV_TRY(hand_off(ctx, st, ds));
     DV_DMA(cudaMemcpyAsync(wire + (uint64_t)(la - reg.layer_begin) * slab, stg, nb,
-                           cudaMemcpyDefault, st));
-    DV_TRY(ctx->staging.release(off, nb, st));
+                           cudaMemcpyDefault, ds));
+    DV_TRY(ctx->staging.release(off, nb, ds));
   }
-  return DV_OK;
+  return hand_off(ctx, ds, st);
 }
 
 // Unpack a wire chunk at `wire` (any memory) into `reg` of cache `c` through HBM staging.
@@ -452,15 +483,20 @@ static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache*
   CopyPlan p[2];
   const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
+  std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+  const uint64_t total = region_bytes_h(&reg, c->n_heads, c->head_dim, c->elem_bytes);
+  cudaStream_t ds = total >= kPipeMin ? ctx->dma : st;
+  DV_TRY(hand_off(ctx, st, ds));  // DMAs start after the caller's prior work (flag waits)
   if (np == 1 && p[0].run_bytes <= half) {
     const uint64_t rb = p[0].run_bytes, runs = p[0].runs();
-    const uint64_t chunk = std::max<uint64_t>(1, half / rb);
+    const uint64_t chunk = std::max<uint64_t>(1, pipe_chunk(runs * rb, half) / rb);
     for (uint64_t q0 = 0; q0 < runs; q0 += chunk) {
       const uint64_t q1 = std::min(runs, q0 + chunk), nb = (q1 - q0) * rb;
       uint8_t* stg;
       uint64_t off;
-      DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
-      DV_DMA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, st));
+      DV_TRY(ctx->staging.acquire(nb, ds, &stg, &off));
+      DV_DMA(cudaMemcpyAsync(stg, wire + q0 * rb, nb, cudaMemcpyDefault, ds));
+      DV_TRY(hand_off(ctx, ds, st));
       CopyPlan pc = p[0];
       pc.src = stg - q0 * rb;
       DV_TRY(launch_copy(pc, q0, q1, none, ctx->max_ctas, st));
@@ -472,7 +508,8 @@ static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache*
   if (slab > half)
     return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
                 "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
-  const int32_t per = (int32_t)std::max<uint64_t>(1, half / slab);
+  const int32_t per = (int32_t)std::max<uint64_t>(
+      1, pipe_chunk((uint64_t)(reg.layer_end - reg.layer_begin) * slab, half) / slab);
   for (int32_t la = reg.layer_begin; la < reg.layer_end; la += per) {
     dv_region sub = reg;
     sub.layer_begin = la;
@@ -480,9 +517,10 @@ static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache*
     const uint64_t nb = (uint64_t)(sub.layer_end - la) * slab;
     uint8_t* stg;
     uint64_t off;
-    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
+    DV_TRY(ctx->staging.acquire(nb, ds, &stg, &off));
     DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)(la - reg.layer_begin) * slab, nb,
-                           cudaMemcpyDefault, st));
+                           cudaMemcpyDefault, ds));
+    DV_TRY(hand_off(ctx, ds, st));
     TView w2[2] = {wire_view(stg, 0, &sub, row), wire_view(stg, 1, &sub, row)};
     TView c2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
     CopyPlan ps[2];
@@ -687,6 +725,12 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
   e = cudaMalloc(&c->tickets, sizeof(unsigned int) * dv_ctx::kTickets);
   if (e == cudaSuccess) e = cudaMemset(c->tickets, 0, sizeof(unsigned int) * dv_ctx::kTickets);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dma, cudaStreamNonBlocking);
+  for (int i = 0; e == cudaSuccess && i < 64; ++i) {
+    cudaEvent_t ev;
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) c->pipe_ev.push_back(ev);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     c->staging.destroy();
@@ -705,6 +749,8 @@ dv_status dv_destroy(dv_ctx* ctx) {
     ctx->staging.destroy();
     cudaFree(ctx->tickets);
     cudaStreamDestroy(ctx->aux);
+    cudaStreamDestroy(ctx->dma);
+    for (auto ev : ctx->pipe_ev) cudaEventDestroy(ev);
   }
   delete ctx;
   return DV_OK;
@@ -952,14 +998,18 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
     }
     return DV_OK;
   }
-  const int32_t per = (int32_t)std::max<uint64_t>(1, half / chunk_bytes);
+  const int32_t per = (int32_t)std::max<uint64_t>(1, pipe_chunk(total, half) / chunk_bytes);
+  std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+  cudaStream_t ds = total >= kPipeMin ? ctx->dma : st;
+  DV_TRY(hand_off(ctx, st, ds));  // DMAs start after the caller's prior work (flag waits)
   for (int32_t k0 = 0; k0 < n_chunks; k0 += per) {
     const int32_t k1 = std::min(n_chunks, k0 + per);
     const uint64_t nb = (uint64_t)(k1 - k0) * chunk_bytes;
     uint8_t* stg;
     uint64_t off;
-    DV_TRY(ctx->staging.acquire(nb, st, &stg, &off));
-    DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)k0 * chunk_bytes, nb, cudaMemcpyDefault, st));
+    DV_TRY(ctx->staging.acquire(nb, ds, &stg, &off));
+    DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)k0 * chunk_bytes, nb, cudaMemcpyDefault, ds));
+    DV_TRY(hand_off(ctx, ds, st));
     DV_TRY(unpack_group(stg, k0, k1));
     DV_TRY(ctx->staging.release(off, nb, st));
   }

@@ -135,6 +135,10 @@ struct dv_ctx {
   unsigned int* tickets;  // device array of kTickets counters
   std::atomic<uint32_t> next_ticket{0};
   cudaStream_t aux;       // private stream for dv_query on device flags
+  cudaStream_t dma;       // copy-engine stream of the pipelined staged transfers
+  std::vector<cudaEvent_t> pipe_ev;  // event ring for kernel <-> DMA hand-offs
+  std::atomic<uint32_t> next_ev{0};
+  std::mutex pipe_mu;     // one pipelined transfer enqueued at a time per context
   unsigned long long* trace_ts = nullptr;  // dvt_trace: publish timestamps land here
   static constexpr uint32_t kTickets = 4096;
 };
