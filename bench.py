@@ -228,10 +228,14 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    dram_traffic, pcie_traffic = _ncu_traffic()
     roof = {"bound": "pcie", "achieved": STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9,
             "peak": pcie_peak, "unit": "GB/s",
             "frac": (STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9 / pcie_peak) if pcie_peak else None,
-            "traffic": None,
+            "traffic": dram_traffic, "traffic_pcie_write": pcie_traffic,
+            "traffic_source": "profiles/r01_io_counters_final.csv (ncu dram__bytes_read+write, "
+                              "pcie__write_bytes per launch, median)",
+            "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
             "kernel": "k_run_copy (fused pack -> pinned host zero-copy PCIe stores + st.release.sys flag)",
             "algorithmic_bytes_per_launch": STEP_BYTES,
             "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
@@ -261,6 +265,28 @@ def run_ours(args):
     dv.dv_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _ncu_traffic():
+    """DRAM and PCIe bytes per launch of the headline kernel from the committed ncu capture
+    (profiles/r01_io_counters_final.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+    pcie__write_bytes.sum on this same command), median over the captured launches."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_io_counters_final.csv")
+    try:
+        rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
+    except OSError:
+        return None, None
+    hdr, body = rows[0], rows[1:]
+    per = {}
+    for r in body:
+        d = dict(zip(hdr, r))
+        per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"])
+    dram = sorted(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in per.values())
+    pcie = sorted(v.get("pcie__write_bytes.sum", 0) for v in per.values())
+    if not dram:
+        return None, None
+    return dram[len(dram) // 2], pcie[len(pcie) // 2]
 
 
 def _spot_check(wire, q, seed):
@@ -330,6 +356,9 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["pcie_dma_d2h_gbs"] = n / ms / 1e6
     ms = _time(lambda: db.copy_(hb, non_blocking=True), stream, 5)
     ex["pcie_dma_h2d_gbs"] = n / ms / 1e6
+    # the same 6.55 MB per transfer as one token step, back to back (fixed costs included)
+    ms = _time(lambda: hb[:STEP_BYTES].copy_(db[:STEP_BYTES], non_blocking=True), stream, 100)
+    ex["pcie_dma_d2h_same_size_gbs"] = STEP_BYTES / ms / 1e6
     del hb, db
 
     # token step: fused vs staged (host), and pack-only into HBM

@@ -269,6 +269,7 @@ struct Tune {
   int vec = 0;        // DV_VEC: force 16-byte vectors when 16
   int bulk = 0;       // DV_BULK: 1 = dense-destination copies use k_pack_bulk
   int per_cta_sys = 0;  // DV_PUBLISH=0: system fence in every CTA before the ticket
+  uint64_t max_vec_per_launch = (1ull << 31) - 1;  // DV_MAX_VEC (tests of the launch split)
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
 };
 static const Tune& tune() {
@@ -278,6 +279,10 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_VEC")) x.vec = atoi(e);
     if (const char* e = getenv("DV_BULK")) x.bulk = atoi(e);
     if (const char* e = getenv("DV_PUBLISH")) x.per_cta_sys = (atoi(e) == 0);
+    if (const char* e = getenv("DV_MAX_VEC")) {
+      const uint64_t v = strtoull(e, nullptr, 10);
+      if (v > 0 && v < x.max_vec_per_launch) x.max_vec_per_launch = v;
+    }
     if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
     return x;
   }();
@@ -397,7 +402,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
   kp.dyn_max = p.dyn_max;
 
   // Split into launches of < 2^31 vectors at run boundaries.
-  const uint64_t runs_per_launch = std::max<uint64_t>(1, ((1ull << 31) - 1) / vpr);
+  const uint64_t runs_per_launch = std::max<uint64_t>(1, tune().max_vec_per_launch / vpr);
   for (uint64_t q0 = q_first; q0 < q_last; q0 += runs_per_launch) {
     const uint64_t nq = std::min(runs_per_launch, q_last - q0);
     const bool last = q0 + nq == q_last;

@@ -11,6 +11,11 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
     config.addinivalue_line("markers", "slow: long-running")
+    # Test infrastructure: make sure the in-tree library is built (nvcc cross-compiles without a
+    # GPU) and up to date before any test loads it. The product binding itself never builds:
+    # it raises if libdvstream.so is missing.
+    from paper_2403_01876_b200 import build
+    build.build()
 
 
 def pytest_collection_modifyitems(config, items):
