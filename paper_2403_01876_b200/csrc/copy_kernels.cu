@@ -68,6 +68,41 @@ __device__ __forceinline__ void ld_vec(Vec<16>& v, const uint8_t* p) {
                : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3])
                : "l"(p));
 }
+// Store cache-operator variants (PTX st.{wb,cs,wt}); selected per launch for sysmem experiments.
+template <int STM>
+__device__ __forceinline__ void st_vec_m(uint8_t* p, const Vec<32>& v) {
+  if (STM == 1)
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]),
+                 "r"(v.w[7])
+                 : "memory");
+  else if (STM == 2)
+    asm volatile("st.global.wt.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]),
+                 "r"(v.w[7])
+                 : "memory");
+  else
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+                 "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]),
+                 "r"(v.w[7])
+                 : "memory");
+}
+template <int STM>
+__device__ __forceinline__ void st_vec_m(uint8_t* p, const Vec<16>& v) {
+  if (STM == 1)
+    asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3])
+                 : "memory");
+  else if (STM == 2)
+    asm volatile("st.global.wt.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3])
+                 : "memory");
+  else
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3])
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_vec(uint8_t* p, const Vec<16>& v) {
   asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
                "r"(v.w[2]), "r"(v.w[3])
@@ -134,7 +169,7 @@ __device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsig
   }
 }
 
-template <int VEC, int U, int THREADS>
+template <int VEC, int U, int THREADS, int STM = 0>
 __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
   // Programmatic dependent launch: this grid may become resident while the kernel that wrote the
   // K/V (e.g. attention) is still draining; wait here until that grid's memory is visible.
@@ -172,7 +207,7 @@ __global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       const uint32_t g = base + i * THREADS + threadIdx.x;
-      if (g < p.n_vec) st_vec(d[i], v[i]);
+      if (g < p.n_vec) st_vec_m<STM>(d[i], v[i]);
     }
   }
   if (p.ts) {
@@ -246,7 +281,7 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int U, int THREADS>
+template <int VEC, int U, int THREADS, int STM = 0>
 static cudaError_t go(const KParams& kp, int blocks, cudaStream_t st) {
   (void)cudaGetLastError();  // clear stale non-sticky errors of unrelated earlier calls
   cudaLaunchConfig_t cfg = {};
@@ -258,7 +293,7 @@ static cudaError_t go(const KParams& kp, int blocks, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_run_copy<VEC, U, THREADS>, kp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_run_copy<VEC, U, THREADS, STM>, kp);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -270,6 +305,7 @@ struct Tune {
   int bulk = 0;       // DV_BULK: 1 = dense-destination copies use k_pack_bulk
   int per_cta_sys = 0;  // DV_PUBLISH=0: system fence in every CTA before the ticket
   uint64_t max_vec_per_launch = (1ull << 31) - 1;  // DV_MAX_VEC (tests of the launch split)
+  int stm = 0;  // DV_STM: store cache operator for U=4 copies (0 default .wb, 1 .cs, 2 .wt)
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
 };
 static const Tune& tune() {
@@ -279,6 +315,7 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_VEC")) x.vec = atoi(e);
     if (const char* e = getenv("DV_BULK")) x.bulk = atoi(e);
     if (const char* e = getenv("DV_PUBLISH")) x.per_cta_sys = (atoi(e) == 0);
+    if (const char* e = getenv("DV_STM")) x.stm = atoi(e);
     if (const char* e = getenv("DV_MAX_VEC")) {
       const uint64_t v = strtoull(e, nullptr, 10);
       if (v > 0 && v < x.max_vec_per_launch) x.max_vec_per_launch = v;
@@ -298,7 +335,10 @@ static cudaError_t launch_vec(const KParams& kp, int u, int max_ctas, cudaStream
     case 1: return go<VEC, 1, 128>(kp, blocks, st);
     case 2: return go<VEC, 2, 256>(kp, blocks, st);
     case 8: return go<VEC, 8, 256>(kp, blocks, st);
-    default: return go<VEC, 4, 256>(kp, blocks, st);
+    default:
+      if (tune().stm == 1) return go<VEC, 4, 256, 1>(kp, blocks, st);
+      if (tune().stm == 2) return go<VEC, 4, 256, 2>(kp, blocks, st);
+      return go<VEC, 4, 256>(kp, blocks, st);
   }
 }
 

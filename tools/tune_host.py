@@ -32,7 +32,7 @@ def child():
     fl = torch.zeros(2, dtype=torch.int64, pin_memory=True)
     dbuf = torch.empty(STEP * 8 // 2, dtype=torch.int16, device="cuda")
     dfl = torch.zeros(2, dtype=torch.int64, device="cuda")
-    out = {"env": {k_: os.environ.get(k_) for k_ in ("DV_U", "DV_VEC", "DV_PDL", "DV_BULK")}}
+    out = {"env": {k_: os.environ.get(k_) for k_ in ("DV_U", "DV_VEC", "DV_PDL", "DV_BULK", "DV_STM")}}
     cnt = [0]
 
     def ev():
@@ -202,7 +202,8 @@ def child():
 
 
 def main():
-    variants = [{}, {"DV_PDL": "0"}]
+    variants = [{}, {"DV_STM": "1"}, {"DV_STM": "2"}, {"DV_VEC": "16"}, {"DV_VEC": "16", "DV_STM": "2"},
+                {"DV_U": "8"}, {"DV_U": "2"}]
     for var in variants:
         env = dict(os.environ)
         env.update(var)
