@@ -756,3 +756,38 @@ def test_remap_dyn_graph_ring_step(dst_layout):
     osrc = oc(K, V, 4, 0, S)
     ok.remap(osrc, ro, (4, 4 + L, 0, B, p, p + T))
     assert np.array_equal(to_np(rk), ro.K) and np.array_equal(to_np(rv), ro.V)
+
+
+def test_inbox_credit_loop_reuses_one_inbox_without_overwrite():
+    """A5 inbox credits composed from the ABI: the sender waits for the receiver's consumed-seq ack
+    (dv_wait) before refilling the single inbox slot; the receiver waits for the data seq, unpacks,
+    then acks (dv_signal). Sender and receiver run on different streams; the sender is slowed down
+    at random, the receiver too; every round must land intact in its own destination positions."""
+    L, B, H, S, D, R = 2, 2, 4, 64, 64, 24
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=71)
+    k, v, c = dev_cache(K, V, 0, 0)
+    chunk = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    inbox = sentinel_like((chunk // 2,))
+    data_f = flags(1)
+    ack_f = flags(1)
+    iep, aep = dv.endpoint_of(inbox, data_f), dv.endpoint_of(ack_f[:1], ack_f)
+    dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    dc = dv.cache(dk, dvv)
+    snd, rcv = torch.cuda.Stream(), torch.cuda.Stream()
+    cx = ctx()
+    rng = random.Random(5)
+    for t in range(1, R + 1):
+        reg = dv.region(0, L, 0, B, t, t + 1)
+        if t > 1:
+            dv.dv_wait(cx, aep, 0, t - 1, stream=snd)          # credit: previous round consumed
+        dv.dvt_spin(rng.randint(0, 30000), 1, stream=snd)
+        dv.dv_scatter(cx, c, reg, iep, 0, flag_slot=0, seq=t, stream=snd)
+        dv.dvt_spin(rng.randint(0, 30000), 1, stream=rcv)
+        dv.dv_gather(cx, iep, 0, dc, reg, flag_slot=0, wait_seq=t, stream=rcv)
+        dv.dv_signal(cx, aep, 0, t, stream=rcv)                # give the credit back
+    torch.cuda.synchronize()
+    assert int(ack_f[0]) == R and int(data_f[0]) == R
+    got_k, got_v = to_np(dk), to_np(dvv)
+    assert np.array_equal(got_k[:, :, :, 1:R + 1], K[:, :, :, 1:R + 1])
+    assert np.array_equal(got_v[:, :, :, 1:R + 1], V[:, :, :, 1:R + 1])
+    assert np.all(got_k[:, :, :, R + 1:] == kvgen.SENTINEL) and np.all(got_k[:, :, :, 0] == kvgen.SENTINEL)

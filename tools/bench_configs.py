@@ -327,13 +327,57 @@ def c5():
     torch.cuda.empty_cache()
 
 
+# =====================================================================================================
+def ft6d():
+    """NEXT-1: C2 shape with the key cache in FasterTransformer's 6-D layout [L][B][H][D/x][S][x]
+    (x = 8 fp16 words = one 16-byte packet): token step -> pinned host, prompt layer pack in HBM,
+    and FT6D -> KV5D remap of a prompt layer (e.g. an FT prompt machine feeding a KV5D token one)."""
+    L, H, D, B, P, S = 40, 40, 128, 8, 1000, 2048
+    k6 = torch.empty((L, B, H, D // 8, S, 8), dtype=torch.int16, device=dev)
+    v = torch.empty((L, B, H, S, D), dtype=torch.int16, device=dev)
+    c = dv.cache(k6, v)
+    dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=SEED + 11)
+    step = 2 * L * B * H * D * 2
+    log = torch.empty(step * 8 // 2, dtype=torch.int16, pin_memory=True)
+    ep = dv.endpoint_of(log)
+    cnt = [0]
+
+    def tok():
+        cnt[0] += 1
+        q = P + cnt[0] % 1000
+        dv.dv_scatter(ctx, c, dv.region(0, L, 0, B, q, q + 1), ep, (cnt[0] % 8) * step, stream=sp)
+    us = timed(tok, reps=100)
+    emit(config="C2-FT6D", op="token_step_to_host (K 16-B packets)", bytes=step, us=us, gbs=step / us / 1e3,
+         bound="pcie")
+    dbuf = torch.empty(2 * B * H * P * D, dtype=torch.int16, device=dev)
+    dep = dv.endpoint_of(dbuf)
+    lay = [0]
+
+    def prm():
+        lay[0] = (lay[0] + 1) % L
+        dv.dv_scatter(ctx, c, dv.region(lay[0], lay[0] + 1, 0, B, 0, P), dep, 0, stream=sp)
+    nb = 2 * B * H * P * D * 2
+    us = timed(prm, reps=10)
+    emit(config="C2-FT6D", op="prompt_layer_pack_hbm (K transposed through 16-B packets)", bytes=nb, us=us,
+         gbs_2R=2 * nb / us / 1e3, bound="hbm", frac=2 * nb / us / 1e3 / HBM)
+    k5 = torch.full((1, B, H, S, D), -1, dtype=torch.int16, device=dev)
+    v5 = torch.full_like(k5, -1)
+    c5 = dv.cache(k5, v5, 3, 0)
+    us = timed(lambda: dv.dv_remap(ctx, c, c5, dv.region(3, 4, 0, B, 0, P), stream=sp), reps=10)
+    bad = sample_check(k5, v5, c5, (3, 4, 0, B, 0, P), SEED + 11)
+    emit(config="C2-FT6D", op="prompt_layer_remap_FT6D_to_KV5D", bytes=nb, us=us, gbs_2R=2 * nb / us / 1e3,
+         bound="hbm", frac=2 * nb / us / 1e3 / HBM, parity_mismatches=bad)
+    del k6, v, dbuf, k5, v5, log
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C1,C3,C4,C5")
+    ap.add_argument("--only", default="C1,C3,C4,C5,FT6D")
     a = ap.parse_args()
     for name in a.only.split(","):
         t0 = time.time()
-        {"C1": c1, "C3": c3, "C4": c4, "C5": c5}[name]()
+        {"C1": c1, "C3": c3, "C4": c4, "C5": c5, "FT6D": ft6d}[name]()
         emit(config=name, op="wall_s", value=time.time() - t0)
 
 
