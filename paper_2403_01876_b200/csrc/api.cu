@@ -214,6 +214,32 @@ static int build_plans(const TView sv[2], const TView dv_[2], const dv_region* r
   for (int q = 0; q < nplans; ++q) {
     const TView& a = sv[only >= 0 ? only : q];
     const TView& b = dv_[only >= 0 ? only : q];
+    // exactly one side packet-major (FT6D key): a 16-byte packet transpose through shared memory
+    const bool a_um = a.st[DS] == 16 && a.st[DU] != 16, b_um = b.st[DS] == 16 && b.st[DU] != 16;
+    // (only for >= 32 positions: a token step's single position is better served by the run copy)
+    if (a_um != b_um && !one && ext[DS] >= 32) {
+      CopyPlan t{};
+      t.kind = kTranspose;
+      t.src = a.base;
+      t.dst = (uint8_t*)b.base;
+      t.tdir = a_um ? 0 : 1;
+      t.tU = ext[DU];
+      t.tN = ext[DS];
+      t.t_su = (a_um ? a : b).st[DU];
+      t.t_ss = (a_um ? b : a).st[DS];
+      t.run_bytes = 16;
+      const uint32_t sn[4] = {outer.n, ext[DL], ext[DR], ext[DH]};
+      const int64_t s1[4] = {outer.ss, a.st[DL], a.st[DR], a.st[DH]};
+      const int64_t d1[4] = {outer.ds, b.st[DL], b.st[DR], b.st[DH]};
+      for (int k = 0; k < kDims; ++k) {
+        const int j = k - (kDims - 4);
+        t.n[k] = j < 0 ? 1 : sn[j];
+        t.ss[k] = j < 0 ? 0 : s1[j];
+        t.ds[k] = j < 0 ? 0 : d1[j];
+      }
+      out[q] = t;
+      continue;
+    }
     // dims outer -> inner, before collapsing
     uint32_t n[8];
     int64_t ss[8], ds[8];

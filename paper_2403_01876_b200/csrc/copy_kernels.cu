@@ -271,6 +271,111 @@ __global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t*
   if (p.flag) publish(p, p.per_cta_sys, p.seq);
 }
 
+// 16-byte packet transpose through shared memory (NEXT-1, FasterTransformer's 6-D key layout):
+// inside each slab the packet-major side holds [u][s] (a column of positions per packet, each
+// column contiguous), the position-major side [s][u] (the wire, KV5D). A CTA moves a tile of all
+// U packets x kTS positions: loads coalesced along the source's contiguous axis, stores coalesced
+// along the destination's, the transposition happens in shared memory (rows padded by one
+// packet so neither phase has bank conflicts).
+constexpr int kTS = 64;
+
+struct TParams {
+  const uint8_t* src;
+  uint8_t* dst;
+  int64_t ss[4], ds[4];
+  DevDiv fd[4];
+  uint32_t n_tiles, tiles_per_slab;
+  DevDiv fU, fT;
+  uint32_t U, N;
+  int64_t su, sps;  // packet stride of the packet-major side, position stride of the position-major side
+  unsigned long long* flag;
+  unsigned long long seq;
+  unsigned int* ticket;
+  unsigned long long* ts;
+  int32_t per_cta_sys;
+  const int32_t* dyn;
+  int64_t dyn_ss, dyn_ds;
+  int32_t dyn_max;
+};
+
+template <int DIR>
+__global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
+  extern __shared__ uint4 tile[];  // kTS rows x (U + 1) packets
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int32_t k = 0;
+  if (p.dyn) {
+    k = *p.dyn;
+    if (k < 0 || k > p.dyn_max) return;
+  }
+  const uint8_t* src0 = p.src + (int64_t)k * p.dyn_ss;
+  uint8_t* dst0 = p.dst + (int64_t)k * p.dyn_ds;
+  const uint32_t row = p.U + 1;
+  const uint32_t elems = p.U * kTS;
+  for (uint32_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+    uint32_t slab, ti;
+    p.fT.divmod(t, slab, ti);
+    const uint32_t s0 = ti * kTS;
+    const uint32_t ns = min((uint32_t)kTS, p.N - s0);
+    int64_t so = 0, dof = 0;
+    uint32_t q = slab;
+#pragma unroll
+    for (int d = 3; d >= 1; --d) {
+      uint32_t i;
+      p.fd[d].divmod(q, q, i);
+      so += (int64_t)i * p.ss[d];
+      dof += (int64_t)i * p.ds[d];
+    }
+    so += (int64_t)q * p.ss[0];
+    dof += (int64_t)q * p.ds[0];
+    const uint8_t* sb = src0 + so;
+    uint8_t* db = dst0 + dof;
+    for (uint32_t i = threadIdx.x; i < elems; i += 256) {
+      uint32_t u, s;
+      if (DIR == 0) {  // packet-major source: consecutive threads walk positions of one packet
+        u = i / kTS;
+        s = i % kTS;
+      } else {         // position-major source: consecutive threads walk packets of one position
+        p.fU.divmod(i, s, u);
+      }
+      if (s < ns) {
+        uint4 v;
+        const uint8_t* a = DIR == 0 ? sb + (int64_t)u * p.su + (int64_t)(s0 + s) * 16
+                                    : sb + (int64_t)(s0 + s) * p.sps + (int64_t)u * 16;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(a));
+        tile[s * row + u] = v;
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < elems; i += 256) {
+      uint32_t u, s;
+      if (DIR == 0) {  // position-major destination: consecutive threads write packets of a position
+        p.fU.divmod(i, s, u);
+      } else {
+        u = i / kTS;
+        s = i % kTS;
+      }
+      if (s < ns) {
+        const uint4 v = tile[s * row + u];
+        uint8_t* a = DIR == 0 ? db + (int64_t)(s0 + s) * p.sps + (int64_t)u * 16
+                              : db + (int64_t)u * p.su + (int64_t)(s0 + s) * 16;
+        asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w)
+                     : "memory");
+      }
+    }
+    __syncthreads();
+  }
+  if (p.flag) {
+    KParams kp{};
+    kp.flag = p.flag;
+    kp.ticket = p.ticket;
+    kp.ts = p.ts;
+    publish(kp, p.per_cta_sys, p.seq + (unsigned long long)k);
+  }
+}
+
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
 
 static bool pdl_enabled() {
@@ -394,8 +499,74 @@ static cudaError_t launch_bulk(const KParams& kp, int vec, uint8_t* dst0, int ma
                    : launch_bulk_vec<16>(kp, dst0, max_ctas, st);
 }
 
+static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max_ctas,
+                                  cudaStream_t stream) {
+  TParams tp{};
+  tp.src = p.src;
+  tp.dst = p.dst;
+  // slab dims: the last four loop dims of the plan (the builder leaves the others at 1)
+  uint64_t slabs = 1;
+  for (int d = 0; d < 4; ++d) {
+    const int k = kDims - 4 + d;
+    tp.ss[d] = p.ss[k];
+    tp.ds[d] = p.ds[k];
+    tp.fd[d] = to_dev(make_fastdiv(p.n[k]));
+    slabs *= p.n[k];
+  }
+  for (int k = 0; k < kDims - 4; ++k)
+    if (p.n[k] != 1) return fail(DV_ENOTSUP, "transpose plan with more than 4 slab dims");
+  const uint64_t tiles = (p.tN + kTS - 1) / kTS;
+  if (slabs * tiles >= (1ull << 31) || p.tU > 256) return fail(DV_ENOTSUP, "transpose too large");
+  tp.n_tiles = (uint32_t)(slabs * tiles);
+  tp.tiles_per_slab = (uint32_t)tiles;
+  tp.fT = to_dev(make_fastdiv((uint32_t)tiles));
+  tp.fU = to_dev(make_fastdiv(p.tU));
+  tp.U = p.tU;
+  tp.N = p.tN;
+  tp.su = p.t_su;
+  tp.sps = p.t_ss;
+  tp.flag = rel.flag;
+  tp.seq = rel.seq;
+  tp.ticket = rel.ticket;
+  tp.ts = rel.ts;
+  tp.per_cta_sys = tune().per_cta_sys;
+  tp.dyn = p.dyn;
+  tp.dyn_ss = p.dyn_ss;
+  tp.dyn_ds = p.dyn_ds;
+  tp.dyn_max = p.dyn_max;
+  const int smem = kTS * (p.tU + 1) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_packet_transpose<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_packet_transpose<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  if (smem > 64 * 1024) return fail(DV_ENOTSUP, "head_dim too large for the packet transpose");
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tp.n_tiles, (uint64_t)max_ctas)));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = p.tdir == 0 ? cudaLaunchKernelEx(&cfg, k_packet_transpose<0>, tp)
+                              : cudaLaunchKernelEx(&cfg, k_packet_transpose<1>, tp);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "transpose kernel launch");
+  return DV_OK;
+}
+
 dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, const Release& rel,
                       int max_ctas, cudaStream_t stream) {
+  if (p.kind == kTranspose) {
+    if (q_first != 0 || q_last < p.runs()) return fail(DV_ENOTSUP, "partial transpose plan");
+    return launch_transpose(p, rel, max_ctas, stream);
+  }
   if (q_last > p.runs()) q_last = p.runs();
   if (q_first > q_last) q_first = q_last;
   if (q_last == q_first || p.run_bytes == 0) {

@@ -41,6 +41,7 @@ FastDiv make_fastdiv(uint32_t d);
 // Run q (row-major over n[0..kDims-1], last innermost) starts at src + sum_k i_k*ss[k] and
 // dst + sum_k i_k*ds[k]; every run is run_bytes contiguous bytes on both sides.
 constexpr int kDims = 6;
+constexpr int kRun = 0, kTranspose = 1;
 struct CopyPlan {
   const uint8_t* src;
   uint8_t* dst;
@@ -54,6 +55,14 @@ struct CopyPlan {
   const int32_t* dyn = nullptr;
   int64_t dyn_ss = 0, dyn_ds = 0;
   int32_t dyn_max = 0;
+  // kind == kTranspose: 16-byte packet transpose (FT6D key <-> position-major). The loop dims
+  // n/ss/ds enumerate slabs (one (layer, request, head) each); inside a slab there are tU packets
+  // x tN positions; the packet-major side addresses u*t_su + s*16, the position-major side
+  // s*t_ss + u*16. tdir = 0: the source is packet-major; 1: the destination is.
+  int kind = 0;
+  uint32_t tU = 0, tN = 0;
+  int64_t t_su = 0, t_ss = 0;
+  int tdir = 0;
   uint64_t runs() const {
     uint64_t r = 1;
     for (int k = 0; k < kDims; ++k) r *= n[k];
