@@ -36,5 +36,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+def build_c_smoke(force: bool = False) -> str:
+    """Compile tests/c/abi_smoke.c against the library with plain gcc (the ABI used from C)."""
+    src = os.path.join(ROOT, "tests", "c", "abi_smoke.c")
+    out = os.path.join(ROOT, "tests", "c", "abi_smoke")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src), os.path.getmtime(OUT)):
+        return out
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-I", os.path.join(ROOT, "include"), src, "-L", HERE, "-ldvstream",
+           "-Wl,-rpath," + HERE, "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("gcc failed building tests/c/abi_smoke")
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,0 +1,151 @@
+/*
+ * abi_smoke.c -- the C ABI used from plain C (no Python, no torch): route a C3-like hand-off on
+ * the host, then (if a GPU is present) stream a small cache out to pinned host memory and back
+ * into a cache with another max_seq, and check every word against the writer's definition
+ * (computed here independently: word = low 16 bits of a simple coordinate code).
+ *
+ *   build:  gcc -O2 -I include tests/c/abi_smoke.c -L paper_2403_01876_b200 -ldvstream
+ *           -Wl,-rpath,paper_2403_01876_b200 -o tests/c/abi_smoke   (done by __graft_entry__.build)
+ *   run:    tests/c/abi_smoke [--route-only]
+ * Exit code 0 = pass.
+ */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "dv.h"
+
+#define CHECK(x)                                                                        \
+  do {                                                                                  \
+    dv_status _s = (x);                                                                 \
+    if (_s != DV_OK) {                                                                  \
+      fprintf(stderr, "%s:%d %s -> %s: %s\n", __FILE__, __LINE__, #x, dv_status_str(_s), \
+              dv_last_error());                                                         \
+      return 1;                                                                         \
+    }                                                                                   \
+  } while (0)
+
+/* cudaMemcpy without including CUDA headers: use the library's own host/device buffers and its
+ * flush/fetch (contiguous copies) so this file needs nothing but dv.h. */
+
+static int route_check(void) {
+  const int32_t pb[] = {0, 16, 32, 48, 64}, tb[] = {0, 13, 30, 47, 64}, rb[] = {0, 8};
+  dv_setup ps = {4, pb, 1, rb, 1024, 0, NULL}, ts = {4, tb, 1, rb, 2048, 0, NULL};
+  dv_region reg = {0, 64, 0, 8, 0, 1000, 0, 0};
+  uint64_t n = 0;
+  CHECK(dv_route(&ps, &ts, &reg, 72, 128, 2, NULL, 0, &n));
+  if (n != 7) {
+    fprintf(stderr, "C3 route: %llu pieces, expected 7\n", (unsigned long long)n);
+    return 1;
+  }
+  dv_piece pieces[7];
+  CHECK(dv_route(&ps, &ts, &reg, 72, 128, 2, pieces, 7, &n));
+  const int32_t exp[7][4] = {{0, 0, 0, 13}, {0, 1, 13, 16}, {1, 1, 16, 30}, {1, 2, 30, 32},
+                             {2, 2, 32, 47}, {2, 3, 47, 48}, {3, 3, 48, 64}};
+  for (int i = 0; i < 7; ++i)
+    if (pieces[i].src_stage != exp[i][0] || pieces[i].dst_stage != exp[i][1] ||
+        pieces[i].layer_begin != exp[i][2] || pieces[i].layer_end != exp[i][3]) {
+      fprintf(stderr, "C3 piece %d wrong\n", i);
+      return 1;
+    }
+  /* a position beyond max_seq is a range error naming the limit */
+  dv_region bad = {0, 64, 0, 8, 0, 1025, 0, 0};
+  if (dv_route(&ps, &ps, &bad, 72, 128, 2, NULL, 0, &n) != DV_ERANGE ||
+      !strstr(dv_last_error(), "1024")) {
+    fprintf(stderr, "expected DV_ERANGE naming 1024\n");
+    return 1;
+  }
+  printf("route ok\n");
+  return 0;
+}
+
+static uint16_t word(int kv, int l, int r, int h, int s, int d) {
+  return (uint16_t)(((((kv * 7 + l) * 13 + r) * 11 + h) * 101 + s) * 17 + d);
+}
+
+static int stream_check(void) {
+  const int L = 2, B = 2, H = 4, S = 40, S2 = 64, D = 16, P = 40;
+  dv_ctx* ctx;
+  CHECK(dv_create(0, NULL, &ctx));
+  const size_t n5 = (size_t)L * B * H * S * D, n6 = (size_t)L * B * H * S2 * D;
+  uint16_t *hk, *hv, *log, *ok2, *ov2;
+  void *dk, *dvv, *dk2, *dv2;
+  uint64_t* flags;
+  CHECK(dv_host_alloc(n5 * 2, (void**)&hk));
+  CHECK(dv_host_alloc(n5 * 2, (void**)&hv));
+  CHECK(dv_host_alloc(n5 * 4, (void**)&log));
+  CHECK(dv_host_alloc(n6 * 2, (void**)&ok2));
+  CHECK(dv_host_alloc(n6 * 2, (void**)&ov2));
+  CHECK(dv_host_alloc(64, (void**)&flags));
+  memset(flags, 0, 64);
+  for (int l = 0; l < L; ++l)
+    for (int r = 0; r < B; ++r)
+      for (int h = 0; h < H; ++h)
+        for (int s = 0; s < S; ++s)
+          for (int d = 0; d < D; ++d) {
+            const size_t i = ((((size_t)l * B + r) * H + h) * S + s) * D + d;
+            hk[i] = word(0, l, r, h, s, d);
+            hv[i] = word(1, l, r, h, s, d);
+          }
+  for (size_t i = 0; i < n6; ++i) ok2[i] = ov2[i] = 0xFFFF;
+  CHECK(dv_device_alloc(0, n5 * 2, &dk));
+  CHECK(dv_device_alloc(0, n5 * 2, &dvv));
+  CHECK(dv_device_alloc(0, n6 * 2, &dk2));
+  CHECK(dv_device_alloc(0, n6 * 2, &dv2));
+  /* upload with level-3 flushes into device endpoints */
+  dv_endpoint ek = {DV_EP_DEVICE, 0, dk, n5 * 2, NULL, 0, 0};
+  dv_endpoint ev = {DV_EP_DEVICE, 0, dvv, n5 * 2, NULL, 0, 0};
+  dv_endpoint ek2 = {DV_EP_DEVICE, 0, dk2, n6 * 2, NULL, 0, 0};
+  dv_endpoint ev2 = {DV_EP_DEVICE, 0, dv2, n6 * 2, NULL, 0, 0};
+  CHECK(dv_flush(ctx, hk, n5 * 2, &ek, 0, -1, 0, DV_XFER_STAGED, NULL));
+  CHECK(dv_flush(ctx, hv, n5 * 2, &ev, 0, -1, 0, DV_XFER_STAGED, NULL));
+  CHECK(dv_flush(ctx, ok2, n6 * 2, &ek2, 0, -1, 0, DV_XFER_STAGED, NULL));
+  CHECK(dv_flush(ctx, ov2, n6 * 2, &ev2, 0, -1, 0, DV_XFER_STAGED, NULL));
+  dv_cache src = {dk, dvv, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S, D, 0};
+  dv_cache dst = {dk2, dv2, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S2, D, 0};
+  const int32_t lb[] = {0, 2}, rb[] = {0, 2};
+  dv_setup one = {1, lb, 1, rb, S, 0, NULL}, big = {1, lb, 1, rb, S2, 0, NULL};
+  dv_region reg = {0, L, 0, B, 0, P, 0, 0};
+  dv_endpoint inbox = {DV_EP_HOST, -1, log, n5 * 4, flags, 1, 0};
+  CHECK(dv_stream_out(ctx, &src, &reg, &one, 0, 0, 0, &big, &inbox, 1, 1, DV_XFER_AUTO, NULL));
+  CHECK(dv_stream_in(ctx, &dst, &reg, &one, &big, 0, 0, 0, &inbox, 1, DV_XFER_AUTO, NULL));
+  /* download with level-3 fetches, then wait for everything */
+  dv_endpoint hk_ep = {DV_EP_HOST, -1, ok2, n6 * 2, NULL, 0, 0};
+  CHECK(dv_fetch(ctx, &ek2, 0, -1, 0, ok2, n6 * 2, DV_XFER_STAGED, NULL));
+  CHECK(dv_fetch(ctx, &ev2, 0, -1, 0, ov2, n6 * 2, DV_XFER_STAGED, NULL));
+  (void)hk_ep;
+  dv_endpoint fl = {DV_EP_HOST, -1, flags, 64, flags, 8, 0};
+  CHECK(dv_signal(ctx, &fl, 1, 42, NULL));
+  int32_t done = 0;
+  for (long spin = 0; spin < 2000000000L && !done; ++spin) CHECK(dv_query(ctx, &fl, 1, 42, &done));
+  if (!done || flags[0] != 1) {
+    fprintf(stderr, "flags not published (%llu)\n", (unsigned long long)flags[0]);
+    return 1;
+  }
+  size_t bad = 0;
+  for (int l = 0; l < L; ++l)
+    for (int r = 0; r < B; ++r)
+      for (int h = 0; h < H; ++h)
+        for (int s = 0; s < S2; ++s)
+          for (int d = 0; d < D; ++d) {
+            const size_t i = ((((size_t)l * B + r) * H + h) * S2 + s) * D + d;
+            const uint16_t ek_ = s < P ? word(0, l, r, h, s, d) : 0xFFFF;
+            const uint16_t ev_ = s < P ? word(1, l, r, h, s, d) : 0xFFFF;
+            bad += (ok2[i] != ek_) + (ov2[i] != ev_);
+          }
+  CHECK(dv_destroy(ctx));
+  if (bad) {
+    fprintf(stderr, "%zu words differ\n", bad);
+    return 1;
+  }
+  printf("stream ok\n");
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (dv_abi_version() != DV_ABI_VERSION) return 1;
+  if (route_check()) return 1;
+  if (argc > 1 && !strcmp(argv[1], "--route-only")) return 0;
+  return stream_check();
+}

@@ -16,6 +16,7 @@ def pytest_configure(config):
     # it raises if libdvstream.so is missing.
     from paper_2403_01876_b200 import build
     build.build()
+    build.build_c_smoke()
 
 
 def pytest_collection_modifyitems(config, items):

@@ -136,3 +136,19 @@ def test_route_with_tp_matches_oracle(seed):
     got = dv.dv_route(dv.Setup(sl, sr, 16, sh), dv.Setup(dl, dr, 16, dh), dv.region(*reg), Hn, 64, 2)
     F = FIELDS + ["src_tp", "dst_tp", "head_begin", "head_end"]
     assert [[getattr(p, f) for f in F] for p in got] == [[getattr(p, f) for f in F] for p in exp]
+
+
+def test_c_program_uses_the_abi_route_only():
+    """tests/c/abi_smoke.c: the ABI from plain C (gcc, no Python) -- host route + error naming."""
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "c", "abi_smoke")
+    r = subprocess.run([exe, "--route-only"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "route ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c_program_streams_through_the_abi():
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "c", "abi_smoke")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "stream ok" in r.stdout, r.stdout + r.stderr
