@@ -22,6 +22,8 @@
 //     observers then see the payload before the flag).
 #include <stdlib.h>
 
+#include <mutex>
+
 #include <algorithm>
 
 #include "dv_internal.h"
@@ -470,11 +472,10 @@ template <int VEC>
 static cudaError_t launch_bulk_vec(const KParams& kp, uint8_t* dst0, int max_ctas, cudaStream_t st) {
   constexpr int T = 256, U = 4;
   const int smem = 2 * T * U * VEC;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag once;
+  std::call_once(once, [smem] {
     cudaFuncSetAttribute(k_pack_bulk<VEC, U, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   const uint64_t need = (kp.n_vec + T * U - 1) / (T * U);
   const int blocks = (int)std::min<uint64_t>(need, (uint64_t)max_ctas);
   (void)cudaGetLastError();
@@ -535,12 +536,11 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
   tp.dyn_ds = p.dyn_ds;
   tp.dyn_max = p.dyn_max;
   const int smem = kTS * (p.tU + 1) * 16;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag once;
+  std::call_once(once, [] {
     cudaFuncSetAttribute(k_packet_transpose<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_packet_transpose<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
+  });
   if (smem > 64 * 1024) return fail(DV_ENOTSUP, "head_dim too large for the packet transpose");
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
