@@ -380,6 +380,19 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
 
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
 
+// Per-device "attribute already set" bits (function attributes are per device context).
+static bool first_use_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
+}
+template <int VEC>
+static std::atomic<uint64_t>& bulk_mask() {
+  static std::atomic<uint64_t> m{0};
+  return m;
+}
+
 static bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("DV_PDL");
@@ -472,10 +485,8 @@ template <int VEC>
 static cudaError_t launch_bulk_vec(const KParams& kp, uint8_t* dst0, int max_ctas, cudaStream_t st) {
   constexpr int T = 256, U = 4;
   const int smem = 2 * T * U * VEC;
-  static std::once_flag once;
-  std::call_once(once, [smem] {
+  if (first_use_on_device(bulk_mask<VEC>()))
     cudaFuncSetAttribute(k_pack_bulk<VEC, U, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
   const uint64_t need = (kp.n_vec + T * U - 1) / (T * U);
   const int blocks = (int)std::min<uint64_t>(need, (uint64_t)max_ctas);
   (void)cudaGetLastError();
@@ -536,11 +547,11 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
   tp.dyn_ds = p.dyn_ds;
   tp.dyn_max = p.dyn_max;
   const int smem = kTS * (p.tU + 1) * 16;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::atomic<uint64_t> mask{0};
+  if (first_use_on_device(mask)) {
     cudaFuncSetAttribute(k_packet_transpose<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_packet_transpose<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  });
+  }
   if (smem > 64 * 1024) return fail(DV_ENOTSUP, "head_dim too large for the packet transpose");
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
