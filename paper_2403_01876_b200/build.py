@@ -9,6 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libdvstream.so")
 SOURCES = ["route.cpp", "api.cu", "copy_kernels.cu", "testing.cu", "baselines.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("DV_NVCC_EXTRA", "").split()   # experiment hook, e.g. -DDV_MIN_BLOCKS=6
 FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-DDV_BUILD"]
@@ -23,7 +24,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         t = os.path.getmtime(OUT)
         if all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d)):
             return OUT
-    cmd = [NVCC] + FLAGS + srcs + ["-o", OUT + ".tmp", "-lrt", "-ldl", "-lpthread"]
+    cmd = [NVCC] + FLAGS + EXTRA + srcs + ["-o", OUT + ".tmp", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

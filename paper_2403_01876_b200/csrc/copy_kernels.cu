@@ -171,8 +171,11 @@ __device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsig
   }
 }
 
+#ifndef DV_MIN_BLOCKS
+#define DV_MIN_BLOCKS 1
+#endif
 template <int VEC, int U, int THREADS, int STM = 0>
-__global__ void __launch_bounds__(THREADS) k_run_copy(const KParams p) {
+__global__ void __launch_bounds__(THREADS, (THREADS == 256 ? DV_MIN_BLOCKS : 1)) k_run_copy(const KParams p) {
   // Programmatic dependent launch: this grid may become resident while the kernel that wrote the
   // K/V (e.g. attention) is still draining; wait here until that grid's memory is visible.
   if (p.ts && threadIdx.x == 0) {
