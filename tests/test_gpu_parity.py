@@ -791,3 +791,72 @@ def test_inbox_credit_loop_reuses_one_inbox_without_overwrite():
     assert np.array_equal(got_k[:, :, :, 1:R + 1], K[:, :, :, 1:R + 1])
     assert np.array_equal(got_v[:, :, :, 1:R + 1], V[:, :, :, 1:R + 1])
     assert np.all(got_k[:, :, :, R + 1:] == kvgen.SENTINEL) and np.all(got_k[:, :, :, 0] == kvgen.SENTINEL)
+
+
+def test_one_context_two_threads_two_streams_staged():
+    """One dv_ctx shared by two host threads on two streams, both hammering the staged paths
+    (shared staging pool with event-guarded reuse): every transfer lands intact."""
+    import threading
+    L, B, H, S, D = 2, 4, 8, 64, 128
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=81)
+    k, v, c = dev_cache(K, V, 0, 0)
+    osrc = oc(K, V, 0, 0, S)
+    cx = dv.dv_create(0, staging_bytes=4 << 20)   # small pool: forces wrap-around and reuse waits
+    errs = []
+
+    def worker(wid):
+        try:
+            st = torch.cuda.Stream()
+            for it in range(12):
+                s0 = (wid * 7 + it * 3) % (S - 16)
+                reg = (0, L, 0, B, s0, s0 + 16)
+                n = ok.region_bytes(*reg, H, D, 2)
+                host = torch.empty(n // 2, dtype=torch.int16, pin_memory=True)
+                dk = torch.full((L, B, H, S, D), -1, dtype=torch.int16, device="cuda")
+                dvv = torch.full_like(dk, -1)
+                with torch.cuda.stream(st):
+                    dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(host), 0, xfer=dv.DV_XFER_STAGED, stream=st)
+                    dv.dv_gather(cx, dv.endpoint_of(host), 0, dv.cache(dk, dvv), dv.region(*reg),
+                                 xfer=dv.DV_XFER_STAGED, stream=st)
+                st.synchronize()
+                if not np.array_equal(to_np(host), ok.pack(osrc, reg)):
+                    errs.append((wid, it, "wire"))
+                if not np.array_equal(to_np(dk)[:, :, :, s0:s0 + 16], K[:, :, :, s0:s0 + 16]):
+                    errs.append((wid, it, "cache"))
+        except Exception as e:  # pragma: no cover
+            errs.append((wid, repr(e)))
+    ths = [threading.Thread(target=worker, args=(w,)) for w in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    cx.close()
+    assert not errs, errs[:5]
+
+
+def test_more_validation_errors():
+    L, B, H, S, D = 2, 2, 2, 16, 16
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=82)
+    k, v, c = dev_cache(K, V, 0, 0)
+    buf = sentinel_like((4096,))
+    fl = flags(2)
+    cx = ctx()
+    cases = [
+        (lambda: dv.dv_scatter(cx, c, dv.region(0, 1, 0, 1, 0, 1), dv.endpoint_of(buf, fl), 0, flag_slot=5, seq=1),
+         dv.DV_EINVAL),                                           # flag slot beyond n_flags
+        (lambda: dv.dv_scatter(cx, c, dv.region(0, 1, 0, 1, 0, 1), dv.endpoint_of(buf), 8), dv.DV_EALIGN),
+        (lambda: dv.dv_scatter(cx, c, dv.region(0, 1, 0, 1, 0, 1, 1, 3), dv.endpoint_of(buf)), dv.DV_EMAP),
+        (lambda: dv.dv_gather_chunks(cx, dv.endpoint_of(buf), 0, c, dv.region(0, 1, 0, 1, 0, 2), 3, 1),
+         dv.DV_EINVAL),                                           # pos_step < positions per chunk
+        (lambda: dv.dv_gather_chunks(cx, dv.endpoint_of(buf), 0, c, dv.region(0, 1, 0, 1, 0, 1), 20, 1),
+         dv.DV_ERANGE),                                           # last chunk beyond max_seq
+        (lambda: dv.dv_ipc_open(b"\0" * 96), dv.DV_EPEER),        # malformed blob
+        (lambda: dv.dv_remap(cx, c, dv.cache(k[:, :, :, :, :8].contiguous(), v[:, :, :, :, :8].contiguous()),
+                             dv.region(0, 1, 0, 1, 0, 1)), dv.DV_EMAP),   # head_dim differs
+    ]
+    for fn, st in cases:
+        with pytest.raises(dv.DVError) as ei:
+            fn()
+        assert ei.value.status == st, (ei.value, st)
+    torch.cuda.synchronize()
+    assert np.all(to_np(buf) == kvgen.SENTINEL)
