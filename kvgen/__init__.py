@@ -138,3 +138,12 @@ def as_ft6d_key(K: np.ndarray, elem_bytes: int = 2) -> np.ndarray:
 def sentinel_cache(n_layers: int, n_reqs: int, n_heads: int, max_seq: int, head_dim: int):
     shape = (n_layers, n_reqs, n_heads, max_seq, head_dim)
     return (np.full(shape, SENTINEL, np.uint16), np.full(shape, SENTINEL, np.uint16))
+
+
+def random_cache(n_layers: int, n_reqs: int, n_heads: int, max_seq: int, head_dim: int,
+                 elem_bytes: int, seed: int):
+    """(K, V) of random words of 1, 2, 4 or 8 bytes (e.g. fp8 / fp32 KV caches), seeded."""
+    dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[elem_bytes]
+    rng = np.random.default_rng(seed)
+    shape = (n_layers, n_reqs, n_heads, max_seq, head_dim)
+    return tuple(rng.integers(0, np.iinfo(dt).max, shape, dtype=dt, endpoint=True) for _ in range(2))

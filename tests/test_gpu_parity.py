@@ -860,3 +860,36 @@ def test_more_validation_errors():
         assert ei.value.status == st, (ei.value, st)
     torch.cuda.synchronize()
     assert np.all(to_np(buf) == kvgen.SENTINEL)
+
+
+@pytest.mark.parametrize("elem_bytes", [1, 4, 8])
+def test_other_word_sizes_fp8_fp32_fp64(elem_bytes):
+    """The kernels move opaque words of any size with D*e % 16 == 0: fp8 (e=1), fp32 (e=4) and
+    fp64 (e=8) caches pack, unpack (other max_seq) and remap bit-exactly."""
+    tdt = {1: torch.int8, 4: torch.int32, 8: torch.int64}[elem_bytes]
+    ndt = {1: np.int8, 4: np.int32, 8: np.int64}[elem_bytes]
+    L, B, H, S, D = 3, 2, 3, 20, 32
+    K, V = kvgen.random_cache(L, B, H, S, D, elem_bytes, seed=90 + elem_bytes)
+    k = torch.from_numpy(K.view(ndt)).cuda()
+    v = torch.from_numpy(V.view(ndt)).cuda()
+    c = dv.cache(k, v, 2, 1)
+    o = ok.Cache(K, V, 2, 1, H, S, D)
+    reg = (3, 5, 1, 3, 4, 17)
+    exp = ok.pack(o, reg)
+    buf = torch.zeros(exp.size, dtype=tdt, device="cuda")
+    dv.dv_scatter(ctx(), c, dv.region(*reg), dv.endpoint_of(buf))
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.cpu().numpy().view(exp.dtype), exp)
+    S2 = 29
+    dk = torch.zeros((L, B, H, S2, D), dtype=tdt, device="cuda")
+    dvv = torch.zeros_like(dk)
+    dv.dv_gather(ctx(), dv.endpoint_of(buf), 0, dv.cache(dk, dvv, 2, 1), dv.region(*reg))
+    torch.cuda.synchronize()
+    od = ok.Cache(np.zeros((L, B, H, S2, D), K.dtype), np.zeros((L, B, H, S2, D), K.dtype), 2, 1, H, S2, D)
+    ok.unpack(od, reg, exp)
+    assert np.array_equal(dk.cpu().numpy().view(K.dtype), od.K) and np.array_equal(dvv.cpu().numpy().view(K.dtype), od.V)
+    rk = torch.zeros_like(dk)
+    rv = torch.zeros_like(dk)
+    dv.dv_remap(ctx(), c, dv.cache(rk, rv, 2, 1), dv.region(*reg))
+    torch.cuda.synchronize()
+    assert np.array_equal(rk.cpu().numpy().view(K.dtype), od.K) and np.array_equal(rv.cpu().numpy().view(K.dtype), od.V)
