@@ -9,6 +9,7 @@
  *   run:    tests/c/abi_smoke [--route-only]
  * Exit code 0 = pass.
  */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -143,9 +144,54 @@ static int stream_check(void) {
   return 0;
 }
 
+#include <time.h>
+
+/* Host-side enqueue cost of one dv_scatter call (validation + plan + kernel launch), measured from
+ * C with no Python in the loop: a C2-shaped per-layer token update (640 runs of 256 B) into a
+ * device buffer; batches of 500 calls (well inside the launch queue, so no call blocks on a
+ * full queue), synchronised between batches through a host-visible flag. */
+static int enqueue_bench(void) {
+  const int L = 40, B = 8, H = 40, S = 2048, D = 128;
+  dv_ctx* ctx;
+  CHECK(dv_create(0, NULL, &ctx));
+  const size_t n = (size_t)L * B * H * S * D * 2;
+  void *k, *v, *buf;
+  CHECK(dv_device_alloc(0, n, &k));
+  CHECK(dv_device_alloc(0, n, &v));
+  CHECK(dv_device_alloc(0, 1 << 20, &buf));
+  uint64_t* fl;
+  CHECK(dv_device_alloc(0, 64, (void**)&fl));
+  dv_cache c = {k, v, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S, D, 0};
+  dv_endpoint ep = {DV_EP_DEVICE, 0, buf, 1 << 20, fl, 1, 0};
+  const int N = 500, REP = 20;
+  uint64_t* hf;
+  CHECK(dv_host_alloc(64, (void**)&hf));
+  memset(hf, 0, 64);
+  dv_endpoint hep = {DV_EP_HOST, -1, hf, 64, hf, 1, 0};
+  double total_ns = 0;
+  for (int rep = 0; rep < REP + 1; ++rep) {
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (int i = 0; i < N; ++i) {
+      dv_region r = {i % L, i % L + 1, 0, B, 1000 + i % 1000, 1001 + i % 1000, 0, 0};
+      CHECK(dv_scatter(ctx, &c, &r, &ep, 0, 0, (uint64_t)(rep * N + i + 1), DV_XFER_FUSED, NULL));
+    }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    if (rep > 0) total_ns += (t1.tv_sec - t0.tv_sec) * 1e9 + (t1.tv_nsec - t0.tv_nsec);
+    CHECK(dv_signal(ctx, &hep, 0, (uint64_t)rep + 1, NULL));   /* drain before the next batch */
+    int32_t done = 0;
+    while (!done) CHECK(dv_query(ctx, &hep, 0, (uint64_t)rep + 1, &done));
+  }
+  const double us = total_ns / 1e3 / ((double)N * REP);
+  printf("{\"host_enqueue_us_per_dv_scatter_from_C\": %.3f, \"calls\": %d}\n", us, N * REP);
+  CHECK(dv_destroy(ctx));
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (dv_abi_version() != DV_ABI_VERSION) return 1;
   if (route_check()) return 1;
   if (argc > 1 && !strcmp(argv[1], "--route-only")) return 0;
+  if (argc > 1 && !strcmp(argv[1], "--enqueue-bench")) return enqueue_bench();
   return stream_check();
 }

@@ -146,6 +146,24 @@ def c3():
     emit(config="C3", op="prompt_gpu_16_layers_stream_out_direct (loopback, 2 pieces)", bytes=16 * layer_bytes,
          us=us_all, gbs_2R=2 * 16 * layer_bytes / us_all / 1e3, bound="hbm",
          frac=2 * 16 * layer_bytes / us_all / 1e3 / HBM, parity_mismatches=bad)
+    # batch sweep (BASELINE configs[2]: b = 8, sweep 16, 32): the 16-layer hand-off per prompt GPU
+    for bb in (16, 32):
+        pk2 = torch.empty((16, bb, H, 1024, D), dtype=torch.int16, device=dev)
+        pv2 = torch.empty_like(pk2)
+        pc2 = dv.cache(pk2, pv2, 0, 0)
+        dv.dvt_fill(pc2, dv.DVT_FILL_HASH, seed=SEED + 2, valid=(0, p))
+        ps2, ts2 = dv.Setup([0, 16, 32, 48, 64], [0, bb], 1024), dv.Setup([0, 13, 30, 47, 64], [0, bb], 2048)
+        a0 = new_cache(13, bb, H, 2048, D, 0, 0)
+        a1 = new_cache(17, bb, H, 2048, D, 13, 0)
+        us2 = timed(lambda: dv.dv_stream_out_direct(ctx, pc2, dv.region(0, 16, 0, bb, 0, p), ps2, 0, 0, ts2,
+                                                    [a0[2], a1[2], None, None], None, stream=sp), reps=2, warm=1)
+        nb2 = 16 * 2 * bb * H * p * D * 2
+        bad = sample_check(a1[0], a1[1], a1[2], (13, 16, 0, bb, 0, p), SEED + 2)
+        emit(config="C3", op=f"prompt_gpu_16_layers_stream_out_direct_b{bb} (loopback)", bytes=nb2, us=us2,
+             gbs_2R=2 * nb2 / us2 / 1e3, bound="hbm", frac=2 * nb2 / us2 / 1e3 / HBM,
+             ideal_nvlink_ms_at_770=nb2 / 770e6, parity_mismatches=bad)
+        del pk2, pv2, a0, a1
+        torch.cuda.empty_cache()
     # inbox form: pack into the token blocks' inboxes, then each token block unpacks
     inb0 = torch.empty(13 * layer_bytes // 2, dtype=torch.int16, device=dev)
     inb1 = torch.empty(17 * layer_bytes // 2, dtype=torch.int16, device=dev)
