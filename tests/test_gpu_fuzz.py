@@ -1,0 +1,111 @@
+"""Seeded random differential test: hundreds of random operations (level 1/2, KV5D/FT6D on either
+side, TP head ranges, fused/staged/auto, device/host endpoints, log chunks, graph-style dynamic
+steps) through the C ABI, each compared word for word with the CPU oracle."""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import paper_2403_01876_b200 as dv
+from oracle import kvstream as ok
+
+pytestmark = pytest.mark.gpu
+
+XF = [dv.DV_XFER_AUTO, dv.DV_XFER_FUSED, dv.DV_XFER_STAGED]
+
+
+def to_dev(a, pinned=False):
+    t = torch.from_numpy(np.ascontiguousarray(a).view(np.int16))
+    if pinned:
+        p = torch.empty(t.shape, dtype=torch.int16, pin_memory=True)
+        p.copy_(t)
+        return p
+    return t.cuda()
+
+
+def to_np(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def mk_cache(rng, lb, nl, rb, nr, hb, nh, S, D, layout, seed, pinned=False, sentinel=False):
+    if sentinel:
+        K, V = kvgen.sentinel_cache(nl, nr, nh, S, D)
+    else:
+        K, V = kvgen.kv5d_cache("hash", lb, nl, rb, nr, nh, S, D, seed=seed, head_begin=hb)
+    Kp = kvgen.as_ft6d_key(K) if layout == ok.LAYOUT_FT6D else K
+    k, v = to_dev(Kp, pinned), to_dev(V, pinned)
+    return k, v, dv.cache(k, v, lb, rb, head_begin=hb), ok.Cache(Kp.copy(), V.copy(), lb, rb, nh, S, D, layout, hb)
+
+
+def rand_region(rng, lb, nl, rb, nr, hb, nh, S):
+    l0 = rng.randint(lb, lb + nl - 1); l1 = rng.randint(l0 + 1, lb + nl)
+    r0 = rng.randint(rb, rb + nr - 1); r1 = rng.randint(r0 + 1, rb + nr)
+    s0 = rng.randint(0, S - 1); s1 = rng.randint(s0 + 1, min(S, s0 + rng.choice([1, 2, 5, 40, S])))
+    if rng.random() < 0.5:
+        return (l0, l1, r0, r1, s0, s1, 0, 0)
+    h0 = rng.randint(hb, hb + nh - 1); h1 = rng.randint(h0 + 1, hb + nh)
+    return (l0, l1, r0, r1, s0, s1, h0, h1)
+
+
+@pytest.mark.parametrize("block", range(12))
+def test_random_ops_against_oracle(block):
+    rng = random.Random(12345 + block)
+    cx = dv.dv_create(0, staging_bytes=rng.choice([1 << 20, 8 << 20, 0]))
+    for it in range(40):
+        D = rng.choice([16, 64, 128])
+        nl, nr, nh = rng.randint(1, 4), rng.randint(1, 3), rng.randint(1, 5)
+        lb, rb, hb = rng.randint(0, 5), rng.randint(0, 5), rng.randint(0, 3)
+        S = rng.randint(4, 48)
+        lay = [rng.choice([ok.LAYOUT_KV5D, ok.LAYOUT_FT6D]) for _ in range(2)]
+        seed = rng.randint(0, 1 << 30)
+        op = rng.choice(["scatter_gather", "remap", "chunks", "dyn"])
+        xf = rng.choice(XF)
+        host = rng.random() < 0.4
+        k, v, c, o = mk_cache(rng, lb, nl, rb, nr, hb, nh, S, D, lay[0], seed, pinned=(op == "remap" and host))
+        reg = rand_region(rng, lb, nl, rb, nr, hb, nh, S)
+        # destination: superset cache with other offsets / max_seq / layout
+        S2 = (S if op == "chunks" else reg[5]) + rng.randint(0, 8)
+        dk, dvv, dc, do = mk_cache(rng, lb, nl, rb, nr, hb, nh, S2, D, lay[1], 0, sentinel=True,
+                                   pinned=(op == "remap" and not host and rng.random() < 0.5))
+        ctx_info = (block, it, op, xf, host, lay, reg)
+        if op in ("scatter_gather", "dyn"):
+            words = ok.region_bytes(reg[0], reg[1], reg[2], reg[3], reg[4], reg[5],
+                                    (reg[7] - reg[6]) if reg[7] > reg[6] else nh, D, 2) // 2
+            if op == "dyn":
+                kmax = S - reg[5]
+                kk = rng.randint(0, kmax) if kmax > 0 else 0
+                buf = torch.full(((kmax + 1) * words,), -1, dtype=torch.int16, device="cuda")
+                d_step = torch.tensor([kk], dtype=torch.int32, device="cuda")
+                dv.dv_scatter_dyn(cx, c, dv.region(*reg), dv.endpoint_of(buf), 0, words * 2, d_step.data_ptr(), kmax)
+                torch.cuda.synchronize()
+                sreg = ok.shifted(reg, kk)
+                got = to_np(buf)
+                assert np.array_equal(got[kk * words:(kk + 1) * words], ok.pack(o, sreg)), ctx_info
+                continue
+            buf = (torch.full((words + 8,), -1, dtype=torch.int16, pin_memory=True) if host
+                   else torch.full((words + 8,), -1, dtype=torch.int16, device="cuda"))
+            dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(buf), 16, xfer=xf)
+            torch.cuda.synchronize()
+            exp = ok.pack(o, reg)
+            assert np.array_equal(to_np(buf)[8:8 + words], exp), ctx_info
+            dv.dv_gather(cx, dv.endpoint_of(buf), 16, dc, dv.region(*reg), xfer=xf)
+            torch.cuda.synchronize()
+            ok.unpack(do, reg, exp)
+        elif op == "remap":
+            dv.dv_remap(cx, c, dc, dv.region(*reg), xfer=xf)
+            torch.cuda.synchronize()
+            ok.remap(o, do, reg)
+        else:  # chunks: a log of single- or multi-position chunks
+            n = reg[5] - reg[4]
+            step = n + rng.randint(0, 2)
+            nck = max(1, (S - reg[5]) // step + 1)
+            first = reg
+            log_np = np.concatenate([ok.pack(o, ok.shifted(first, kq * step)) for kq in range(nck)])
+            log = to_dev(log_np, pinned=host)
+            dv.dv_gather_chunks(cx, dv.endpoint_of(log), 0, dc, dv.region(*first), nck, step, xfer=xf)
+            torch.cuda.synchronize()
+            ok.unpack_chunks(do, first, log_np, nck, step)
+        assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V), ctx_info
+    cx.close()
