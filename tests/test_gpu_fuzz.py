@@ -109,3 +109,77 @@ def test_random_ops_against_oracle(block):
             ok.unpack_chunks(do, first, log_np, nck, step)
         assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V), ctx_info
     cx.close()
+
+
+def _bounds(rng, lo, hi, k):
+    cuts = sorted(rng.sample(range(lo + 1, hi), k - 1)) if k > 1 else []
+    return [lo] + cuts + [hi]
+
+
+@pytest.mark.parametrize("block", range(8))
+def test_random_stream_out_in_against_oracle(block):
+    """Random pipeline setups on both sides (layer partitions, microbatch splits, optional TP head
+    splits, either cache layout per block), inbox (device or pinned host) or direct form."""
+    rng = random.Random(777 + block)
+    cx = dv.dv_create(0)
+    for it in range(6):
+        D = rng.choice([16, 64])
+        L, R, Hn = rng.randint(1, 8), rng.randint(1, 4), rng.randint(1, 6)
+        tp = rng.random() < 0.5
+        sl, dl = _bounds(rng, 0, L, rng.randint(1, min(L, 3))), _bounds(rng, 0, L, rng.randint(1, min(L, 3)))
+        sr, dr = _bounds(rng, 0, R, rng.randint(1, min(R, 2))), _bounds(rng, 0, R, rng.randint(1, min(R, 2)))
+        sh = _bounds(rng, 0, Hn, rng.randint(1, min(Hn, 3))) if tp else None
+        dh = _bounds(rng, 0, Hn, rng.randint(1, min(Hn, 3))) if tp else None
+        S1, S2 = rng.randint(4, 24), rng.randint(4, 24)
+        p = rng.randint(1, min(S1, S2))
+        ps, ts = ok.Setup(sl, sr, S1, sh), ok.Setup(dl, dr, S2, dh)
+        dps, dts = dv.Setup(sl, sr, S1, sh), dv.Setup(dl, dr, S2, dh)
+        seed = rng.randint(0, 1 << 30)
+        form = rng.choice(["inbox_dev", "inbox_host", "direct"])
+        xf = rng.choice(XF)
+
+        def blocks(s, lb_, rb_, hb_):
+            hbs = hb_ if hb_ is not None else [0, Hn]
+            for i in range(len(lb_) - 1):
+                for u in range(len(rb_) - 1):
+                    for t in range(len(hbs) - 1):
+                        key = (i, u, t) if hb_ is not None else (i, u)
+                        yield key, (i, u, t), lb_[i], lb_[i + 1] - lb_[i], rb_[u], rb_[u + 1] - rb_[u], hbs[t], hbs[t + 1] - hbs[t]
+        src, osrc, dst, odst = {}, {}, {}, {}
+        for key, (i, u, t), a, nl, c0, nr, h0, nh in blocks(ps, sl, sr, sh):
+            k, v, c, o = mk_cache(rng, a, nl, c0, nr, h0, nh, S1, D, rng.choice([0, 1]), seed)
+            src[key], osrc[key] = (k, v, c, (i, u, t)), o
+        for key, (j, w, t), a, nl, c0, nr, h0, nh in blocks(ts, dl, dr, dh):
+            k, v, c, o = mk_cache(rng, a, nl, c0, nr, h0, nh, S2, D, rng.choice([0, 1]), 0, sentinel=True)
+            dst[key], odst[key] = (k, v, c, (j, w, t)), o
+        reg = (0, L, 0, R, 0, p)
+        dkeys = sorted(dst, key=lambda kk: dts.flat(*dst[kk][3]))
+        nsrc = ps.n_stages * ps.n_micro * ps.n_tp
+        keep = []
+        if form == "direct":
+            caches = [dst[kk][2] for kk in dkeys]
+            for key, (k, v, c, (i, u, t)) in src.items():
+                dv.dv_stream_out_direct(cx, c, dv.region(*reg), dps, i, u, dts, caches, None, seq=1, my_tp=t)
+        else:
+            eps = []
+            for kk in dkeys:
+                c = dst[kk][2]
+                words = c.n_layers * 2 * c.n_reqs * c.n_heads * p * D
+                buf = (torch.full((words,), -1, dtype=torch.int16, pin_memory=True) if form == "inbox_host"
+                       else torch.full((words,), -1, dtype=torch.int16, device="cuda"))
+                fl = (torch.zeros(nsrc, dtype=torch.int64, pin_memory=True) if form == "inbox_host"
+                      else torch.zeros(nsrc, dtype=torch.int64, device="cuda"))
+                keep += [buf, fl]
+                eps.append(dv.endpoint_of(buf, fl))
+            for key, (k, v, c, (i, u, t)) in src.items():
+                dv.dv_stream_out(cx, c, dv.region(*reg), dps, i, u, dts, eps, seq=1, xfer=xf, my_tp=t)
+            for n_, kk in enumerate(dkeys):
+                j, w, t = dst[kk][3]
+                dv.dv_stream_in(cx, dst[kk][2], dv.region(*reg), dps, dts, j, w, eps[n_], 1, xfer=xf, my_tp=t)
+        torch.cuda.synchronize()
+        ok.stream(osrc, ps, odst, ts, reg)
+        for kk in dst:
+            k, v = dst[kk][0], dst[kk][1]
+            assert np.array_equal(to_np(k), odst[kk].K) and np.array_equal(to_np(v), odst[kk].V), \
+                (block, it, form, xf, sl, dl, sr, dr, sh, dh, kk)
+    cx.close()
