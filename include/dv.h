@@ -210,6 +210,11 @@ DV_API dv_status dv_host_free(void* p);
 DV_API dv_status dv_device_alloc(int32_t device, uint64_t bytes, void** out); /* IPC-exportable */
 DV_API dv_status dv_device_free(void* p);
 
+/* One process driving several GPUs: let `device` access `peer`'s memory directly (NVLink P2P);
+ * idempotent. Pointers of `peer` allocations can then be used as DV_EP_PEER endpoints or caches
+ * in calls on `device`'s context. DV_EPEER if the pair cannot access each other. */
+DV_API dv_status dv_peer_enable(int32_t device, int32_t peer);
+
 typedef struct dv_ipc_blob { uint8_t bytes[96]; } dv_ipc_blob; /* opaque, copyable between processes */
 /* Export device memory at `ptr` (any address inside a cudaMalloc allocation). */
 DV_API dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out);

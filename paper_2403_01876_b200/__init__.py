@@ -91,6 +91,7 @@ _SIGS = {
     "dv_host_free": (C.c_int, [C.c_void_p]),
     "dv_device_alloc": (C.c_int, [C.c_int32, C.c_uint64, P(C.c_void_p)]),
     "dv_device_free": (C.c_int, [C.c_void_p]),
+    "dv_peer_enable": (C.c_int, [C.c_int32, C.c_int32]),
     "dv_ipc_export": (C.c_int, [C.c_void_p, P(dv_ipc_blob)]),
     "dv_ipc_open": (C.c_int, [P(dv_ipc_blob), P(C.c_void_p)]),
     "dv_ipc_close": (C.c_int, [C.c_void_p]),
@@ -351,6 +352,10 @@ def dv_device_alloc(device, nbytes) -> int:
 
 def dv_device_free(p):
     _call("dv_device_free", C.c_void_p(p))
+
+
+def dv_peer_enable(device, peer):
+    _call("dv_peer_enable", device, peer)
 
 
 def dv_ipc_export(ptr) -> bytes:

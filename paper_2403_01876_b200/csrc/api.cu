@@ -805,6 +805,25 @@ dv_status dv_device_free(void* p) {
   return DV_OK;
 }
 
+dv_status dv_peer_enable(int32_t device, int32_t peer) {
+  int n = 0;
+  DV_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n || peer < 0 || peer >= n)
+    return fail(DV_EINVAL, "device pair (%d,%d) out of range [0,%d)", device, peer, n);
+  if (device == peer) return DV_OK;  // a device always reaches its own memory
+  int can = 0;
+  DV_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return fail(DV_EPEER, "device %d cannot access device %d", device, peer);
+  DV_ON_DEVICE(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();
+    return DV_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return DV_OK;
+}
+
 dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out) {
   if (!ptr || !out) return fail(DV_EINVAL, "NULL argument");
   const Driver* d;

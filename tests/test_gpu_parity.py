@@ -893,3 +893,14 @@ def test_other_word_sizes_fp8_fp32_fp64(elem_bytes):
     dv.dv_remap(ctx(), c, dv.cache(rk, rv, 2, 1), dv.region(*reg))
     torch.cuda.synchronize()
     assert np.array_equal(rk.cpu().numpy().view(K.dtype), od.K) and np.array_equal(rv.cpu().numpy().view(K.dtype), od.V)
+
+
+def test_peer_enable():
+    dv.dv_peer_enable(0, 0)                       # self: always reachable
+    n = torch.cuda.device_count()
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_peer_enable(0, n)                   # out of range
+    assert ei.value.status == dv.DV_EINVAL
+    for peer in range(1, n):                      # only on multi-GPU boxes
+        dv.dv_peer_enable(0, peer)
+        dv.dv_peer_enable(0, peer)                # idempotent
