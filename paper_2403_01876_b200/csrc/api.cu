@@ -361,6 +361,12 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
                                 cudaStream_t st, int ctas) {
   const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
   const Release none{nullptr, 0, nullptr};
+  if (np == 2) {
+    DV_TRY(launch_copy2(p[0], p[1], streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag),
+                        ctas, st));
+    if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
+    return DV_OK;
+  }
   for (int q = 0; q < np; ++q) {
     const bool last = q == np - 1;
     DV_TRY(launch_copy(p[q], 0, p[q].runs(),
@@ -622,9 +628,8 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
   const int ctas = (op.src->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas : ctx->max_ctas;
-  for (int q = 0; q < np; ++q)
-    DV_TRY(launch_copy(p[q], 0, p[q].runs(), Release{nullptr, 0, nullptr}, ctas, st));
-  return DV_OK;
+  if (np == 2) return launch_copy2(p[0], p[1], Release{nullptr, 0, nullptr}, ctas, st);
+  return launch_copy(p[0], 0, p[0].runs(), Release{nullptr, 0, nullptr}, ctas, st);
 }
 
 struct RemapOp {

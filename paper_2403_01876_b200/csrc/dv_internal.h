@@ -86,6 +86,10 @@ struct Release {
 // the last launch carries `rel` (an empty range still publishes the flag).
 dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, const Release& rel,
                       int max_ctas, cudaStream_t stream);
+// Two whole plans (K and V of different structure) in ONE launch when possible, else two; the
+// release goes with the (last) launch.
+dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel, int max_ctas,
+                       cudaStream_t stream);
 
 // ---- CUDA driver entry points (resolved through the runtime; no -lcuda) --------------------
 struct Driver {
