@@ -495,7 +495,10 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
     TView w2[2] = {wire_view(stg, 0, &sub, row), wire_view(stg, 1, &sub, row)};
     CopyPlan ps[2];
     const int n2 = build_plans(s2, w2, &sub, row, ORDER_WIRE, Outer{}, ps);
-    for (int q = 0; q < n2; ++q) DV_TRY(launch_copy(ps[q], 0, ps[q].runs(), none, ctx->max_ctas, st));
+    if (n2 == 2)
+      DV_TRY(launch_copy2(ps[0], ps[1], none, ctx->max_ctas, st));
+    else
+      DV_TRY(launch_copy(ps[0], 0, ps[0].runs(), none, ctx->max_ctas, st));
     DV_TRY(hand_off(ctx, st, ds));
     DV_DMA(cudaMemcpyAsync(wire + (uint64_t)(la - reg.layer_begin) * slab, stg, nb,
                            cudaMemcpyDefault, ds));
@@ -557,7 +560,10 @@ static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache*
     TView c2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
     CopyPlan ps[2];
     const int n2 = build_plans(w2, c2, &sub, row, ORDER_WIRE, Outer{}, ps);
-    for (int q = 0; q < n2; ++q) DV_TRY(launch_copy(ps[q], 0, ps[q].runs(), none, ctx->max_ctas, st));
+    if (n2 == 2)
+      DV_TRY(launch_copy2(ps[0], ps[1], none, ctx->max_ctas, st));
+    else
+      DV_TRY(launch_copy(ps[0], 0, ps[0].runs(), none, ctx->max_ctas, st));
     DV_TRY(ctx->staging.release(off, nb, st));
   }
   return DV_OK;
@@ -1034,8 +1040,8 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
       np += 1;
     }
     const int ctas = (base == wire && src->kind == DV_EP_HOST) ? ctx->host_ctas : ctx->max_ctas;
-    for (int q = 0; q < np; ++q) DV_TRY(launch_copy(p[q], 0, p[q].runs(), none, ctas, st));
-    return DV_OK;
+    if (np == 2) return launch_copy2(p[0], p[1], none, ctas, st);
+    return launch_copy(p[0], 0, p[0].runs(), none, ctas, st);
   };
   if (mode == DV_XFER_FUSED) return unpack_group(wire, 0, n_chunks);
   const uint64_t half = ctx->staging.capacity() / 2;

@@ -171,6 +171,31 @@ __device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsig
   }
 }
 
+// The grid-stride body of the run copy: CTA `bid` of `nb` moves chunks of THREADS*U vectors.
+template <int VEC, int U, int THREADS, int STM = 0>
+__device__ __forceinline__ void run_chunks(const KParams& p, const uint8_t* src, uint8_t* dst,
+                                           uint32_t bid, uint32_t nb) {
+  const uint32_t chunk = THREADS * U;
+  for (uint32_t base = bid * chunk; base < p.n_vec; base += nb * chunk) {
+    Vec<VEC> v[U];
+    uint8_t* d[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t g = base + i * THREADS + threadIdx.x;
+      if (g < p.n_vec) {
+        const uint8_t* s;
+        locate<VEC>(p, src, dst, g, s, d[i]);
+        ld_vec(v[i], s);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t g = base + i * THREADS + threadIdx.x;
+      if (g < p.n_vec) st_vec_m<STM>(d[i], v[i]);
+    }
+  }
+}
+
 #ifndef DV_MIN_BLOCKS
 #define DV_MIN_BLOCKS 1
 #endif
@@ -194,27 +219,8 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 ? DV_MIN_BLOCKS : 1))
     k = *p.dyn;
     if (k < 0 || k > p.dyn_max) return;  // uniform across the grid: nothing moves, nothing published
   }
-  const uint8_t* src = p.src + (int64_t)k * p.dyn_ss;
-  uint8_t* dst = p.dst + (int64_t)k * p.dyn_ds;
-  const uint32_t chunk = THREADS * U;
-  for (uint32_t base = blockIdx.x * chunk; base < p.n_vec; base += gridDim.x * chunk) {
-    Vec<VEC> v[U];
-    uint8_t* d[U];
-#pragma unroll
-    for (int i = 0; i < U; ++i) {
-      const uint32_t g = base + i * THREADS + threadIdx.x;
-      if (g < p.n_vec) {
-        const uint8_t* s;
-        locate<VEC>(p, src, dst, g, s, d[i]);
-        ld_vec(v[i], s);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < U; ++i) {
-      const uint32_t g = base + i * THREADS + threadIdx.x;
-      if (g < p.n_vec) st_vec_m<STM>(d[i], v[i]);
-    }
-  }
+  run_chunks<VEC, U, THREADS, STM>(p, p.src + (int64_t)k * p.dyn_ss, p.dst + (int64_t)k * p.dyn_ds,
+                                   blockIdx.x, gridDim.x);
   if (p.ts) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -345,19 +351,11 @@ struct TParams {
 };
 
 template <int DIR>
-__global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
-  extern __shared__ uint4 tile[];  // kTS rows x (U + 1) packets
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  int32_t k = 0;
-  if (p.dyn) {
-    k = *p.dyn;
-    if (k < 0 || k > p.dyn_max) return;
-  }
-  const uint8_t* src0 = p.src + (int64_t)k * p.dyn_ss;
-  uint8_t* dst0 = p.dst + (int64_t)k * p.dyn_ds;
+__device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, const uint8_t* src0,
+                                                uint8_t* dst0, uint32_t bid, uint32_t nb) {
   const uint32_t row = p.U + 1;
   const uint32_t elems = p.U * kTS;
-  for (uint32_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+  for (uint32_t t = bid; t < p.n_tiles; t += nb) {
     uint32_t slab, ti;
     p.fT.divmod(t, slab, ti);
     const uint32_t s0 = ti * kTS;
@@ -413,12 +411,53 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
     }
     __syncthreads();
   }
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
+  extern __shared__ uint4 tile[];  // kTS rows x (U + 1) packets
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int32_t k = 0;
+  if (p.dyn) {
+    k = *p.dyn;
+    if (k < 0 || k > p.dyn_max) return;
+  }
+  const uint8_t* src0 = p.src + (int64_t)k * p.dyn_ss;
+  uint8_t* dst0 = p.dst + (int64_t)k * p.dyn_ds;
+  transpose_tiles<DIR>(p, tile, src0, dst0, blockIdx.x, gridDim.x);
   if (p.flag) {
     KParams kp{};
     kp.flag = p.flag;
     kp.ticket = p.ticket;
     kp.ts = p.ts;
     publish(kp, p.per_cta_sys, p.seq + (unsigned long long)k);
+  }
+}
+
+// An FT6D key transpose and the value's run copy in ONE launch: CTAs [0, t_blocks) transpose, the
+// rest run-copy; both halves share the dependency wait, the step counter and the release.
+template <int DIR, int VEC>
+__global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KParams r,
+                                                       uint32_t t_blocks) {
+  extern __shared__ uint4 tile[];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int32_t k = 0;
+  if (t.dyn) {
+    k = *t.dyn;
+    if (k < 0 || k > t.dyn_max) return;
+  }
+  if (blockIdx.x < t_blocks)
+    transpose_tiles<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
+                         blockIdx.x, t_blocks);
+  else
+    run_chunks<VEC, 4, 256>(r, r.src + (int64_t)k * r.dyn_ss, r.dst + (int64_t)k * r.dyn_ds,
+                            blockIdx.x - t_blocks, gridDim.x - t_blocks);
+  if (t.flag) {
+    KParams kp{};
+    kp.flag = t.flag;
+    kp.ticket = t.ticket;
+    kp.ts = t.ts;
+    publish(kp, t.per_cta_sys, t.seq + (unsigned long long)k);
   }
 }
 
@@ -555,8 +594,7 @@ static cudaError_t launch_bulk(const KParams& kp, int vec, uint8_t* dst0, int ma
                    : launch_bulk_vec<16>(kp, dst0, max_ctas, st);
 }
 
-static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max_ctas,
-                                  cudaStream_t stream) {
+static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* out) {
   TParams tp{};
   tp.src = p.src;
   tp.dst = p.dst;
@@ -573,6 +611,7 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
     if (p.n[k] != 1) return fail(DV_ENOTSUP, "transpose plan with more than 4 slab dims");
   const uint64_t tiles = (p.tN + kTS - 1) / kTS;
   if (slabs * tiles >= (1ull << 31) || p.tU > 256) return fail(DV_ENOTSUP, "transpose too large");
+  if (kTS * (p.tU + 1) * 16 > 64 * 1024) return fail(DV_ENOTSUP, "head_dim too large for the packet transpose");
   tp.n_tiles = (uint32_t)(slabs * tiles);
   tp.tiles_per_slab = (uint32_t)tiles;
   tp.fT = to_dev(make_fastdiv((uint32_t)tiles));
@@ -590,13 +629,28 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
   tp.dyn_ss = p.dyn_ss;
   tp.dyn_ds = p.dyn_ds;
   tp.dyn_max = p.dyn_max;
-  const int smem = kTS * (p.tU + 1) * 16;
+  *out = tp;
+  return DV_OK;
+}
+
+static void set_transpose_smem() {
   static std::atomic<uint64_t> mask{0};
   if (first_use_on_device(mask)) {
     cudaFuncSetAttribute(k_packet_transpose<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_packet_transpose<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   }
-  if (smem > 64 * 1024) return fail(DV_ENOTSUP, "head_dim too large for the packet transpose");
+}
+
+static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max_ctas,
+                                  cudaStream_t stream) {
+  TParams tp;
+  DV_TRY(fill_tparams(p, rel, &tp));
+  const int smem = kTS * (p.tU + 1) * 16;
+  set_transpose_smem();
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tp.n_tiles, (uint64_t)max_ctas)));
@@ -659,8 +713,55 @@ static cudaError_t go2(const KParams& a, const KParams& b, int blocks, cudaStrea
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// FT6D key transpose + value run copy in one launch; CTAs split in proportion to the bytes.
+static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, const Release& rel,
+                                      int max_ctas, cudaStream_t stream) {
+  TParams tp;
+  DV_TRY(fill_tparams(t, rel, &tp));
+  const uint64_t orall = align_bits(r);
+  if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
+  const int VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
+  KParams kr;
+  fill_kparams(r, VEC, &kr);
+  const double tb = (double)tp.n_tiles * kTS * t.tU * 16, rb = (double)r.runs() * r.run_bytes;
+  const uint64_t t_need = tp.n_tiles, r_need = (kr.n_vec + 1023) / 1024;
+  const uint64_t grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, t_need + r_need));
+  uint64_t t_blocks = (uint64_t)(grid * tb / (tb + rb) + 0.5);
+  t_blocks = std::min(std::max<uint64_t>(1, t_blocks), grid - 1);
+  set_transpose_smem();
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kTS * (t.tU + 1) * 16;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const uint32_t tbk = (uint32_t)t_blocks;
+  cudaError_t e;
+  if (t.tdir == 0)
+    e = VEC == 32 ? cudaLaunchKernelEx(&cfg, k_transpose_run<0, 32>, tp, kr, tbk)
+                  : cudaLaunchKernelEx(&cfg, k_transpose_run<0, 16>, tp, kr, tbk);
+  else
+    e = VEC == 32 ? cudaLaunchKernelEx(&cfg, k_transpose_run<1, 32>, tp, kr, tbk)
+                  : cudaLaunchKernelEx(&cfg, k_transpose_run<1, 16>, tp, kr, tbk);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "transpose+run kernel launch");
+  return DV_OK;
+}
+
 dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel, int max_ctas,
                        cudaStream_t stream) {
+  if ((a.kind == kTranspose) != (b.kind == kTranspose) && a.dyn == b.dyn) {
+    const CopyPlan& t = a.kind == kTranspose ? a : b;
+    const CopyPlan& r = a.kind == kTranspose ? b : a;
+    if (r.runs() && r.run_bytes && r.runs() * r.run_bytes / 16 < (1ull << 31))
+      return launch_transpose_run(t, r, rel, max_ctas, stream);
+  }
   // Fall back to two launches when the pair does not fit the single-launch form.
   const bool fits = a.kind == kRun && b.kind == kRun && a.run_bytes && b.run_bytes &&
                     a.runs() && b.runs() && a.dyn == b.dyn &&
