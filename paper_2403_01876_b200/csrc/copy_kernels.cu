@@ -348,7 +348,98 @@ struct TParams {
   const int32_t* dyn;
   int64_t dyn_ss, dyn_ds;
   int32_t dyn_max;
+  // register form (transpose_regs): items = slabs x (U / PK) packet groups x N positions
+  uint32_t n_items;
+  DevDiv fN, fG;
+  int32_t pk;    // packets per thread item (1 or 2); 0 = shared-memory tiles
 };
+
+// Register form of the packet transpose: no shared memory, no barrier. A thread item is PK
+// adjacent packets of ONE position: on the packet-major side the PK 16-byte loads (or stores) of a
+// warp's 32 consecutive positions are PK fully coalesced 512-byte segments; on the
+// position-major side each item is one PK*16-byte vector (PK = 2: a whole 32-byte sector). Four
+// items per thread are in flight before the first store.
+template <int DIR, int PK>
+__device__ __forceinline__ void transpose_regs(const TParams& p, const uint8_t* src0, uint8_t* dst0,
+                                               uint32_t bid, uint32_t nb) {
+  constexpr int IT = PK == 4 ? 2 : 4;
+  for (uint32_t b0 = bid * IT * 256; b0 < p.n_items; b0 += nb * IT * 256) {
+    Vec<16 * PK> v[IT];
+    uint8_t* d[IT];
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const uint32_t i = b0 + j * 256 + threadIdx.x;
+      d[j] = nullptr;
+      if (i < p.n_items) {
+        uint32_t rest, s, slab, g;
+        p.fN.divmod(i, rest, s);
+        p.fG.divmod(rest, slab, g);
+        int64_t so = 0, dof = 0;
+        uint32_t q = slab;
+#pragma unroll
+        for (int k = 3; k >= 1; --k) {
+          uint32_t x;
+          p.fd[k].divmod(q, q, x);
+          so += (int64_t)x * p.ss[k];
+          dof += (int64_t)x * p.ds[k];
+        }
+        so += (int64_t)q * p.ss[0];
+        dof += (int64_t)q * p.ds[0];
+        const uint32_t u0 = g * PK;
+        if (DIR == 0) {  // packet-major source, position-major destination
+          const uint8_t* a = src0 + so + (int64_t)u0 * p.su + (int64_t)s * 16;
+#pragma unroll
+          for (int k = 0; k < PK; ++k) {
+            Vec<16> w;
+            ld_vec(w, a + (int64_t)k * p.su);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[j].w[4 * k + c] = w.w[c];
+          }
+          d[j] = dst0 + dof + (int64_t)s * p.sps + (int64_t)u0 * 16;
+        } else {         // position-major source, packet-major destination
+          const uint8_t* a = src0 + so + (int64_t)s * p.sps + (int64_t)u0 * 16;
+          if constexpr (PK == 4) {
+            Vec<32> x, y;
+            ld_vec(x, a);
+            ld_vec(y, a + 32);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[j].w[c] = x.w[c], v[j].w[8 + c] = y.w[c];
+          } else {
+            ld_vec(v[j], a);
+          }
+          d[j] = dst0 + dof + (int64_t)u0 * p.su + (int64_t)s * 16;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      if (!d[j]) continue;
+      if (DIR == 0) {
+        if constexpr (PK == 4) {
+          Vec<32> a, b;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) a.w[c] = v[j].w[c], b.w[c] = v[j].w[8 + c];
+          st_vec(d[j], a);
+          st_vec(d[j] + 32, b);
+        } else {
+          st_vec(d[j], v[j]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PK; ++k) {
+          Vec<16> w;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w.w[c] = v[j].w[4 * k + c];
+          st_vec(d[j] + (int64_t)k * p.su, w);
+        }
+      }
+    }
+  }
+}
+
+template <int DIR>
+__device__ __forceinline__ void transpose_any(const TParams& p, uint4* tile, const uint8_t* src0,
+                                              uint8_t* dst0, uint32_t bid, uint32_t nb);
 
 template <int DIR>
 __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, const uint8_t* src0,
@@ -373,23 +464,34 @@ __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, c
     dof += (int64_t)q * p.ds[0];
     const uint8_t* sb = src0 + so;
     uint8_t* db = dst0 + dof;
-    for (uint32_t i = threadIdx.x; i < elems; i += 256) {
-      uint32_t u, s;
-      if (DIR == 0) {  // packet-major source: consecutive threads walk positions of one packet
-        u = i / kTS;
-        s = i % kTS;
-      } else {         // position-major source: consecutive threads walk packets of one position
-        p.fU.divmod(i, s, u);
+    // 4 independent 16-byte loads in flight per thread before their shared-memory stores
+    for (uint32_t i0 = threadIdx.x; i0 < elems; i0 += 4 * 256) {
+      uint4 v[4];
+      uint32_t slot[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + j * 256;
+        uint32_t u = 0, s = kTS;
+        if (i < elems) {
+          if (DIR == 0) {  // packet-major source: consecutive threads walk positions of one packet
+            u = i / kTS;
+            s = i % kTS;
+          } else {         // position-major source: consecutive threads walk packets of one position
+            p.fU.divmod(i, s, u);
+          }
+        }
+        slot[j] = s < ns ? s * row + u : 0xFFFFFFFFu;
+        if (s < ns) {
+          const uint8_t* a = DIR == 0 ? sb + (int64_t)u * p.su + (int64_t)(s0 + s) * 16
+                                      : sb + (int64_t)(s0 + s) * p.sps + (int64_t)u * 16;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[j].x), "=r"(v[j].y), "=r"(v[j].z), "=r"(v[j].w)
+                       : "l"(a));
+        }
       }
-      if (s < ns) {
-        uint4 v;
-        const uint8_t* a = DIR == 0 ? sb + (int64_t)u * p.su + (int64_t)(s0 + s) * 16
-                                    : sb + (int64_t)(s0 + s) * p.sps + (int64_t)u * 16;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(a));
-        tile[s * row + u] = v;
-      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (slot[j] != 0xFFFFFFFFu) tile[slot[j]] = v[j];
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < elems; i += 256) {
@@ -414,6 +516,19 @@ __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, c
 }
 
 template <int DIR>
+__device__ __forceinline__ void transpose_any(const TParams& p, uint4* tile, const uint8_t* src0,
+                                              uint8_t* dst0, uint32_t bid, uint32_t nb) {
+  if (p.pk == 4)
+    transpose_regs<DIR, 4>(p, src0, dst0, bid, nb);
+  else if (p.pk == 2)
+    transpose_regs<DIR, 2>(p, src0, dst0, bid, nb);
+  else if (p.pk == 1)
+    transpose_regs<DIR, 1>(p, src0, dst0, bid, nb);
+  else
+    transpose_tiles<DIR>(p, tile, src0, dst0, bid, nb);
+}
+
+template <int DIR>
 __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
   extern __shared__ uint4 tile[];  // kTS rows x (U + 1) packets
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -424,7 +539,7 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
   }
   const uint8_t* src0 = p.src + (int64_t)k * p.dyn_ss;
   uint8_t* dst0 = p.dst + (int64_t)k * p.dyn_ds;
-  transpose_tiles<DIR>(p, tile, src0, dst0, blockIdx.x, gridDim.x);
+  transpose_any<DIR>(p, tile, src0, dst0, blockIdx.x, gridDim.x);
   if (p.flag) {
     KParams kp{};
     kp.flag = p.flag;
@@ -446,9 +561,14 @@ __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KP
     k = *t.dyn;
     if (k < 0 || k > t.dyn_max) return;
   }
-  if (blockIdx.x < t_blocks)
-    transpose_tiles<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
-                         blockIdx.x, t_blocks);
+  if (t_blocks == 0) {  // every CTA takes its share of both halves
+    transpose_any<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
+                       blockIdx.x, gridDim.x);
+    run_chunks<VEC, 4, 256>(r, r.src + (int64_t)k * r.dyn_ss, r.dst + (int64_t)k * r.dyn_ds,
+                            blockIdx.x, gridDim.x);
+  } else if (blockIdx.x < t_blocks)
+    transpose_any<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
+                       blockIdx.x, t_blocks);
   else
     run_chunks<VEC, 4, 256>(r, r.src + (int64_t)k * r.dyn_ss, r.dst + (int64_t)k * r.dyn_ds,
                             blockIdx.x - t_blocks, gridDim.x - t_blocks);
@@ -510,6 +630,7 @@ struct Tune {
   uint64_t max_vec_per_launch = (1ull << 31) - 1;  // DV_MAX_VEC (tests of the launch split)
   int stm = 0;  // DV_STM: store cache operator for U=4 copies (0 default .wb, 1 .cs, 2 .wt)
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
+  int trs = 0;  // DV_TRS: packet transpose form (0 registers PK<=4; 1 shared-memory tiles; 2 PK=1; 3 PK<=2)
 };
 static const Tune& tune() {
   static Tune t = [] {
@@ -524,6 +645,7 @@ static const Tune& tune() {
       if (v > 0 && v < x.max_vec_per_launch) x.max_vec_per_launch = v;
     }
     if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
+    if (const char* e = getenv("DV_TRS")) x.trs = atoi(e);
     return x;
   }();
   return t;
@@ -629,9 +751,30 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
   tp.dyn_ss = p.dyn_ss;
   tp.dyn_ds = p.dyn_ds;
   tp.dyn_max = p.dyn_max;
+  // register form: PK = 2 when the packet count is even and the position-major side's 32-byte
+  // vectors are aligned (base, position stride, slab strides, step stride)
+  const uint64_t items1 = slabs * p.tN * p.tU;
+  uint64_t pm = p.t_ss | (uint64_t)(p.tdir == 0 ? p.dyn_ds : p.dyn_ss) |
+                (uint64_t)(uintptr_t)(p.tdir == 0 ? p.dst : p.src);
+  for (int d = 0; d < 4; ++d) pm |= (uint64_t)(p.tdir == 0 ? tp.ds[d] : tp.ss[d]);
+  const int want = tune().trs == 3 ? 2 : tune().trs == 2 ? 1 : 4;
+  tp.pk = tune().trs == 1 || items1 >= (1ull << 31) ? 0
+          : (want >= 4 && p.tU % 4 == 0 && pm % 32 == 0) ? 4
+          : (want >= 2 && p.tU % 2 == 0 && pm % 32 == 0) ? 2 : 1;
+  if (tp.pk) {
+    tp.n_items = (uint32_t)(items1 / tp.pk);
+    tp.fN = to_dev(make_fastdiv(p.tN));
+    tp.fG = to_dev(make_fastdiv(p.tU / tp.pk));
+  }
   *out = tp;
   return DV_OK;
 }
+
+// CTAs a transpose plan can use, and its dynamic shared memory.
+static uint64_t transpose_ctas(const TParams& tp) {
+  return tp.pk == 4 ? (tp.n_items + 511) / 512 : tp.pk ? (tp.n_items + 1023) / 1024 : tp.n_tiles;
+}
+static int transpose_smem(const TParams& tp) { return tp.pk ? 0 : kTS * (tp.U + 1) * 16; }
 
 static void set_transpose_smem() {
   static std::atomic<uint64_t> mask{0};
@@ -649,11 +792,11 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
                                   cudaStream_t stream) {
   TParams tp;
   DV_TRY(fill_tparams(p, rel, &tp));
-  const int smem = kTS * (p.tU + 1) * 16;
+  const int smem = transpose_smem(tp);
   set_transpose_smem();
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tp.n_tiles, (uint64_t)max_ctas)));
+  cfg.gridDim = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(transpose_ctas(tp), (uint64_t)max_ctas)));
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -724,16 +867,20 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   KParams kr;
   fill_kparams(r, VEC, &kr);
   const double tb = (double)tp.n_tiles * kTS * t.tU * 16, rb = (double)r.runs() * r.run_bytes;
-  const uint64_t t_need = tp.n_tiles, r_need = (kr.n_vec + 1023) / 1024;
+  const uint64_t t_need = transpose_ctas(tp), r_need = (kr.n_vec + 1023) / 1024;
   const uint64_t grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, t_need + r_need));
-  uint64_t t_blocks = (uint64_t)(grid * tb / (tb + rb) + 0.5);
+  // transpose CTAs get 0.45 of their byte share (measured on the C2 FT6D prompt layer: the run
+  // half is the straggler at 1.0; DV_TSPLIT=0 = every CTA does both halves)
+  static const double tscale = getenv("DV_TSPLIT") ? atof(getenv("DV_TSPLIT")) : 0.45;
+  uint64_t t_blocks = (uint64_t)(grid * tscale * tb / (tscale * tb + rb) + 0.5);
   t_blocks = std::min(std::max<uint64_t>(1, t_blocks), grid - 1);
+  if (tscale == 0) t_blocks = 0;
   set_transpose_smem();
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = kTS * (t.tU + 1) * 16;
+  cfg.dynamicSmemBytes = transpose_smem(tp);
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
