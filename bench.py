@@ -115,7 +115,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    xfer = {"auto": dv.DV_XFER_AUTO, "fused": dv.DV_XFER_FUSED, "staged": dv.DV_XFER_STAGED}[args.xfer]
+    xfer = {"auto": dv.DV_XFER_AUTO, "fused": dv.DV_XFER_FUSED, "staged": dv.DV_XFER_STAGED,
+            "decoupled": dv.DV_XFER_DECOUPLED}[args.xfer]
     ctx = dv.dv_create(local)
     k = torch.empty((L, B, H, S, D), dtype=torch.int16, device=dev)
     v = torch.empty_like(k)
@@ -152,9 +153,14 @@ def run_ours(args):
     st_all, en_all = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0, _ = dv.dv_stats()
     st_all.record(stream)
+    h0 = time.perf_counter()
     for i in range(args.steps):
         t_ += 1
         step(t_)
+    host_us = (time.perf_counter() - h0) / args.steps * 1e6
+    # the consumer's view: the timed region ends when the last step's flag is published (with
+    # DV_XFER_DECOUPLED the DMA and flag run on the library's DMA stream, not on `stream`)
+    dv.dv_wait(ctx, ep, 0, t_, stream=sp)
     en_all.record(stream)
     torch.cuda.synchronize()
     l1, dma1 = dv.dv_stats()
@@ -181,7 +187,9 @@ def run_ours(args):
                       xfer=dv.DV_XFER_FUSED, stream=sp)
     torch.cuda.synchronize()
 
-    s_in = torch.cuda.Stream()
+    # two input streams, alternating by step: step t+1's H2D need not queue behind step t's
+    # unpack kernel (the copy engine stays busy); each step still orders its own gather -> scatter
+    s_ins = [torch.cuda.Stream(), torch.cuda.Stream()]
     evs = [torch.cuda.Event() for _ in range(8)]
 
     def e2e_step(t):
@@ -189,6 +197,7 @@ def run_ours(args):
         # full duplex), then the stream-out of step t on the main stream once it has landed.
         q = pos_of(t)
         j = (t - 1) % RING
+        s_in = s_ins[t % 2]
         dv.dv_gather(ctx, dep, j * STEP_BYTES, cache, dv.region(0, L, 0, B, q, q + 1), stream=s_in)
         e = evs[t % 8]
         e.record(s_in)
@@ -202,9 +211,13 @@ def run_ours(args):
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    s_in.wait_event(e0)
+    for s_in in s_ins:
+        s_in.wait_event(e0)
+    h0 = time.perf_counter()
     for t in range(1, args.steps + 1):
         e2e_step(t)
+    host_e2e_us = (time.perf_counter() - h0) / args.steps * 1e6
+    dv.dv_wait(ctx, ep, 0, 10_000_000 + args.steps, stream=sp)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -228,18 +241,38 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    dram_traffic, pcie_traffic = _ncu_traffic()
-    roof = {"bound": "pcie", "achieved": STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9,
-            "peak": pcie_peak, "unit": "GB/s",
-            "frac": (STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9 / pcie_peak) if pcie_peak else None,
-            "traffic": dram_traffic, "traffic_pcie_write": pcie_traffic,
-            "traffic_source": "profiles/r01_io_counters_final.csv (ncu dram__bytes_read+write, "
-                              "pcie__write_bytes per launch, median)",
-            "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
-            "kernel": "k_run_copy (fused pack -> pinned host zero-copy PCIe stores + st.release.sys flag)",
-            "algorithmic_bytes_per_launch": STEP_BYTES,
-            "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
-                           "PCIe Gen5 x16 nominal 64 GB/s"}
+    if args.xfer in ("auto", "fused"):
+        dram_traffic, pcie_traffic = _ncu_traffic("final")
+        roof = {"bound": "pcie", "achieved": STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9,
+                "peak": pcie_peak, "unit": "GB/s",
+                "frac": (STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9 / pcie_peak) if pcie_peak else None,
+                "traffic": dram_traffic, "traffic_pcie_write": pcie_traffic,
+                "traffic_source": "profiles/r01_io_counters_final.csv (ncu dram__bytes_read+write, "
+                                  "pcie__write_bytes per launch, median)",
+                "kernel": "k_run_copy (fused pack -> pinned host zero-copy PCIe stores + st.release.sys flag)"}
+    else:
+        # decoupled / staged: the step's bytes cross PCIe by the copy engine (one cudaMemcpyAsync of
+        # the packed step per step, back to back on the library's DMA stream); the pack kernel
+        # (k_run_copy, cache -> HBM staging) is a few us of HBM work beside it. achieved = bytes per
+        # step / device time per step (a lower bound of the DMA's own rate).
+        dram_traffic, pcie_traffic = _ncu_traffic("decoupled")
+        ach = STEP_BYTES / (elapsed_ms / args.steps * 1e-3) / 1e9
+        roof = {"bound": "pcie", "achieved": ach, "peak": pcie_peak, "unit": "GB/s",
+                "frac": ach / pcie_peak if pcie_peak else None,
+                "traffic": dram_traffic,
+                "traffic_source": "profiles/r01_io_counters_decoupled.csv: ncu dram__bytes_read+write "
+                                  "per launch of the pack kernel (HBM side; the copy engine's PCIe "
+                                  "bytes are not a kernel counter), median",
+                "kernel": "copy-engine D2H of the packed step (cudaMemcpyAsync on the library DMA "
+                          "stream), fed by k_run_copy pack (cache -> HBM staging), flag by a stream "
+                          "write on the library flag stream",
+                "pack_kernel_us": extras.get("token_step_pack_hbm_us"),
+                "pack_kernel_hbm_frac": extras.get("token_step_pack_hbm_frac")}
+    roof.update({
+        "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
+        "algorithmic_bytes_per_launch": STEP_BYTES,
+        "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
+                       "PCIe Gen5 x16 nominal 64 GB/s"})
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -253,6 +286,7 @@ def run_ours(args):
                        "(H2D, side stream) then dv_scatter to the pinned-host log (D2H, main stream); "
                        "step t's H2D overlaps step t-1's D2H"},
         "gpu_launches": int(launches),
+        "host_enqueue_us_per_step": {"value": host_us, "e2e": host_e2e_us},
         "roofline": roof,
         "clocks": clk,
         "parity_spot_check": spot,
@@ -267,12 +301,12 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _ncu_traffic():
+def _ncu_traffic(name="final"):
     """DRAM and PCIe bytes per launch of the headline kernel from the committed ncu capture
-    (profiles/r01_io_counters_final.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+    (profiles/r01_io_counters_<name>.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
     pcie__write_bytes.sum on this same command), median over the captured launches."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_io_counters_final.csv")
+    path = os.path.join(ROOT, "profiles", f"r01_io_counters_{name}.csv")
     try:
         rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
     except OSError:
@@ -329,7 +363,7 @@ def sample_region(k, v, layer_begin, req_begin, n_heads, max_seq, head_dim, regi
     return int(np.sum(np.where(kv == 0, gk, gv) != exp))
 
 
-def _time(fn, stream, reps, warm=2):
+def _time(fn, stream, reps, warm=2, tail=None):
     import torch
     for _ in range(warm):
         fn()
@@ -338,6 +372,8 @@ def _time(fn, stream, reps, warm=2):
     a.record(stream)
     for _ in range(reps):
         fn()
+    if tail:
+        tail()
     b.record(stream)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
@@ -368,16 +404,22 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     dep = dv.endpoint_of(dbuf)
     cnt = [0]
 
-    def tok(epx, xf):
+    tfl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    epf = dv.endpoint_of(log, tfl)
+
+    def tok(epx, xf, flag=False):
         def f():
             cnt[0] += 1
             q = pos_of(cnt[0])
             dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), epx, (cnt[0] % 8) * STEP_BYTES,
-                          xfer=xf, stream=sp)
+                          flag_slot=0 if flag else -1, seq=cnt[0], xfer=xf, stream=sp)
         return f
     reps = 200
-    for name, epx, xf in (("fused", ep, dv.DV_XFER_FUSED), ("staged", ep, dv.DV_XFER_STAGED)):
-        ms = _time(tok(epx, xf), stream, reps)
+    for name, epx, xf in (("fused", ep, dv.DV_XFER_FUSED), ("staged", ep, dv.DV_XFER_STAGED),
+                          ("decoupled", epf, dv.DV_XFER_DECOUPLED)):
+        dec = name == "decoupled"
+        ms = _time(tok(epx, xf, dec), stream, reps,
+                   tail=(lambda: dv.dv_wait(ctx, epf, 0, cnt[0], stream=sp)) if dec else None)
         ex[f"token_step_host_{name}_gbs"] = STEP_BYTES / ms / 1e6
         ex[f"token_step_host_{name}_us"] = ms * 1e3
     for name, xf in (("fused", dv.DV_XFER_FUSED), ("staged", dv.DV_XFER_STAGED)):
@@ -392,7 +434,7 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["token_step_pack_hbm_us"] = ms * 1e3
     ex["token_step_pack_hbm_gbs_2R"] = 2 * STEP_BYTES / ms / 1e6
     ex["token_step_pack_hbm_frac"] = ex["token_step_pack_hbm_gbs_2R"] / HBM_PEAK
-    ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else "staged"
+    ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else args.xfer
 
     # per-layer token latency: from "layer l's new K/V written" to "bytes resident at
     # the destination and seq flag visible". The writer is dvt_fill of that layer's new position
@@ -593,7 +635,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--xfer", default="auto", choices=["auto", "fused", "staged"])
+    ap.add_argument("--xfer", default="decoupled", choices=["auto", "fused", "staged", "decoupled"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

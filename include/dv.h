@@ -161,6 +161,15 @@ enum {
   DV_XFER_STAGED = 1u << 1, /* kernel <-> local staging, copy engine DMA for the contiguous chunk */
   DV_PUBLISH_STREAMOP = 1u << 2, /* publish flags with a stream memory operation after the kernel
                                     instead of the kernel's own fenced release store            */
+  DV_XFER_DECOUPLED = 1u << 3, /* scatter / stream_out to a pinned-HOST endpoint only: the caller's
+                                  stream is ordered after the pack (the source may be rewritten),
+                                  the copy-engine DMA and the flag store run on the context's DMA
+                                  stream -- the FLAG is the only completion signal (PAPER.md:171,
+                                  stream_out is non-blocking; the receiver's stream_in / dv_wait
+                                  waits on the flag). Successive steps then overlap step t's DMA
+                                  with step t+1's pack. Requires a flag (flag_slot >= 0, no
+                                  DV_NO_FLAG); with AUTO it selects STAGED. Ignored for device and
+                                  peer endpoints (the caller's stream already covers them).     */
   DV_NO_FLAG = 1u << 8      /* do not publish / wait on sequence flags                           */
 };
 

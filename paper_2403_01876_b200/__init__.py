@@ -23,6 +23,7 @@ DV_OK, DV_EINVAL, DV_EMAP, DV_ERANGE, DV_EALIGN, DV_ENOMEM, DV_EPEER, DV_EBUSY, 
 DV_LAYOUT_KV5D, DV_LAYOUT_FT6D = 0, 1
 DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
 DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_PUBLISH_STREAMOP, DV_NO_FLAG = 0, 1, 2, 4, 256
+DV_XFER_DECOUPLED = 8
 DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
 
 

@@ -385,6 +385,9 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
 // (SM zero-copy reads do not overlap with concurrent D2H traffic).
 static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes, bool reading) {
   uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
+  // decoupled host writes: pack + DMA on the context's DMA stream overlaps consecutive steps
+  if (!reading && (xfer & DV_XFER_DECOUPLED) && ep->kind == DV_EP_HOST && m != DV_XFER_FUSED)
+    return DV_XFER_STAGED;
   if (m == DV_XFER_FUSED || m == DV_XFER_STAGED) {
     if (m == DV_XFER_STAGED && ep->kind == DV_EP_DEVICE) return DV_XFER_FUSED;  // already local
     return m;
@@ -410,6 +413,9 @@ static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
   DV_TRY(check_region_shape(&op.reg));
   DV_TRY(check_cache_holds(op.src, &op.reg, "source"));
   const bool use_flag = !(op.xfer & DV_NO_FLAG);
+  if ((op.xfer & DV_XFER_DECOUPLED) && op.dst && op.dst->kind == DV_EP_HOST &&
+      (!use_flag || op.slot < 0))
+    return fail(DV_EINVAL, "DV_XFER_DECOUPLED needs a flag: the flag is its only completion signal");
   return check_ep(op.dst, op.dst_off, region_bytes(&op.reg, op.src), op.slot, use_flag,
                   "destination");
 }
@@ -445,8 +451,11 @@ static uint64_t pipe_chunk(uint64_t total, uint64_t half) {
 // Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
 // the kernel packs a group of layer slabs (or, with one plan, a range of runs) into staging, the
 // copy engine moves that contiguous piece to its place in the wire.
+// decoupled: the DMAs (and the caller's flag after them) stay on ctx->dma, the caller's stream only
+// waits for the packs; *flag_stream is the stream the flag must be published on.
 static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, uint8_t* wire,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool decoupled, cudaStream_t* flag_stream) {
+  *flag_stream = st;
   const int64_t row = row_bytes(c);
   const uint64_t half = ctx->staging.capacity() / 2;
   const Release none{nullptr, 0, nullptr};
@@ -457,7 +466,13 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
   std::lock_guard<std::mutex> lk(ctx->pipe_mu);
   const uint64_t total = region_bytes_h(&reg, c->n_heads, c->head_dim, c->elem_bytes);
-  cudaStream_t ds = total >= kPipeMin ? ctx->dma : st;  // copy-engine stream (pipelined or not)
+  cudaStream_t ds = (total >= kPipeMin || decoupled) ? ctx->dma : st;  // copy-engine stream
+  // the caller's stream rejoins after the DMAs, or (decoupled) after the last pack
+  auto finish = [&]() -> dv_status {
+    if (!decoupled) return hand_off(ctx, ds, st);
+    *flag_stream = ds;
+    return DV_OK;
+  };
   if (np == 1 && p[0].run_bytes <= half) {  // dense wire in run order: chunk by runs
     const uint64_t rb = p[0].run_bytes, runs = p[0].runs();
     const uint64_t chunk = std::max<uint64_t>(1, pipe_chunk(runs * rb, half) / rb);
@@ -474,7 +489,7 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
       DV_DMA(cudaMemcpyAsync(wire + q0 * rb, stg, nb, cudaMemcpyDefault, ds));
       DV_TRY(ctx->staging.release(off, nb, ds));
     }
-    return hand_off(ctx, ds, st);
+    return finish();
   }
   const uint64_t slab = layer_slab_bytes(&reg, row);
   if (slab > half)
@@ -504,7 +519,7 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
                            cudaMemcpyDefault, ds));
     DV_TRY(ctx->staging.release(off, nb, ds));
   }
-  return hand_off(ctx, ds, st);
+  return finish();
 }
 
 // Unpack a wire chunk at `wire` (any memory) into `reg` of cache `c` through HBM staging.
@@ -593,8 +608,18 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
                           (op.dst->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas
                                                                          : ctx->max_ctas);
   }
-  DV_TRY(staged_pack(ctx, c, reg, wire, st));
-  if (use_flag) DV_TRY(stream_signal(op.dst, op.slot, op.seq, st));
+  const bool decoupled = (op.xfer & DV_XFER_DECOUPLED) && op.dst->kind == DV_EP_HOST;
+  cudaStream_t fs;
+  DV_TRY(staged_pack(ctx, c, reg, wire, st, decoupled, &fs));
+  if (use_flag && fs != st) {
+    // A stream memory op serialises its stream for ~5.7 us (tools/probe_dma_gaps.py): the flag
+    // store goes to its own stream, ordered after this DMA by an event, so the next step's DMA
+    // starts at once. One flag stream per context keeps flags monotonic.
+    std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+    DV_TRY(hand_off(ctx, fs, ctx->flag_st));
+    return stream_signal(op.dst, op.slot, op.seq, ctx->flag_st);
+  }
+  if (use_flag) DV_TRY(stream_signal(op.dst, op.slot, op.seq, fs));
   return DV_OK;
 }
 
@@ -763,6 +788,7 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(c->tickets, 0, sizeof(unsigned int) * dv_ctx::kTickets);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dma, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->flag_st, cudaStreamNonBlocking);
   for (int i = 0; e == cudaSuccess && i < 64; ++i) {
     cudaEvent_t ev;
     e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -787,6 +813,7 @@ dv_status dv_destroy(dv_ctx* ctx) {
     cudaFree(ctx->tickets);
     cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->dma);
+    cudaStreamDestroy(ctx->flag_st);
     for (auto ev : ctx->pipe_ev) cudaEventDestroy(ev);
   }
   delete ctx;

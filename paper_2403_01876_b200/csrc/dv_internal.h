@@ -149,6 +149,7 @@ struct dv_ctx {
   std::atomic<uint32_t> next_ticket{0};
   cudaStream_t aux;       // private stream for dv_query on device flags
   cudaStream_t dma;       // copy-engine stream of the pipelined staged transfers
+  cudaStream_t flag_st;   // decoupled transfers' flag stores (off the DMA stream's critical path)
   std::vector<cudaEvent_t> pipe_ev;  // event ring for kernel <-> DMA hand-offs
   std::atomic<uint32_t> next_ev{0};
   std::mutex pipe_mu;     // one pipelined transfer enqueued at a time per context

@@ -136,7 +136,7 @@ def test_random_stream_out_in_against_oracle(block):
         dps, dts = dv.Setup(sl, sr, S1, sh), dv.Setup(dl, dr, S2, dh)
         seed = rng.randint(0, 1 << 30)
         form = rng.choice(["inbox_dev", "inbox_host", "direct"])
-        xf = rng.choice(XF)
+        xf = rng.choice(XF + [dv.DV_XFER_DECOUPLED])   # decoupled: flags are the only completion
 
         def blocks(s, lb_, rb_, hb_):
             hbs = hb_ if hb_ is not None else [0, Hn]

@@ -478,7 +478,8 @@ def test_paper_baselines_produce_the_wire():
     assert calls == 2 * nL * nR + 1 and np.array_equal(to_np(out), exp)
 
 
-@pytest.mark.parametrize("xfer", [dv.DV_XFER_FUSED, dv.DV_XFER_FUSED | dv.DV_PUBLISH_STREAMOP, dv.DV_XFER_STAGED])
+@pytest.mark.parametrize("xfer", [dv.DV_XFER_FUSED, dv.DV_XFER_FUSED | dv.DV_PUBLISH_STREAMOP, dv.DV_XFER_STAGED,
+                                  dv.DV_XFER_DECOUPLED])
 def test_host_poller_never_sees_flag_before_payload(xfer):
     """Release protocol (A5) observed from the CPU: a host thread spins on the pinned flag while
     the GPU streams 300 per-layer chunks; whenever it sees seq k it immediately compares chunk k
@@ -523,6 +524,41 @@ def test_host_poller_never_sees_flag_before_payload(xfer):
     th.join(timeout=60)
     assert not bad, f"flag seen before payload for chunks {bad[:10]}"
     assert len(seen) > 10 and seen[-1] == n
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_decoupled_scatter_flag_is_completion_and_source_is_free(big):
+    """DV_XFER_DECOUPLED (stream_out is non-blocking): the caller's stream is only
+    ordered after the pack, so rewriting the source right after the call must not change what
+    lands in the host log; the flag (waited on by a consumer stream) is the completion signal.
+    big: a region >= 32 MB (pipelined chunks on the DMA stream)."""
+    L, B, H, S, D = (4, 8, 16, 160, 128) if big else (4, 4, 8, 64, 128)
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=31)
+    k, v, c = dev_cache(K, V, 0, 0)
+    osrc = oc(K, V, 0, 0, S)
+    regs = [(0, L, 0, B, 0, S)] if big else [(0, L, 0, B, q, q + 1) for q in range(12)] + [(1, 3, 1, 4, 20, 50)]
+    sizes = [ok.region_bytes(*r, H, D, 2) for r in regs]
+    offs = np.cumsum([0] + sizes)
+    log = pinned_u16(int(offs[-1]) // 2 + 8)
+    log.fill_(-1)
+    fl = flags(1, pinned=True)
+    ep = dv.endpoint_of(log, fl)
+    cx = ctx()
+    for i, r in enumerate(regs):
+        dv.dv_scatter(cx, c, dv.region(*r), ep, int(offs[i]), flag_slot=0, seq=i + 1, xfer=dv.DV_XFER_DECOUPLED)
+        # the caller's stream may rewrite the source at once (different seed)
+        dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=1000 + i, reg=dv.region(*r))
+    cons = torch.cuda.Stream()
+    dv.dv_wait(cx, ep, 0, len(regs), stream=cons.cuda_stream)
+    cons.synchronize()
+    assert int(fl[0]) == len(regs)
+    got = log.numpy().view(np.uint16)
+    for i, r in enumerate(regs):
+        assert np.array_equal(got[offs[i] // 2:offs[i + 1] // 2], ok.pack(osrc, r)), i
+    torch.cuda.synchronize()
+    with pytest.raises(dv.DVError) as e:   # the flag is the only completion signal: required
+        dv.dv_scatter(cx, c, dv.region(*regs[0]), ep, 0, flag_slot=-1, xfer=dv.DV_XFER_DECOUPLED)
+    assert e.value.status == dv.DV_EINVAL
 
 
 @pytest.mark.parametrize("seed", range(8))
