@@ -35,7 +35,7 @@ def emit(**kw):
     print(json.dumps(kw), flush=True)
 
 
-def timed(fn, reps=5, warm=2):
+def timed(fn, reps=5, warm=2, tail=None):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -43,6 +43,8 @@ def timed(fn, reps=5, warm=2):
     a.record(st)
     for _ in range(reps):
         fn()
+    if tail:     # e.g. the consumer's flag wait after decoupled transfers
+        tail()
     b.record(st)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / reps * 1e3   # us
@@ -254,6 +256,8 @@ def c4():
     cnt = [0]
     logo = torch.empty(b * C * nL * 64 // 2, dtype=torch.int16, pin_memory=True)
     loep = dv.endpoint_of(logo)
+    lofl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    lofep = dv.endpoint_of(logo, lofl)
     for name, fn in (
             ("mirror_fused", lambda q: dv.dv_remap(ctx, dc, hc, dv.region(0, nL, 0, b, q, q + 1),
                                                    xfer=dv.DV_XFER_FUSED, stream=sp)),
@@ -262,12 +266,17 @@ def c4():
             ("log_fused", lambda q: dv.dv_scatter(ctx, dc, dv.region(0, nL, 0, b, q, q + 1), loep,
                                                   (q % 64) * b * C * nL, xfer=dv.DV_XFER_FUSED, stream=sp)),
             ("log_staged", lambda q: dv.dv_scatter(ctx, dc, dv.region(0, nL, 0, b, q, q + 1), loep,
-                                                   (q % 64) * b * C * nL, xfer=dv.DV_XFER_STAGED, stream=sp))):
+                                                   (q % 64) * b * C * nL, xfer=dv.DV_XFER_STAGED, stream=sp)),
+            ("log_decoupled", lambda q: dv.dv_scatter(ctx, dc, dv.region(0, nL, 0, b, q, q + 1), lofep,
+                                                      (q % 64) * b * C * nL, flag_slot=0, seq=cnt[0],
+                                                      xfer=dv.DV_XFER_DECOUPLED, stream=sp))):
         def swap_out(fn=fn):
             q = 1024 + cnt[0] % 1000
             cnt[0] += 1
             fn(q)
-        us = timed(swap_out, reps=200)
+        dec = name == "log_decoupled"
+        us = timed(swap_out, reps=200,
+                   tail=(lambda: dv.dv_wait(ctx, lofep, 0, cnt[0] - 1, stream=sp)) if dec else None)
         emit(config="C4", op=f"swap_out_step_delta_{name}", bytes=b * C * nL, us=us, gbs=b * C * nL / us / 1e3,
              bound="pcie/latency", ideal_us_at_64=b * C * nL / 64e3)
     bad = sample_check(hk, hv, hc, (0, nL, 0, b, 1024, 1024 + min(cnt[0], 1000)), SEED + 3)
