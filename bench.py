@@ -174,6 +174,16 @@ def run_ours(args):
     wire = log[(t_ % RING) * STEP_BYTES // 2:(t_ % RING + 1) * STEP_BYTES // 2]
     assert int(fl[0]) == t_, "flag not published"
     spot = _spot_check(wire, last_q, seed)
+    # and every word of the last 8 steps' wires on the device (dvt_verify vs the generator)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    for tt in range(max(1, t_ - 7), t_ + 1):
+        w = log[(tt % RING) * STEP_BYTES // 2:(tt % RING + 1) * STEP_BYTES // 2]
+        dv.dvt_verify(cache, cnt.data_ptr(), seed=seed, reg=dv.region(0, L, 0, B, pos_of(tt), pos_of(tt) + 1),
+                      wire_ptr=w.data_ptr(), stream=sp)
+    torch.cuda.synchronize()
+    spot["full_steps_verified"] = min(8, t_)
+    spot["full_words"] = min(8, t_) * STEP_BYTES // 2
+    spot["full_mismatches"] = int(cnt.item())
     if world > 1:
         elapsed_ms = max_over_ranks(elapsed_ms)
 

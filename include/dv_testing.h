@@ -28,6 +28,16 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
                    int32_t valid_begin, int32_t valid_end, const dv_region* region,
                    uint64_t* t_end, void* stream);
 
+/* Verifier (the second, on-device parity check of SURVEY §8(c) C-5 at full sizes): adds to
+ * *mismatches (device memory, uint64) the number of words of `region` that differ from the
+ * generator word dvt_fill would write there (same kind / seed / box / valid range). wire == NULL:
+ * the words are read from cache `c` (either layout). wire != NULL: they are read from the dense
+ * canonical wire [l][kv][r][h][s][d] of `region` at `wire` (device or mapped pinned host memory;
+ * `c` then only supplies head_dim, head range and the global-id frame). Stream-ordered. */
+DV_API dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kind, uint64_t seed,
+                     const int32_t* box, int32_t valid_begin, int32_t valid_end,
+                     const dv_region* region, uint64_t* mismatches, void* stream);
+
 /* Latency tracing: while `ts` (device memory, 4 x uint64) is set, every fused copy of `ctx` that
  * publishes a flag records %globaltimer (ns): ts[0] = right after the release store of the flag,
  * ts[1] = min over CTAs of "resident" (before the programmatic-dependency wait; initialise to

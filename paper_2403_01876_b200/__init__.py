@@ -127,6 +127,8 @@ _SIGS = {
     "dv_query": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, P(C.c_int32)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
+    "dvt_verify": (C.c_int, [P(dv_cache), C.c_void_p, C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32,
+                             C.c_int32, P(dv_region), C.c_void_p, C.c_void_p]),
     "dvt_trace": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dvt_spin": (C.c_int, [C.c_uint64, C.c_int32, C.c_void_p]),
     "dvb_per_run_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, P(C.c_uint64)]),
@@ -465,6 +467,15 @@ def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_re
     b = (C.c_int32 * 5)(*box) if box is not None else None
     _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], _ref(reg), C.c_void_p(t_end_ptr),
           _stream(stream))
+
+
+def dvt_verify(c: dv_cache, counter_ptr, seed=0, kind=0, reg: dv_region = None, wire_ptr=0, box=None,
+               valid=(0, 1 << 30), stream=None):
+    """Adds to the uint64 at counter_ptr (device) the words of `reg` (in cache c, or in the dense
+    wire at wire_ptr) that differ from the generator (dvt_fill's word)."""
+    b = (C.c_int32 * 5)(*box) if box is not None else None
+    _call("dvt_verify", C.byref(c), C.c_void_p(wire_ptr), kind, seed, b, valid[0], valid[1], _ref(reg),
+          C.c_void_p(counter_ptr), _stream(stream))
 
 
 def dvt_trace(ctx, ts_ptr=0):

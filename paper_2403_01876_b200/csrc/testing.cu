@@ -27,6 +27,21 @@ struct FillParams {
   unsigned long long* t_end;  // optional: max over CTAs of %globaltimer after their stores
 };
 
+// The generator's word at global coordinate (kv, l, r, h, s, d) (kvgen.hash_words / uid / const).
+__device__ __forceinline__ uint16_t gen_word(const FillParams& p, int kv, int l, int r, int h, int s,
+                                             int d) {
+  if (s < p.vlo || s >= p.vhi) return 0xFFFE;
+  if (p.kind == DVT_FILL_HASH) {
+    const uint64_t key = ((uint64_t)kv << 62) | ((uint64_t)l << 52) | ((uint64_t)r << 40) |
+                         ((uint64_t)h << 30) | ((uint64_t)s << 10) | (uint64_t)d;
+    return (uint16_t)(splitmix64(key ^ p.seedmix) >> 48);
+  }
+  if (p.kind == DVT_FILL_UID)
+    return (uint16_t)((((((int64_t)kv * p.box[0] + l) * p.box[1] + r) * p.box[2] + h) * p.box[3] +
+                       s) * p.box[4] + d);
+  return (uint16_t)p.seedmix;
+}
+
 __global__ void k_fill(const FillParams p) {
   // Behave like a PDL-aware producer (an attention kernel would do the same): let the dependent
   // streaming kernel be scheduled now; it still waits (griddepcontrol.wait) for our memory.
@@ -45,21 +60,7 @@ __global__ void k_fill(const FillParams p) {
   for (int64_t i = threadIdx.x; i < words; i += blockDim.x) {
     const int s = p.s0 + (int)(i / p.D);
     const int d = (int)(i % p.D);
-    uint16_t w;
-    if (s < p.vlo || s >= p.vhi) {
-      w = 0xFFFE;
-    } else if (p.kind == DVT_FILL_HASH) {
-      const uint64_t key = ((uint64_t)kv << 62) | ((uint64_t)l << 52) | ((uint64_t)r << 40) |
-                           ((uint64_t)h << 30) | ((uint64_t)s << 10) | (uint64_t)d;
-      w = (uint16_t)(splitmix64(key ^ p.seedmix) >> 48);
-    } else if (p.kind == DVT_FILL_UID) {
-      const int64_t id =
-          (((((int64_t)kv * p.box[0] + l) * p.box[1] + r) * p.box[2] + h) * p.box[3] + s) *
-              p.box[4] + d;
-      w = (uint16_t)id;
-    } else {
-      w = (uint16_t)p.seedmix;
-    }
+    const uint16_t w = gen_word(p, kv, l, r, h, s, d);
     if (ft)  // x = 8 16-bit words per 16-byte packet
       base[((int64_t)(d >> 3) * p.S + s) * 8 + (d & 7)] = w;
     else
@@ -76,6 +77,38 @@ __global__ void k_fill(const FillParams p) {
   }
 }
 
+// Verifier: counts the words of a region that differ from the generator. Cache form (wire == NULL):
+// the same slab walk and addressing as k_fill. Wire form: the canonical wire [l][kv][r][h][s][d]
+// of the region, dense, at `wire` (device or mapped pinned host memory).
+__global__ void k_verify(const FillParams p, const uint16_t* wire, unsigned long long* bad) {
+  uint32_t slab = blockIdx.x;
+  const int hi = (int)(slab % p.H);
+  slab /= p.H;
+  const int ri = (int)(slab % p.nR);
+  const int li = (int)(slab / p.nR);
+  const int h = p.h0 + hi, r = p.r0 + ri, l = p.l0 + li;
+  const int kv = blockIdx.y;
+  const int64_t words = (int64_t)p.n * p.D;
+  const uint16_t* base;
+  if (wire)
+    base = wire + ((((int64_t)li * 2 + kv) * p.nR + ri) * p.H + hi) * words;
+  else
+    base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
+           (int64_t)(h - p.hb) * p.s_h;
+  const bool ft = !wire && p.ft6d && kv == 0;
+  unsigned long long n_bad = 0;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) {
+    const int si = (int)(i / p.D);
+    const int s = p.s0 + si;
+    const int d = (int)(i % p.D);
+    const uint16_t got = wire ? base[i]
+                         : ft ? base[((int64_t)(d >> 3) * p.S + s) * 8 + (d & 7)]
+                              : base[(int64_t)s * p.D + d];
+    n_bad += got != gen_word(p, kv, l, r, h, s, d);
+  }
+  if (n_bad) atomicAdd(bad, n_bad);
+}
+
 __global__ void k_spin(uint64_t ns) {
   uint64_t t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -88,9 +121,10 @@ __global__ void k_spin(uint64_t ns) {
 
 using namespace dv;
 
-extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
-                              int32_t valid_begin, int32_t valid_end, const dv_region* region,
-                              uint64_t* t_end, void* stream) {
+// FillParams of `region` (NULL = whole cache) of cache `c`; *slabs = (l, r, h) slabs in it.
+static dv_status fill_params(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                             int32_t valid_begin, int32_t valid_end, const dv_region* region,
+                             FillParams* out, uint64_t* slabs) {
   DV_TRY(check_cache(c, "cache"));
   if (c->elem_bytes != 2) return fail(DV_ENOTSUP, "dvt_fill supports 16-bit words only");
   dv_region whole{c->layer_begin, c->layer_begin + c->n_layers, c->req_begin,
@@ -125,10 +159,20 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
     for (int i = 0; i < 5; ++i) p.box[i] = box[i];
   p.vlo = valid_begin;
   p.vhi = valid_end;
+  *slabs = p.n ? (uint64_t)(r->layer_end - r->layer_begin) * p.nR * p.H : 0;
+  if (*slabs >= (1ull << 31)) return fail(DV_ENOTSUP, "region too large for dvt_fill / dvt_verify");
+  *out = p;
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                              int32_t valid_begin, int32_t valid_end, const dv_region* region,
+                              uint64_t* t_end, void* stream) {
+  FillParams p;
+  uint64_t slabs;
+  DV_TRY(fill_params(c, kind, seed, box, valid_begin, valid_end, region, &p, &slabs));
   p.t_end = (unsigned long long*)t_end;
-  const uint64_t slabs = (uint64_t)(r->layer_end - r->layer_begin) * p.nR * p.H;
-  if (!slabs || !p.n) return DV_OK;
-  if (slabs >= (1ull << 31)) return fail(DV_ENOTSUP, "region too large for dvt_fill");
+  if (!slabs) return DV_OK;
   const int threads = p.n * p.D >= 256 ? 256 : 128;
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
@@ -136,6 +180,21 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
   cfg.blockDim = dim3(threads);
   cfg.stream = (cudaStream_t)stream;
   DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill, p));
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kind, uint64_t seed,
+                                const int32_t* box, int32_t valid_begin, int32_t valid_end,
+                                const dv_region* region, uint64_t* mismatches, void* stream) {
+  if (!mismatches) return fail(DV_EINVAL, "NULL mismatch counter");
+  FillParams p;
+  uint64_t slabs;
+  DV_TRY(fill_params(c, kind, seed, box, valid_begin, valid_end, region, &p, &slabs));
+  if (!slabs) return DV_OK;
+  (void)cudaGetLastError();
+  k_verify<<<dim3((unsigned)slabs, 2), p.n * p.D >= 256 ? 256 : 128, 0, (cudaStream_t)stream>>>(
+      p, (const uint16_t*)wire, (unsigned long long*)mismatches);
   DV_CUDA(cudaGetLastError());
   return DV_OK;
 }

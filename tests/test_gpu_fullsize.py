@@ -47,6 +47,46 @@ def _sample_cache(k, v, c, region, seed, n=30000):
     return int(np.sum(got != kvgen.hash_words(kv, l, r, h, s, d, seed)))
 
 
+class _Verify:
+    """Every word, on the device (dvt_verify): the second parity check at full sizes (SURVEY §8(c)
+    C-5), beside the sampled oracle comparisons."""
+
+    def __init__(self):
+        self.cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def __call__(self, c, reg, wire=None, valid=(0, 1 << 30)):
+        self.cnt.zero_()
+        dv.dvt_verify(c, self.cnt.data_ptr(), seed=SEED, reg=dv.region(*reg),
+                      wire_ptr=wire.data_ptr() if wire is not None else 0, valid=valid)
+        torch.cuda.synchronize()
+        return int(self.cnt.item())
+
+
+def test_verifier_matches_kvgen_and_detects_one_flipped_word():
+    """Pins dvt_verify: a cache filled on the HOST by kvgen verifies clean (device generator ==
+    kvgen), its oracle-packed wire verifies clean, and one flipped word anywhere is counted once."""
+    L, B, H, S, D = 3, 2, 5, 24, 32
+    K, V = kvgen.kv5d_cache("hash", 2, L, 1, B, H, S, D, seed=SEED)
+    k = torch.from_numpy(K.view(np.int16)).cuda()
+    v = torch.from_numpy(V.view(np.int16)).cuda()
+    c = dv.cache(k, v, 2, 1)
+    ver = _Verify()
+    assert ver(c, (2, 5, 1, 3, 0, S)) == 0
+    reg = (3, 5, 1, 3, 4, 19)
+    wire = torch.from_numpy(ok.pack(ok.Cache(K, V, 2, 1, H, S, D), reg).view(np.int16)).cuda()
+    assert ver(c, reg, wire) == 0
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        i = int(rng.integers(0, wire.numel()))
+        wire[i] ^= 0x10
+        assert ver(c, reg, wire) == 1
+        wire[i] ^= 0x10
+        j = tuple(int(rng.integers(0, n)) for n in k.shape)
+        v[j] ^= 1
+        assert ver(c, (2, 5, 1, 3, 0, S)) == 1
+        v[j] ^= 1
+
+
 def test_c2_full_size_token_step_and_prompt_layer():
     """C2 (OPT-13B, b8, S2048, 13.4 GB cache): token steps fused and staged, prompt layer fused and
     staged (pipelined), into pinned host -- sampled parity vs oracle mapping + kvgen."""
@@ -56,6 +96,7 @@ def test_c2_full_size_token_step_and_prompt_layer():
     c = dv.cache(k, v)
     dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=SEED)
     cx = _ctx()
+    ver = _Verify()
     step = 2 * L * B * H * D * 2
     log = torch.full((step,), -1, dtype=torch.int16, pin_memory=True)
     for xf in (dv.DV_XFER_FUSED, dv.DV_XFER_STAGED, dv.DV_XFER_AUTO):
@@ -63,6 +104,7 @@ def test_c2_full_size_token_step_and_prompt_layer():
         dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(log), 0, xfer=xf)
         torch.cuda.synchronize()
         assert _sample_wire(log, reg, H, D, SEED) == 0
+        assert ver(c, reg, log) == 0
     layer = 2 * B * H * P * D * 2
     pbuf = torch.full((layer // 2,), -1, dtype=torch.int16, pin_memory=True)
     for xf in (dv.DV_XFER_FUSED, dv.DV_XFER_STAGED):
@@ -70,6 +112,7 @@ def test_c2_full_size_token_step_and_prompt_layer():
         dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(pbuf), 0, xfer=xf)
         torch.cuda.synchronize()
         assert _sample_wire(pbuf, reg, H, D, SEED) == 0
+        assert ver(c, reg, pbuf) == 0
     # and back: gather the prompt layer into an S=4096 cache (other max_seq), staged pipelined
     k2 = torch.full((1, B, H, 4096, D), -1, dtype=torch.int16, device="cuda")
     v2 = torch.full_like(k2, -1)
@@ -77,6 +120,7 @@ def test_c2_full_size_token_step_and_prompt_layer():
     dv.dv_gather(cx, dv.endpoint_of(pbuf), 0, c2, dv.region(9, 10, 0, B, 0, P))
     torch.cuda.synchronize()
     assert _sample_cache(k2, v2, c2, (9, 10, 0, B, 0, P), SEED) == 0
+    assert ver(c2, (9, 10, 0, B, 0, P)) == 0
     assert int(k2[0, :, :, P:].ne(-1).sum()) == 0
     cx.close()
 
@@ -99,6 +143,8 @@ def test_c3_full_size_direct_remap_16_layers():
     torch.cuda.synchronize()
     assert _sample_cache(t0k, t0v, c0, (0, 13, 0, b, 0, p), SEED) == 0
     assert _sample_cache(t1k, t1v, c1, (13, 16, 0, b, 0, p), SEED) == 0
+    ver = _Verify()   # every word of the 4.72 GB hand-off
+    assert ver(c0, (0, 13, 0, b, 0, p)) == 0 and ver(c1, (13, 16, 0, b, 0, p)) == 0
     assert int(t0k[:, :, :, p:].ne(-1).sum()) == 0 and int(t1k[3:].ne(-1).sum()) == 0
     cx.close()
 
@@ -123,6 +169,7 @@ def test_c4_full_size_swap_in_from_log():
     dv.dv_gather_chunks(cx, ep, p0 * step_b, sc, dv.region(0, nL, 0, b, p0, p0 + 1), i - p0, 1)
     torch.cuda.synchronize()
     assert _sample_cache(sk, sv, sc, (0, nL, 0, b, 0, i), SEED) == 0
+    assert _Verify()(sc, (0, nL, 0, b, 0, i)) == 0   # every word of the 4.23 GB prefix
     cx.close()
 
 
