@@ -53,5 +53,44 @@ def run(mode):
     return {"mode": mode, "us_per_step": us, "gbs_per_dir": N / us / 1e3}
 
 
-for m in ("independent", "chained", "kernel"):
-    print(json.dumps(run(m)))
+if __name__ == "__main__" and len(sys.argv) == 1:
+    for m in ("independent", "chained", "kernel"):
+        print(json.dumps(run(m)))
+
+
+def trace(mode="kernel", n=60):
+    """Per-step event stamps (ms since the first): when each H2D, kernel and D2H ended."""
+    ev = {k: [torch.cuda.Event(enable_timing=True) for _ in range(n)] for k in ("h", "k", "d")}
+    t0 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(s_in)
+    s_out.wait_stream(s_in)
+    s_k.wait_stream(s_in)
+    for i in range(n):
+        with torch.cuda.stream(s_in):
+            sl(d1, i).copy_(sl(hsrc, i), non_blocking=True)
+        ev["h"][i].record(s_in)
+        src = d1
+        if mode == "kernel":
+            s_k.wait_event(ev["h"][i])
+            with torch.cuda.stream(s_k):
+                sl(d2, i).copy_(sl(d1, i))
+            ev["k"][i].record(s_k)
+            s_out.wait_event(ev["k"][i])
+            src = d2
+        else:
+            s_out.wait_event(ev["h"][i])
+        with torch.cuda.stream(s_out):
+            sl(hdst, i).copy_(sl(src, i), non_blocking=True)
+        ev["d"][i].record(s_out)
+    torch.cuda.synchronize()
+    rows = []
+    for i in range(n):
+        rows.append({k: round(t0.elapsed_time(ev[k][i]) * 1e3, 1) for k in ("h", "k", "d") if mode == "kernel" or k != "k"})
+    return rows
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
+    for m in ("chained", "kernel"):
+        r = trace(m)
+        print(m, json.dumps(r[20:30]))
