@@ -103,6 +103,7 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cpu_affinity = _bind_gpu_local_cpus(local)   # pinned buffers then land on the GPU's NUMA node
     backend = args.dist_backend
     if world > 1:
         if backend == "nccl":
@@ -289,7 +290,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
         "data": "synthetic (splitmix64 coordinate-hash fill, seed 20240305)",
         "config": dict(CONFIG, parallelism=f"independent stages x{world}" if world > 1 else "1 stage",
-                       xfer=args.xfer),
+                       xfer=args.xfer, cpu_affinity=cpu_affinity),
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": STEP_BYTES,
                 "d2h_bytes_per_step": STEP_BYTES,
                 "how": "per step: dv_gather of the token's K/V from pinned host into the device cache "
@@ -309,6 +310,24 @@ def run_ours(args):
     dv.dv_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _bind_gpu_local_cpus(index):
+    """Bind this process to the CPUs NVML reports as local to GPU `index` (one rank per GPU on a
+    multi-socket box: the first touch of its pinned host buffers then allocates on the socket whose
+    PCIe root the GPU hangs off). Returns the CPU list, or None if NVML is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+        ident = vis[index] if index < len(vis) else str(index)
+        h = (pynvml.nvmlDeviceGetHandleByIndex(int(ident)) if ident.isdigit()
+             else pynvml.nvmlDeviceGetHandleByUUID(ident))
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+        cpus = sorted(os.sched_getaffinity(0))
+        return f"{cpus[0]}-{cpus[-1]} ({len(cpus)} cpus)" if cpus else None
+    except Exception:   # noqa: BLE001 -- affinity is an optimisation, never a failure
+        return None
 
 
 def _ncu_traffic(name="final"):
