@@ -215,6 +215,13 @@ DV_API dv_status dv_destroy(dv_ctx* ctx); /* synchronises the device, frees libr
 
 /* ---- memory and peers -------------------------------------------------------------------- */
 DV_API dv_status dv_host_alloc(uint64_t bytes, void** out);  /* pinned, portable, device-mapped */
+/* Pinned host arena NUMA-local to `device` (SURVEY §8(b) "host memory"): on a multi-socket host
+ * the pages are bound (mbind MPOL_BIND) to the host NUMA node closest to the GPU
+ * (cudaDevAttrHostNumaId), populated, then page-locked and mapped (cudaHostRegister portable |
+ * mapped), so PCIe transfers of that GPU never cross the socket interconnect. *node_out (may be
+ * NULL) receives the node used, or -1 when the system has no NUMA information, in which case
+ * this is dv_host_alloc. Free with dv_host_free. */
+DV_API dv_status dv_host_alloc_near(int32_t device, uint64_t bytes, void** out, int32_t* node_out);
 DV_API dv_status dv_host_free(void* p);
 DV_API dv_status dv_device_alloc(int32_t device, uint64_t bytes, void** out); /* IPC-exportable */
 DV_API dv_status dv_device_free(void* p);

@@ -89,6 +89,7 @@ _SIGS = {
     "dv_create": (C.c_int, [C.c_int32, P(dv_config), P(C.c_void_p)]),
     "dv_destroy": (C.c_int, [C.c_void_p]),
     "dv_host_alloc": (C.c_int, [C.c_uint64, P(C.c_void_p)]),
+    "dv_host_alloc_near": (C.c_int, [C.c_int32, C.c_uint64, P(C.c_void_p), P(C.c_int32)]),
     "dv_host_free": (C.c_int, [C.c_void_p]),
     "dv_device_alloc": (C.c_int, [C.c_int32, C.c_uint64, P(C.c_void_p)]),
     "dv_device_free": (C.c_int, [C.c_void_p]),
@@ -341,6 +342,13 @@ def dv_host_alloc(nbytes) -> int:
     p = C.c_void_p()
     _call("dv_host_alloc", nbytes, C.byref(p))
     return p.value
+
+
+def dv_host_alloc_near(device, nbytes):
+    """Pinned host arena NUMA-local to `device`: returns (pointer, numa node or -1)."""
+    p, node = C.c_void_p(), C.c_int32()
+    _call("dv_host_alloc_near", device, nbytes, C.byref(p), C.byref(node))
+    return p.value, node.value
 
 
 def dv_host_free(p):

@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <limits.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -826,8 +828,57 @@ dv_status dv_host_alloc(uint64_t bytes, void** out) {
   return DV_OK;
 }
 
+// NUMA-bound arenas from dv_host_alloc_near: registered mmap regions (ptr -> bytes).
+static std::mutex g_near_mu;
+static std::map<void*, uint64_t> g_near;
+
+dv_status dv_host_alloc_near(int32_t device, uint64_t bytes, void** out, int32_t* node_out) {
+  if (!out) return fail(DV_EINVAL, "NULL out");
+  int node = -1;
+  if (cudaDeviceGetAttribute(&node, cudaDevAttrHostNumaId, device) != cudaSuccess) node = -1;
+  (void)cudaGetLastError();
+  if (node_out) *node_out = node;
+  if (node < 0 || node >= 1024) return dv_host_alloc(bytes, out);
+  const uint64_t page = (uint64_t)sysconf(_SC_PAGESIZE);
+  const uint64_t len = ((bytes ? bytes : 1) + page - 1) / page * page;
+  void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return fail(DV_ENOMEM, "mmap of %llu bytes failed", (unsigned long long)len);
+  unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+  mask[node / (8 * sizeof(unsigned long))] = 1ul << (node % (8 * sizeof(unsigned long)));
+  const long MPOL_BIND_ = 2;
+  if (syscall(SYS_mbind, p, len, MPOL_BIND_, mask, 1024ul, 0u) != 0 && node_out)
+    *node_out = -1;  // binding refused (e.g. a container without the capability): first touch
+  memset(p, 0, len);  // populate on the bound node
+  cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    munmap(p, len);
+    return cuda_fail(e, "cudaHostRegister");
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_near_mu);
+    g_near[p] = len;
+  }
+  *out = p;
+  return DV_OK;
+}
+
 dv_status dv_host_free(void* p) {
-  if (p) DV_CUDA(cudaFreeHost(p));
+  if (!p) return DV_OK;
+  uint64_t len = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_near_mu);
+    auto it = g_near.find(p);
+    if (it != g_near.end()) {
+      len = it->second;
+      g_near.erase(it);
+    }
+  }
+  if (len) {
+    DV_CUDA(cudaHostUnregister(p));
+    munmap(p, len);
+    return DV_OK;
+  }
+  DV_CUDA(cudaFreeHost(p));
   return DV_OK;
 }
 

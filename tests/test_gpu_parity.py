@@ -940,3 +940,45 @@ def test_peer_enable():
     for peer in range(1, n):                      # only on multi-GPU boxes
         dv.dv_peer_enable(0, peer)
         dv.dv_peer_enable(0, peer)                # idempotent
+
+
+@pytest.mark.parametrize("near", [False, True])
+def test_library_host_arena_stream_out_and_back(near):
+    """Library-owned pinned arenas (dv_host_alloc, dv_host_alloc_near: NUMA-local to the GPU) as
+    the host endpoint of a token-step stream-out (fused and decoupled, flags in the arena) and of
+    the gather back into another cache; every word checked on the device (dvt_verify)."""
+    L, B, H, S, D = 3, 2, 4, 32, 64
+    k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
+    v = torch.empty_like(k)
+    c = dv.cache(k, v)
+    dv.dvt_fill(c, dv.DVT_FILL_HASH, seed=77)
+    step = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    nbytes = 8 * step + 64
+    if near:
+        p, node = dv.dv_host_alloc_near(0, nbytes)
+        assert node >= -1
+    else:
+        p = dv.dv_host_alloc(nbytes)
+    try:
+        ep = dv.endpoint(dv.DV_EP_HOST, p, 8 * step, flags_ptr=p + 8 * step, n_flags=1)
+        torch.cuda.synchronize()
+        import ctypes
+        ctypes.memset(p + 8 * step, 0, 8)
+        cx = ctx()
+        for t in range(8):
+            dv.dv_scatter(cx, c, dv.region(0, L, 0, B, t, t + 1), ep, t * step, flag_slot=0, seq=t + 1,
+                          xfer=dv.DV_XFER_DECOUPLED if t % 2 else dv.DV_XFER_FUSED)
+        dv.dv_wait(cx, ep, 0, 8)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for t in range(8):
+            dv.dvt_verify(c, cnt.data_ptr(), seed=77, reg=dv.region(0, L, 0, B, t, t + 1), wire_ptr=p + t * step)
+        k2, v2 = torch.full_like(k, -1), torch.full_like(v, -1)
+        c2 = dv.cache(k2, v2)
+        dv.dv_gather_chunks(cx, ep, 0, c2, dv.region(0, L, 0, B, 0, 1), 8, 1)
+        dv.dvt_verify(c2, cnt.data_ptr(), seed=77, reg=dv.region(0, L, 0, B, 0, 8))
+        torch.cuda.synchronize()
+        assert int(cnt.item()) == 0
+        assert int(k2[:, :, :, 8:].ne(-1).sum()) == 0
+    finally:
+        torch.cuda.synchronize()
+        dv.dv_host_free(p)
