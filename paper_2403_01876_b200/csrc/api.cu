@@ -324,14 +324,32 @@ static dv_status check_ctx(dv_ctx* ctx) {
   return DV_OK;
 }
 
+// Is `p` memory of this context's GPU (its own HBM)? Then every reader of it -- SMs, copy
+// engines, stream memory operations, peers over NVLink -- is served by this GPU's L2.
+static bool local_vidmem(const dv_ctx* ctx, const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device == ctx->device;
+}
+
+// The release of a fused copy: the endpoint's flag, a ticket, and the scope. Payload (the plans'
+// destinations) and flag all in this GPU's HBM -> a gpu-scope release suffices (publish() protocol
+// 3); anything in pinned host or peer memory -> system scope.
 static Release ticket_release(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
-                              bool use_flag) {
+                              bool use_flag, const CopyPlan* p, int np) {
   Release r{nullptr, 0, nullptr};
   if (use_flag && slot >= 0 && ep && ep->flags) {
     r.flag = (unsigned long long*)&ep->flags[slot];
     r.seq = seq;
     r.ticket = ctx->tickets + (ctx->next_ticket.fetch_add(1) % dv_ctx::kTickets);
     r.ts = ctx->trace_ts;
+    bool local = local_vidmem(ctx, r.flag);
+    for (int q = 0; q < np && local; ++q)
+      if (p[q].dst && p[q].runs() && p[q].run_bytes) local = local_vidmem(ctx, p[q].dst);
+    r.gpu_scope = local;
   }
   return r;
 }
@@ -364,7 +382,7 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
   const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
   const Release none{nullptr, 0, nullptr};
   if (np == 2) {
-    DV_TRY(launch_copy2(p[0], p[1], streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag),
+    DV_TRY(launch_copy2(p[0], p[1], streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag, p, np),
                         ctas, st));
     if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
     return DV_OK;
@@ -372,7 +390,7 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
   for (int q = 0; q < np; ++q) {
     const bool last = q == np - 1;
     DV_TRY(launch_copy(p[q], 0, p[q].runs(),
-                       (last && !streamop) ? ticket_release(ctx, ep, slot, seq, use_flag) : none,
+                       (last && !streamop) ? ticket_release(ctx, ep, slot, seq, use_flag, p, np) : none,
                        ctas, st));
   }
   if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));

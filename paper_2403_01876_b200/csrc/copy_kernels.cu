@@ -50,7 +50,7 @@ struct KParams {
   DevDiv fd[kDims];   // n[k] (fd[0] unused: the outermost index is what remains)
   uint32_t q_begin;  // first run of this launch
   uint32_t n_vec;    // vectors in this launch (< 2^31)
-  int32_t per_cta_sys;  // publish variant (see publish())
+  int32_t pub;  // publish protocol (see publish())
   unsigned long long* flag;
   unsigned long long seq;
   unsigned int* ticket;
@@ -145,13 +145,19 @@ __device__ __forceinline__ void locate(const KParams& p, const uint8_t* src, uin
 // Publish protocol: every CTA orders its stores before a GPU-scope release
 // (bar.sync, then thread 0's fence.acq_rel.gpu + ticket atomic); the CTA that takes the last
 // ticket has, by the acquire on that atomic, every CTA's stores ordered before it, and makes them
-// visible to the system with ONE fence.sc.sys before the st.release.sys of the flag (PTX memory
-// model: causality order is transitive, fences are cumulative). DV_PUBLISH=0 selects the older,
-// more conservative variant with a system fence in every CTA.
-__device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsigned long long seq) {
+// visible to the system with the ONE system-scope release of the flag, st.release.sys (PTX memory
+// model: causality order is transitive, fences are cumulative). Protocols (`pub`, DV_PUBLISH;
+// measured per-layer latency in DESIGN.md §6):
+//   0  system fence in every CTA before the ticket (the most conservative form);
+//   1  gpu-scope ticket chain, then fence.sc.sys + st.release.sys in the last CTA;
+//   2  gpu-scope ticket chain, then st.release.sys alone (its own fence is the cumulative one);
+//   3  gpu-scope ticket chain, then st.release.gpu: only when payload and flag both live in this
+//      GPU's HBM, whose every reader (SMs, copy engines, stream memory ops, peers over NVLink) is
+//      served by this GPU's L2, where the gpu-scope release has already made the stores visible.
+__device__ __forceinline__ void publish(const KParams& p, int pub, unsigned long long seq) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (per_cta_sys) {
+    if (pub == 0) {
       __threadfence_system();
     } else {
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -159,9 +165,12 @@ __device__ __forceinline__ void publish(const KParams& p, int per_cta_sys, unsig
     unsigned int prev = atomicAdd(p.ticket, 1u);
     if (prev == gridDim.x - 1) {
       asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire side of the ticket chain
-      __threadfence_system();                          // fence.sc.sys: everything -> system scope
+      if (pub <= 1) __threadfence_system();            // fence.sc.sys: everything -> system scope
       *p.ticket = 0u;  // ready for the next stream-ordered user of this ticket
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
+      if (pub == 3)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
+      else
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
       if (p.ts) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 ? DV_MIN_BLOCKS : 1))
       atomicMax(p.ts + 3, t);  // last CTA done with its stores (issued)
     }
   }
-  if (p.flag) publish(p, p.per_cta_sys, p.seq + (unsigned long long)k);
+  if (p.flag) publish(p, p.pub, p.seq + (unsigned long long)k);
 }
 
 // Two plans in one launch (K and V with different structures, e.g. an FT6D key + a KV5D value
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(THREADS) k_run_copy2(const KParams a, const KP
       if (g < total) st_vec(d[i], v[i]);
     }
   }
-  if (a.flag) publish(a, a.per_cta_sys, a.seq + (unsigned long long)k);
+  if (a.flag) publish(a, a.pub, a.seq + (unsigned long long)k);
 }
 
 // Dense-destination variant: the destination of vectors [q_begin*vpr, ...) is one contiguous
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t*
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
-  if (p.flag) publish(p, p.per_cta_sys, p.seq);
+  if (p.flag) publish(p, p.pub, p.seq);
 }
 
 // 16-byte packet transpose through shared memory (NEXT-1, FasterTransformer's 6-D key layout):
@@ -344,7 +353,7 @@ struct TParams {
   unsigned long long seq;
   unsigned int* ticket;
   unsigned long long* ts;
-  int32_t per_cta_sys;
+  int32_t pub;
   const int32_t* dyn;
   int64_t dyn_ss, dyn_ds;
   int32_t dyn_max;
@@ -545,7 +554,7 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
     kp.flag = p.flag;
     kp.ticket = p.ticket;
     kp.ts = p.ts;
-    publish(kp, p.per_cta_sys, p.seq + (unsigned long long)k);
+    publish(kp, p.pub, p.seq + (unsigned long long)k);
   }
 }
 
@@ -577,7 +586,7 @@ __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KP
     kp.flag = t.flag;
     kp.ticket = t.ticket;
     kp.ts = t.ts;
-    publish(kp, t.per_cta_sys, t.seq + (unsigned long long)k);
+    publish(kp, t.pub, t.seq + (unsigned long long)k);
   }
 }
 
@@ -626,7 +635,7 @@ struct Tune {
   int u = 0;          // DV_U: vectors in flight per thread (1,2,4,8); 0 = automatic
   int vec = 0;        // DV_VEC: force 16-byte vectors when 16
   int bulk = 0;       // DV_BULK: 1 = dense-destination copies use k_pack_bulk
-  int per_cta_sys = 0;  // DV_PUBLISH=0: system fence in every CTA before the ticket
+  int pub = 2;  // DV_PUBLISH: publish protocol (see publish()); 3 only where the scope allows
   uint64_t max_vec_per_launch = (1ull << 31) - 1;  // DV_MAX_VEC (tests of the launch split)
   int stm = 0;  // DV_STM: store cache operator for U=4 copies (0 default .wb, 1 .cs, 2 .wt)
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
@@ -638,7 +647,7 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_U")) x.u = atoi(e);
     if (const char* e = getenv("DV_VEC")) x.vec = atoi(e);
     if (const char* e = getenv("DV_BULK")) x.bulk = atoi(e);
-    if (const char* e = getenv("DV_PUBLISH")) x.per_cta_sys = (atoi(e) == 0);
+    if (const char* e = getenv("DV_PUBLISH")) x.pub = atoi(e);
     if (const char* e = getenv("DV_STM")) x.stm = atoi(e);
     if (const char* e = getenv("DV_MAX_VEC")) {
       const uint64_t v = strtoull(e, nullptr, 10);
@@ -649,6 +658,14 @@ static const Tune& tune() {
     return x;
   }();
   return t;
+}
+
+// Publish protocol of a release: the environment's (default 2, system scope), narrowed to gpu
+// scope (3) when payload and flag are all in this GPU's HBM; DV_PUBLISH=0/1 keep their forms.
+static int pub_of(const Release& rel) {
+  const int t = tune().pub;
+  if (t < 2) return t;
+  return rel.gpu_scope ? 3 : 2;
 }
 
 template <int VEC>
@@ -746,7 +763,7 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
   tp.seq = rel.seq;
   tp.ticket = rel.ticket;
   tp.ts = rel.ts;
-  tp.per_cta_sys = tune().per_cta_sys;
+  tp.pub = pub_of(rel);
   tp.dyn = p.dyn;
   tp.dyn_ss = p.dyn_ss;
   tp.dyn_ds = p.dyn_ds;
@@ -927,7 +944,7 @@ dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel,
   ka.seq = rel.seq;
   ka.ticket = rel.ticket;
   ka.ts = rel.ts;
-  ka.per_cta_sys = tune().per_cta_sys;
+  ka.pub = pub_of(rel);
   const uint64_t total = (uint64_t)ka.n_vec + kb.n_vec;
   cudaError_t e;
   if (total <= tune().small) {
@@ -958,7 +975,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
       kp.seq = rel.seq;
       kp.ticket = rel.ticket;
       kp.ts = rel.ts;
-      kp.per_cta_sys = tune().per_cta_sys;
+      kp.pub = pub_of(rel);
       kp.dyn = p.dyn;
       kp.dyn_max = p.dyn_max;
       cudaError_t e = go<16, 1, 32>(kp, 1, stream);
@@ -1003,7 +1020,7 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.seq = rel.seq;
     kp.ticket = rel.ticket;
     kp.ts = last ? rel.ts : nullptr;
-    kp.per_cta_sys = tune().per_cta_sys;
+    kp.pub = pub_of(rel);
     cudaError_t e = (tune().bulk && dense_dst(p) && !p.dyn)
                         ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
                         : launch_cfg(kp, VEC, max_ctas, stream);

@@ -80,6 +80,7 @@ struct Release {
   unsigned long long seq;
   unsigned int* ticket;      // per-launch CTA counter (library-owned, zero between uses)
   unsigned long long* ts = nullptr;  // optional publish timestamp (dvt_trace)
+  bool gpu_scope = false;  // payload and flag in this GPU's HBM: gpu-scope release
 };
 
 // Enqueue the copy kernel(s) for runs [q_first, q_last) of the (collapsed) plan `p` on `stream`;
