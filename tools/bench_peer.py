@@ -72,9 +72,11 @@ def run_c5(args, bench):
     rep_k = torch.full((Ls, b, H, S, D), -1, dtype=torch.int16, device=dev)
     rep_v = torch.full_like(rep_k, -1)
     flags = torch.zeros(P, dtype=torch.int64, device=dev)
+    ack = torch.zeros(1, dtype=torch.int64, device=dev)   # the successor's ping-pong acks land here
     torch.cuda.synchronize()
     blob = {"k": dv.dv_ipc_export(rep_k.data_ptr()), "v": dv.dv_ipc_export(rep_v.data_ptr()),
-            "f": dv.dv_ipc_export(flags.data_ptr()), "layer_begin": pred * Ls}
+            "f": dv.dv_ipc_export(flags.data_ptr()), "a": dv.dv_ipc_export(ack.data_ptr()),
+            "layer_begin": pred * Ls}
     blobs = _gather(blob, world)
     succ = (rank + 1) % P
     sb = blobs[succ]
@@ -129,6 +131,8 @@ def run_c5(args, bench):
     torch.cuda.synchronize()
     l1, _ = dv.dv_stats()
     ms = _max(a.elapsed_time(e), world, dev, args.dist_backend)
+    pingpong = None if nccl else _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, blobs[pred]["a"],
+                                           lb, Ls, b, p, S, P, world, dev, args, st)
     # the predecessor's last step landed in our replica store: sampled parity vs kvgen
     if world > 1:
         dist.barrier()
@@ -148,13 +152,58 @@ def run_c5(args, bench):
                                    f"one position per step -> successor's replica store",
                        "bytes_per_step_per_stage": step_bytes, "parallelism": f"pp{P} ring",
                        "transport": "CUDA IPC peer stores" if world > 1 else "loopback (same GPU)"},
-            "gpu_launches": int(l1 - l0), "parity_spot_check": {"mismatches": bad},
+            "gpu_launches": int(l1 - l0), "parity_spot_check": {"mismatches": bad}, "pingpong": pingpong,
             "ideal_us_per_step_at_770GBps": step_bytes / 770e3}), flush=True)
     for x in (kp, vp, fp):
         dv.dv_ipc_close(x)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, pred_ack_blob, lb, Ls, b, p, S, P, world, dev,
+              args, st, iters=500):
+    """SURVEY §8(d) peer latency, second form: a ping-pong per token·layer (one layer, one
+    position, b 16 = 589,824 B). Every iteration each stage x (1) puts the layer into the replica
+    store at (x+1)%P with its seq flag (dv_stream_out_direct), (2) waits on the stream for the flag
+    its predecessor puts into its own memory, (3) writes an ack into the predecessor's memory
+    (dv_signal over the peer mapping) and (4) waits for its successor's ack. RTT = device time per
+    iteration (a spin head start hides the host enqueue); one-way ~ RTT / 2. At N = 1 the peer is
+    this GPU (loopback)."""
+    pa = dv.dv_ipc_open(pred_ack_blob)
+    pred_ack = dv.endpoint(dv.DV_EP_PEER, pa, 8, pa, 1)
+    own_ack = dv.endpoint(dv.DV_EP_DEVICE, ack.data_ptr(), 8, ack.data_ptr(), 1)
+    inbox = dv.endpoint(dv.DV_EP_DEVICE, flags.data_ptr(), 8 * P, flags.data_ptr(), P)
+    sp = st.cuda_stream
+    q = S - 1
+    base = 10 ** 7
+
+    def one(i):
+        layer = lb + i % Ls
+        dv.dv_stream_out_direct(ctx, own, dv.region(layer, layer + 1, 0, b, q, q + 1), setup, 0, 0, setup,
+                                [rep_at_succ], [sig], seq=base + i, stream=sp)
+        dv.dv_wait(ctx, inbox, 0, base + i, stream=sp)
+        dv.dv_signal(ctx, pred_ack, 0, base + i, stream=sp)
+        dv.dv_wait(ctx, own_ack, 0, base + i, stream=sp)
+    for i in range(20):
+        one(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dv.dvt_spin(max(4_000_000, iters * 12_000), 1, stream=sp)
+    a.record(st)
+    for i in range(20, 20 + iters):
+        one(i)
+    e.record(st)
+    torch.cuda.synchronize()
+    rtt = _max(a.elapsed_time(e) * 1e3 / iters, world, dev, args.dist_backend)
+    if world > 1:
+        dist.barrier()
+    dv.dv_ipc_close(pa)
+    return {"rtt_us": rtt, "one_way_us": rtt / 2, "bytes": 2 * b * H * D * 2, "iters": iters,
+            "how": "put+flag -> stream wait on the predecessor's flag -> ack into its memory -> wait own ack; "
+                   "device time per iteration, max over ranks"}
 
 
 def _token_bounds(n):
