@@ -468,6 +468,20 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["token_step_pack_hbm_us"] = ms * 1e3
     ex["token_step_pack_hbm_gbs_2R"] = 2 * STEP_BYTES / ms / 1e6
     ex["token_step_pack_hbm_frac"] = ex["token_step_pack_hbm_gbs_2R"] / HBM_PEAK
+    # the practical floor for a launch of this size: a contiguous 6.55 MB device-to-device copy
+    # (cudaMemcpyAsync via torch), source ring larger than L2, same head start, back to back
+    src_d = torch.empty(STEP_BYTES * 40, dtype=torch.uint8, device="cuda")   # 262 MB ring > L2
+    dst_d = torch.empty(STEP_BYTES, dtype=torch.uint8, device="cuda")
+    ce = [0]
+
+    def d2d():
+        ce[0] += 1
+        o = (ce[0] % 40) * STEP_BYTES
+        dst_d.copy_(src_d[o:o + STEP_BYTES], non_blocking=True)
+    ms = _time(d2d, stream, reps, head_start_ns=4_000_000)
+    ex["token_step_same_size_d2d_copy_us"] = ms * 1e3
+    ex["token_step_pack_vs_same_size_copy"] = ex["token_step_same_size_d2d_copy_us"] / ex["token_step_pack_hbm_us"]
+    del src_d, dst_d
     ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else args.xfer
 
     # per-layer token latency: from "layer l's new K/V written" to "bytes resident at
@@ -614,14 +628,26 @@ class OracleStep:
         self.log = np.empty(STEP_BYTES // 2 * 4, np.uint16)
         self.t = 0
 
-    def step(self):
+    def step(self, pool=None):
         ok = self.ok
         q = P + self.t % self.n_pos
         reg = (0, L, 0, B, q, q + 1)
+        o = (self.t % 4) * (STEP_BYTES // 2)
         for p in ok.route(self.setup, self.setup, reg, H, D, E):
-            wire = ok.transfer(ok.pack(self.cache, p.region()))
-            o = (self.t % 4) * (STEP_BYTES // 2)
-            self.log[o:o + wire.size] = wire
+            r = p.region()
+            if pool is None:
+                wire = ok.transfer(ok.pack(self.cache, r))
+                self.log[o:o + wire.size] = wire
+                continue
+            # all cores (SURVEY §8(d) oracle timing (ii)): the same oracle calls, one per layer
+            # slab of the piece, on a thread pool (numpy releases the GIL while copying)
+            slab = LAYER_BYTES // 2 * (r[5] - r[4])
+
+            def one(layer, r=r):
+                w = ok.transfer(ok.pack(self.cache, (layer, layer + 1) + tuple(r[2:])))
+                j = o + (layer - r[0]) * slab
+                self.log[j:j + w.size] = w
+            list(pool.map(one, range(r[0], r[1])))
         self.t += 1
 
 
@@ -634,10 +660,24 @@ def cpu_baseline(seconds=10.0):
         o.step()
         n += 1
     dt = time.perf_counter() - t0
-    return {"value": n * STEP_BYTES / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} C2 token steps (route+pack+transfer of 6,553,600 B each) over "
-                      f"{o.n_pos} distinct positions of a lazily materialised 13.4 GB host cache, "
-                      f"{dt:.1f} s, numpy single-threaded"}
+    out = {"value": n * STEP_BYTES / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+           "sample": f"{n} C2 token steps (route+pack+transfer of 6,553,600 B each) over "
+                     f"{o.n_pos} distinct positions of a lazily materialised 13.4 GB host cache, "
+                     f"{dt:.1f} s, numpy single-threaded"}
+    from concurrent.futures import ThreadPoolExecutor
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    with ThreadPoolExecutor(cores) as pool:
+        o.step(pool)
+        t0 = time.perf_counter()
+        m = 0
+        while time.perf_counter() - t0 < seconds / 2:
+            o.step(pool)
+            m += 1
+        dt2 = time.perf_counter() - t0
+    out["all_cores"] = {"value": m * STEP_BYTES / dt2 / 1e9, "unit": "GB/s", "cores": cores,
+                        "sample": f"{m} C2 token steps, the same oracle calls per layer slab on a "
+                                  f"{cores}-thread pool, {dt2:.1f} s"}
+    return out
 
 
 def run_reference(args):
