@@ -8,7 +8,8 @@ import torch  # noqa: E402
 
 import paper_2403_01876_b200 as dv  # noqa: E402
 
-L, H, D, B, P, S = 40, 40, 128, 8, 1000, 2048
+L, H, D, B, P = 40, 40, 128, 8, 1000
+S = int(os.environ.get("PROBE_S", "2048"))   # max_seq of the cache (TLB reach experiments)
 k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
 v = torch.empty_like(k)
 c = dv.cache(k, v)
@@ -22,7 +23,7 @@ cnt = [0]
 
 def one():
     cnt[0] += 1
-    q = P + cnt[0] % 1000
+    q = (P + cnt[0] % 1000) % S
     dv.dv_scatter(ctx, c, dv.region(0, L, 0, B, q, q + 1), ep, (cnt[0] % 8) * nb)
 
 
@@ -41,5 +42,5 @@ def t1(n=200):
 
 
 us = sorted(t1() for _ in range(7))[3]
-print(f"U={os.environ.get('DV_U', 'auto')} SMALL={os.environ.get('DV_SMALL', 'default')} "
+print(f"S={S} U={os.environ.get('DV_U', 'auto')} SMALL={os.environ.get('DV_SMALL', 'default')} "
       f"us={us:.2f} frac_2R={2 * nb / us / 1e3 / 6534.8:.3f}")
