@@ -46,6 +46,39 @@ def test_no_cpu_fallback_without_gpu():
     assert ei.value.status == dv.DV_ECUDA
 
 
+def test_oracle_used_only_by_tests_smoke_and_cpu_baseline():
+    """The oracle is test infrastructure: the package, kvgen and tools/ never import it, and
+    bench.py imports it only inside its CPU-oracle arm (OracleStep: cpu_baseline, --impl reference)."""
+    import ast
+    import pathlib
+    root = pathlib.Path(__file__).resolve().parents[1]
+
+    def oracle_imports(path):
+        tree = ast.parse(path.read_text())
+        out = []
+        for node in ast.walk(tree):
+            names = []
+            if isinstance(node, ast.Import):
+                names = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom):
+                names = [node.module or ""]
+            if any(n == "oracle" or n.startswith("oracle.") for n in names):
+                out.append(node.lineno)
+        return out
+    files = [*root.glob("paper_2403_01876_b200/**/*.py"), *root.glob("kvgen/**/*.py"), *root.glob("tools/*.py")]
+    assert files
+    for f in files:
+        assert not oracle_imports(f), f"{f} imports the oracle"
+    src = (root / "bench.py").read_text()
+    lo = src.index("class OracleStep")
+    hi = src.index("\ndef ", src.index("def cpu_baseline"))
+    for line in oracle_imports(root / "bench.py"):
+        off = sum(len(x) + 1 for x in src.splitlines()[:line - 1])
+        assert lo <= off < hi, f"bench.py:{line} imports the oracle outside its CPU-oracle arm"
+    for f in root.glob("paper_2403_01876_b200/csrc/*"):
+        assert "oracle" not in f.read_text(), f"{f} mentions the oracle"
+
+
 def _region_bytes_oracle(r, H, D, e):
     return ok.region_bytes(r.layer_begin, r.layer_end, r.req_begin, r.req_end, r.pos_begin, r.pos_end, H, D, e)
 

@@ -21,7 +21,6 @@ import torch  # noqa: E402
 
 import kvgen  # noqa: E402
 import paper_2403_01876_b200 as dv  # noqa: E402
-from oracle import kvstream as ok  # noqa: E402
 
 HBM = 6534.8
 SEED = 20240304
