@@ -376,18 +376,23 @@ struct TParams {
   // register form (transpose_regs): items = slabs x (U / PK) packet groups x N positions
   uint32_t n_items;
   DevDiv fN, fG;
-  int32_t pk;    // packets per thread item (1 or 2); 0 = shared-memory tiles
+  int32_t pk;    // packets per thread item (1, 2, 4, 8, 16); 0 = shared-memory tiles
 };
 
 // Register form of the packet transpose: no shared memory, no barrier. A thread item is PK
 // adjacent packets of ONE position: on the packet-major side the PK 16-byte loads (or stores) of a
-// warp's 32 consecutive positions are PK fully coalesced 512-byte segments; on the
-// position-major side each item is one PK*16-byte vector (PK = 2: a whole 32-byte sector). Four
-// items per thread are in flight before the first store.
+// warp's 32 consecutive positions are PK fully coalesced 512-byte segments; on the position-major
+// side each item is one contiguous PK*16-byte piece moved as 32-byte vectors (PK = 16: a whole
+// 256-byte row, i.e. two full 128-byte lines per thread). IT items per thread are in flight before
+// the first store (PK*IT*16 = 128 bytes for PK <= 4 and 8, 256 for PK = 16).
+template <int PK>
+struct TrIt {
+  static constexpr int value = PK >= 8 ? 1 : PK == 4 ? 2 : 4;
+};
 template <int DIR, int PK>
 __device__ __forceinline__ void transpose_regs(const TParams& p, const uint8_t* src0, uint8_t* dst0,
                                                uint32_t bid, uint32_t nb) {
-  constexpr int IT = PK == 4 ? 2 : 4;
+  constexpr int IT = TrIt<PK>::value;
   for (uint32_t b0 = bid * IT * 256; b0 < p.n_items; b0 += nb * IT * 256) {
     Vec<16 * PK> v[IT];
     uint8_t* d[IT];
@@ -423,14 +428,16 @@ __device__ __forceinline__ void transpose_regs(const TParams& p, const uint8_t* 
           d[j] = dst0 + dof + (int64_t)s * p.sps + (int64_t)u0 * 16;
         } else {         // position-major source, packet-major destination
           const uint8_t* a = src0 + so + (int64_t)s * p.sps + (int64_t)u0 * 16;
-          if constexpr (PK == 4) {
-            Vec<32> x, y;
-            ld_vec(x, a);
-            ld_vec(y, a + 32);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) v[j].w[c] = x.w[c], v[j].w[8 + c] = y.w[c];
-          } else {
+          if constexpr (PK == 1) {
             ld_vec(v[j], a);
+          } else {
+#pragma unroll
+            for (int k = 0; k < PK / 2; ++k) {
+              Vec<32> x;
+              ld_vec(x, a + 32 * k);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) v[j].w[8 * k + c] = x.w[c];
+            }
           }
           d[j] = dst0 + dof + (int64_t)u0 * p.su + (int64_t)s * 16;
         }
@@ -440,14 +447,16 @@ __device__ __forceinline__ void transpose_regs(const TParams& p, const uint8_t* 
     for (int j = 0; j < IT; ++j) {
       if (!d[j]) continue;
       if (DIR == 0) {
-        if constexpr (PK == 4) {
-          Vec<32> a, b;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) a.w[c] = v[j].w[c], b.w[c] = v[j].w[8 + c];
-          st_vec(d[j], a);
-          st_vec(d[j] + 32, b);
-        } else {
+        if constexpr (PK == 1) {
           st_vec(d[j], v[j]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < PK / 2; ++k) {
+            Vec<32> x;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x.w[c] = v[j].w[8 * k + c];
+            st_vec(d[j] + 32 * k, x);
+          }
         }
       } else {
 #pragma unroll
@@ -461,10 +470,6 @@ __device__ __forceinline__ void transpose_regs(const TParams& p, const uint8_t* 
     }
   }
 }
-
-template <int DIR>
-__device__ __forceinline__ void transpose_any(const TParams& p, uint4* tile, const uint8_t* src0,
-                                              uint8_t* dst0, uint32_t bid, uint32_t nb);
 
 template <int DIR>
 __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, const uint8_t* src0,
@@ -540,20 +545,18 @@ __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, c
   }
 }
 
-template <int DIR>
+// PK is a template parameter of the kernels (not a runtime branch): the register budget of each
+// instantiation is that of its own form (59-64 registers at PK <= 4, 1024 threads per SM).
+template <int DIR, int PK>
 __device__ __forceinline__ void transpose_any(const TParams& p, uint4* tile, const uint8_t* src0,
                                               uint8_t* dst0, uint32_t bid, uint32_t nb) {
-  if (p.pk == 4)
-    transpose_regs<DIR, 4>(p, src0, dst0, bid, nb);
-  else if (p.pk == 2)
-    transpose_regs<DIR, 2>(p, src0, dst0, bid, nb);
-  else if (p.pk == 1)
-    transpose_regs<DIR, 1>(p, src0, dst0, bid, nb);
-  else
+  if constexpr (PK == 0)
     transpose_tiles<DIR>(p, tile, src0, dst0, bid, nb);
+  else
+    transpose_regs<DIR, PK>(p, src0, dst0, bid, nb);
 }
 
-template <int DIR>
+template <int DIR, int PK>
 __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
   extern __shared__ uint4 tile[];  // kTS rows x (U + 1) packets
   pdl_enter();
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
   }
   const uint8_t* src0 = p.src + (int64_t)k * p.dyn_ss;
   uint8_t* dst0 = p.dst + (int64_t)k * p.dyn_ds;
-  transpose_any<DIR>(p, tile, src0, dst0, blockIdx.x, gridDim.x);
+  transpose_any<DIR, PK>(p, tile, src0, dst0, blockIdx.x, gridDim.x);
   if (p.flag) {
     KParams kp{};
     kp.flag = p.flag;
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(256) k_packet_transpose(const TParams p) {
 
 // An FT6D key transpose and the value's run copy in ONE launch: CTAs [0, t_blocks) transpose, the
 // rest run-copy; both halves share the dependency wait, the step counter and the release.
-template <int DIR, int VEC>
+template <int DIR, int VEC, int PK>
 __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KParams r,
                                                        uint32_t t_blocks) {
   extern __shared__ uint4 tile[];
@@ -587,12 +590,12 @@ __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KP
     if (k < 0 || k > t.dyn_max) return;
   }
   if (t_blocks == 0) {  // every CTA takes its share of both halves
-    transpose_any<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
+    transpose_any<DIR, PK>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
                        blockIdx.x, gridDim.x);
     run_chunks<VEC, 4, 256>(r, r.src + (int64_t)k * r.dyn_ss, r.dst + (int64_t)k * r.dyn_ds,
                             blockIdx.x, gridDim.x);
   } else if (blockIdx.x < t_blocks)
-    transpose_any<DIR>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
+    transpose_any<DIR, PK>(t, tile, t.src + (int64_t)k * t.dyn_ss, t.dst + (int64_t)k * t.dyn_ds,
                        blockIdx.x, t_blocks);
   else
     run_chunks<VEC, 4, 256>(r, r.src + (int64_t)k * r.dyn_ss, r.dst + (int64_t)k * r.dyn_ds,
@@ -655,7 +658,8 @@ struct Tune {
   uint64_t max_vec_per_launch = (1ull << 31) - 1;  // DV_MAX_VEC (tests of the launch split)
   int stm = 0;  // DV_STM: store cache operator for U=4 copies (0 default .wb, 1 .cs, 2 .wt)
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
-  int trs = 0;  // DV_TRS: packet transpose form (0 registers PK<=4; 1 shared-memory tiles; 2 PK=1; 3 PK<=2)
+  int trs = 0;  // DV_TRS: packet transpose form (0 registers PK<=pk; 1 shared-memory tiles; 2 PK=1; 3 PK<=2)
+  int pk = 16;  // DV_PK: largest packets per register-transpose item (1, 2, 4, 8, 16)
 };
 static const Tune& tune() {
   static Tune t = [] {
@@ -671,6 +675,7 @@ static const Tune& tune() {
     }
     if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
     if (const char* e = getenv("DV_TRS")) x.trs = atoi(e);
+    if (const char* e = getenv("DV_PK")) x.pk = atoi(e);
     return x;
   }();
   return t;
@@ -790,10 +795,16 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
   uint64_t pm = p.t_ss | (uint64_t)(p.tdir == 0 ? p.dyn_ds : p.dyn_ss) |
                 (uint64_t)(uintptr_t)(p.tdir == 0 ? p.dst : p.src);
   for (int d = 0; d < 4; ++d) pm |= (uint64_t)(p.tdir == 0 ? tp.ds[d] : tp.ss[d]);
-  const int want = tune().trs == 3 ? 2 : tune().trs == 2 ? 1 : 4;
-  tp.pk = tune().trs == 1 || items1 >= (1ull << 31) ? 0
-          : (want >= 4 && p.tU % 4 == 0 && pm % 32 == 0) ? 4
-          : (want >= 2 && p.tU % 2 == 0 && pm % 32 == 0) ? 2 : 1;
+  const int want = tune().trs == 3 ? 2 : tune().trs == 2 ? 1 : tune().pk;
+  tp.pk = 0;
+  if (tune().trs != 1 && items1 < (1ull << 31)) {
+    tp.pk = 1;
+    for (int k = 16; k >= 2; k /= 2)
+      if (want >= k && p.tU % k == 0 && pm % 32 == 0) {
+        tp.pk = k;
+        break;
+      }
+  }
   if (tp.pk) {
     tp.n_items = (uint32_t)(items1 / tp.pk);
     tp.fN = to_dev(make_fastdiv(p.tN));
@@ -805,19 +816,47 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
 
 // CTAs a transpose plan can use, and its dynamic shared memory.
 static uint64_t transpose_ctas(const TParams& tp) {
-  return tp.pk == 4 ? (tp.n_items + 511) / 512 : tp.pk ? (tp.n_items + 1023) / 1024 : tp.n_tiles;
+  if (!tp.pk) return tp.n_tiles;
+  const uint64_t per = tp.pk >= 8 ? 256 : tp.pk == 4 ? 512 : 1024;  // IT * 256 items per CTA pass
+  return (tp.n_items + per - 1) / per;
 }
 static int transpose_smem(const TParams& tp) { return tp.pk ? 0 : kTS * (tp.U + 1) * 16; }
 
 static void set_transpose_smem() {
   static std::atomic<uint64_t> mask{0};
   if (first_use_on_device(mask)) {
-    cudaFuncSetAttribute(k_packet_transpose<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_packet_transpose<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_transpose_run<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_transpose_run<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_transpose_run<0, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_transpose_run<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_packet_transpose<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_packet_transpose<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<0, 16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<1, 16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<0, 32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_transpose_run<1, 32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  }
+}
+
+// Kernel instantiation for a (direction, vector width, PK) triple.
+using PtFn = void (*)(TParams);
+using TrFn = void (*)(TParams, KParams, uint32_t);
+template <int DIR>
+static PtFn pt_fn(int pk) {
+  switch (pk) {
+    case 16: return k_packet_transpose<DIR, 16>;
+    case 8: return k_packet_transpose<DIR, 8>;
+    case 4: return k_packet_transpose<DIR, 4>;
+    case 2: return k_packet_transpose<DIR, 2>;
+    case 1: return k_packet_transpose<DIR, 1>;
+    default: return k_packet_transpose<DIR, 0>;
+  }
+}
+template <int DIR, int VEC>
+static TrFn tr_fn(int pk) {
+  switch (pk) {
+    case 16: return k_transpose_run<DIR, VEC, 16>;
+    case 8: return k_transpose_run<DIR, VEC, 8>;
+    case 4: return k_transpose_run<DIR, VEC, 4>;
+    case 2: return k_transpose_run<DIR, VEC, 2>;
+    case 1: return k_transpose_run<DIR, VEC, 1>;
+    default: return k_transpose_run<DIR, VEC, 0>;
   }
 }
 
@@ -838,8 +877,7 @@ static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = p.tdir == 0 ? cudaLaunchKernelEx(&cfg, k_packet_transpose<0>, tp)
-                              : cudaLaunchKernelEx(&cfg, k_packet_transpose<1>, tp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, p.tdir == 0 ? pt_fn<0>(tp.pk) : pt_fn<1>(tp.pk), tp);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "transpose kernel launch");
@@ -902,9 +940,9 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   const double tb = (double)tp.n_tiles * kTS * t.tU * 16, rb = (double)r.runs() * r.run_bytes;
   const uint64_t t_need = transpose_ctas(tp), r_need = (kr.n_vec + 1023) / 1024;
   const uint64_t grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, t_need + r_need));
-  // transpose CTAs get 0.45 of their byte share (measured on the C2 FT6D prompt layer: the run
-  // half is the straggler at 1.0; DV_TSPLIT=0 = every CTA does both halves)
-  static const double tscale = getenv("DV_TSPLIT") ? atof(getenv("DV_TSPLIT")) : 0.45;
+  // transpose CTAs get 0.7 of their byte share (measured on the C2 FT6D prompt layer with PK = 16,
+  // tools/ft6d_cmp.sh: 0.96 of HBM peak at 0.7, 0.94 at 1.0; DV_TSPLIT=0 = every CTA does both)
+  static const double tscale = getenv("DV_TSPLIT") ? atof(getenv("DV_TSPLIT")) : 0.7;
   uint64_t t_blocks = (uint64_t)(grid * tscale * tb / (tscale * tb + rb) + 0.5);
   t_blocks = std::min(std::max<uint64_t>(1, t_blocks), grid - 1);
   if (tscale == 0) t_blocks = 0;
@@ -922,12 +960,9 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   const uint32_t tbk = (uint32_t)t_blocks;
   cudaError_t e;
-  if (t.tdir == 0)
-    e = VEC == 32 ? cudaLaunchKernelEx(&cfg, k_transpose_run<0, 32>, tp, kr, tbk)
-                  : cudaLaunchKernelEx(&cfg, k_transpose_run<0, 16>, tp, kr, tbk);
-  else
-    e = VEC == 32 ? cudaLaunchKernelEx(&cfg, k_transpose_run<1, 32>, tp, kr, tbk)
-                  : cudaLaunchKernelEx(&cfg, k_transpose_run<1, 16>, tp, kr, tbk);
+  const TrFn fn = t.tdir == 0 ? (VEC == 32 ? tr_fn<0, 32>(tp.pk) : tr_fn<0, 16>(tp.pk))
+                               : (VEC == 32 ? tr_fn<1, 32>(tp.pk) : tr_fn<1, 16>(tp.pk));
+  e = cudaLaunchKernelEx(&cfg, fn, tp, kr, tbk);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "transpose+run kernel launch");
