@@ -45,6 +45,12 @@ DV_API dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kind, u
  * over CTAs of "stores issued". NULL disables. */
 DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
 
+/* Release scope the fused publish of `ctx` would use for a flag at `flag` after stores to
+ * `payload`: *gpu_scope = 1 when both are this context's GPU's own device memory (not mapped from
+ * another process), 0 otherwise (system scope). Host-only query; DESIGN.md §6 protocols 2/3. */
+DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
+                                   int32_t* gpu_scope);
+
 /* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */
 DV_API dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream);
 

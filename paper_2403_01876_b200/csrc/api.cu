@@ -13,6 +13,7 @@
 #include <mutex>
 
 #include "dv_internal.h"
+#include "../../include/dv_testing.h"
 
 namespace dv {
 
@@ -324,9 +325,13 @@ static dv_status check_ctx(dv_ctx* ctx) {
   return DV_OK;
 }
 
+static bool in_ipc_mapping(const void* p);
+
 // Is `p` memory of this context's GPU (its own HBM)? Then every reader of it -- SMs, copy
-// engines, stream memory operations, peers over NVLink -- is served by this GPU's L2.
+// engines, stream memory operations, peers over NVLink -- is served by this GPU's L2. Memory
+// mapped from another process (dv_ipc_open) never counts as local, whatever GPU it lives on.
 static bool local_vidmem(const dv_ctx* ctx, const void* p) {
+  if (in_ipc_mapping(p)) return false;
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -771,6 +776,17 @@ static_assert(sizeof(Blob) <= sizeof(dv_ipc_blob), "blob too large");
 static const uint32_t kBlobMagic = 0x44564950;  // "DVIP"
 static std::mutex g_ipc_mu;
 static std::map<uintptr_t, std::pair<void*, int>> g_ipc_open;  // mapped -> (base, refcount)
+static std::map<uintptr_t, std::pair<uint64_t, int>> g_ipc_ranges;  // base -> (end, refcount)
+
+static bool in_ipc_mapping(const void* p) {
+  const uintptr_t a = (uintptr_t)p;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  if (g_ipc_ranges.empty()) return false;
+  auto it = g_ipc_ranges.upper_bound(a);
+  if (it == g_ipc_ranges.begin()) return false;
+  --it;
+  return a < it->second.first;
+}
 
 }  // namespace dv
 
@@ -973,7 +989,16 @@ dv_status dv_ipc_open(const dv_ipc_blob* blob, void** out) {
   cudaError_t e = cudaIpcOpenMemHandle(&base, b.handle, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return fail(DV_EPEER, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
   void* mapped = (uint8_t*)base + b.offset;
+  unsigned long long rb = 0;
+  size_t rsize = 0;
+  const Driver* d;
+  DV_TRY(driver(&d));
+  if (d->memGetAddressRange(&rb, &rsize, (unsigned long long)(uintptr_t)base))
+    rsize = ~0ull - (uintptr_t)base;  // unknown extent: treat everything above as mapped
   std::lock_guard<std::mutex> lk(g_ipc_mu);
+  auto& rg = g_ipc_ranges[(uintptr_t)base];
+  rg.first = std::max<uint64_t>(rg.first, (uint64_t)(uintptr_t)base + rsize);
+  rg.second += 1;
   auto& ent = g_ipc_open[(uintptr_t)mapped];
   ent.first = base;
   ent.second += 1;
@@ -985,6 +1010,8 @@ dv_status dv_ipc_close(void* mapped) {
   std::lock_guard<std::mutex> lk(g_ipc_mu);
   auto it = g_ipc_open.find((uintptr_t)mapped);
   if (it == g_ipc_open.end()) return DV_OK;  // same-process mapping or already closed
+  auto rg = g_ipc_ranges.find((uintptr_t)it->second.first);
+  if (rg != g_ipc_ranges.end() && --rg->second.second == 0) g_ipc_ranges.erase(rg);
   if (--it->second.second == 0) {
     cudaError_t e = cudaIpcCloseMemHandle(it->second.first);
     g_ipc_open.erase(it);
@@ -1369,6 +1396,15 @@ dv_status dv_signal(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint6
   if (flag_slot < 0) return fail(DV_EINVAL, "negative flag slot");
   DV_ON_DEVICE(ctx->device);
   return stream_signal(ep, flag_slot, seq, (cudaStream_t)stream);
+}
+
+dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
+                            int32_t* gpu_scope) {
+  DV_TRY(check_ctx(ctx));
+  if (!flag || !gpu_scope) return fail(DV_EINVAL, "NULL flag or gpu_scope");
+  DV_ON_DEVICE(ctx->device);
+  *gpu_scope = local_vidmem(ctx, flag) && (!payload || local_vidmem(ctx, payload)) ? 1 : 0;
+  return DV_OK;
 }
 
 dv_status dv_query(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq,

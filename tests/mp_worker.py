@@ -100,6 +100,8 @@ def mode_ipc(rank, world, direct):
             ib = dv.dv_ipc_open(inf["inbox"])
             fp = dv.dv_ipc_open(inf["flags"])
             opened += [ib, fp]
+            # memory mapped from another process is never "this GPU's own HBM": system-scope release
+            assert not dv.dvt_release_scope(ctx, fp, ib) and not dv.dvt_release_scope(ctx, fp + 8, ib + 64)
             eps.append(dv.endpoint(dv.DV_EP_PEER, ib, inf["words"] * 2, fp, n_src, device=0))
             sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8, fp, n_src, device=0))
             if direct:
@@ -119,6 +121,7 @@ def mode_ipc(rank, world, direct):
     else:                                                   # token block: receive
         j, w = tb[rank - n_src]
         iep = dv.endpoint(dv.DV_EP_DEVICE, mine["inbox"], mine["words"] * 2, mine["flagp"], n_src, device=0)
+        assert dv.dvt_release_scope(ctx, mine["flagp"], mine["inbox"])   # own allocation: gpu scope
         if direct:
             # wait for every source block that routes to us, then the bytes are already in place
             for pc in dv.dv_route(ps, ts, reg, H, D, 2):

@@ -211,6 +211,25 @@ def test_flag_orders_consumer_after_producer():
         assert int(fl[2]) == 7
 
 
+def test_release_scope_follows_memory():
+    """A5 publish protocol: gpu-scope release only when the flag AND the payload are
+    this GPU's own HBM; pinned host on either side -> system scope. (Memory mapped from another
+    process is checked in tests/mp_worker.py.)"""
+    cx = ctx()
+    d = torch.zeros(64, dtype=torch.int64, device="cuda")
+    h = torch.zeros(64, dtype=torch.int64, pin_memory=True)
+    raw = dv.dv_device_alloc(0, 4096)
+    try:
+        assert dv.dvt_release_scope(cx, d.data_ptr(), d.data_ptr() + 64)
+        assert dv.dvt_release_scope(cx, raw, raw + 256)
+        assert dv.dvt_release_scope(cx, d.data_ptr())            # flag only (empty payload)
+        assert not dv.dvt_release_scope(cx, h.data_ptr(), d.data_ptr())
+        assert not dv.dvt_release_scope(cx, d.data_ptr(), h.data_ptr())
+        assert not dv.dvt_release_scope(cx, h.data_ptr(), h.data_ptr())
+    finally:
+        dv.dv_device_free(raw)
+
+
 def test_staged_publish_and_fetch_flush():
     L, B, H, S, D = 1, 1, 2, 8, 16
     cx = ctx()
@@ -513,15 +532,18 @@ def test_host_poller_never_sees_flag_before_payload(xfer):
                 last = cur
             if stop.is_set() and cur >= n:
                 break
-    th = threading.Thread(target=poll)
+    th = threading.Thread(target=poll, daemon=True)   # daemon: a failing test must not hang pytest
     th.start()
-    cx = ctx()
-    for i, r in enumerate(regs):
-        dv.dvt_spin(3000, 1)   # spread the chunks out so the poller samples many of them
-        dv.dv_scatter(cx, c, dv.region(*r), ep, i * chunk, flag_slot=0, seq=i + 1, xfer=xfer)
-    torch.cuda.synchronize()
-    stop.set()
-    th.join(timeout=60)
+    try:
+        cx = ctx()
+        for i, r in enumerate(regs):
+            dv.dvt_spin(3000, 1)   # spread the chunks out so the poller samples many of them
+            dv.dv_scatter(cx, c, dv.region(*r), ep, i * chunk, flag_slot=0, seq=i + 1, xfer=xfer)
+        torch.cuda.synchronize()
+    finally:
+        stop.set()
+        th.join(timeout=60)
+    assert not th.is_alive(), "poller never saw the last flag"
     assert not bad, f"flag seen before payload for chunks {bad[:10]}"
     assert len(seen) > 10 and seen[-1] == n
 
