@@ -491,7 +491,7 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     lep = dv.endpoint_of(log, fl)
     dlog = torch.empty(LAYER_BYTES // 2 * L, dtype=torch.int16, device="cuda")
     dfl = torch.zeros(1, dtype=torch.int64, device="cuda")
-    n = 400
+    n = 1040   # SURVEY §8(d) latency runs: 1000 token·layer samples after a 40-sample warm-up
     for name, epx in (("host", lep), ("hbm", dv.endpoint_of(dlog, dfl))):
         te = torch.zeros(n, dtype=torch.int64, device="cuda")
         ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
@@ -675,6 +675,20 @@ def cpu_baseline(seconds=10.0):
     out["all_cores"] = {"value": m * STEP_BYTES / dt2 / 1e9, "unit": "GB/s", "cores": cores,
                         "sample": f"{m} C2 token steps, the same oracle calls per layer slab on a "
                                   f"{cores}-thread pool, {dt2:.1f} s"}
+    # the host's own roofline: one 1 GiB numpy copy (single thread), and the CPU model
+    import numpy as np
+    a = np.ones(1 << 30, np.uint8)
+    b = np.empty_like(a)
+    np.copyto(b, a)
+    t0 = time.perf_counter()
+    np.copyto(b, a)
+    out["host_copy_1GiB_gbs"] = (1 << 30) / (time.perf_counter() - t0) / 1e9
+    del a, b
+    try:
+        out["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if "model name" in l)
+    except (OSError, StopIteration):
+        out["cpu_model"] = None
+    out["os_cpu_count"] = os.cpu_count()
     return out
 
 
