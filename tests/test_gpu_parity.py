@@ -497,19 +497,22 @@ def test_paper_baselines_produce_the_wire():
     assert calls == 2 * nL * nR + 1 and np.array_equal(to_np(out), exp)
 
 
-@pytest.mark.parametrize("xfer", [dv.DV_XFER_FUSED, dv.DV_XFER_FUSED | dv.DV_PUBLISH_STREAMOP, dv.DV_XFER_STAGED,
-                                  dv.DV_XFER_DECOUPLED])
-def test_host_poller_never_sees_flag_before_payload(xfer):
+@pytest.mark.parametrize("xfer,npos", [(dv.DV_XFER_FUSED, 1), (dv.DV_XFER_FUSED | dv.DV_PUBLISH_STREAMOP, 1),
+                                       (dv.DV_XFER_STAGED, 1), (dv.DV_XFER_DECOUPLED, 1),
+                                       (dv.DV_XFER_FUSED, 24)])
+def test_host_poller_never_sees_flag_before_payload(xfer, npos):
     """Release protocol (A5) observed from the CPU: a host thread spins on the pinned flag while
     the GPU streams 300 per-layer chunks; whenever it sees seq k it immediately compares chunk k
-    with the oracle. A flag visible before its payload would show up as a mismatch."""
+    with the oracle. A flag visible before its payload would show up as a mismatch. npos = 24:
+    768 KiB chunks written by 192 CTAs, so the one system-scope release of the last CTA must
+    cover every other CTA's PCIe stores (cumulativity, DESIGN.md §6 protocol 2)."""
     import threading
     L, B, H, S, D = 4, 8, 8, 64, 128
     K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=12)
     k, v, c = dev_cache(K, V, 0, 0)
     osrc = oc(K, V, 0, 0, S)
     n = 300
-    regs = [(i % L, i % L + 1, 0, B, i % S, i % S + 1) for i in range(n)]
+    regs = [(i % L, i % L + 1, 0, B, (i * npos) % (S - npos), (i * npos) % (S - npos) + npos) for i in range(n)]
     chunk = ok.region_bytes(*regs[0], H, D, 2)
     exp = [ok.pack(osrc, r) for r in regs]
     log = pinned_u16(n * chunk // 2)
