@@ -49,12 +49,14 @@ def rand_region(rng, lb, nl, rb, nr, hb, nh, S):
     return (l0, l1, r0, r1, s0, s1, h0, h1)
 
 
-@pytest.mark.parametrize("block", range(12))
+@pytest.mark.parametrize("block", range(18))
 def test_random_ops_against_oracle(block):
+    """Blocks 12..17 draw the less common head dims: 8 (one 16-byte packet), 40 / 80 (5 / 10
+    packets: odd register-transpose groups, PK 1 / 2), 96 (PK 4) and 256 (32 packets, PK 16 x 2)."""
     rng = random.Random(12345 + block)
     cx = dv.dv_create(0, staging_bytes=rng.choice([1 << 20, 8 << 20, 0]))
     for it in range(40):
-        D = rng.choice([16, 64, 128])
+        D = rng.choice([16, 64, 128] if block < 12 else [8, 40, 80, 96, 256])
         nl, nr, nh = rng.randint(1, 4), rng.randint(1, 3), rng.randint(1, 5)
         lb, rb, hb = rng.randint(0, 5), rng.randint(0, 5), rng.randint(0, 3)
         S = rng.randint(4, 48)

@@ -697,6 +697,34 @@ def test_ft6d_pack_unpack_remap(seed, layouts, xfer):
     assert np.array_equal(to_np(ek), eo.K) and np.array_equal(to_np(ev), eo.V)
 
 
+@pytest.mark.parametrize("D", [8, 40, 80, 96, 128, 256])
+@pytest.mark.parametrize("layouts", [(ok.LAYOUT_FT6D, ok.LAYOUT_KV5D), (ok.LAYOUT_KV5D, ok.LAYOUT_FT6D)])
+def test_ft6d_transpose_every_packet_group(D, layouts):
+    """The register packet transpose (taken for regions of >= 32 positions) at every packet-group
+    size PK the head dim allows: D = 8 (1 packet), 40 (5: PK 1), 80 (10: PK 2), 96 (12: PK 4),
+    128 (16: PK 16), 256 (32: two PK-16 groups); pack, unpack and remap == the oracle."""
+    H, nL, nR, S, hb = 3, 2, 2, 70, 1
+    reg = (0, nL, 0, nR, 3, 67, 0, 0)
+    K, V = kvgen.kv5d_cache("hash", 0, nL, 0, nR, H, S, D, seed=D, head_begin=hb)
+    k, v, c, o = _mk(K, V, 0, 0, layouts[0], hb=hb)
+    exp = ok.pack(o, reg)
+    buf = sentinel_like((exp.size,))
+    dv.dv_scatter(ctx(), c, dv.region(*reg), dv.endpoint_of(buf))
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(buf), exp)
+    Ks, Vs = kvgen.sentinel_cache(nL, nR, H, S + 3, D)
+    dk, dvv, dc, do = _mk(Ks, Vs, 0, 0, layouts[1], hb=hb)
+    dv.dv_gather(ctx(), dv.endpoint_of(buf), 0, dc, dv.region(*reg))
+    torch.cuda.synchronize()
+    ok.unpack(do, reg, exp)
+    assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
+    ek, ev, ec, eo = _mk(Ks, Vs, 0, 0, layouts[1], hb=hb)
+    dv.dv_remap(ctx(), c, ec, dv.region(*reg))
+    torch.cuda.synchronize()
+    ok.remap(o, eo, reg)
+    assert np.array_equal(to_np(ek), eo.K) and np.array_equal(to_np(ev), eo.V)
+
+
 @pytest.mark.parametrize("sh,th", [([0, 6], [0, 3, 6]), ([0, 2, 4, 6], [0, 3, 6]), ([0, 3, 6], [0, 1, 2, 3, 4, 5, 6])])
 @pytest.mark.parametrize("direct", [False, True])
 def test_tp_resplit_stream_out_in(sh, th, direct):
