@@ -198,9 +198,10 @@ def run_ours(args):
                       xfer=dv.DV_XFER_FUSED, stream=sp)
     torch.cuda.synchronize()
 
-    # two input streams, alternating by step: step t+1's H2D need not queue behind step t's
-    # unpack kernel (the copy engine stays busy); each step still orders its own gather -> scatter
-    s_ins = [torch.cuda.Stream(), torch.cuda.Stream()]
+    # input stream(s): with one, the input side (H2D + unpack) runs in lockstep with the output
+    # side; two alternating streams let H2Ds overlap each other (DV_E2E_INSTREAMS, measured in
+    # tools/probe_e2e_trace.py)
+    s_ins = [torch.cuda.Stream() for _ in range(int(os.environ.get("DV_E2E_INSTREAMS", "1")))]
     evs = [torch.cuda.Event() for _ in range(8)]
 
     def e2e_step(t):
@@ -208,7 +209,7 @@ def run_ours(args):
         # full duplex), then the stream-out of step t on the main stream once it has landed.
         q = pos_of(t)
         j = (t - 1) % RING
-        s_in = s_ins[t % 2]
+        s_in = s_ins[t % len(s_ins)]
         dv.dv_gather(ctx, dep, j * STEP_BYTES, cache, dv.region(0, L, 0, B, q, q + 1), stream=s_in)
         e = evs[t % 8]
         e.record(s_in)
@@ -294,8 +295,8 @@ def run_ours(args):
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": STEP_BYTES,
                 "d2h_bytes_per_step": STEP_BYTES,
                 "how": "per step: dv_gather of the token's K/V from pinned host into the device cache "
-                       "(H2D, side stream) then dv_scatter to the pinned-host log (D2H, main stream); "
-                       "step t's H2D overlaps step t-1's D2H"},
+                       "(H2D + unpack, input stream) then dv_scatter to the pinned-host log (pack + D2H, "
+                       "main stream); step t+1's H2D overlaps step t's D2H (PCIe full duplex)"},
         "gpu_launches": int(launches),
         "host_enqueue_us_per_step": {"value": host_us, "e2e": host_e2e_us},
         "roofline": roof,
