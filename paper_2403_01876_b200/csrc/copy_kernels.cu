@@ -257,6 +257,77 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 ? DV_MIN_BLOCKS : 1))
   if (p.flag) publish(p, p.pub, p.seq + (unsigned long long)k);
 }
 
+// Small released copies as ONE thread-block cluster (kClusterCtas CTAs): the CTAs meet at a
+// cluster barrier instead of a global ticket, so the publish needs no L2 atomic round trip.
+// Every thread orders its own stores at gpu scope (fence.acq_rel.gpu: its stores are performed
+// in L2), arrives at the cluster barrier with release and waits with acquire; cluster rank 0's
+// thread 0 then holds every CTA's stores in its causality past and releases the flag at the
+// scope the destination needs (st.release.gpu for this GPU's HBM, st.release.sys otherwise).
+constexpr int kClusterCtas = 8;
+template <int VEC, int U>
+__global__ void __launch_bounds__(1024) k_copy_cluster(const KParams p) {
+  if (p.ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.ts + 1, t);
+  }
+  pdl_enter();
+  if (p.ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(p.ts + 2, t);
+  }
+  int32_t k = 0;
+  if (p.dyn) {
+    k = *p.dyn;
+    if (k < 0 || k > p.dyn_max) return;  // uniform across the cluster
+  }
+  const uint8_t* src = p.src + (int64_t)k * p.dyn_ss;
+  uint8_t* dst = p.dst + (int64_t)k * p.dyn_ds;
+  const uint32_t T = blockDim.x * gridDim.x;
+  const uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x;
+  Vec<VEC> v[U];
+  uint8_t* d[U];
+#pragma unroll
+  for (int i = 0; i < U; ++i) {
+    const uint32_t g = g0 + i * T;
+    d[i] = nullptr;
+    if (g < p.n_vec) {
+      const uint8_t* sp;
+      locate<VEC>(p, src, dst, g, sp, d[i]);
+      ld_vec(v[i], sp);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+    if (d[i]) st_vec(d[i], v[i]);
+  if (p.ts) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p.ts + 3, t);
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (p.flag && rank == 0 && threadIdx.x == 0) {
+    const unsigned long long seq = p.seq + (unsigned long long)k;
+    if (p.pub == 3)
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
+    else
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag), "l"(seq) : "memory");
+    if (p.ts) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.ts[0] = t;
+    }
+  }
+}
+
 // Two plans in one launch (K and V with different structures, e.g. an FT6D key + a KV5D value
 // at a token step): vector g < a.n_vec belongs to plan a, the rest to plan b. Release fields
 // travel in `a`. One launch instead of two halves the fixed cost of small two-plan copies.
@@ -660,6 +731,8 @@ struct Tune {
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
   int trs = 0;  // DV_TRS: packet transpose form (0 registers PK<=pk; 1 shared-memory tiles; 2 PK=1; 3 PK<=2)
   int pk = 16;  // DV_PK: largest packets per register-transpose item (1, 2, 4, 8, 16)
+  int cluster = 1;  // DV_CLUSTER: small released copies as one cluster (0 off; 1 gpu-scope releases of
+                    // <= 8192 vectors; 2 whenever it fits -- see launch_copy)
 };
 static const Tune& tune() {
   static Tune t = [] {
@@ -676,6 +749,7 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_SMALL")) x.small = strtoull(e, nullptr, 10);
     if (const char* e = getenv("DV_TRS")) x.trs = atoi(e);
     if (const char* e = getenv("DV_PK")) x.pk = atoi(e);
+    if (const char* e = getenv("DV_CLUSTER")) x.cluster = atoi(e);
     return x;
   }();
   return t;
@@ -703,6 +777,49 @@ static cudaError_t launch_vec(const KParams& kp, int u, int max_ctas, cudaStream
       if (tune().stm == 2) return go<VEC, 4, 256, 2>(kp, blocks, st);
       return go<VEC, 4, 256>(kp, blocks, st);
   }
+}
+
+// Cluster form of a small released copy (DV_CLUSTER=1): one cluster of kClusterCtas CTAs, up to
+// 1024 threads each, U <= 4 vectors per thread. Returns cudaErrorNotSupported when it does not fit.
+template <int VEC, int U>
+static cudaError_t go_cluster(const KParams& kp, int threads, cudaStream_t st) {
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCtas);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kClusterCtas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_copy_cluster<VEC, U>, kp);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+static bool cluster_fits(uint64_t n_vec) { return n_vec <= (uint64_t)kClusterCtas * 1024 * 4; }
+// Measured (tools/probe_latency.py, C2 layer 160 KiB = 5,120 vectors): into HBM (gpu-scope
+// release) writer end -> flag 3.55 -> 3.20 us; to pinned host (system scope) 6.02 -> 6.18 us (8 SMs
+// issue the PCIe stores more slowly); a 576 KiB peer put gets slower (ping-pong RTT 11.3 -> 12.5 us).
+// So by default only gpu-scope releases of <= one vector per thread of the cluster use it.
+static bool use_cluster(const KParams& kp) {
+  const int c = tune().cluster;
+  if (c == 2) return cluster_fits(kp.n_vec);
+  return c == 1 && kp.pub == 3 && kp.n_vec <= (uint64_t)kClusterCtas * 1024;
+}
+static cudaError_t launch_cluster(const KParams& kp, int vec, cudaStream_t st) {
+  const uint64_t per_cta = (kp.n_vec + kClusterCtas - 1) / kClusterCtas;
+  const int u = per_cta <= 1024 ? 1 : per_cta <= 2048 ? 2 : 4;
+  const int threads = (int)std::min<uint64_t>(1024, ((per_cta + u - 1) / u + 31) / 32 * 32);
+  if (vec == 32)
+    return u == 1 ? go_cluster<32, 1>(kp, threads, st) : u == 2 ? go_cluster<32, 2>(kp, threads, st)
+                                                         : go_cluster<32, 4>(kp, threads, st);
+  return u == 1 ? go_cluster<16, 1>(kp, threads, st) : u == 2 ? go_cluster<16, 2>(kp, threads, st)
+                                                       : go_cluster<16, 4>(kp, threads, st);
 }
 
 // Small copies (per-token updates): one vector per thread, 128-thread CTAs, as many CTAs as
@@ -1074,6 +1191,8 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.pub = pub_of(rel);
     cudaError_t e = (tune().bulk && dense_dst(p) && !p.dyn)
                         ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
+                    : (kp.flag && q0 == 0 && last && use_cluster(kp))
+                        ? launch_cluster(kp, VEC, stream)
                         : launch_cfg(kp, VEC, max_ctas, stream);
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");
   }
