@@ -406,8 +406,8 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
 // profiles/r01_tune_host*.jsonl): writes to pinned host go through the kernel's own PCIe stores up
 // to 32 MB (same throughput as pack+DMA for a 6.55 MB token step, lower latency, no staging) and
 // through pipelined pack + copy-engine DMA above (54.8 vs 52.6 GB/s for a 163.8 MB prompt layer,
-// and no SMs held during the transfer); reads from pinned host always go through the copy engine
-// (SM zero-copy reads do not overlap with concurrent D2H traffic).
+// and no SMs held during the transfer); reads from pinned host below 4 MiB are SM zero-copy loads,
+// larger ones go through the copy engine (see below).
 static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes, bool reading) {
   uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   // decoupled host writes: pack + DMA on the context's DMA stream overlaps consecutive steps
@@ -417,7 +417,12 @@ static uint32_t pick_xfer(uint32_t xfer, const dv_endpoint* ep, uint64_t bytes, 
     if (m == DV_XFER_STAGED && ep->kind == DV_EP_DEVICE) return DV_XFER_FUSED;  // already local
     return m;
   }
-  if (ep->kind == DV_EP_HOST && (reading || bytes >= (32ull << 20))) return DV_XFER_STAGED;
+  // reads: SM zero-copy loads win alone at every size (160 KiB 6.8 vs 12.3 us, 1.3 MB 28.6 vs
+  // 39.3 us, 6.55 MB 130.6 vs 132.7 us -- tools/probe_small_reads.py) but do not overlap with a
+  // concurrent D2H stream (e2e 25 vs 39.8 GB/s at 6.55 MB), so the copy engine takes reads from
+  // 4 MiB up, where a read is a bulk transfer rather than a latency-bound one
+  if (ep->kind == DV_EP_HOST && reading) return bytes < (4ull << 20) ? DV_XFER_FUSED : DV_XFER_STAGED;
+  if (ep->kind == DV_EP_HOST && bytes >= (32ull << 20)) return DV_XFER_STAGED;
   return DV_XFER_FUSED;
 }
 
