@@ -96,3 +96,24 @@ def test_bench_peer_workloads(workload, world):
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == world and d["value"] > 0 and d["parity_spot_check"]["mismatches"] == 0
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_bench_reference_arm_cpu(world):
+    """bench.py --impl reference (the CPU oracle arm) on CPU: at N = 1 directly, at N = 2 under
+    torchrun -- rank 0 alone runs and prints ONE JSON line, the other rank exits 0 without work."""
+    import json
+    root = os.path.dirname(HERE)
+    args = ["--impl", "reference", "--steps", "3", "--warmup", "3", "--gpus", str(world)]
+    if world == 1:
+        cmd = [sys.executable, os.path.join(root, "bench.py")] + args
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py")] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == world and d["steps"] == 3 and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
