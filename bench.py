@@ -728,7 +728,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--peer-baseline", default="none", choices=["none", "nccl"],
-                    help="c5 only: run the NCCL send/recv baseline instead of dvstream's peer stores")
+                    help="c3/c5: run the NCCL send/recv baseline (pack -> ncclSend/ncclRecv -> unpack) instead of dvstream's peer stores")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
                     help="c2 (default, BASELINE configs[1]): token steps -> pinned host; "
                          "c3: prompt->token disaggregation over NVLink; c5: ring replication over NVLink")

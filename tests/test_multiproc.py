@@ -117,3 +117,24 @@ def test_bench_reference_arm_cpu(world):
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == world and d["steps"] == 3 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["c3", "c5"])
+def test_bench_sendrecv_baseline_two_ranks(workload):
+    """The send/recv baseline of the peer workloads (pack -> send/recv -> unpack; NCCL on a
+    multi-GPU box, gloo + host staging here with both ranks on the one GPU): runs, and the
+    delivered KV passes the sampled parity check."""
+    import json
+    root = os.path.dirname(HERE)
+    env = dict(os.environ, DV_BENCH_SAME_DEVICE="1", DV_C3_PROMPT="16")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--workload", workload, "--peer-baseline", "nccl", "--steps", "2", "--warmup", "3",
+           "--dist-backend", "gloo", "--gpus", "2"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"].startswith("sendrecv-baseline") and d["parity_spot_check"]["mismatches"] == 0

@@ -52,6 +52,37 @@ def _max(x, world, dev, backend):
     return float(t.item())
 
 
+def _sendrecv(args, sbuf, dst, rbuf, src):
+    """The baseline's exchange: NCCL grouped send/recv of device buffers; with the gloo backend
+    (multi-process tests on one GPU) the same exchange staged through host copies."""
+    if args.dist_backend == "nccl":
+        ops = []
+        if sbuf is not None:
+            ops.append(dist.P2POp(dist.isend, sbuf, dst))
+        if rbuf is not None:
+            ops.append(dist.P2POp(dist.irecv, rbuf, src))
+        for r_ in dist.batch_isend_irecv(ops):
+            r_.wait()
+        return
+    torch.cuda.synchronize()
+    reqs, rh = [], None
+    if sbuf is not None:
+        reqs.append(dist.isend(sbuf.cpu(), dst))
+    if rbuf is not None:
+        rh = torch.empty(rbuf.shape, dtype=rbuf.dtype)
+        reqs.append(dist.irecv(rh, src))
+    for r_ in reqs:
+        r_.wait()
+    if rbuf is not None:
+        rbuf.copy_(rh)
+
+
+def _impl(args, baseline):
+    if not baseline:
+        return "dvstream"
+    return "nccl-baseline" if args.dist_backend == "nccl" else "sendrecv-baseline (gloo, host-staged; tests only)"
+
+
 def run_c5(args, bench):
     world, rank, local = _env()
     torch.cuda.set_device(local)
@@ -93,7 +124,7 @@ def run_c5(args, bench):
         # BASELINE (north_star: "NCCL send/recv kept only as the baseline"): pack the step into a
         # device buffer, ncclSend it to the successor / ncclRecv the predecessor's, unpack it into
         # the replica store. Needs >= 2 GPUs and the nccl backend.
-        assert world > 1 and args.dist_backend == "nccl", "--peer-baseline nccl needs >= 2 GPUs"
+        assert world > 1, "--peer-baseline nccl needs >= 2 ranks"
         sbuf = torch.empty(step_bytes // 2, dtype=torch.int16, device=dev)
         rbuf = torch.empty_like(sbuf)
         rep_local = dv.cache(rep_k, rep_v, pred * Ls, 0)
@@ -105,9 +136,7 @@ def run_c5(args, bench):
                                     [rep_at_succ], [sig], seq=t, stream=sp)
             return
         dv.dv_scatter(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), dv.endpoint_of(sbuf), 0, stream=sp)
-        ops = [dist.P2POp(dist.isend, sbuf, succ), dist.P2POp(dist.irecv, rbuf, pred)]
-        for r_ in dist.batch_isend_irecv(ops):
-            r_.wait()
+        _sendrecv(args, sbuf, succ, rbuf, pred)
         dv.dv_gather(ctx, dv.endpoint_of(rbuf), 0, rep_local, dv.region(pred * Ls, pred * Ls + Ls, 0, b, q, q + 1),
                      stream=sp)
     # prompt replica first (bulk, Q13), then token steps
@@ -144,7 +173,7 @@ def run_c5(args, bench):
     if rank == 0:
         print(json.dumps({
             "metric": "KV stream GB/s (ring replication, token step per stage)", "value": value, "unit": "GB/s",
-            "impl": "nccl-baseline" if nccl else "dvstream",
+            "impl": _impl(args, nccl),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
             "data": "synthetic (splitmix64 coordinate-hash fill)",
@@ -217,7 +246,8 @@ def run_c3(args, bench):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group(args.dist_backend, **({"device_id": dev} if args.dist_backend == "nccl" else {}))
-    b, p, Sp, St = 8, 1000, 1024, 2048
+    b, Sp, St = 8, 1024, 2048
+    p = int(os.environ.get("DV_C3_PROMPT", "1000"))   # test hook: shorter prompts (C3 is p = 1000)
     n_p = max(1, world // 2)
     n_t = max(1, world - n_p) if world > 1 else 1
     pb = [round(64 * k / n_p) for k in range(n_p + 1)]
@@ -259,9 +289,36 @@ def run_c3(args, bench):
     st = torch.cuda.current_stream()
     sp = st.cuda_stream
     seq = [0]
+    nccl = getattr(args, "peer_baseline", "none") == "nccl"
+    if nccl:
+        # BASELINE: each prompt layer packed into a device buffer, sent with NCCL
+        # to the token rank that holds the layer, received and unpacked there.
+        assert world > 1, "--peer-baseline nccl needs >= 2 ranks"
+        lbytes = 2 * b * H * p * D * 2
+        xbuf = torch.empty(lbytes // 2, dtype=torch.int16, device=dev)
+        if is_token:
+            j = mine["j"]
+            mine["tc"] = dv.cache(mine["tk"], mine["tv"], tb[j], 0)
+
+    def owner(bounds, layer):
+        return max(x for x in range(len(bounds) - 1) if bounds[x] <= layer)
 
     def handoff():
         seq[0] += 1
+        if nccl:
+            if is_prompt:
+                i = mine["i"]
+                for layer in range(pb[i], pb[i + 1]):
+                    dv.dv_scatter(ctx, mine["pc"], dv.region(layer, layer + 1, 0, b, 0, p), dv.endpoint_of(xbuf), 0,
+                                  stream=sp)
+                    _sendrecv(args, xbuf, n_p + owner(tb, layer), None, None)
+            else:
+                j = mine["j"]
+                for layer in range(tb[j], tb[j + 1]):
+                    _sendrecv(args, None, None, xbuf, owner(pb, layer))
+                    dv.dv_gather(ctx, dv.endpoint_of(xbuf), 0, mine["tc"], dv.region(layer, layer + 1, 0, b, 0, p),
+                                 stream=sp)
+            return
         if is_prompt:
             i = mine["i"]
             for layer in range(pb[i], pb[i + 1]):      # layer by layer (Opt 2)
@@ -298,7 +355,7 @@ def run_c3(args, bench):
                                    f"S 1024 -> 2048, layer by layer, direct remap",
                        "bytes_per_step": total, "parallelism": f"pp{n_p} -> pp{n_t}",
                        "transport": "CUDA IPC peer stores" if world > 1 else "loopback (same GPU, HBM)"},
-            "parity_spot_check": {"mismatches": bad},
+            "parity_spot_check": {"mismatches": bad}, "impl": _impl(args, nccl),
             "ideal_ms_per_step_at_770GBps_per_prompt_gpu": total / n_p / 770e6}), flush=True)
     for x in mine.get("opened", []):
         dv.dv_ipc_close(x)
