@@ -7,7 +7,9 @@ Launch order (each preceded by one warm-up call that ncu also sees):
   1. C2 token step (6.55 MB, 25,600 runs of 256 B) packed into an HBM wire buffer
   2. C2 prompt layer (163.8 MB, 640 runs of 256 KB) packed into an HBM wire buffer
   3. C3 prompt layer remap, S 1024 -> 2048 (294.9 MB)
-  4. FT6D prompt layer pack: K via k_packet_transpose, V via k_run_copy
+  4. FT6D prompt layer pack: K transpose + V run copy in one k_transpose_run launch
+  5. one C2 token-layer (160 KiB) into HBM with a seq flag: k_copy_cluster (gpu-scope release)
+  6. the same to pinned host with a seq flag: k_run_copy + system-scope release (PCIe stores)
 """
 import os
 import sys
@@ -47,6 +49,20 @@ def main():
     v6 = torch.empty((2, B, H, S, D), dtype=torch.int16, device="cuda")
     for _ in range(2):
         dv.dv_scatter(ctx, dv.cache(k6, v6), dv.region(0, 1, 0, B, 0, P), ep, 0)
+    torch.cuda.synchronize()
+    del k6, v6
+    k5 = torch.empty((2, B, H, S, D), dtype=torch.int16, device="cuda")
+    v5 = torch.empty_like(k5)
+    c6 = dv.cache(k5, v5)
+    dfl = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for i in range(2):
+        dv.dv_scatter(ctx, c6, dv.region(1, 2, 0, B, P, P + 1), dv.endpoint_of(wire, dfl), 0, flag_slot=0,
+                      seq=1 + i)
+    host = torch.empty(2 * B * H * D, dtype=torch.int16, pin_memory=True)
+    hfl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    for i in range(2):
+        dv.dv_scatter(ctx, c6, dv.region(1, 2, 0, B, P, P + 1), dv.endpoint_of(host, hfl), 0, flag_slot=0,
+                      seq=1 + i)
     torch.cuda.synchronize()
     ctx.close()
 
