@@ -160,6 +160,27 @@ def run_c5(args, bench):
     torch.cuda.synchronize()
     l1, _ = dv.dv_stats()
     ms = _max(a.elapsed_time(e), world, dev, args.dist_backend)
+    host_us = None
+    dev_us = None
+    if not nccl:
+        # the same steps queued behind a spin head start: device time per step without the host's
+        # enqueue rate (the timed region above includes it: one dv_stream_out_direct per step)
+        import time as _t
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dv.dvt_spin(max(2_000_000, args.steps * 40_000), 1, stream=sp)
+        a2.record(st)
+        h0 = _t.perf_counter()
+        for _ in range(args.steps):
+            t += 1
+            step(t)
+        host_us = (_t.perf_counter() - h0) / args.steps * 1e6
+        e2.record(st)
+        torch.cuda.synchronize()
+        dev_us = _max(a2.elapsed_time(e2) * 1e3 / args.steps, world, dev, args.dist_backend)
+    graph = None if nccl else _graph_steps(ctx, own, rep_at_succ, sig, lb, Ls, b, p, S, world, dev, args, st)
     pingpong = None if nccl else _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, blobs[pred]["a"],
                                            lb, Ls, b, p, S, P, world, dev, args, st)
     # the predecessor's last step landed in our replica store: sampled parity vs kvgen
@@ -182,12 +203,52 @@ def run_c5(args, bench):
                        "bytes_per_step_per_stage": step_bytes, "parallelism": f"pp{P} ring",
                        "transport": "CUDA IPC peer stores" if world > 1 else "loopback (same GPU)"},
             "gpu_launches": int(l1 - l0), "parity_spot_check": {"mismatches": bad}, "pingpong": pingpong,
+            "device_us_per_step": dev_us, "host_enqueue_us_per_step": host_us, "graph": graph,
             "ideal_us_per_step_at_770GBps": step_bytes / 770e3}), flush=True)
     for x in (kp, vp, fp):
         dv.dv_ipc_close(x)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _graph_steps(ctx, own, rep_at_succ, sig, lb, Ls, b, p, S, world, dev, args, st):
+    """The token step as a CUDA graph (captured once: a device step counter bump + dv_remap_dyn of
+    this stage's new position into the successor's replica store with its seq flag), replayed
+    per token: device time and host cost per step."""
+    d_step = torch.full((1,), -1, dtype=torch.int32, device=dev)
+    g = torch.cuda.CUDAGraph()
+    gs = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(gs):
+        with torch.cuda.graph(g, stream=gs):
+            d_step.add_(1)
+            dv.dv_remap_dyn(ctx, own, rep_at_succ, dv.region(lb, lb + Ls, 0, b, p, p + 1), d_step.data_ptr(),
+                            S - p - 1, signal=sig, flag_slot=0, seq=2 * 10 ** 7, stream=gs.cuda_stream)
+    torch.cuda.synchronize()
+    reps = min(args.steps, S - p - 10)
+    import time as _t
+    with torch.cuda.stream(gs):
+        d_step.fill_(-1)
+        for _ in range(5):
+            g.replay()
+        d_step.fill_(-1)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dv.dvt_spin(max(2_000_000, reps * 20_000), 1, stream=gs.cuda_stream)
+        a.record(gs)
+        h0 = _t.perf_counter()
+        for _ in range(reps):
+            g.replay()
+        host_us = (_t.perf_counter() - h0) / reps * 1e6
+        e.record(gs)
+        torch.cuda.synchronize()
+    dev_us = _max(a.elapsed_time(e) * 1e3 / reps, world, dev, args.dist_backend)
+    return {"device_us_per_step": dev_us, "host_us_per_step": host_us, "steps": reps,
+            "gbs_per_stage": 2 * Ls * b * H * D * 2 / dev_us / 1e3,
+            "how": "one captured graph per token step (step-counter bump + dv_remap_dyn), replayed"}
 
 
 def _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, pred_ack_blob, lb, Ls, b, p, S, P, world, dev,
