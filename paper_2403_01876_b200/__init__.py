@@ -160,8 +160,14 @@ def exported_symbols():
     return list(_SIGS)
 
 
+_fns = {}
+
+
 def _call(name, *args):
-    st = getattr(lib(), name)(*args)
+    f = _fns.get(name)
+    if f is None:
+        f = _fns[name] = getattr(lib(), name)
+    st = f(*args)
     if st != DV_OK:
         raise DVError(st, name, lib().dv_last_error().decode())
     return st
@@ -262,6 +268,8 @@ def endpoint_of(buf, flags=None, kind=None) -> dv_endpoint:
 
 
 def endpoint_array(eps):
+    if isinstance(eps, C.Array):   # prebuilt (e.g. reused every token step)
+        return eps
     arr = (dv_endpoint * max(1, len(eps)))()
     for i, e in enumerate(eps):
         if e is not None:
@@ -270,6 +278,8 @@ def endpoint_array(eps):
 
 
 def cache_array(cs):
+    if isinstance(cs, C.Array):
+        return cs
     arr = (dv_cache * max(1, len(cs)))()
     for i, c in enumerate(cs):
         if c is not None:

@@ -129,11 +129,13 @@ def run_c5(args, bench):
         rbuf = torch.empty_like(sbuf)
         rep_local = dv.cache(rep_k, rep_v, pred * Ls, 0)
 
+    dst_arr, sig_arr = dv.cache_array([rep_at_succ]), dv.endpoint_array([sig])   # reused every step
+
     def step(t):
         q = p + (t - 1) % (S - p)
         if not nccl:
             dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
-                                    [rep_at_succ], [sig], seq=t, stream=sp)
+                                    dst_arr, sig_arr, seq=t, stream=sp)
             return
         dv.dv_scatter(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), dv.endpoint_of(sbuf), 0, stream=sp)
         _sendrecv(args, sbuf, succ, rbuf, pred)
