@@ -497,6 +497,24 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
         te = torch.zeros(n, dtype=torch.int64, device="cuda")
         ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
         ts[:, 1:3] = 2 ** 63 - 1
+        tw = torch.zeros(n, dtype=torch.int64, device="cuda")
+        # an independent observer: one GPU thread on its own stream polls the flag (system-scope
+        # acquire loads; over PCIe for the host flag) and stamps when each seq becomes visible.
+        # Every kernel of the loop runs once first: with CUDA lazy loading, loading a kernel while
+        # the watcher spins would wait for the watcher.
+        wst = torch.cuda.Stream()
+        for j in range(2):
+            reg = dv.region(j, j + 1, 0, B, P, P + 1)
+            dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp, t_end_ptr=te[0].data_ptr())
+            dv.dvt_trace(ctx, ts[0].data_ptr())
+            dv.dv_scatter(ctx, cache, reg, epx, j * LAYER_BYTES, flag_slot=0, seq=10 ** 7 + j,
+                          xfer=dv.DV_XFER_FUSED, stream=sp)
+            dv.dvt_trace(ctx, 0)
+        dv.dvt_watch(epx.flags, 0, 1, tw.data_ptr(), 1000, stream=wst.cuda_stream)
+        torch.cuda.synchronize()
+        ts[0] = 0
+        ts[0, 1:3] = 2 ** 63 - 1
+        dv.dvt_watch(epx.flags, 10 ** 8, n, tw.data_ptr(), 5_000_000_000, stream=wst.cuda_stream)
         # head start: the GPU must run behind the host (as it does in serving), so the stream-out
         # launch is queued before its producer finishes and PDL can take effect
         dv.dvt_spin(20_000_000, 1, stream=sp)
@@ -511,8 +529,12 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
         dv.dvt_trace(ctx, 0)
         torch.cuda.synchronize()
         d = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
+        w = sorted(((tw - te).double() / 1e3).tolist()[L:])
         lat[name] = {"p50_us": d[len(d) // 2], "p99_us": d[int(len(d) * 0.99)], "min_us": d[0], "n": len(d),
-                     "how": "writer-end -> flag-published, %globaltimer"}
+                     "how": "writer-end -> flag-published, %globaltimer",
+                     "observed": {"p50_us": w[len(w) // 2], "p99_us": w[int(len(w) * 0.99)],
+                                  "how": "writer-end -> a polling GPU thread reads the seq (dvt_watch; "
+                                         "for the host flag each poll is a PCIe read)"}}
     # the same with a CUDA event between writer and stream-out (breaks PDL, adds the launch gap)
     samples = []
     for i in range(n):

@@ -51,6 +51,14 @@ DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
 DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
                                    int32_t* gpu_scope);
 
+/* Flag watcher: one GPU thread polls `flag` (device memory, or pinned host memory through its
+ * device-mapped address) with system-scope acquire loads and writes %globaltimer to ts[i] (device
+ * memory) the first time it reads >= seq0 + i, i = 0..n-1; gives up after timeout_ns. Launch it on
+ * its own stream, concurrent with the producer. Latency measurement: "flag visible to an
+ * independent observer". */
+DV_API dv_status dvt_watch(const uint64_t* flag, uint64_t seq0, int32_t n, uint64_t* ts,
+                           uint64_t timeout_ns, void* stream);
+
 /* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */
 DV_API dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream);
 

@@ -117,6 +117,26 @@ __global__ void k_spin(uint64_t ns) {
   } while (t - t0 < ns);
 }
 
+// One thread watches a 64-bit seq flag (device or mapped pinned host memory) with system-scope
+// acquire loads and stamps %globaltimer the first time it reads >= seq0 + i, for i = 0..n-1:
+// "the flag became visible to an independent observer" (for a host flag every poll is a PCIe
+// read, so a stamp includes up to one read round trip). Gives up after timeout_ns.
+__global__ void k_watch(const unsigned long long* flag, unsigned long long seq0, int32_t n,
+                        unsigned long long* ts, unsigned long long timeout_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int32_t i = 0; i < n; ++i) {
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (v >= seq0 + (unsigned long long)i) break;
+      if (t - t0 > timeout_ns) return;
+    }
+    ts[i] = t;
+  }
+}
+
 }  // namespace dv
 
 using namespace dv;
@@ -202,6 +222,16 @@ extern "C" dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kin
 extern "C" dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts) {
   if (!ctx) return fail(DV_EINVAL, "NULL context");
   ctx->trace_ts = (unsigned long long*)ts;
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_watch(const uint64_t* flag, uint64_t seq0, int32_t n, uint64_t* ts,
+                               uint64_t timeout_ns, void* stream) {
+  if (!flag || !ts || n < 0) return fail(DV_EINVAL, "bad dvt_watch arguments");
+  (void)cudaGetLastError();
+  k_watch<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)flag, seq0, n,
+                                             (unsigned long long*)ts, timeout_ns);
+  DV_CUDA(cudaGetLastError());
   return DV_OK;
 }
 

@@ -1035,3 +1035,24 @@ def test_library_host_arena_stream_out_and_back(near):
     finally:
         torch.cuda.synchronize()
         dv.dv_host_free(p)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_flag_watcher_sees_each_seq_in_order(pinned):
+    """dvt_watch (the latency observer of bench.py): a GPU thread on its own stream stamps the
+    first time it reads each seq of a flag (device or pinned host) written by stream signals."""
+    cx = ctx()
+    fl = flags(1, pinned=pinned)
+    ep = dv.endpoint_of(pinned_u16(16) if pinned else torch.empty(16, dtype=torch.int16, device="cuda"), fl)
+    tw = torch.zeros(3, dtype=torch.int64, device="cuda")
+    main, ws = torch.cuda.current_stream(), torch.cuda.Stream()
+    dv.dvt_spin(1000, 1, stream=main)                  # every kernel loaded before the watcher spins
+    dv.dvt_watch(ep.flags, 0, 1, tw.data_ptr(), 1000, stream=ws)
+    torch.cuda.synchronize()
+    dv.dvt_watch(ep.flags, 1, 3, tw.data_ptr(), 2_000_000_000, stream=ws)
+    for i in range(3):
+        dv.dvt_spin(50_000, 1, stream=main)
+        dv.dv_signal(cx, ep, 0, i + 1, stream=main)
+    torch.cuda.synchronize()
+    t = tw.tolist()
+    assert all(x > 0 for x in t) and t[0] < t[1] < t[2] and t[2] - t[0] >= 80_000
