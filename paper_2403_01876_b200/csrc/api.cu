@@ -819,6 +819,7 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   c->max_ctas = (cfg && cfg->max_ctas > 0) ? cfg->max_ctas : c->sm_count * 8;
   c->host_ctas = std::min(c->max_ctas, (cfg && cfg->host_ctas > 0) ? cfg->host_ctas : 16);
+  if (!getenv("DV_NO_PRELOAD")) preload_kernels();  // before a spinning consumer can wait on a flag
   uint64_t stg = (cfg && cfg->staging_bytes) ? cfg->staging_bytes : (256ull << 20);
   dv_status s = c->staging.init(device, stg);
   if (s != DV_OK) {

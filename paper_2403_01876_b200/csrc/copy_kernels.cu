@@ -1086,6 +1086,45 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   return DV_OK;
 }
 
+// Load every kernel of the library on the current device now (cudaFuncGetAttributes needs the
+// loaded function). Under CUDA lazy loading a kernel is otherwise loaded at its first launch, and
+// that load waits for the device: a consumer kernel already spinning on one of our flags would
+// then block the very stream-out it waits for (observed with the dvt_watch latency observer).
+template <typename F>
+static void load_fn(F f) {
+  cudaFuncAttributes a;
+  (void)cudaFuncGetAttributes(&a, f);
+}
+template <int VEC>
+static void load_vec() {
+  load_fn(k_run_copy<VEC, 1, 128>);
+  load_fn(k_run_copy<VEC, 2, 256>);
+  load_fn(k_run_copy<VEC, 4, 256>);
+  load_fn(k_run_copy<VEC, 8, 256>);
+  load_fn(k_run_copy<VEC, 4, 256, 1>);
+  load_fn(k_run_copy<VEC, 4, 256, 2>);
+  load_fn(k_run_copy2<VEC, 1, 128>);
+  load_fn(k_run_copy2<VEC, 4, 256>);
+  load_fn(k_pack_bulk<VEC, 4, 256>);
+  load_fn(k_copy_cluster<VEC, 1>);
+  load_fn(k_copy_cluster<VEC, 2>);
+  load_fn(k_copy_cluster<VEC, 4>);
+  for (int pk : {0, 1, 2, 4, 8, 16}) {
+    load_fn(tr_fn<0, VEC>(pk));
+    load_fn(tr_fn<1, VEC>(pk));
+  }
+}
+void preload_kernels() {
+  load_fn(k_run_copy<16, 1, 32>);
+  load_vec<16>();
+  load_vec<32>();
+  for (int pk : {0, 1, 2, 4, 8, 16}) {
+    load_fn(pt_fn<0>(pk));
+    load_fn(pt_fn<1>(pk));
+  }
+  (void)cudaGetLastError();
+}
+
 dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel, int max_ctas,
                        cudaStream_t stream) {
   if ((a.kind == kTranspose) != (b.kind == kTranspose) && a.dyn == b.dyn) {

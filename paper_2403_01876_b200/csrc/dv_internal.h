@@ -91,6 +91,8 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
 // release goes with the (last) launch.
 dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel, int max_ctas,
                        cudaStream_t stream);
+// Load every library kernel on the current device (no lazy loading at first launch).
+void preload_kernels();
 
 // ---- CUDA driver entry points (resolved through the runtime; no -lcuda) --------------------
 struct Driver {

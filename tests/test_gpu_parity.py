@@ -3,6 +3,7 @@
 Inputs come from kvgen only (numpy on the host side; the device fill kernel is itself pinned to
 kvgen here). Expected values come from oracle/ only.
 """
+import os
 import random
 
 import numpy as np
@@ -1056,3 +1057,32 @@ def test_flag_watcher_sees_each_seq_in_order(pinned):
     torch.cuda.synchronize()
     t = tw.tolist()
     assert all(x > 0 for x in t) and t[0] < t[1] < t[2] and t[2] - t[0] >= 80_000
+
+
+def test_spinning_consumer_does_not_block_first_stream_out():
+    """dv_create loads every library kernel: a consumer kernel that is already spinning on a flag
+    (here the dvt_watch observer) cannot deadlock against the lazy loading of the stream-out
+    kernel's first launch. Fresh process, so no earlier test has loaded anything."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, time, torch
+sys.path.insert(0, %r)
+import paper_2403_01876_b200 as dv
+ctx = dv.dv_create(0)
+k = torch.zeros((2, 2, 4, 16, 64), dtype=torch.int16, device="cuda"); v = torch.zeros_like(k)
+buf = torch.empty(2 * 2 * 2 * 4 * 64, dtype=torch.int16, device="cuda")
+fl = torch.zeros(1, dtype=torch.int64, device="cuda")
+tw = torch.zeros(1, dtype=torch.int64, device="cuda")
+ws = torch.cuda.Stream()
+torch.cuda.synchronize()
+dv.dvt_watch(fl.data_ptr(), 1, 1, tw.data_ptr(), 3_000_000_000, stream=ws)
+t0 = time.time()
+dv.dv_scatter(ctx, dv.cache(k, v), dv.region(0, 2, 0, 2, 5, 6), dv.endpoint_of(buf, fl), 0, flag_slot=0, seq=1)
+torch.cuda.synchronize()
+dt = time.time() - t0
+assert int(tw[0]) > 0 and dt < 1.5, (int(tw[0]), dt)
+print("ok", dt)
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
