@@ -56,7 +56,8 @@ class Clocks:
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu,"
+         "clocks.mem")
 
     def __init__(self, index):
         self.index = index
@@ -75,15 +76,17 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
-        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 9]
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 10]
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         busy = [float(r[1]) for r in rows if r[9].strip().isdigit() and int(r[9]) > 0
                 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        mem = [float(r[10]) for r in rows if r[10].strip().replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(busy or sm) if (busy or sm) else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "mem_mhz": statistics.median(mem) if mem else None,
                 "samples": len(rows), "samples_busy": len(busy)}
 
 
