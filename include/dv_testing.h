@@ -59,6 +59,12 @@ DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* pa
 DV_API dv_status dvt_watch(const uint64_t* flag, uint64_t seq0, int32_t n, uint64_t* ts,
                            uint64_t timeout_ns, void* stream);
 
+/* In-kernel consumer (include/dv_device.cuh): 4 CTAs; thread 0 of each waits with dv_flag_wait
+ * until *flag >= seq, then the CTAs copy `bytes` (multiple of 16) from src to dst (device
+ * memory). *ok (device int32, preset to 1 by the caller) becomes 0 if the wait timed out. */
+DV_API dv_status dvt_consume(const uint64_t* flag, uint64_t seq, const void* src, void* dst,
+                             uint64_t bytes, uint64_t timeout_ns, int32_t* ok, void* stream);
+
 /* Busy-wait kernel: `ctas` CTAs of 128 threads spin for `ns` nanoseconds (globaltimer). */
 DV_API dv_status dvt_spin(uint64_t ns, int32_t ctas, void* stream);
 

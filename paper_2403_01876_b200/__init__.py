@@ -132,6 +132,8 @@ _SIGS = {
                              C.c_int32, P(dv_region), C.c_void_p, C.c_void_p]),
     "dvt_trace": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dvt_spin": (C.c_int, [C.c_uint64, C.c_int32, C.c_void_p]),
+    "dvt_consume": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                              C.c_void_p]),
     "dvt_watch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "dvt_release_scope": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     "dvb_per_run_copy": (C.c_int, [P(dv_cache), P(dv_region), C.c_void_p, C.c_void_p, P(C.c_uint64)]),
@@ -511,6 +513,11 @@ def dvt_release_scope(ctx, flag_ptr, payload_ptr=0) -> bool:
 
 def dvt_watch(flag_ptr, seq0, n, ts_ptr, timeout_ns=2_000_000_000, stream=None):
     _call("dvt_watch", C.c_void_p(flag_ptr), seq0, n, C.c_void_p(ts_ptr), timeout_ns, _stream(stream))
+
+
+def dvt_consume(flag_ptr, seq, src_ptr, dst_ptr, nbytes, ok_ptr, timeout_ns=2_000_000_000, stream=None):
+    _call("dvt_consume", C.c_void_p(flag_ptr), seq, C.c_void_p(src_ptr), C.c_void_p(dst_ptr), nbytes, timeout_ns,
+          C.c_void_p(ok_ptr), _stream(stream))
 
 
 def dvt_spin(ns, ctas, stream=None):

@@ -18,7 +18,7 @@ FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidde
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "dv_internal.h"), os.path.join(ROOT, "include", "dv.h"),
-                   os.path.join(ROOT, "include", "dv_testing.h"),
+                   os.path.join(ROOT, "include", "dv_testing.h"), os.path.join(ROOT, "include", "dv_device.cuh"),
                    os.path.join(ROOT, "include", "dv_baselines.h")]
     if not force and os.path.exists(OUT):
         t = os.path.getmtime(OUT)

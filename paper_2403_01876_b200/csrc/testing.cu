@@ -1,4 +1,5 @@
 // Test-only kernels (include/dv_testing.h): synthetic KV writer with the kvgen generator, spin.
+#include "../../include/dv_device.cuh"
 #include "../../include/dv_testing.h"
 #include "dv_internal.h"
 
@@ -127,13 +128,33 @@ __global__ void k_watch(const unsigned long long* flag, unsigned long long seq0,
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int32_t i = 0; i < n; ++i) {
     for (;;) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      const unsigned long long v = dv_flag_load((const uint64_t*)flag);
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (v >= seq0 + (unsigned long long)i) break;
       if (t - t0 > timeout_ns) return;
     }
     ts[i] = t;
+  }
+}
+
+// An in-kernel consumer (A5's second form, include/dv_device.cuh): thread 0 acquires the flag
+// (dv_flag_wait), the CTA synchronises, then every thread copies the released payload. *ok = 0
+// if the wait timed out.
+__global__ void k_consume(const uint64_t* flag, uint64_t seq, const uint4* src, uint4* dst,
+                          uint64_t n16, uint64_t timeout_ns, int32_t* ok) {
+  __shared__ int got;
+  if (threadIdx.x == 0) got = dv_flag_wait(flag, seq, timeout_ns);
+  __syncthreads();
+  if (!got) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *ok = 0;
+    return;
+  }
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 v;
+    asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i));
+    dst[i] = v;
   }
 }
 
@@ -231,6 +252,16 @@ extern "C" dv_status dvt_watch(const uint64_t* flag, uint64_t seq0, int32_t n, u
   (void)cudaGetLastError();
   k_watch<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)flag, seq0, n,
                                              (unsigned long long*)ts, timeout_ns);
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_consume(const uint64_t* flag, uint64_t seq, const void* src, void* dst,
+                                 uint64_t bytes, uint64_t timeout_ns, int32_t* ok, void* stream) {
+  if (!flag || !src || !dst || !ok || bytes % 16) return fail(DV_EINVAL, "bad dvt_consume arguments");
+  (void)cudaGetLastError();
+  k_consume<<<4, 256, 0, (cudaStream_t)stream>>>(flag, seq, (const uint4*)src, (uint4*)dst,
+                                                 bytes / 16, timeout_ns, ok);
   DV_CUDA(cudaGetLastError());
   return DV_OK;
 }

@@ -1086,3 +1086,32 @@ print("ok", dt)
 ''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("npos", [1, 24])
+def test_in_kernel_consumer_acquires_released_payload(host, npos):
+    """A5, consumer form 2 (include/dv_device.cuh): a kernel launched BEFORE the stream-out, on its
+    own stream, spins with dv_flag_wait on the flag, then copies the wire. It must read exactly the
+    oracle's packed bytes: the release (gpu-scope cluster/ticket for HBM, system scope for pinned
+    host) orders every CTA's payload before the flag for a GPU-side acquirer too."""
+    L, B, H, S, D = 2, 4, 8, 64, 128
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=41 + npos)
+    k, v, c = dev_cache(K, V, 0, 0)
+    reg = (0, L, 0, B, 5, 5 + npos)
+    exp = ok.pack(oc(K, V, 0, 0, S), reg)
+    wire = pinned_u16(exp.size) if host else sentinel_like((exp.size,))
+    fl = flags(1, pinned=host)
+    ep = dv.endpoint_of(wire, fl)
+    out = torch.full((exp.size,), -1, dtype=torch.int16, device="cuda")
+    okf = torch.ones(1, dtype=torch.int32, device="cuda")
+    cx = ctx()
+    prod, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    dv.dvt_spin(1000, 1, stream=prod)   # every kernel loaded before the consumer spins
+    torch.cuda.synchronize()
+    dv.dvt_consume(ep.flags, 9, wire.data_ptr(), out.data_ptr(), exp.size * 2, okf.data_ptr(), stream=cons)
+    dv.dvt_spin(2_000_000, 1, stream=prod)
+    dv.dv_scatter(cx, c, dv.region(*reg), ep, 0, flag_slot=0, seq=9, xfer=dv.DV_XFER_FUSED, stream=prod)
+    torch.cuda.synchronize()
+    assert int(okf[0]) == 1
+    assert np.array_equal(to_np(out), exp)
