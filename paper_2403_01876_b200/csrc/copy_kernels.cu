@@ -1057,9 +1057,11 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   const double tb = (double)tp.n_tiles * kTS * t.tU * 16, rb = (double)r.runs() * r.run_bytes;
   const uint64_t t_need = transpose_ctas(tp), r_need = (kr.n_vec + 1023) / 1024;
   const uint64_t grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, t_need + r_need));
-  // transpose CTAs get 0.7 of their byte share (measured on the C2 FT6D prompt layer with PK = 16,
-  // tools/ft6d_cmp.sh: 0.96 of HBM peak at 0.7, 0.94 at 1.0; DV_TSPLIT=0 = every CTA does both)
-  static const double tscale = getenv("DV_TSPLIT") ? atof(getenv("DV_TSPLIT")) : 0.7;
+  // transpose CTAs get 0.6 of their byte share (C2 FT6D prompt layer, PK = 16, both directions,
+  // tools/ft6d_cmp.sh + tools/probe_ft6d_dirs.py: pack / unpack / KV5D->FT6D remap 0.954 / 0.942 /
+  // 0.935 of HBM peak at 0.6, 0.950 / 0.934 / 0.925 at 0.7, 0.939 / 0.933 / 0.924 at 1.0;
+  // DV_TSPLIT=0 = every CTA does both halves)
+  static const double tscale = getenv("DV_TSPLIT") ? atof(getenv("DV_TSPLIT")) : 0.6;
   uint64_t t_blocks = (uint64_t)(grid * tscale * tb / (tscale * tb + rb) + 0.5);
   t_blocks = std::min(std::max<uint64_t>(1, t_blocks), grid - 1);
   if (tscale == 0) t_blocks = 0;
