@@ -173,6 +173,73 @@ def test_c4_full_size_swap_in_from_log():
     cx.close()
 
 
+def test_c5_full_size_replica_token_steps_and_recovery():
+    """C5 (OPT-66B, b 16, P = 8 stage shape: 8 layers, S 2048; 9.66 GB per cache) in the form
+    bench.py --workload c5 times: prompt replica p = 1024 into the successor's replica store with
+    dv_stream_out_direct, then token steps, then the two recovery copies of PAPER.md:288 into wiped
+    caches -- sampled parity vs kvgen's definition + every word checked on the device."""
+    H, D, b, S, p, Ls, T = 72, 128, 16, 2048, 1024, 8, 6
+    lb = 8   # stage x = 1 of 8: layers [8, 16)
+    own_k = torch.empty((Ls, b, H, S, D), dtype=torch.int16, device="cuda")
+    own_v = torch.empty_like(own_k)
+    own = dv.cache(own_k, own_v, lb, 0)
+    dv.dvt_fill(own, dv.DVT_FILL_HASH, seed=SEED)
+    rep_k = torch.full_like(own_k, -1)
+    rep_v = torch.full_like(own_v, -1)
+    rep = dv.cache(rep_k, rep_v, lb, 0)
+    fl = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sig = dv.endpoint(dv.DV_EP_DEVICE, fl.data_ptr(), 8, fl.data_ptr(), 1)
+    setup = dv.Setup([lb, lb + Ls], [0, b], S)
+    cx = _ctx()
+    dv.dv_stream_out_direct(cx, own, dv.region(lb, lb + Ls, 0, b, 0, p), setup, 0, 0, setup, [rep], [sig], seq=1)
+    for t in range(1, T + 1):
+        dv.dv_stream_out_direct(cx, own, dv.region(lb, lb + Ls, 0, b, p + t - 1, p + t), setup, 0, 0, setup,
+                                [rep], [sig], seq=1 + t)
+    torch.cuda.synchronize()
+    n = p + T
+    assert int(fl[0]) == 1 + T
+    assert _sample_cache(rep_k, rep_v, rep, (lb, lb + Ls, 0, b, 0, n), SEED) == 0
+    ver = _Verify()
+    assert ver(rep, (lb, lb + Ls, 0, b, 0, n)) == 0
+    assert int(rep_k[:, :, :, n:].ne(-1).sum()) == 0
+    # recovery (NEXT-3): the failed stage's own cache comes back from the replica
+    own_k.fill_(-1)
+    own_v.fill_(-1)
+    dv.dv_remap(cx, rep, own, dv.region(lb, lb + Ls, 0, b, 0, n))
+    torch.cuda.synchronize()
+    assert _sample_cache(own_k, own_v, own, (lb, lb + Ls, 0, b, 0, n), SEED) == 0
+    assert ver(own, (lb, lb + Ls, 0, b, 0, n)) == 0
+    cx.close()
+
+
+def test_ft6d_full_size_prompt_layer_pack_and_remap():
+    """C2 shape with FasterTransformer's 6-D keys (NEXT-1): a prompt layer (163.8 MB) packed through
+    the register packet transpose, and remapped FT6D -> KV5D into a cache with another max_seq --
+    sampled parity vs the oracle's wire order and kvgen + every word on the device."""
+    L, H, D, B, P, S = 4, 40, 128, 8, 1000, 2048
+    k6 = torch.empty((L, B, H, D // 8, S, 8), dtype=torch.int16, device="cuda")
+    v6 = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
+    c6 = dv.cache(k6, v6)
+    dv.dvt_fill(c6, dv.DVT_FILL_HASH, seed=SEED)
+    cx = _ctx()
+    reg = (2, 3, 0, B, 0, P)
+    wire = torch.full((2 * B * H * P * D,), -1, dtype=torch.int16, device="cuda")
+    dv.dv_scatter(cx, c6, dv.region(*reg), dv.endpoint_of(wire), 0)
+    torch.cuda.synchronize()
+    assert _sample_wire(wire, reg, H, D, SEED) == 0
+    ver = _Verify()
+    assert ver(c6, reg, wire) == 0
+    k5 = torch.full((1, B, H, 1536, D), -1, dtype=torch.int16, device="cuda")
+    v5 = torch.full_like(k5, -1)
+    c5 = dv.cache(k5, v5, 2, 0)
+    dv.dv_remap(cx, c6, c5, dv.region(*reg))
+    torch.cuda.synchronize()
+    assert _sample_cache(k5, v5, c5, reg, SEED) == 0
+    assert ver(c5, reg) == 0
+    assert int(k5[:, :, :, P:].ne(-1).sum()) == 0
+    cx.close()
+
+
 def test_launch_split_path_matches_oracle():
     """Copies larger than the per-launch vector limit are split at run boundaries; forced here with
     DV_MAX_VEC=1000 in a subprocess (the limit is read once per process)."""
