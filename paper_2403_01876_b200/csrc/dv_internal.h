@@ -157,7 +157,10 @@ struct dv_ctx {
   std::atomic<uint32_t> next_ev{0};
   std::mutex pipe_mu;     // one pipelined transfer enqueued at a time per context
   unsigned long long* trace_ts = nullptr;  // dvt_trace: publish timestamps land here
-  static constexpr uint32_t kTickets = 4096;
+  // A ticket is held only while its kernel runs (the last CTA resets it), and tickets are handed
+  // out round robin at enqueue, so a ticket is reused only after 65,536 later publishing launches
+  // of this context -- far more than can be in flight while one copy kernel is still running.
+  static constexpr uint32_t kTickets = 65536;
 };
 
 namespace dv {
