@@ -78,6 +78,9 @@ def loop3(xfer, n=120, seq0=0, slots=8):
         j = (t - 1) % slots
         if t > slots:
             s_h2d.wait_event(eu[t - 1 - slots])          # slot j free: its unpack is done
+        lag = int(os.environ.get("LAG", "0"))
+        if lag and t > lag:                               # bounded run-ahead: step t's H2D after
+            dv.dv_wait(ctx, ep, 0, seq0 + t - lag, stream=s_h2d)   # step t-lag's D2H landed
         dv.dv_fetch(ctx, dep, ((t - 1) % RING) * STEP, wire.data_ptr() + j * STEP, STEP, stream=s_h2d)
         eh[t - 1].record(s_h2d)
         s_unp.wait_event(eh[t - 1])
@@ -102,6 +105,7 @@ if os.environ.get("FORM") == "3":
             r = loop3(xf, n, 50_000 + n * 10 + (0 if name == "staged" else 100_000))
             r["xfer"] = name
             r["n"] = n
+            r["lag"] = os.environ.get("LAG", "0")
             print(json.dumps(r), flush=True)
     sys.exit(0)
 
