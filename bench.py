@@ -140,7 +140,7 @@ def run_ours(args):
 
     def step(t, xf=xfer):
         q = pos_of(t)
-        dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
+        dv.dv_scatter(ctx, cache, (0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
                       flag_slot=0, seq=t, xfer=xf, stream=sp)
 
     torch.cuda.synchronize()

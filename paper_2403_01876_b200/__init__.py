@@ -163,6 +163,42 @@ def exported_symbols():
     return list(_SIGS)
 
 
+_fast = None
+
+
+def fast():
+    """The CPython fast-path module (csrc/pyfast.c) for the per-call entry points: same library,
+    no ctypes per-argument conversion. None when it has not been built (ctypes is used then)."""
+    global _fast
+    if _fast is None:
+        lib()   # loads libdvstream.so first (the module links against it by rpath)
+        if os.environ.get("DV_NO_FAST") == "1":   # ctypes path only (tests of both bindings)
+            _fast = False
+            return None
+        try:
+            from . import _dvfast
+            _fast = _dvfast
+        except ImportError:  # pragma: no cover - built by build.build_fast / __graft_entry__.build
+            _fast = False
+    return _fast or None
+
+
+def _check(st, name):
+    if st != DV_OK:
+        raise DVError(st, name, lib().dv_last_error().decode())
+    return st
+
+
+def _sint(s):
+    """Stream handle as an int (None = torch's current stream)."""
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if hasattr(s, "cuda_stream"):
+        return s.cuda_stream
+    return int(s)
+
+
 _fns = {}
 
 
@@ -330,6 +366,7 @@ class Context:
         cfg = dv_config(staging_bytes, max_ctas, host_ctas)
         _call("dv_create", device, C.byref(cfg), C.byref(h))
         self.h = h
+        self.addr = h.value   # the dv_ctx* as an int (fast path)
         self.device = device
 
     def close(self):
@@ -411,15 +448,40 @@ def dv_fetch(ctx, src: dv_endpoint, src_off, dst_ptr, nbytes, flag_slot=-1, wait
           xfer, _stream(stream))
 
 
+_addr = C.addressof
+
+
+def _reg_fast(reg):
+    """Region for the fast path: a tuple passes as is (no ctypes structure), a dv_region by address."""
+    return reg if isinstance(reg, tuple) else _addr(reg)
+
+
+def _reg_ct(reg):
+    """Region for the ctypes path."""
+    if isinstance(reg, tuple):
+        if len(reg) not in (6, 8):
+            raise ValueError("region tuple needs 6 or 8 entries")
+        reg = region(*reg)
+    return C.byref(reg)
+
+
 def dv_scatter(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off=0, flag_slot=-1, seq=0,
                xfer=0, stream=None):
-    _call("dv_scatter", ctx.h, C.byref(src), C.byref(reg), C.byref(dst), dst_off, flag_slot, seq, xfer,
+    f = _fast or fast()
+    if f:
+        return _check(f.scatter(ctx.addr, _addr(src), _reg_fast(reg), _addr(dst), dst_off, flag_slot, seq, xfer,
+                                _sint(stream)), "dv_scatter")
+    _call("dv_scatter", ctx.h, C.byref(src), _reg_ct(reg), C.byref(dst), dst_off, flag_slot, seq, xfer,
           _stream(stream))
 
 
 def dv_gather(ctx, src: dv_endpoint, src_off, dst: dv_cache, reg: dv_region, flag_slot=-1, wait_seq=0,
               xfer=0, stream=None):
-    _call("dv_gather", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), C.byref(reg),
+    f = _fast or fast()
+    if f:
+        return _check(f.gather(ctx.addr, _addr(src), src_off, flag_slot, wait_seq, _addr(dst), _reg_fast(reg), xfer,
+                               _sint(stream)), "dv_gather")
+    _call("dv_gather", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), _reg_ct(reg),
           xfer, _stream(stream))
 
 
@@ -431,7 +493,12 @@ def dv_gather_chunks(ctx, src: dv_endpoint, src_off, dst: dv_cache, first: dv_re
 
 def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpoint = None, flag_slot=-1,
              seq=0, xfer=0, stream=None):
-    _call("dv_remap", ctx.h, C.byref(src), C.byref(dst), C.byref(reg), _ref(signal), flag_slot, seq,
+    f = _fast or fast()
+    if f:
+        return _check(f.remap(ctx.addr, _addr(src), _addr(dst), _reg_fast(reg),
+                              None if signal is None else _addr(signal), flag_slot, seq, xfer, _sint(stream)),
+                      "dv_remap")
+    _call("dv_remap", ctx.h, C.byref(src), C.byref(dst), _reg_ct(reg), _ref(signal), flag_slot, seq,
           xfer, _stream(stream))
 
 
@@ -465,15 +532,27 @@ def dv_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, m
                          dst_setup: Setup, dst_caches, signals=None, seq=0, xfer=0, stream=None, my_tp=0):
     carr = cache_array(dst_caches)
     sarr = endpoint_array(signals) if signals is not None else None
-    _call("dv_stream_out_direct", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage,
+    f = _fast or fast()
+    if f:
+        return _check(f.stream_out_direct(ctx.addr, _addr(src), _reg_fast(reg), _addr(src_setup.c), my_stage, my_micro,
+                                          my_tp, _addr(dst_setup.c), _addr(carr),
+                                          None if sarr is None else _addr(sarr), len(dst_caches), seq, xfer,
+                                          _sint(stream)), "dv_stream_out_direct")
+    _call("dv_stream_out_direct", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage,
           my_micro, my_tp, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, xfer, _stream(stream))
 
 
 def dv_wait(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):
+    f = _fast or fast()
+    if f:
+        return _check(f.wait(ctx.addr, _addr(ep), flag_slot, seq, _sint(stream)), "dv_wait")
     _call("dv_wait", ctx.h, C.byref(ep), flag_slot, seq, _stream(stream))
 
 
 def dv_signal(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):
+    f = _fast or fast()
+    if f:
+        return _check(f.signal(ctx.addr, _addr(ep), flag_slot, seq, _sint(stream)), "dv_signal")
     _call("dv_signal", ctx.h, C.byref(ep), flag_slot, seq, _stream(stream))
 
 

@@ -37,6 +37,23 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+def build_fast(force: bool = False) -> str:
+    """Compile the CPython fast-path module _dvfast (csrc/pyfast.c) against libdvstream.so."""
+    import sysconfig
+    src = os.path.join(CSRC, "pyfast.c")
+    out = os.path.join(HERE, "_dvfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    deps = [src, OUT, os.path.join(ROOT, "include", "dv.h")]
+    if not force and os.path.exists(out) and all(os.path.getmtime(d) <= os.path.getmtime(out) for d in deps):
+        return out
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+           "-I", os.path.join(ROOT, "include"), src, "-L", HERE, "-ldvstream", "-Wl,-rpath,$ORIGIN", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("gcc failed building _dvfast")
+    return out
+
+
 def build_c_smoke(force: bool = False) -> str:
     """Compile tests/c/abi_smoke.c against the library with plain gcc (the ABI used from C)."""
     src = os.path.join(ROOT, "tests", "c", "abi_smoke.c")
@@ -54,3 +71,4 @@ def build_c_smoke(force: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build_fast(force="-f" in sys.argv))

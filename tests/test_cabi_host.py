@@ -79,6 +79,17 @@ def test_oracle_used_only_by_tests_smoke_and_cpu_baseline():
         assert "oracle" not in f.read_text(), f"{f} mentions the oracle"
 
 
+def test_fast_path_module_builds_and_exports():
+    """The CPython fast path (csrc/pyfast.c) is built beside libdvstream.so and exposes the per-call
+    entry points; a malformed call raises instead of reaching the library."""
+    f = dv.fast()
+    assert f is not None and f.__file__.startswith(os.path.dirname(dv.__file__))
+    for name in ("scatter", "gather", "remap", "stream_out_direct", "wait", "signal"):
+        assert callable(getattr(f, name))
+    with pytest.raises(TypeError):
+        f.scatter(0, 0)
+
+
 def _region_bytes_oracle(r, H, D, e):
     return ok.region_bytes(r.layer_begin, r.layer_end, r.req_begin, r.req_end, r.pos_begin, r.pos_end, H, D, e)
 

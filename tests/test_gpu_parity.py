@@ -1115,3 +1115,26 @@ def test_in_kernel_consumer_acquires_released_payload(host, npos):
     torch.cuda.synchronize()
     assert int(okf[0]) == 1
     assert np.array_equal(to_np(out), exp)
+
+
+def test_region_tuples_equal_region_structs():
+    """The binding's fast path takes a region as a plain tuple (no ctypes structure per call):
+    scatter, gather and remap with tuples give the same bytes as with dv_region structures."""
+    L, B, H, S, D = 2, 3, 4, 20, 64
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=61)
+    k, v, c = dev_cache(K, V, 0, 0)
+    for reg in [(0, 2, 1, 3, 4, 17), (1, 2, 0, 3, 0, 20, 1, 3)]:
+        exp = ok.pack(oc(K, V, 0, 0, S), reg)
+        a, b = sentinel_like((exp.size,)), sentinel_like((exp.size,))
+        dv.dv_scatter(ctx(), c, reg, dv.endpoint_of(a))
+        dv.dv_scatter(ctx(), c, dv.region(*reg), dv.endpoint_of(b))
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(a), exp) and np.array_equal(to_np(b), exp)
+        dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+        dv.dv_gather(ctx(), dv.endpoint_of(a), 0, dv.cache(dk, dvv), reg)
+        ek, ev = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+        dv.dv_remap(ctx(), c, dv.cache(ek, ev), reg)
+        torch.cuda.synchronize()
+        assert torch.equal(dk, ek) and torch.equal(dvv, ev)
+    with pytest.raises(ValueError):
+        dv.dv_scatter(ctx(), c, (0, 1, 0, 1), dv.endpoint_of(a))

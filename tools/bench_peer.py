@@ -134,7 +134,7 @@ def run_c5(args, bench):
     def step(t):
         q = p + (t - 1) % (S - p)
         if not nccl:
-            dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
+            dv.dv_stream_out_direct(ctx, own, (lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
                                     dst_arr, sig_arr, seq=t, stream=sp)
             return
         dv.dv_scatter(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), dv.endpoint_of(sbuf), 0, stream=sp)
