@@ -45,9 +45,11 @@ def main():
         "hbm_copy_2GiB": lambda: big_dst.copy_(big_src),
     }
     ctxs = {"fused": dv.dv_create(0), "fused_16ctas": dv.dv_create(0, max_ctas=16),
-            "fused_64ctas": dv.dv_create(0, max_ctas=64), "staged": dv.dv_create(0)}
+            "fused_64ctas": dv.dv_create(0, max_ctas=64), "staged": dv.dv_create(0),
+            "decoupled": dv.dv_create(0)}
     xfers = {"fused": dv.DV_XFER_FUSED, "fused_16ctas": dv.DV_XFER_FUSED, "fused_64ctas": dv.DV_XFER_FUSED,
-             "staged": dv.DV_XFER_STAGED}
+             "staged": dv.DV_XFER_STAGED, "decoupled": dv.DV_XFER_DECOUPLED}
+    seq0 = [0]
     n = 30
     for (cname, cfn), strm_name in [(kv, sn) for kv in computes.items() for sn in ("normal", "high")]:
         strm = strm_hi if strm_name == "high" else strm_lo
@@ -70,9 +72,14 @@ def main():
                     sev[i][0].record(strm)
                     # the previous step's K/V (the cache is resident; its position is fresh)
                     dv.dv_scatter(ctxs[variant], cache, dv.region(0, L, 0, B, q, q + 1), ep, (i % 8) * STEP,
-                                  flag_slot=0, seq=i + 1, xfer=xfers[variant], stream=strm)
+                                  flag_slot=0, seq=seq0[0] + i + 1, xfer=xfers[variant], stream=strm)
                     sev[i][1].record(strm)
             comp.wait_stream(strm)
+            if variant is not None:
+                # the step ends when the last chunk's flag is visible (decoupled: DMA + flag run on the
+                # library's streams, not on strm)
+                dv.dv_wait(ctxs[variant], ep, 0, seq0[0] + n, stream=comp)
+                seq0[0] += n
             t1.record(comp)
             torch.cuda.synchronize()
             c_ms = sorted(x.elapsed_time(y) for x, y in ev)[n // 2]
@@ -90,7 +97,8 @@ def main():
                               "compute_ms_p50": c, "stream_ms_p50": sm,
                               "step_ms": tot, "compute_slowdown_pct": 100 * (c - base_c) / base_c,
                               "step_slowdown_pct": 100 * (tot - base_tot) / base_tot,
-                              "stream_gbs_under_load": STEP / (sm * 1e-3) / 1e9 if sm else None,
+                              "stream_gbs_under_load": (STEP / (sm * 1e-3) / 1e9 if sm and var != "decoupled"
+                                                        else None),
                               "m_factor": tot / base_tot}), flush=True)
 
 
