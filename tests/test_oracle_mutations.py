@@ -1,0 +1,98 @@
+"""Mutation check of the oracle's pins (③: "chosen so that a plausible mistake anywhere in it fails
+one of them"): each case below plants one plausible mistake in a COPY of oracle/kvstream.py -- a
+dropped term, a wrong sign or index, a transposed operand, an off-by-one -- and runs
+tests/test_oracle_pins.py against the mutant. Every mutant must be caught (the pins fail); the
+unmutated copy must pass. CPU only, a few seconds per mutant."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (name, exact source snippet of oracle/kvstream.py, mutated snippet)
+MUTANTS = [
+    ("region_bytes drops the K+V factor",
+     "    return 2 * nL * nR * n * n_heads * head_dim * elem_bytes",
+     "    return nL * nR * n * n_heads * head_dim * elem_bytes"),
+    ("wire order: heads before requests",
+     "    return (((((l - l0) * 2 + kv) * nR + (r - r0)) * nH + (h - h0)) * n + (s - s0)) * head_dim + d",
+     "    return (((((l - l0) * 2 + kv) * nH + (h - h0)) * nR + (r - r0)) * n + (s - s0)) * head_dim + d"),
+    ("pack stacks K/V outermost instead of under the layer",
+     "    wire = np.stack(blocks, axis=1)",
+     "    wire = np.stack(blocks, axis=0)"),
+    ("route intersection off by one (empty pieces kept)",
+     "                            if a < b and c < d and (not tp or e < f):",
+     "                            if a <= b and c <= d and (not tp or e < f):"),
+    ("route destination offsets accumulated per source block",
+     "        p.dst_wire_off = dst_acc.get(kd, 0)\n        dst_acc[kd] = p.dst_wire_off + p.bytes",
+     "        p.dst_wire_off = dst_acc.get(ks, 0)\n        dst_acc[ks] = p.dst_wire_off + p.bytes"),
+    ("route ignores the destination's layer bounds",
+     "                            a = max(l0, src.layer_bounds[i], dst.layer_bounds[j])",
+     "                            a = max(l0, src.layer_bounds[i])"),
+    ("FT6D key: packet and in-packet index swapped",
+     "            return (lp, rp, hp, d // x, s, d % x)",
+     "            return (lp, rp, hp, d % x, s, d // x)"),
+    ("cache addressing forgets the request offset",
+     "        lp, rp, hp = l - self.layer_begin, r - self.req_begin, h - self.head_begin",
+     "        lp, rp, hp = l - self.layer_begin, r, h - self.head_begin"),
+    ("token step t writes position p+t (reading Q4 violated)",
+     "    return prompt_len + step - 1",
+     "    return prompt_len + step"),
+    ("swap rotation direction reversed",
+     "    return (x + 1) % n, (x - 1) % n",
+     "    return (x - 1) % n, (x + 1) % n"),
+    ("uneven layer split gives the extra layers to the last stages",
+     "        b.append(b[-1] + q + (1 if st < rem else 0))",
+     "        b.append(b[-1] + q + (1 if st >= n_stages - rem else 0))"),
+    ("recovery takes the replica from the predecessor",
+     '    return [((x + 1) % n, x, "replica_of_x"), ((x - 1) % n, x, "own_cache_of_prev")]',
+     '    return [((x - 1) % n, x, "replica_of_x"), ((x - 1) % n, x, "own_cache_of_prev")]'),
+    ("swap-in moves only the newest position",
+     "    return i * batch * c_bytes",
+     "    return batch * c_bytes"),
+]
+
+
+def _tree(tmp, mutant):
+    for d in ("oracle", "kvgen"):
+        shutil.copytree(os.path.join(ROOT, d), os.path.join(tmp, d),
+                        ignore=shutil.ignore_patterns("__pycache__"))
+    os.makedirs(os.path.join(tmp, "tests"))
+    shutil.copy(os.path.join(ROOT, "tests", "test_oracle_pins.py"), os.path.join(tmp, "tests"))
+    shutil.copytree(os.path.join(ROOT, "tests", "golden"), os.path.join(tmp, "tests", "golden"))
+    with open(os.path.join(tmp, "tests", "conftest.py"), "w") as f:
+        f.write("import json, os, sys\nimport pytest\n"
+                "sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))\n"
+                "G = os.path.join(os.path.dirname(os.path.abspath(__file__)), 'golden')\n"
+                "@pytest.fixture\ndef golden():\n"
+                "    return lambda n: json.load(open(os.path.join(G, n)))\n")
+    if mutant is not None:
+        _, old, new = mutant
+        p = os.path.join(tmp, "oracle", "kvstream.py")
+        src = open(p).read()
+        assert src.count(old) == 1, f"snippet not found exactly once: {old!r}"
+        open(p, "w").write(src.replace(old, new))
+
+
+def _run(tmp):
+    env = dict(os.environ, PYTHONPATH=tmp, PYTHONDONTWRITEBYTECODE="1")
+    return subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                           os.path.join(tmp, "tests", "test_oracle_pins.py")],
+                          cwd=tmp, env=env, capture_output=True, text=True, timeout=300)
+
+
+def test_unmutated_copy_passes(tmp_path):
+    _tree(str(tmp_path), None)
+    r = _run(str(tmp_path))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("mutant", MUTANTS, ids=[m[0] for m in MUTANTS])
+def test_pins_catch_mutant(tmp_path, mutant):
+    _tree(str(tmp_path), mutant)
+    r = _run(str(tmp_path))
+    assert r.returncode == 1, f"no pin caught the mutant: {mutant[0]}\n{r.stdout[-1500:]}"
+    assert "FAILED tests/test_oracle_pins.py::" in r.stdout   # a pin failed (not a collection error)
