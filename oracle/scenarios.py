@@ -17,7 +17,8 @@ from .kvstream import (Cache, Setup, remap, ring_successor, stream, swap_rotatio
 
 
 def swap_simulate(host: Dict[int, Cache], slots: List[Cache], prompt_len: int, rounds: int,
-                  write_token: Callable[[Cache, int, int], None], log: list | None = None):
+                  write_token: Callable[[Cache, int, int], None], log: list | None = None,
+                  after_swap_in: Callable[[int, Cache, int], None] | None = None):
     """One stage of a depth-D pipeline (D = len(host) >= 3) with two device slots.
 
     host[x] is microbatch x's host arena in mirror form (same layout, holds [0, len_x));
@@ -31,7 +32,9 @@ def swap_simulate(host: Dict[int, Cache], slots: List[Cache], prompt_len: int, r
           the slot (x-1)%D just released; (c) completes before (d) overwrites that slot (Q10).
     Before the first event microbatch 0 is swapped into slot 0; after the last event the final
     delta is swapped out. Mutates host/slots; returns {x: len_x}.
-    ``log`` (optional) receives ('in'|'out', x, pos_begin, pos_end, slot) tuples.
+    ``log`` (optional) receives ('in'|'out', x, pos_begin, pos_end, slot) tuples (the regions
+    actually moved); ``after_swap_in`` (optional) is called as (x, slot seen as x's cache, len_x)
+    right after each swap-in, so a test can check the slot's contents at that moment.
     """
     D = len(host)
     if D < 3:
@@ -47,14 +50,16 @@ def swap_simulate(host: Dict[int, Cache], slots: List[Cache], prompt_len: int, r
         remap(host[x], relabel(slots[slot], host[x].req_begin), reg)
         slot_of[x] = slot
         if log is not None:
-            log.append(("in", x, 0, length[x], slot))
+            log.append(("in", x, reg[4], reg[5], slot))
+        if after_swap_in is not None:
+            after_swap_in(x, relabel(slots[slot], host[x].req_begin), length[x])
 
     def swap_out(x):
         pos = length[x] - 1
         reg = (L0, L1, host[x].req_begin, host[x].req_begin + host[x].n_reqs, pos, pos + 1)
         remap(relabel(slots[slot_of[x]], host[x].req_begin), host[x], reg)
         if log is not None:
-            log.append(("out", x, pos, pos + 1, slot_of[x]))
+            log.append(("out", x, reg[4], reg[5], slot_of[x]))
 
     swap_in(0, 0)
     last = None

@@ -1,5 +1,5 @@
 """Mutation check of the oracle's pins (③: "chosen so that a plausible mistake anywhere in it fails
-one of them"): each case below plants one plausible mistake in a COPY of oracle/kvstream.py -- a
+one of them"): each case below plants one plausible mistake in a COPY of oracle/ -- a
 dropped term, a wrong sign or index, a transposed operand, an off-by-one -- and runs
 tests/test_oracle_pins.py against the mutant. Every mutant must be caught (the pins fail); the
 unmutated copy must pass. CPU only, a few seconds per mutant."""
@@ -53,6 +53,17 @@ MUTANTS = [
     ("swap-in moves only the newest position",
      "    return i * batch * c_bytes",
      "    return batch * c_bytes"),
+    # scenario oracles (oracle/scenarios.py)
+    ("swap-out writes the position after the last token",
+     "        pos = length[x] - 1\n",
+     "        pos = length[x]\n", "scenarios.py"),
+    ("swap-in brings back only the newest position",
+     "        reg = (L0, L1, host[x].req_begin, host[x].req_begin + host[x].n_reqs, 0, length[x])",
+     "        reg = (L0, L1, host[x].req_begin, host[x].req_begin + host[x].n_reqs, length[x] - 1, length[x])",
+     "scenarios.py"),
+    ("ring replicates into its own store instead of the successor's",
+     "        remap(own[x], replica[ring_successor(x, n)], region_of(x))",
+     "        remap(own[x], replica[x], region_of(x))", "scenarios.py"),
 ]
 
 
@@ -70,8 +81,8 @@ def _tree(tmp, mutant):
                 "@pytest.fixture\ndef golden():\n"
                 "    return lambda n: json.load(open(os.path.join(G, n)))\n")
     if mutant is not None:
-        _, old, new = mutant
-        p = os.path.join(tmp, "oracle", "kvstream.py")
+        old, new = mutant[1], mutant[2]
+        p = os.path.join(tmp, "oracle", mutant[3] if len(mutant) > 3 else "kvstream.py")
         src = open(p).read()
         assert src.count(old) == 1, f"snippet not found exactly once: {old!r}"
         open(p, "w").write(src.replace(old, new))

@@ -383,7 +383,17 @@ def test_swap_simulation_invariants(depth, rounds):
         host[x] = Cache(K, V, L0, x * b, H, S, D)
     slots = [Cache(*kvgen.sentinel_cache(nL, b, H, S, D), L0, 0, H, S, D) for _ in range(2)]
     log = []
-    length = scenarios.swap_simulate(host, slots, p, rounds, _write_token_factory(H, D, seed), log)
+    seen = []
+
+    def slot_holds_prefix(x, slot, n):
+        # after each swap-in the slot equals the writer's words on [0, len)
+        exp = kvgen.kv5d_cache("hash", L0, nL, x * b, b, H, S, D, seed=seed)
+        for kv in (0, 1):
+            assert np.array_equal(slot.arr(kv)[:, :, :, :n], exp[kv][:, :, :, :n]), (x, n)
+        seen.append((x, n))
+    length = scenarios.swap_simulate(host, slots, p, rounds, _write_token_factory(H, D, seed), log,
+                                     after_swap_in=slot_holds_prefix)
+    assert len(seen) == len([e for e in log if e[0] == "in"]) > 0
     for x in range(depth):
         assert length[x] == p + rounds
         exp = kvgen.kv5d_cache("hash", L0, nL, x * b, b, H, S, D, seed=seed)
