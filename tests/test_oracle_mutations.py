@@ -64,6 +64,30 @@ MUTANTS = [
     ("ring replicates into its own store instead of the successor's",
      "        remap(own[x], replica[ring_successor(x, n)], region_of(x))",
      "        remap(own[x], replica[x], region_of(x))", "scenarios.py"),
+    ("unpack swaps K and V",
+     "        dst.set_logical(kv, l0, l1, r0, r1, s0, s1, w[:, kv], (h0, h1))",
+     "        dst.set_logical(kv, l0, l1, r0, r1, s0, s1, w[:, 1 - kv], (h0, h1))"),
+    ("route source offsets accumulated per destination block",
+     "        p.src_wire_off = src_acc.get(ks, 0)\n        src_acc[ks] = p.src_wire_off + p.bytes",
+     "        p.src_wire_off = src_acc.get(kd, 0)\n        src_acc[kd] = p.src_wire_off + p.bytes"),
+    ("range check off by one (pos_end == max_seq rejected)",
+     "        if s1 > s.max_seq:",
+     "        if s1 >= s.max_seq:"),
+    ("TP head intersection ignores the destination's head bounds",
+     "                                e = max(heads[0], sh[t], dh[v])",
+     "                                e = max(heads[0], sh[t])"),
+    ("ring successor is the predecessor",
+     "    return (x + 1) % n\n\n\ndef recovery_copies",
+     "    return (x - 1) % n\n\n\ndef recovery_copies"),
+    ("log chunks unpacked without the position shift",
+     "        unpack(dst, shifted(first, k * pos_step), log[k * w:(k + 1) * w], mode)",
+     "        unpack(dst, first, log[k * w:(k + 1) * w], mode)"),
+    ("FT6D packet width fixed at 8 words (wrong for non-16-bit words)",
+     "            x = 16 // self.elem_bytes\n            return (lp, rp, hp, d // x, s, d % x)",
+     "            x = 8\n            return (lp, rp, hp, d // x, s, d % x)"),
+    ("recovery: own cache of the successor instead of the predecessor",
+     '((x - 1) % n, x, "own_cache_of_prev")]',
+     '((x + 1) % n, x, "own_cache_of_prev")]'),
 ]
 
 

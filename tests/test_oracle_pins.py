@@ -558,3 +558,23 @@ def test_ft6d_key_layout_matches_fastertransformer_indexing():
         assert c.K[c.word_index(0, l, r, h, s_, d)] == K[l, r, h, s_, d]
     assert np.array_equal(pack(c, (0, L, 0, B, 1, 5), "brute"),
                           pack(Cache(K, V, 0, 0, H, S, D), (0, L, 0, B, 1, 5), "vector"))
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.uint32, np.uint64])
+def test_ft6d_packet_width_is_16_bytes_for_every_word_size(dtype):
+    """NEXT-1 for opaque words of 1/2/4/8 bytes: a FasterTransformer key packet is 16 BYTES, so it
+    holds x = 16/e words; the element (l,r,h,s,d) sits at [l][r][h][d//x][s][d%x]. K6 is built here
+    by explicit loops from that definition (independent of kvgen.as_ft6d_key and of the oracle)."""
+    e = np.dtype(dtype).itemsize
+    x = 16 // e
+    L, B, H, S, D = 2, 2, 2, 5, 2 * x
+    K = np.arange(L * B * H * S * D, dtype=np.uint64).astype(dtype).reshape(L, B, H, S, D)
+    V = (K + 1).astype(dtype)
+    K6 = np.zeros((L, B, H, D // x, S, x), dtype)
+    for l, r, h, s_, d in itertools.product(range(L), range(B), range(H), range(S), range(D)):
+        K6[l, r, h, d // x, s_, d % x] = K[l, r, h, s_, d]
+    c6 = Cache(K6, V, 0, 0, H, S, D, layout=LAYOUT_FT6D)
+    for l, r, h, s_, d in itertools.product(range(L), range(B), range(H), range(S), range(D)):
+        assert c6.K[c6.word_index(0, l, r, h, s_, d)] == K[l, r, h, s_, d]
+    reg = (0, L, 0, B, 1, 4)
+    assert np.array_equal(pack(c6, reg, "brute"), pack(Cache(K, V, 0, 0, H, S, D), reg, "vector"))
