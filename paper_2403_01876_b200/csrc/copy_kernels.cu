@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 ? DV_MIN_BLOCKS : 1))
 // in L2), arrives at the cluster barrier with release and waits with acquire; cluster rank 0's
 // thread 0 then holds every CTA's stores in its causality past and releases the flag at the
 // scope the destination needs (st.release.gpu for this GPU's HBM, st.release.sys otherwise).
-constexpr int kClusterCtas = 8;
+constexpr int kClusterCtas = 8;   // the portable cluster size (see cluster_ctas())
 template <int VEC, int U>
 __global__ void __launch_bounds__(1024) k_copy_cluster(const KParams p) {
   if (p.ts && threadIdx.x == 0) {
@@ -781,16 +781,47 @@ static cudaError_t launch_vec(const KParams& kp, int u, int max_ctas, cudaStream
 
 // Cluster form of a small released copy (DV_CLUSTER=1): one cluster of kClusterCtas CTAs, up to
 // 1024 threads each, U <= 4 vectors per thread. Returns cudaErrorNotSupported when it does not fit.
+// Cluster size of the small-copy publish: 16 CTAs (non-portable, allowed per kernel) when the
+// device accepts it, else the portable 8. Measured (tools/probe_latency.py, C2 layer into HBM):
+// 8 CTAs 3.23 us, 16 CTAs 2.78 us writer end -> flag. DV_CLUSTER_CTAS=8 forces the portable size.
+static int cluster_ctas() {
+  static const int n = [] {
+    const char* e = getenv("DV_CLUSTER_CTAS");
+    if (e && atoi(e) == 8) return 8;
+    bool ok = true;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<32, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    ok &= cudaFuncSetAttribute(k_copy_cluster<32, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    (void)cudaGetLastError();
+    return ok ? 16 : kClusterCtas;
+  }();
+  return n;
+}
 template <int VEC, int U>
 static cudaError_t go_cluster(const KParams& kp, int threads, cudaStream_t st) {
   (void)cudaGetLastError();
+  const int nc = cluster_ctas();
+  if (nc > 8) {   // the attribute is per device: set it on every device this process uses
+    static std::atomic<uint64_t> mask{0};
+    if (first_use_on_device(mask)) {
+      cudaFuncSetAttribute(k_copy_cluster<16, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_copy_cluster<16, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_copy_cluster<16, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_copy_cluster<32, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_copy_cluster<32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_copy_cluster<32, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kClusterCtas);
+  cfg.gridDim = dim3(nc);
   cfg.blockDim = dim3(threads);
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kClusterCtas;
+  at[0].val.clusterDim.x = nc;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -801,18 +832,19 @@ static cudaError_t go_cluster(const KParams& kp, int threads, cudaStream_t st) {
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
-static bool cluster_fits(uint64_t n_vec) { return n_vec <= (uint64_t)kClusterCtas * 1024 * 4; }
+static bool cluster_fits(uint64_t n_vec) { return n_vec <= (uint64_t)cluster_ctas() * 1024 * 4; }
 // Measured (tools/probe_latency.py, C2 layer 160 KiB = 5,120 vectors): into HBM (gpu-scope
-// release) writer end -> flag 3.55 -> 3.20 us; to pinned host (system scope) 6.02 -> 6.18 us (8 SMs
-// issue the PCIe stores more slowly); a 576 KiB peer put gets slower (ping-pong RTT 11.3 -> 12.5 us).
-// So by default only gpu-scope releases of <= one vector per thread of the cluster use it.
+// release) writer end -> flag 3.55 (ticket) -> 3.20 (8-CTA cluster) -> 2.78 us (16-CTA cluster); to
+// pinned host (system scope) 5.89 (ticket) / 6.05 (8) / 5.89 us (16) -- no gain, the PCIe flush
+// dominates; a 576 KiB peer put with 8 CTAs got slower (ping-pong RTT 11.3 -> 12.5 us). So by
+// default only gpu-scope releases of <= 8,192 vectors use it.
 static bool use_cluster(const KParams& kp) {
   const int c = tune().cluster;
   if (c == 2) return cluster_fits(kp.n_vec);
   return c == 1 && kp.pub == 3 && kp.n_vec <= (uint64_t)kClusterCtas * 1024;
 }
 static cudaError_t launch_cluster(const KParams& kp, int vec, cudaStream_t st) {
-  const uint64_t per_cta = (kp.n_vec + kClusterCtas - 1) / kClusterCtas;
+  const uint64_t per_cta = (kp.n_vec + cluster_ctas() - 1) / cluster_ctas();
   const int u = per_cta <= 1024 ? 1 : per_cta <= 2048 ? 2 : 4;
   const int threads = (int)std::min<uint64_t>(1024, ((per_cta + u - 1) / u + 31) / 32 * 32);
   if (vec == 32)
