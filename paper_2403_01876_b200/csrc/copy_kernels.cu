@@ -1149,6 +1149,7 @@ static void load_vec() {
   }
 }
 void preload_kernels() {
+  (void)cluster_ctas();   // decide the cluster size (and set the attribute) outside any capture
   load_fn(k_run_copy<16, 1, 32>);
   load_vec<16>();
   load_vec<32>();
