@@ -81,6 +81,14 @@ if __name__ == "__main__":
     print(f"# ncu summary {title}\n")
     print("## Launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold, serialised)\n")
     print(launches(tag) + "\n")
+    print("Reading the list: the command is `bench.py --steps 20 --warmup 3 --no-extras "
+          "--no-cpu-baseline`. Its TIMED region launches exactly one kernel per token step, the "
+          "200-CTA `k_run_copy<32, 4, 256>` pack (cache -> HBM staging, 6.55 MB); the step's bytes "
+          "then cross PCIe by copy-engine DMA, which ncu does not list. `k_fill` (writing the 13.4 GB "
+          "synthetic cache), the 16-CTA copies (preparing the e2e loop's host-side K/V) and `k_verify` "
+          "(every-word parity of the last 8 steps) run outside the timed region. Inside a step the pack "
+          "is ~4-5.5 us of ~119 us (3-5 %); the rest is the DMA, which is why the headline roofline "
+          "is the PCIe link.\n")
     print("## Top kernel, --set full\n")
     print(full(tag) + "\n")
     print("## DRAM / PCIe counters per launch\n")
