@@ -3,7 +3,7 @@
 #   bench line + ncu launch list + ncu --set full of the headline pack kernel + DRAM/PCIe counters
 #   (tools/gpu_round.sh), the per-config suite, latency stamps, the FT6D direction probe, the
 #   HBM-kernel ncu capture and the link probe. Outputs land in gpurun_out/ with the tag ${TAG}.
-T=${TAG:-r01e}
+T=${TAG:-r01f}
 mkdir -p gpurun_out
 TAG=$T bash tools/gpu_round.sh > gpurun_out/round_$T.log 2>&1
 timeout 900 python tools/bench_configs.py > gpurun_out/configs_$T.jsonl 2> gpurun_out/configs_$T.err
