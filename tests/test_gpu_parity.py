@@ -1138,3 +1138,30 @@ def test_region_tuples_equal_region_structs():
         assert torch.equal(dk, ek) and torch.equal(dvv, ev)
     with pytest.raises(ValueError):
         dv.dv_scatter(ctx(), c, (0, 1, 0, 1), dv.endpoint_of(a))
+
+
+def test_enomem_and_epeer_have_no_partial_effect():
+    """DV_ENOMEM: a staged transfer that must stage whole layer slabs (K in the FT6D layout, V in
+    KV5D: two plans, staged per layer slab) whose one-layer slab exceeds half the staging pool is
+    refused before anything is enqueued (the destination stays untouched); a single-plan copy
+    would instead be chunked by runs. DV_EPEER: exporting pinned host memory over CUDA IPC."""
+    L, B, H, S, D = 2, 4, 8, 64, 128          # one layer slab over [0, 64): 2*4*8*64*128*2 = 1 MiB
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=71)
+    k, v, c, o = _mk(K, V, 0, 0, ok.LAYOUT_FT6D)
+    cx = dv.dv_create(0, staging_bytes=1 << 20)
+    nbytes = ok.region_bytes(0, L, 0, B, 0, S, H, D, 2)
+    host = pinned_u16(nbytes // 2)
+    host.fill_(-1)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(cx, c, dv.region(0, L, 0, B, 0, S), dv.endpoint_of(host), xfer=dv.DV_XFER_STAGED)
+    assert ei.value.status == dv.DV_ENOMEM and "staging" in str(ei.value)
+    torch.cuda.synchronize()
+    assert bool((host == -1).all())
+    # the same call fused (no staging) succeeds and matches the oracle
+    dv.dv_scatter(cx, c, dv.region(0, L, 0, B, 0, S), dv.endpoint_of(host), xfer=dv.DV_XFER_FUSED)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(host), ok.pack(o, (0, L, 0, B, 0, S)))
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_ipc_export(host.data_ptr())
+    assert ei.value.status == dv.DV_EPEER
+    cx.close()
