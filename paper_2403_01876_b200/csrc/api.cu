@@ -478,6 +478,23 @@ static uint64_t pipe_chunk(uint64_t total, uint64_t half) {
   return std::min<uint64_t>(half, std::max<uint64_t>(4ull << 20, total / 8));
 }
 
+// Can the staged path move `reg` of cache `c` with this context's staging pool? A single run plan
+// is chunked by runs (one run must fit half the pool); two plans (K and V of different structure)
+// are staged per layer slab (one slab must fit half the pool).
+static bool staged_fits(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, const uint8_t* wire,
+                        bool pack) {
+  const int64_t row = row_bytes(c);
+  const uint64_t half = ctx->staging.capacity() / 2;
+  TView cv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  CopyPlan p[2];
+  const int np = pack ? build_plans(cv, wv, &reg, row, ORDER_WIRE, Outer{}, p)
+                      : build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np < 0) return true;   // let the staged path report it
+  if (np == 1 && p[0].run_bytes <= half) return true;
+  return layer_slab_bytes(&reg, row) <= half;
+}
+
 // Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
 // the kernel packs a group of layer slabs (or, with one plan, a range of runs) into staging, the
 // copy engine moves that contiguous piece to its place in the wire.
@@ -619,9 +636,14 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
   const dv_region reg = resolve_heads(&op.reg, c);
   const uint64_t bytes = region_bytes(&reg, c);
   const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
-  const uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
+  uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
   uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off;
   const int64_t row = row_bytes(c);
+  // AUTO picked staging but the pool cannot hold one layer slab of this region: the kernel's own
+  // stores move it instead (an explicit STAGED / DECOUPLED request still reports DV_ENOMEM)
+  if (mode == DV_XFER_STAGED && !(op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED | DV_XFER_DECOUPLED)) &&
+      !region_empty(&reg) && !staged_fits(ctx, c, reg, wire, true))
+    mode = DV_XFER_FUSED;
   if (mode == DV_XFER_FUSED || region_empty(&reg)) {
     CopyPlan p[2];
     int np = 0;
@@ -676,11 +698,20 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   const dv_cache* c = op.dst;
   const dv_region reg = resolve_heads(&op.reg, c);
   const uint64_t bytes = region_bytes(&reg, c);
+  uint32_t mode = bytes ? pick_xfer(op.xfer, op.src, bytes, true) : DV_XFER_FUSED;
+  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
+  // decided before anything is enqueued (no partial effect): AUTO falls back to the kernel's own
+  // loads when one layer slab does not fit half the staging pool; explicit STAGED reports it
+  if (mode == DV_XFER_STAGED && !staged_fits(ctx, c, reg, wire, false)) {
+    if (op.xfer & DV_XFER_STAGED)
+      return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+                  "dv_config.staging_bytes or DV_XFER_FUSED",
+                  (unsigned long long)layer_slab_bytes(&reg, row_bytes(c)));
+    mode = DV_XFER_FUSED;
+  }
   if (!(op.xfer & DV_NO_FLAG) && op.slot >= 0 && op.wait_seq)
     DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
   if (!bytes) return DV_OK;
-  const uint32_t mode = pick_xfer(op.xfer, op.src, bytes, true);
-  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
   if (mode == DV_XFER_STAGED) return staged_unpack(ctx, wire, c, reg, st);
   const int64_t row = row_bytes(c);
   TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};

@@ -1165,3 +1165,33 @@ def test_enomem_and_epeer_have_no_partial_effect():
         dv.dv_ipc_export(host.data_ptr())
     assert ei.value.status == dv.DV_EPEER
     cx.close()
+
+
+def test_auto_falls_back_to_kernel_copies_when_staging_cannot_hold_a_slab():
+    """AUTO picks staging for large host transfers (writes >= 32 MB, reads >= 4 MiB); with an FT6D
+    key (two plans, staged per layer slab) and a pool smaller than two slabs it must fall back to
+    the kernel's own PCIe stores / loads instead of failing -- bytes == the oracle. An explicit
+    STAGED request still reports DV_ENOMEM."""
+    L, B, H, S, D = 4, 8, 32, 128, 128       # 67 MB region, 16.8 MB per layer slab
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=73)
+    k, v, c, o = _mk(K, V, 0, 0, ok.LAYOUT_FT6D)
+    cx = dv.dv_create(0, staging_bytes=8 << 20)
+    reg = (0, L, 0, B, 0, S)
+    exp = ok.pack(o, reg)
+    host = pinned_u16(exp.size)
+    host.fill_(-1)
+    dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(host))            # AUTO
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(host), exp)
+    Ks, Vs = kvgen.sentinel_cache(L, B, H, S, D)
+    dk, dvv, dc, do = _mk(Ks, Vs, 0, 0, ok.LAYOUT_FT6D)
+    dv.dv_gather(cx, dv.endpoint_of(host), 0, dc, dv.region(*reg))           # AUTO read, 67 MB
+    torch.cuda.synchronize()
+    ok.unpack(do, reg, exp)
+    assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
+    for call in (lambda: dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(host), xfer=dv.DV_XFER_STAGED),
+                 lambda: dv.dv_gather(cx, dv.endpoint_of(host), 0, dc, dv.region(*reg), xfer=dv.DV_XFER_STAGED)):
+        with pytest.raises(dv.DVError) as ei:
+            call()
+        assert ei.value.status == dv.DV_ENOMEM
+    cx.close()
