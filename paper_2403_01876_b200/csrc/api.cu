@@ -480,7 +480,8 @@ static uint64_t pipe_chunk(uint64_t total, uint64_t half) {
 
 // Can the staged path move `reg` of cache `c` with this context's staging pool? A single run plan
 // is chunked by runs (one run must fit half the pool); two plans (K and V of different structure)
-// are staged per layer slab (one slab must fit half the pool).
+// are staged per layer slab, or per (layer, K or V) half-slab when a slab does not fit half the
+// pool (one half-slab must).
 static bool staged_fits(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, const uint8_t* wire,
                         bool pack) {
   const int64_t row = row_bytes(c);
@@ -492,7 +493,7 @@ static bool staged_fits(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, co
                       : build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return true;   // let the staged path report it
   if (np == 1 && p[0].run_bytes <= half) return true;
-  return layer_slab_bytes(&reg, row) <= half;
+  return layer_slab_bytes(&reg, row) / 2 <= half;   // per (layer, K or V) when a slab is too big
 }
 
 // Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
@@ -539,9 +540,38 @@ static dv_status staged_pack(dv_ctx* ctx, const dv_cache* c, const dv_region& re
     return finish();
   }
   const uint64_t slab = layer_slab_bytes(&reg, row);
-  if (slab > half)
-    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+  if (slab / 2 > half)
+    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds the staging pool; use a larger "
                 "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
+  if (slab > half) {
+    // one layer slab does not fit half the pool: stage per (layer, K or V) -- each half of a
+    // layer slab is contiguous in the wire ([l][kv][...]); one plan per tensor (the K plan may be
+    // a packet transpose, which moves a whole layer's key in one launch)
+    const uint64_t hs = slab / 2;
+    DV_TRY(hand_off(ctx, st, ds));
+    for (int32_t la = reg.layer_begin; la < reg.layer_end; ++la) {
+      dv_region sub = reg;
+      sub.layer_begin = la;
+      sub.layer_end = la + 1;
+      for (int kv = 0; kv < 2; ++kv) {
+        uint8_t* stg;
+        uint64_t off;
+        DV_TRY(ctx->staging.acquire(hs, st, &stg, &off));
+        // the wire view of tensor kv starts kv*hs into the layer: shift it back onto the staging
+        TView s2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
+        TView w2[2] = {wire_view(stg - kv * hs, 0, &sub, row), wire_view(stg - kv * hs, 1, &sub, row)};
+        CopyPlan ps[2];
+        if (build_plans(s2, w2, &sub, row, ORDER_WIRE, Outer{}, ps, kv) != 1)
+          return fail(DV_ENOTSUP, "copy not expressible");
+        DV_TRY(launch_copy(ps[0], 0, ps[0].runs(), none, ctx->max_ctas, st));
+        DV_TRY(hand_off(ctx, st, ds));
+        DV_DMA(cudaMemcpyAsync(wire + (uint64_t)(la - reg.layer_begin) * slab + kv * hs, stg, hs,
+                               cudaMemcpyDefault, ds));
+        DV_TRY(ctx->staging.release(off, hs, ds));
+      }
+    }
+    return finish();
+  }
   const int32_t per = (int32_t)std::max<uint64_t>(
       1, pipe_chunk((uint64_t)(reg.layer_end - reg.layer_begin) * slab, half) / slab);
   DV_TRY(hand_off(ctx, st, ds));
@@ -602,9 +632,33 @@ static dv_status staged_unpack(dv_ctx* ctx, const uint8_t* wire, const dv_cache*
     return DV_OK;
   }
   const uint64_t slab = layer_slab_bytes(&reg, row);
-  if (slab > half)
-    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+  if (slab / 2 > half)
+    return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds the staging pool; use a larger "
                 "dv_config.staging_bytes or DV_XFER_FUSED", (unsigned long long)slab);
+  if (slab > half) {   // per (layer, K or V), as in staged_pack
+    const uint64_t hs = slab / 2;
+    for (int32_t la = reg.layer_begin; la < reg.layer_end; ++la) {
+      dv_region sub = reg;
+      sub.layer_begin = la;
+      sub.layer_end = la + 1;
+      for (int kv = 0; kv < 2; ++kv) {
+        uint8_t* stg;
+        uint64_t off;
+        DV_TRY(ctx->staging.acquire(hs, ds, &stg, &off));
+        DV_DMA(cudaMemcpyAsync(stg, wire + (uint64_t)(la - reg.layer_begin) * slab + kv * hs, hs,
+                               cudaMemcpyDefault, ds));
+        DV_TRY(hand_off(ctx, ds, st));
+        TView w2[2] = {wire_view(stg - kv * hs, 0, &sub, row), wire_view(stg - kv * hs, 1, &sub, row)};
+        TView c2[2] = {cache_view(c, 0, &sub), cache_view(c, 1, &sub)};
+        CopyPlan ps[2];
+        if (build_plans(w2, c2, &sub, row, ORDER_WIRE, Outer{}, ps, kv) != 1)
+          return fail(DV_ENOTSUP, "copy not expressible");
+        DV_TRY(launch_copy(ps[0], 0, ps[0].runs(), none, ctx->max_ctas, st));
+        DV_TRY(ctx->staging.release(off, hs, st));
+      }
+    }
+    return DV_OK;
+  }
   const int32_t per = (int32_t)std::max<uint64_t>(
       1, pipe_chunk((uint64_t)(reg.layer_end - reg.layer_begin) * slab, half) / slab);
   for (int32_t la = reg.layer_begin; la < reg.layer_end; la += per) {
@@ -704,7 +758,7 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   // loads when one layer slab does not fit half the staging pool; explicit STAGED reports it
   if (mode == DV_XFER_STAGED && !staged_fits(ctx, c, reg, wire, false)) {
     if (op.xfer & DV_XFER_STAGED)
-      return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds half the staging pool; use a larger "
+      return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds the staging pool; use a larger "
                   "dv_config.staging_bytes or DV_XFER_FUSED",
                   (unsigned long long)layer_slab_bytes(&reg, row_bytes(c)));
     mode = DV_XFER_FUSED;

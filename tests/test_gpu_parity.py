@@ -1141,11 +1141,11 @@ def test_region_tuples_equal_region_structs():
 
 
 def test_enomem_and_epeer_have_no_partial_effect():
-    """DV_ENOMEM: a staged transfer that must stage whole layer slabs (K in the FT6D layout, V in
-    KV5D: two plans, staged per layer slab) whose one-layer slab exceeds half the staging pool is
+    """DV_ENOMEM: a staged transfer with K in the FT6D layout and V in KV5D (two plans: staged per
+    layer slab, or per (layer, K or V) half-slab) whose half-slab exceeds half the staging pool is
     refused before anything is enqueued (the destination stays untouched); a single-plan copy
     would instead be chunked by runs. DV_EPEER: exporting pinned host memory over CUDA IPC."""
-    L, B, H, S, D = 2, 4, 8, 64, 128          # one layer slab over [0, 64): 2*4*8*64*128*2 = 1 MiB
+    L, B, H, S, D = 2, 4, 8, 128, 128         # one layer slab over [0, 128): 2 MiB; half-slab 1 MiB
     K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=71)
     k, v, c, o = _mk(K, V, 0, 0, ok.LAYOUT_FT6D)
     cx = dv.dv_create(0, staging_bytes=1 << 20)
@@ -1194,4 +1194,31 @@ def test_auto_falls_back_to_kernel_copies_when_staging_cannot_hold_a_slab():
         with pytest.raises(dv.DVError) as ei:
             call()
         assert ei.value.status == dv.DV_ENOMEM
+    cx.close()
+
+
+
+@pytest.mark.parametrize("pool_mib", [24, 64])
+def test_staged_two_plan_copies_per_layer_or_per_half_slab(pool_mib):
+    """Staged FT6D transfers (two plans) move whole layer slabs when a slab fits half the pool
+    (64 MiB pool, 16.8 MB slab) and (layer, K or V) half-slabs when only a half fits (24 MiB pool):
+    scatter to and gather from pinned host, explicit STAGED and AUTO, == the oracle."""
+    L, B, H, S, D = 3, 8, 32, 128, 128
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=79)
+    k, v, c, o = _mk(K, V, 0, 0, ok.LAYOUT_FT6D)
+    cx = dv.dv_create(0, staging_bytes=pool_mib << 20)
+    reg = (0, L, 0, B, 2, 126)
+    exp = ok.pack(o, reg)
+    for xf in (dv.DV_XFER_STAGED, dv.DV_XFER_AUTO):
+        host = pinned_u16(exp.size)
+        host.fill_(-1)
+        dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(host), xfer=xf)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(host), exp)
+        Ks, Vs = kvgen.sentinel_cache(L, B, H, S, D)
+        dk, dvv, dc, do = _mk(Ks, Vs, 0, 0, ok.LAYOUT_FT6D)
+        dv.dv_gather(cx, dv.endpoint_of(host), 0, dc, dv.region(*reg), xfer=xf)
+        torch.cuda.synchronize()
+        ok.unpack(do, reg, exp)
+        assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
     cx.close()

@@ -359,6 +359,7 @@ def ft6d():
     (x = 8 fp16 words = one 16-byte packet): token step -> pinned host, prompt layer pack in HBM,
     and FT6D -> KV5D remap of a prompt layer (e.g. an FT prompt machine feeding a KV5D token one)."""
     L, H, D, B, P, S = 40, 40, 128, 8, 1000, 2048
+    ctx2 = dv.dv_create(0)   # the default 256 MB staging pool
     k6 = torch.empty((L, B, H, D // 8, S, 8), dtype=torch.int16, device=dev)
     v = torch.empty((L, B, H, S, D), dtype=torch.int16, device=dev)
     c = dv.cache(k6, v)
@@ -386,6 +387,15 @@ def ft6d():
     us = timed(prm, reps=10)
     emit(config="C2-FT6D", op="prompt_layer_pack_hbm (K transposed through 16-B packets)", bytes=nb, us=us,
          gbs_2R=2 * nb / us / 1e3, bound="hbm", frac=2 * nb / us / 1e3 / HBM)
+    # a prompt layer to pinned host: AUTO stages it per (layer, K or V) half-slab (163.8 MB > half the
+    # default 256 MB pool), against the kernel's own PCIe stores
+    hp = torch.empty(nb // 2, dtype=torch.int16, pin_memory=True)
+    hep = dv.endpoint_of(hp)
+    for name, xf in (("auto_staged_half_slabs", dv.DV_XFER_AUTO), ("fused", dv.DV_XFER_FUSED)):
+        us = timed(lambda xf=xf: dv.dv_scatter(ctx2, c, dv.region(lay[0], lay[0] + 1, 0, B, 0, P), hep, 0,
+                                               xfer=xf, stream=sp), reps=5)
+        emit(config="C2-FT6D", op=f"prompt_layer_to_host_{name}", bytes=nb, us=us, gbs=nb / us / 1e3, bound="pcie")
+    del hp
     k5 = torch.full((1, B, H, S, D), -1, dtype=torch.int16, device=dev)
     v5 = torch.full_like(k5, -1)
     c5 = dv.cache(k5, v5, 3, 0)
