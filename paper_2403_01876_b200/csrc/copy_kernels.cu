@@ -903,6 +903,16 @@ static cudaError_t launch_bulk(const KParams& kp, int vec, uint8_t* dst0, int ma
                    : launch_bulk_vec<16>(kp, dst0, max_ctas, st);
 }
 
+// Is `p` pinned (or otherwise host-resident) memory rather than device memory?
+static bool is_host_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
 static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* out) {
   TParams tp{};
   tp.src = p.src;
@@ -945,8 +955,14 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
                 (uint64_t)(uintptr_t)(p.tdir == 0 ? p.dst : p.src);
   for (int d = 0; d < 4; ++d) pm |= (uint64_t)(p.tdir == 0 ? tp.ds[d] : tp.ss[d]);
   const int want = tune().trs == 3 ? 2 : tune().trs == 2 ? 1 : tune().pk;
+  // Pinned host memory on either side: the shared-memory tile form, whose warps store (load)
+  // consecutive 16-byte packets of a position row -- whole 128-byte lines per warp instruction,
+  // which PCIe carries in full TLPs. The register form's per-thread 256-byte rows leave partial
+  // lines per instruction: C2 FT6D prompt layer to pinned host 35 GB/s (registers) vs 48-49 GB/s
+  // (tiles), tools/probe_ft6d_host_ctas.py. In HBM the register form is the faster one.
+  const bool host_side = tune().trs == 0 && (is_host_ptr(p.src) || is_host_ptr(p.dst));
   tp.pk = 0;
-  if (tune().trs != 1 && items1 < (1ull << 31)) {
+  if (tune().trs != 1 && !host_side && items1 < (1ull << 31)) {
     tp.pk = 1;
     for (int k = 16; k >= 2; k /= 2)
       if (want >= k && p.tU % k == 0 && pm % 32 == 0) {
