@@ -903,14 +903,18 @@ static cudaError_t launch_bulk(const KParams& kp, int vec, uint8_t* dst0, int ma
                    : launch_bulk_vec<16>(kp, dst0, max_ctas, st);
 }
 
-// Is `p` pinned (or otherwise host-resident) memory rather than device memory?
-static bool is_host_ptr(const void* p) {
+// Is `p` reached over a link (pinned host memory over PCIe, or another GPU's memory over NVLink)
+// rather than this GPU's own HBM?
+static bool over_link(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     (void)cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+  if (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered) return true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return at.type == cudaMemoryTypeDevice && at.device != dev;
 }
 
 static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* out) {
@@ -959,8 +963,10 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
   // consecutive 16-byte packets of a position row -- whole 128-byte lines per warp instruction,
   // which PCIe carries in full TLPs. The register form's per-thread 256-byte rows leave partial
   // lines per instruction: C2 FT6D prompt layer to pinned host 35 GB/s (registers) vs 48-49 GB/s
-  // (tiles), tools/probe_ft6d_host_ctas.py. In HBM the register form is the faster one.
-  const bool host_side = tune().trs == 0 && (is_host_ptr(p.src) || is_host_ptr(p.dst));
+  // (tiles), tools/probe_ft6d_host_ctas.py. In HBM the register form is the faster one. A peer
+  // GPU's memory is treated like the host's (NVLink is packetised like PCIe; not measurable on
+  // one GPU -- memory IPC-mapped from another process on the SAME GPU stays on the register form).
+  const bool host_side = tune().trs == 0 && (over_link(p.src) || over_link(p.dst));
   tp.pk = 0;
   if (tune().trs != 1 && !host_side && items1 < (1ull << 31)) {
     tp.pk = 1;
