@@ -40,15 +40,21 @@ CONFIG = {"workload": "C2 OPT-13B shape (L40 H40 D128, fp16 words) b8 p1000 S204
           "l2": "inputs larger than L2: 13.4 GB device cache, every step reads a fresh position "
                 "(new 256-B lines); host log ring 64 steps = 419 MB"}
 METRIC = "KV stream GB/s (token-step stream-out to pinned host)"
-HBM_PEAK = 6534.8   # MEASURED_PEAKS.json hbm_gbs (copy, read+write)
-
-
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f)
     except Exception:
         return {}
+
+
+# HBM roofline denominator (copy, read + write): the driver-written MEASURED_PEAKS.json of the box
+# when present; else the value that file held on this round's first box (6534.8 GB/s; the
+# profiling guide's own fallback is 6650)
+_HBM = _peaks().get("hbm_gbs")
+HBM_PEAK = float(_HBM) if _HBM else 6534.8
+HBM_PEAK_SOURCE = "MEASURED_PEAKS.json (this box)" if _HBM else \
+    "MEASURED_PEAKS.json hbm_gbs recorded earlier this round (file absent on this box)"
 
 
 class Clocks:
@@ -470,6 +476,8 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["token_step_pack_hbm_us"] = ms * 1e3
     ex["token_step_pack_hbm_gbs_2R"] = 2 * STEP_BYTES / ms / 1e6
     ex["token_step_pack_hbm_frac"] = ex["token_step_pack_hbm_gbs_2R"] / HBM_PEAK
+    ex["hbm_peak_gbs"] = HBM_PEAK
+    ex["hbm_peak_source"] = HBM_PEAK_SOURCE
     # the practical floor for a launch of this size: a contiguous 6.55 MB device-to-device copy
     # (cudaMemcpyAsync via torch), source ring larger than L2, same head start, back to back
     src_d = torch.empty(STEP_BYTES * 40, dtype=torch.uint8, device="cuda")   # 262 MB ring > L2
