@@ -437,6 +437,10 @@ struct ScatterOp {
   uint32_t xfer;
 };
 
+static dv_status staged_capacity_check(dv_ctx* ctx, uint32_t xfer, const dv_endpoint* ep,
+                                       const dv_cache* c, const dv_region& reg0, uint64_t off,
+                                       bool pack);
+
 static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
   DV_TRY(check_ctx(ctx));
   DV_TRY(check_cache(op.src, "source"));
@@ -446,8 +450,9 @@ static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
   if ((op.xfer & DV_XFER_DECOUPLED) && op.dst && op.dst->kind == DV_EP_HOST &&
       (!use_flag || op.slot < 0))
     return fail(DV_EINVAL, "DV_XFER_DECOUPLED needs a flag: the flag is its only completion signal");
-  return check_ep(op.dst, op.dst_off, region_bytes(&op.reg, op.src), op.slot, use_flag,
-                  "destination");
+  DV_TRY(check_ep(op.dst, op.dst_off, region_bytes(&op.reg, op.src), op.slot, use_flag,
+                  "destination"));
+  return staged_capacity_check(ctx, op.xfer, op.dst, op.src, op.reg, op.dst_off, true);
 }
 
 // Layer slabs of a region's wire: [l][...] -- slab l starts at (l - l0) * slab bytes.
@@ -494,6 +499,23 @@ static bool staged_fits(dv_ctx* ctx, const dv_cache* c, const dv_region& reg, co
   if (np < 0) return true;   // let the staged path report it
   if (np == 1 && p[0].run_bytes <= half) return true;
   return layer_slab_bytes(&reg, row) / 2 <= half;   // per (layer, K or V) when a slab is too big
+}
+
+// Validation-time capacity check (so a multi-piece call fails before enqueueing anything): an
+// EXPLICIT staged / decoupled host transfer whose staging unit does not fit the pool -> DV_ENOMEM.
+// (AUTO falls back to the kernel's own copies instead, in scatter_run / gather_run.)
+static dv_status staged_capacity_check(dv_ctx* ctx, uint32_t xfer, const dv_endpoint* ep,
+                                       const dv_cache* c, const dv_region& reg0, uint64_t off,
+                                       bool pack) {
+  if (!(xfer & (DV_XFER_STAGED | DV_XFER_DECOUPLED)) || (xfer & DV_XFER_FUSED)) return DV_OK;
+  const dv_region reg = resolve_heads(&reg0, c);
+  const uint64_t bytes = region_bytes(&reg, c);
+  if (!bytes || pick_xfer(xfer, ep, bytes, !pack) != DV_XFER_STAGED) return DV_OK;
+  const uint8_t* wire = (const uint8_t*)ep->base + off;
+  if (staged_fits(ctx, c, reg, wire, pack)) return DV_OK;
+  return fail(DV_ENOMEM, "one layer slab (%llu B) exceeds the staging pool; use a larger "
+              "dv_config.staging_bytes or DV_XFER_FUSED",
+              (unsigned long long)layer_slab_bytes(&reg, row_bytes(c)));
 }
 
 // Pack `reg` (heads resolved) of cache `c` into a wire chunk at `wire` through HBM staging:
@@ -745,7 +767,8 @@ static dv_status gather_check(dv_ctx* ctx, const GatherOp& op) {
   DV_TRY(check_region_shape(&op.reg));
   DV_TRY(check_cache_holds(op.dst, &op.reg, "destination"));
   const bool use_flag = !(op.xfer & DV_NO_FLAG);
-  return check_ep(op.src, op.src_off, region_bytes(&op.reg, op.dst), op.slot, use_flag, "source");
+  DV_TRY(check_ep(op.src, op.src_off, region_bytes(&op.reg, op.dst), op.slot, use_flag, "source"));
+  return staged_capacity_check(ctx, op.xfer, op.src, op.dst, op.reg, op.src_off, false);
 }
 
 static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
