@@ -154,7 +154,15 @@ typedef struct dv_endpoint {
   int32_t reserved;
 } dv_endpoint;
 
-/* Transfer-method flags for the data calls. DV_XFER_AUTO lets the library pick. */
+/* Transfer-method flags for the data calls. DV_XFER_AUTO lets the library pick (DESIGN.md §6
+ * "Transfer choice"): kernel stores for host writes < 32 MB, staged pipelined DMA above; kernel
+ * loads for host reads < 4 MiB, staged DMA above; kernel copies for device / peer memory. When AUTO
+ * picks staging but the pool cannot hold one staging unit (a run, a layer slab, or -- for K and V
+ * of different layouts -- a (layer, K or V) half-slab), AUTO uses the kernel's own copies; an
+ * explicit DV_XFER_STAGED / DV_XFER_DECOUPLED then fails with DV_ENOMEM before enqueueing anything.
+ * Flags are released by the copy kernel itself at the scope the memory needs: system scope when
+ * the payload or the flag is in pinned host or peer memory, GPU scope when both are this GPU's
+ * HBM (every reader of that memory is served by this GPU's L2). */
 enum {
   DV_XFER_AUTO = 0,
   DV_XFER_FUSED = 1u << 0,  /* SM kernel reads/writes the endpoint memory directly (zero-copy / P2P) */
