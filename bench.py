@@ -773,9 +773,10 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--peer-baseline", default="none", choices=["none", "nccl"],
                     help="c3/c5: run the NCCL send/recv baseline (pack -> ncclSend/ncclRecv -> unpack) instead of dvstream's peer stores")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2 (default, BASELINE configs[1]): token steps -> pinned host; "
-                         "c3: prompt->token disaggregation over NVLink; c5: ring replication over NVLink")
+                         "c3: prompt->token disaggregation over NVLink; c4: microbatch swap over PCIe; "
+                         "c5: ring replication over NVLink")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
@@ -784,6 +785,9 @@ def main():
         run_reference(args)
     elif args.workload == "c2":
         run_ours(args)
+    elif args.workload == "c4":
+        from tools import bench_swap
+        bench_swap.run_c4(args, sys.modules[__name__])
     else:
         from tools import bench_peer
         (bench_peer.run_c3 if args.workload == "c3" else bench_peer.run_c5)(args, sys.modules[__name__])

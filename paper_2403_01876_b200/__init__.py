@@ -344,16 +344,16 @@ def dv_stats():
 
 def dv_region_bytes(reg: dv_region, n_heads, head_dim, elem_bytes) -> int:
     out = C.c_uint64()
-    _call("dv_region_bytes", C.byref(reg), n_heads, head_dim, elem_bytes, C.byref(out))
+    _call("dv_region_bytes", _reg_ct(reg), n_heads, head_dim, elem_bytes, C.byref(out))
     return out.value
 
 
 def dv_route(src: Setup, dst: Setup, reg: dv_region, n_heads, head_dim, elem_bytes):
     n = C.c_uint64()
-    _call("dv_route", C.byref(src.c), C.byref(dst.c), C.byref(reg), n_heads, head_dim, elem_bytes,
+    _call("dv_route", C.byref(src.c), C.byref(dst.c), _reg_ct(reg), n_heads, head_dim, elem_bytes,
           None, 0, C.byref(n))
     arr = (dv_piece * max(1, n.value))()
-    _call("dv_route", C.byref(src.c), C.byref(dst.c), C.byref(reg), n_heads, head_dim, elem_bytes,
+    _call("dv_route", C.byref(src.c), C.byref(dst.c), _reg_ct(reg), n_heads, head_dim, elem_bytes,
           arr, n.value, C.byref(n))
     return [arr[i] for i in range(n.value)]
 
@@ -487,7 +487,7 @@ def dv_gather(ctx, src: dv_endpoint, src_off, dst: dv_cache, reg: dv_region, fla
 
 def dv_gather_chunks(ctx, src: dv_endpoint, src_off, dst: dv_cache, first: dv_region, n_chunks, pos_step,
                      flag_slot=-1, wait_seq=0, xfer=0, stream=None):
-    _call("dv_gather_chunks", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), C.byref(first),
+    _call("dv_gather_chunks", ctx.h, C.byref(src), src_off, flag_slot, wait_seq, C.byref(dst), _reg_ct(first),
           n_chunks, pos_step, xfer, _stream(stream))
 
 
@@ -504,13 +504,13 @@ def dv_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpo
 
 def dv_scatter_dyn(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off, dst_step_bytes, d_step_ptr,
                    max_step, flag_slot=-1, seq=0, stream=None):
-    _call("dv_scatter_dyn", ctx.h, C.byref(src), C.byref(reg), C.byref(dst), dst_off, dst_step_bytes, flag_slot,
+    _call("dv_scatter_dyn", ctx.h, C.byref(src), _reg_ct(reg), C.byref(dst), dst_off, dst_step_bytes, flag_slot,
           seq, C.c_void_p(d_step_ptr), max_step, _stream(stream))
 
 
 def dv_remap_dyn(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, d_step_ptr, max_step, signal: dv_endpoint = None,
                  flag_slot=-1, seq=0, stream=None):
-    _call("dv_remap_dyn", ctx.h, C.byref(src), C.byref(dst), C.byref(reg), _ref(signal), flag_slot, seq,
+    _call("dv_remap_dyn", ctx.h, C.byref(src), C.byref(dst), _reg_ct(reg), _ref(signal), flag_slot, seq,
           C.c_void_p(d_step_ptr), max_step, _stream(stream))
 
 
@@ -518,13 +518,13 @@ def dv_remap_dyn(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, d_step_ptr, 
 def dv_stream_out(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
                   dst_setup: Setup, inboxes, seq, xfer=0, stream=None, my_tp=0):
     arr = endpoint_array(inboxes)
-    _call("dv_stream_out", ctx.h, C.byref(src), C.byref(reg), C.byref(src_setup.c), my_stage, my_micro,
+    _call("dv_stream_out", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage, my_micro,
           my_tp, C.byref(dst_setup.c), arr, len(inboxes), seq, xfer, _stream(stream))
 
 
 def dv_stream_in(ctx, dst: dv_cache, reg: dv_region, src_setup: Setup, dst_setup: Setup, my_stage,
                  my_micro, inbox: dv_endpoint, wait_seq, xfer=0, stream=None, my_tp=0):
-    _call("dv_stream_in", ctx.h, C.byref(dst), C.byref(reg), C.byref(src_setup.c), C.byref(dst_setup.c),
+    _call("dv_stream_in", ctx.h, C.byref(dst), _reg_ct(reg), C.byref(src_setup.c), C.byref(dst_setup.c),
           my_stage, my_micro, my_tp, C.byref(inbox), wait_seq, xfer, _stream(stream))
 
 
@@ -566,7 +566,7 @@ def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
 def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_region = None, stream=None,
              t_end_ptr=0):
     b = (C.c_int32 * 5)(*box) if box is not None else None
-    _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], _ref(reg), C.c_void_p(t_end_ptr),
+    _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], (None if reg is None else _reg_ct(reg)), C.c_void_p(t_end_ptr),
           _stream(stream))
 
 
@@ -575,7 +575,7 @@ def dvt_verify(c: dv_cache, counter_ptr, seed=0, kind=0, reg: dv_region = None, 
     """Adds to the uint64 at counter_ptr (device) the words of `reg` (in cache c, or in the dense
     wire at wire_ptr) that differ from the generator (dvt_fill's word)."""
     b = (C.c_int32 * 5)(*box) if box is not None else None
-    _call("dvt_verify", C.byref(c), C.c_void_p(wire_ptr), kind, seed, b, valid[0], valid[1], _ref(reg),
+    _call("dvt_verify", C.byref(c), C.c_void_p(wire_ptr), kind, seed, b, valid[0], valid[1], (None if reg is None else _reg_ct(reg)),
           C.c_void_p(counter_ptr), _stream(stream))
 
 
@@ -605,12 +605,12 @@ def dvt_spin(ns, ctas, stream=None):
 
 def dvb_per_run_copy(src: dv_cache, reg: dv_region, dst_ptr, stream=None) -> int:
     n = C.c_uint64()
-    _call("dvb_per_run_copy", C.byref(src), C.byref(reg), C.c_void_p(dst_ptr), _stream(stream), C.byref(n))
+    _call("dvb_per_run_copy", C.byref(src), _reg_ct(reg), C.c_void_p(dst_ptr), _stream(stream), C.byref(n))
     return n.value
 
 
 def dvb_buffered_copy(src: dv_cache, reg: dv_region, staging_ptr, dst_ptr, stream=None) -> int:
     n = C.c_uint64()
-    _call("dvb_buffered_copy", C.byref(src), C.byref(reg), C.c_void_p(staging_ptr), C.c_void_p(dst_ptr),
+    _call("dvb_buffered_copy", C.byref(src), _reg_ct(reg), C.c_void_p(staging_ptr), C.c_void_p(dst_ptr),
           _stream(stream), C.byref(n))
     return n.value

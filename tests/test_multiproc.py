@@ -76,11 +76,11 @@ def test_bench_multirank_launch_path():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("workload,world", [("c5", 1), ("c5", 2), ("c3", 1), ("c3", 2)])
+@pytest.mark.parametrize("workload,world", [("c5", 1), ("c5", 2), ("c3", 1), ("c3", 2), ("c4", 1), ("c4", 2)])
 def test_bench_peer_workloads(workload, world):
-    """bench.py --workload c3/c5 (the NVLink peer paths: CUDA-IPC-mapped destinations, seq flags):
-    loopback at N=1, and 2 ranks (both on the one available GPU, gloo plumbing) at N=2; the
-    sampled parity of the delivered KV must be clean."""
+    """bench.py --workload c3/c5 (the NVLink peer paths: CUDA-IPC-mapped destinations, seq flags)
+    and c4 (the PCIe swap path): loopback at N=1, and 2 ranks (both on the one available GPU, gloo
+    plumbing) at N=2; the parity of the delivered KV must be clean."""
     import json
     root = os.path.dirname(HERE)
     env = dict(os.environ, DV_BENCH_SAME_DEVICE="1")
