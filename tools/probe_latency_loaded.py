@@ -1,0 +1,56 @@
+"""Per-layer token latency INTO HBM (gpu-scope release) while the GPU is busy: a bf16 GEMM loop
+runs on a low-priority stream; writer + stream-out run on a high-priority stream (the NEXT-2
+recommendation). Compares the publish forms under load (DV_CLUSTER=0 ticket, 1 cluster): a
+cluster must be co-scheduled on SMs of one GPC, the ticket form's CTAs can start anywhere."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2403_01876_b200 as dv  # noqa: E402
+
+L, H, D, B, P, S = 40, 40, 128, 8, 1000, 2048
+LAYER = 2 * B * H * D * 2
+k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
+v = torch.empty_like(k)
+cache = dv.cache(k, v)
+ctx = dv.dv_create(0)
+dlog = torch.empty(LAYER // 2 * L, dtype=torch.int16, device="cuda")
+dfl = torch.zeros(1, dtype=torch.int64, device="cuda")
+ep = dv.endpoint_of(dlog, dfl)
+lo, hi = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+bm = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+n = 400
+for i in range(2 * L):   # warm every kernel first (lazy loading, first-use costs)
+    reg = (i % L, i % L + 1, 0, B, P, P + 1)
+    dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=1, reg=reg, stream=hi.cuda_stream)
+    dv.dv_scatter(ctx, cache, reg, ep, (i % L) * LAYER, flag_slot=0, seq=10 ** 7 + i, stream=hi.cuda_stream)
+torch.matmul(a, bm)
+torch.cuda.synchronize()
+for loaded in (False, True):
+    te = torch.zeros(n, dtype=torch.int64, device="cuda")
+    ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
+    ts[:, 1:3] = 2 ** 63 - 1
+    torch.cuda.synchronize()
+    if loaded:
+        with torch.cuda.stream(lo):
+            for _ in range(120):
+                torch.matmul(a, bm)
+    dv.dvt_spin(20_000_000, 1, stream=hi.cuda_stream)
+    for i in range(n):
+        layer = i % L
+        q = P + 1 + i // L
+        reg = (layer, layer + 1, 0, B, q, q + 1)
+        dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=1, reg=reg, stream=hi.cuda_stream, t_end_ptr=te[i].data_ptr())
+        dv.dvt_trace(ctx, ts[i].data_ptr())
+        dv.dv_scatter(ctx, cache, reg, ep, layer * LAYER, flag_slot=0, seq=10 ** 8 * (2 if loaded else 1) + i,
+                      stream=hi.cuda_stream)
+    dv.dvt_trace(ctx, 0)
+    torch.cuda.synchronize()
+    d = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
+    print(json.dumps({"cluster": os.environ.get("DV_CLUSTER", "1"), "ctas": os.environ.get("DV_CLUSTER_CTAS", "16"),
+                      "loaded": loaded, "p50_us": round(d[len(d) // 2], 3), "p99_us": round(d[int(len(d) * 0.99)], 3)}),
+          flush=True)
