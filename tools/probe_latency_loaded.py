@@ -17,8 +17,9 @@ k = torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda")
 v = torch.empty_like(k)
 cache = dv.cache(k, v)
 ctx = dv.dv_create(0)
-dlog = torch.empty(LAYER // 2 * L, dtype=torch.int16, device="cuda")
-dfl = torch.zeros(1, dtype=torch.int64, device="cuda")
+HOST = os.environ.get("DST") == "host"   # DST=host: the pinned-host destination (system scope)
+dlog = torch.empty(LAYER // 2 * L, dtype=torch.int16, device="cpu" if HOST else "cuda", pin_memory=HOST)
+dfl = torch.zeros(1, dtype=torch.int64, device="cpu" if HOST else "cuda", pin_memory=HOST)
 ep = dv.endpoint_of(dlog, dfl)
 lo, hi = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
 a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
@@ -51,6 +52,6 @@ for loaded in (False, True):
     dv.dvt_trace(ctx, 0)
     torch.cuda.synchronize()
     d = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
-    print(json.dumps({"cluster": os.environ.get("DV_CLUSTER", "1"), "ctas": os.environ.get("DV_CLUSTER_CTAS", "16"),
+    print(json.dumps({"dst": "host" if HOST else "hbm", "cluster": os.environ.get("DV_CLUSTER", "1"), "ctas": os.environ.get("DV_CLUSTER_CTAS", "16"),
                       "loaded": loaded, "p50_us": round(d[len(d) // 2], 3), "p99_us": round(d[int(len(d) * 0.99)], 3)}),
           flush=True)
