@@ -281,7 +281,7 @@ def run_ours(args):
         roof = {"bound": "pcie", "achieved": ach, "peak": pcie_peak, "unit": "GB/s",
                 "frac": ach / pcie_peak if pcie_peak else None,
                 "traffic": dram_traffic,
-                "traffic_source": "profiles/r01f_io_counters.csv: ncu dram__bytes_read+write "
+                "traffic_source": "profiles/r01g_io_counters.csv: ncu dram__bytes_read+write "
                                   "per launch of the pack kernel (HBM side; the copy engine's PCIe "
                                   "bytes are not a kernel counter), median",
                 "kernel": "copy-engine D2H of the packed step (cudaMemcpyAsync on the library DMA "
@@ -345,7 +345,7 @@ def _ncu_traffic(name="final"):
     (profiles/r01_io_counters_<name>.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
     pcie__write_bytes.sum on this same command), median over the captured launches."""
     import csv
-    path = os.path.join(ROOT, "profiles", {"decoupled": "r01f_io_counters.csv"}.get(name, f"r01_io_counters_{name}.csv"))
+    path = os.path.join(ROOT, "profiles", {"decoupled": "r01g_io_counters.csv"}.get(name, f"r01_io_counters_{name}.csv"))
     try:
         rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
     except OSError:
