@@ -10,6 +10,8 @@ Launch order (each preceded by one warm-up call that ncu also sees):
   4. FT6D prompt layer pack: K transpose + V run copy in one k_transpose_run launch
   5. one C2 token-layer (160 KiB) into HBM with a seq flag: k_copy_cluster (gpu-scope release)
   6. the same to pinned host with a seq flag: k_run_copy + system-scope release (PCIe stores)
+  7. a C2-shaped 9-layer swap-in slice read from a pinned host log with the kernel's own loads
+     (fused gather, 16 host CTAs): PCIe read bytes vs payload
 """
 import os
 import sys
@@ -63,6 +65,12 @@ def main():
     for i in range(2):
         dv.dv_scatter(ctx, c6, dv.region(1, 2, 0, B, P, P + 1), dv.endpoint_of(host, hfl), 0, flag_slot=0,
                       seq=1 + i)
+    torch.cuda.synchronize()
+    reg7 = (0, 2, 0, B, 1000, 1064)                       # 2 layers x 64 positions = 10.5 MB
+    nb7 = 2 * 2 * B * H * 64 * D * 2
+    hlog = torch.zeros(nb7 // 2, dtype=torch.int16, pin_memory=True)
+    for _ in range(2):
+        dv.dv_gather(ctx, dv.endpoint_of(hlog), 0, c6, reg7, xfer=dv.DV_XFER_FUSED)
     torch.cuda.synchronize()
     ctx.close()
 
