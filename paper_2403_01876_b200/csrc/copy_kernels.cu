@@ -65,8 +65,21 @@ struct alignas(VEC) Vec {
   uint32_t w[VEC / 4];
 };
 
+// DV_LD_PREFETCH=N (build-time experiment, N = 64/128/256): .L2::NB prefetch-size hint on the loads.
+#ifndef DV_LD_PREFETCH
+#define DV_LD_PREFETCH 0
+#endif
+#if DV_LD_PREFETCH == 256
+#define DV_LDQ ".L2::256B"
+#elif DV_LD_PREFETCH == 128
+#define DV_LDQ ".L2::128B"
+#elif DV_LD_PREFETCH == 64
+#define DV_LDQ ".L2::64B"
+#else
+#define DV_LDQ ""
+#endif
 __device__ __forceinline__ void ld_vec(Vec<16>& v, const uint8_t* p) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate" DV_LDQ ".v4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3])
                : "l"(p));
 }
@@ -111,7 +124,7 @@ __device__ __forceinline__ void st_vec(uint8_t* p, const Vec<16>& v) {
                : "memory");
 }
 __device__ __forceinline__ void ld_vec(Vec<32>& v, const uint8_t* p) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc.L1::no_allocate" DV_LDQ ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]),
                  "=r"(v.w[5]), "=r"(v.w[6]), "=r"(v.w[7])
                : "l"(p));
