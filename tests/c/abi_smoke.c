@@ -6,7 +6,7 @@
  *
  *   build:  gcc -O2 -I include tests/c/abi_smoke.c -L paper_2403_01876_b200 -ldvstream
  *           -Wl,-rpath,paper_2403_01876_b200 -o tests/c/abi_smoke   (done by __graft_entry__.build)
- *   run:    tests/c/abi_smoke [--route-only]
+ *   run:    tests/c/abi_smoke [--route-only | --enqueue-bench | --token-bench]
  * Exit code 0 = pass.
  */
 #define _POSIX_C_SOURCE 199309L
@@ -208,10 +208,55 @@ static int enqueue_bench(void) {
   return 0;
 }
 
+/* The headline workload from plain C: C2 token steps (40 layers x 8 requests x 40 heads x one
+ * position x head_dim 128, fp16 words = 6,553,600 B) streamed to a pinned host log with
+ * DV_XFER_DECOUPLED and a seq flag per step; wall time from the first call to the last flag seen
+ * by dv_query. The cache content is whatever dv_device_alloc returned (bytes are opaque). */
+static double now_s(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return t.tv_sec + t.tv_nsec * 1e-9;
+}
+static int token_bench(void) {
+  const int L = 40, B = 8, H = 40, S = 2048, D = 128, RING = 64, N = 500, W = 10;
+  const uint64_t step = 2ull * L * B * H * D * 2;
+  dv_ctx* ctx;
+  CHECK(dv_create(0, NULL, &ctx));
+  void *k, *v, *log;
+  const size_t n = (size_t)L * B * H * S * D * 2;
+  CHECK(dv_device_alloc(0, n, &k));
+  CHECK(dv_device_alloc(0, n, &v));
+  CHECK(dv_host_alloc_near(0, step * RING, &log, NULL));
+  uint64_t* fl;
+  CHECK(dv_host_alloc(64, (void**)&fl));
+  memset(fl, 0, 64);
+  dv_cache c = {k, v, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S, D, 0};
+  dv_endpoint ep = {DV_EP_HOST, -1, log, step * RING, fl, 1, 0};
+  double t0 = 0;
+  for (int t = 1; t <= W + N; ++t) {
+    if (t == W + 1) {
+      int32_t done = 0;
+      while (!done) CHECK(dv_query(ctx, &ep, 0, (uint64_t)W, &done));
+      t0 = now_s();
+    }
+    const int32_t q = 1000 + t % 1000;
+    dv_region r = {0, L, 0, B, q, q + 1, 0, 0};
+    CHECK(dv_scatter(ctx, &c, &r, &ep, (uint64_t)(t % RING) * step, 0, (uint64_t)t, DV_XFER_DECOUPLED, NULL));
+  }
+  int32_t done = 0;
+  while (!done) CHECK(dv_query(ctx, &ep, 0, (uint64_t)(W + N), &done));
+  const double dt = now_s() - t0;
+  printf("{\"c2_token_steps_from_C_gbs\": %.2f, \"us_per_step\": %.2f, \"steps\": %d}\n",
+         N * (double)step / dt / 1e9, dt / N * 1e6, N);
+  CHECK(dv_destroy(ctx));
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (dv_abi_version() != DV_ABI_VERSION) return 1;
   if (route_check()) return 1;
   if (argc > 1 && !strcmp(argv[1], "--route-only")) return 0;
   if (argc > 1 && !strcmp(argv[1], "--enqueue-bench")) return enqueue_bench();
+  if (argc > 1 && !strcmp(argv[1], "--token-bench")) return token_bench();
   return stream_check();
 }

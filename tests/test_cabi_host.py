@@ -196,3 +196,16 @@ def test_c_program_streams_through_the_abi():
     exe = os.path.join(ROOT, "tests", "c", "abi_smoke")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "stream ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_c_program_runs_the_headline_token_steps():
+    """The headline workload driven from plain C through the ABI alone (decoupled C2 token steps to
+    pinned host, completion by the flags): it runs to the last flag and reports its rate."""
+    import json
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "c", "abi_smoke")
+    r = subprocess.run([exe, "--token-bench"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["steps"] == 500 and d["c2_token_steps_from_C_gbs"] > 0
