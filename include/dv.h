@@ -242,7 +242,10 @@ DV_API dv_status dv_device_free(void* p);
 DV_API dv_status dv_peer_enable(int32_t device, int32_t peer);
 
 typedef struct dv_ipc_blob { uint8_t bytes[96]; } dv_ipc_blob; /* opaque, copyable between processes */
-/* Export device memory at `ptr` (any address inside a cudaMalloc allocation). */
+/* Export device memory at `ptr` (any address inside a cudaMalloc allocation -- legacy CUDA IPC;
+ * memory from the virtual-memory API, e.g. PyTorch with expandable_segments, or from
+ * cudaMallocAsync pools cannot be exported this way: use dv_device_alloc or plain cudaMalloc for
+ * inboxes, replica stores and flags that other processes map). DV_EPEER on failure. */
 DV_API dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out);
 /* Map a blob exported by another process (same or other GPU) into this process; returns the
  * address corresponding to the exported `ptr`. Same-process blobs map to the original pointer. */
