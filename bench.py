@@ -161,7 +161,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     st_all, en_all = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0, _ = dv.dv_stats()
+    l0, dma0 = dv.dv_stats()
     st_all.record(stream)
     h0 = time.perf_counter()
     for i in range(args.steps):
@@ -307,6 +307,7 @@ def run_ours(args):
                        "(H2D + unpack, input stream) then dv_scatter to the pinned-host log (pack + D2H, "
                        "main stream); step t+1's H2D overlaps step t's D2H (PCIe full duplex)"},
         "gpu_launches": int(launches),
+        "copy_engine_dmas": int(dma1 - dma0),   # library cudaMemcpyAsync calls in the timed region
         "host_enqueue_us_per_step": {"value": host_us, "e2e": host_e2e_us},
         "roofline": roof,
         "clocks": clk,
