@@ -219,7 +219,9 @@ DV_API dv_status dv_route(const dv_setup* src, const dv_setup* dst, const dv_reg
 /* One context per (process, device). Owns the staging pool, the release tickets and the CUDA
  * driver entry points it needs. `cfg` may be NULL. Loads every library kernel on `device` up front:
  * under CUDA lazy loading a first launch would otherwise wait for the device, and a consumer
- * kernel already spinning on one of our flags would block the very stream-out it waits for. */
+ * kernel already spinning on one of our flags would block the very stream-out it waits for.
+ * DV_ECUDA without a usable GPU (no CPU fallback); DV_ENOTSUP on a GPU other than sm_100 (B200):
+ * the kernels are built for sm_100a only. */
 DV_API dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out);
 DV_API dv_status dv_destroy(dv_ctx* ctx); /* synchronises the device, frees library-owned memory */
 

@@ -919,6 +919,14 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
     return fail(DV_ECUDA, "no CUDA device available (dvstream has no CPU fallback): %s",
                 cudaGetErrorString(e));
   if (device < 0 || device >= n) return fail(DV_EINVAL, "device %d out of range [0,%d)", device, n);
+  {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0)   // the kernels are built for sm_100a only (B200)
+      return fail(DV_ENOTSUP, "device %d is sm_%d%d; libdvstream is built for sm_100a (B200) only",
+                  device, major, minor);
+  }
   const Driver* d;
   DV_TRY(driver(&d));
   DV_ON_DEVICE(device);
