@@ -1,6 +1,7 @@
 """Seeded random differential test: hundreds of random operations (level 1/2, KV5D/FT6D on either
 side, TP head ranges, fused/staged/auto, device/host endpoints, log chunks, graph-style dynamic
 steps) through the C ABI, each compared word for word with the CPU oracle."""
+import os
 import random
 
 import numpy as np
@@ -49,14 +50,18 @@ def rand_region(rng, lb, nl, rb, nr, hb, nh, S):
     return (l0, l1, r0, r1, s0, s1, h0, h1)
 
 
-@pytest.mark.parametrize("block", range(18))
+# DV_FUZZ_SCALE=k multiplies the number of seeded blocks (a long stress run; default 1)
+_SCALE = max(1, int(os.environ.get("DV_FUZZ_SCALE", "1")))
+
+
+@pytest.mark.parametrize("block", list(range(18)) + list(range(1000, 1000 + 18 * (_SCALE - 1))))
 def test_random_ops_against_oracle(block):
     """Blocks 12..17 draw the less common head dims: 8 (one 16-byte packet), 40 / 80 (5 / 10
     packets: odd register-transpose groups, PK 1 / 2), 96 (PK 4) and 256 (32 packets, PK 16 x 2)."""
     rng = random.Random(12345 + block)
     cx = dv.dv_create(0, staging_bytes=rng.choice([1 << 20, 8 << 20, 0]))
     for it in range(40):
-        D = rng.choice([16, 64, 128] if block < 12 else [8, 40, 80, 96, 256])
+        D = rng.choice([16, 64, 128] if (block < 12 or (block >= 1000 and block % 3)) else [8, 40, 80, 96, 256])
         nl, nr, nh = rng.randint(1, 4), rng.randint(1, 3), rng.randint(1, 5)
         lb, rb, hb = rng.randint(0, 5), rng.randint(0, 5), rng.randint(0, 3)
         S = rng.randint(4, 48)
@@ -118,7 +123,7 @@ def _bounds(rng, lo, hi, k):
     return [lo] + cuts + [hi]
 
 
-@pytest.mark.parametrize("block", range(8))
+@pytest.mark.parametrize("block", list(range(8)) + list(range(1000, 1000 + 8 * (_SCALE - 1))))
 def test_random_stream_out_in_against_oracle(block):
     """Random pipeline setups on both sides (layer partitions, microbatch splits, optional TP head
     splits, either cache layout per block), inbox (device or pinned host) or direct form."""
