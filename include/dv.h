@@ -177,7 +177,13 @@ enum {
                                   waits on the flag). Successive steps then overlap step t's DMA
                                   with step t+1's pack. Requires a flag (flag_slot >= 0, no
                                   DV_NO_FLAG); with AUTO it selects STAGED. Ignored for device and
-                                  peer endpoints (the caller's stream already covers them).     */
+                                  peer endpoints (the caller's stream already covers them). A
+                                  slot may mix modes: once a context has published decoupled
+                                  flags, its other publishes to pinned-host flags are ordered
+                                  after them (an empty decoupled region publishes on the flag
+                                  stream too), so a slot's seq never runs ahead of a DMA in
+                                  flight -- except for launches captured into a CUDA graph, which
+                                  the caller orders after earlier decoupled transfers.          */
   DV_NO_FLAG = 1u << 8      /* do not publish / wait on sequence flags                           */
 };
 

@@ -105,16 +105,21 @@ dv_status Staging::acquire(uint64_t n, cudaStream_t stream, uint8_t** out, uint6
                             (unsigned long long)cap_);
   if (head_ + n > cap_) head_ = 0;
   const uint64_t a = head_, b = head_ + n;
-  // records are in allocation order; wait for (and retire) every one overlapping [a, b)
+  // Wait for every record overlapping [a, b). Retire only the records [a, b) covers entirely: the
+  // record this acquisition's release() adds is ordered after them and stands in for them. A
+  // partly covered record stays: another stream may later acquire its uncovered rest, and must
+  // still wait for the work that reads or writes it.
   for (auto it = recs_.begin(); it != recs_.end();) {
     if (it->off < b && a < it->off + it->len) {
       cudaError_t e = cudaStreamWaitEvent(stream, it->ev, 0);
       if (e != cudaSuccess) return cuda_fail(e, "staging wait");
-      free_ev_.push_back(it->ev);
-      it = recs_.erase(it);
-    } else {
-      ++it;
+      if (a <= it->off && it->off + it->len <= b) {
+        free_ev_.push_back(it->ev);
+        it = recs_.erase(it);
+        continue;
+      }
     }
+    ++it;
   }
   head_ = b;
   *out = base_ + a;
@@ -343,20 +348,32 @@ static bool local_vidmem(const dv_ctx* ctx, const void* p) {
 // The release of a fused copy: the endpoint's flag, a ticket, and the scope. Payload (the plans'
 // destinations) and flag all in this GPU's HBM -> a gpu-scope release suffices (publish() protocol
 // 3); anything in pinned host or peer memory -> system scope.
-static Release ticket_release(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
-                              bool use_flag, const CopyPlan* p, int np) {
+static dv_status ticket_release(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
+                                bool use_flag, const CopyPlan* p, int np, cudaStream_t st,
+                                Release* out) {
   Release r{nullptr, 0, nullptr};
   if (use_flag && slot >= 0 && ep && ep->flags) {
     r.flag = (unsigned long long*)&ep->flags[slot];
     r.seq = seq;
-    r.ticket = ctx->tickets + (ctx->next_ticket.fetch_add(1) % dv_ctx::kTickets);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    DV_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) {  // a graph keeps this ticket: never hand it out again
+      const uint32_t g = ctx->next_graph_ticket.fetch_add(1);
+      if (g >= dv_ctx::kGraphTickets)
+        return fail(DV_ENOMEM, "more than %u publishing launches captured into CUDA graphs by this "
+                    "context", dv_ctx::kGraphTickets);
+      r.ticket = ctx->tickets + dv_ctx::kTickets + g;
+    } else {
+      r.ticket = ctx->tickets + (ctx->next_ticket.fetch_add(1) % dv_ctx::kTickets);
+    }
     r.ts = ctx->trace_ts;
     bool local = local_vidmem(ctx, r.flag);
     for (int q = 0; q < np && local; ++q)
       if (p[q].dst && p[q].runs() && p[q].run_bytes) local = local_vidmem(ctx, p[q].dst);
     r.gpu_scope = local;
   }
-  return r;
+  *out = r;
+  return DV_OK;
 }
 
 static dv_status stream_signal(const dv_endpoint* ep, int32_t slot, uint64_t seq,
@@ -379,6 +396,35 @@ static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
   return DV_OK;
 }
 
+static dv_status hand_off(dv_ctx* ctx, cudaStream_t from, cudaStream_t to);
+// Once this context has published a decoupled flag (on ctx->flag_st, after its DMA), a publish to
+// a pinned-host flag from another stream is ordered after flag_st: a slot used in both modes then
+// never sees seq t+1 before step t's decoupled flag (and never drops back).
+// Costs nothing when every decoupled flag has already landed (the event has completed), so the
+// per-layer latency path keeps its programmatic dependent launch behind the writer. Not applied
+// to launches captured into a CUDA graph (a graph cannot wait on work outside it; event queries
+// are illegal during capture): the caller orders a replay after earlier decoupled transfers of
+// the same slot (dv.h, DV_XFER_DECOUPLED).
+static dv_status after_decoupled_flags(dv_ctx* ctx, cudaStream_t st) {
+  if (!ctx->decoupled_used.load(std::memory_order_relaxed)) return DV_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DV_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return DV_OK;
+  std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+  const cudaError_t q = cudaEventQuery(ctx->flag_ev);
+  if (q == cudaSuccess) return DV_OK;
+  if (q != cudaErrorNotReady) return cuda_fail(q, "decoupled flag event");
+  (void)cudaGetLastError();
+  DV_CUDA(cudaStreamWaitEvent(st, ctx->flag_ev, 0));
+  return DV_OK;
+}
+// A decoupled flag store was just enqueued on ctx->flag_st (pipe_mu held).
+static dv_status note_decoupled_flag(dv_ctx* ctx) {
+  DV_CUDA(cudaEventRecord(ctx->flag_ev, ctx->flag_st));
+  ctx->decoupled_used.store(true, std::memory_order_relaxed);
+  return DV_OK;
+}
+
 // The fused kernels of 1-2 plans, then the flag: by the last kernel itself (fenced st.release.sys
 // from its last CTA) or, with DV_PUBLISH_STREAMOP, by a stream memory operation after it.
 static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv_endpoint* ep,
@@ -386,17 +432,17 @@ static dv_status launch_publish(dv_ctx* ctx, const CopyPlan* p, int np, const dv
                                 cudaStream_t st, int ctas) {
   const bool streamop = (xfer & DV_PUBLISH_STREAMOP) != 0;
   const Release none{nullptr, 0, nullptr};
+  Release rel = none;
+  if (!streamop) DV_TRY(ticket_release(ctx, ep, slot, seq, use_flag, p, np, st, &rel));
+  if (use_flag && ep->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, st));
   if (np == 2) {
-    DV_TRY(launch_copy2(p[0], p[1], streamop ? none : ticket_release(ctx, ep, slot, seq, use_flag, p, np),
-                        ctas, st));
+    DV_TRY(launch_copy2(p[0], p[1], rel, ctas, st));
     if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
     return DV_OK;
   }
   for (int q = 0; q < np; ++q) {
     const bool last = q == np - 1;
-    DV_TRY(launch_copy(p[q], 0, p[q].runs(),
-                       (last && !streamop) ? ticket_release(ctx, ep, slot, seq, use_flag, p, np) : none,
-                       ctas, st));
+    DV_TRY(launch_copy(p[q], 0, p[q].runs(), last ? rel : none, ctas, st));
   }
   if (streamop && use_flag) DV_TRY(stream_signal(ep, slot, seq, st));
   return DV_OK;
@@ -720,6 +766,16 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
   if (mode == DV_XFER_STAGED && !(op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED | DV_XFER_DECOUPLED)) &&
       !region_empty(&reg) && !staged_fits(ctx, c, reg, wire, true))
     mode = DV_XFER_FUSED;
+  const bool decoupled = (op.xfer & DV_XFER_DECOUPLED) && op.dst->kind == DV_EP_HOST;
+  if (decoupled && use_flag && region_empty(&reg)) {
+    // nothing to move: the flag still goes out on the flag stream, behind the caller's prior work
+    // and behind every earlier decoupled flag (FIFO), so the slot's seq never runs ahead of a
+    // DMA still in flight
+    std::lock_guard<std::mutex> lk(ctx->pipe_mu);
+    DV_TRY(hand_off(ctx, st, ctx->flag_st));
+    DV_TRY(stream_signal(op.dst, op.slot, op.seq, ctx->flag_st));
+    return note_decoupled_flag(ctx);
+  }
   if (mode == DV_XFER_FUSED || region_empty(&reg)) {
     CopyPlan p[2];
     int np = 0;
@@ -736,7 +792,6 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
                           (op.dst->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas
                                                                          : ctx->max_ctas);
   }
-  const bool decoupled = (op.xfer & DV_XFER_DECOUPLED) && op.dst->kind == DV_EP_HOST;
   cudaStream_t fs;
   DV_TRY(staged_pack(ctx, c, reg, wire, st, decoupled, &fs));
   if (use_flag && fs != st) {
@@ -745,9 +800,13 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
     // starts at once. One flag stream per context keeps flags monotonic.
     std::lock_guard<std::mutex> lk(ctx->pipe_mu);
     DV_TRY(hand_off(ctx, fs, ctx->flag_st));
-    return stream_signal(op.dst, op.slot, op.seq, ctx->flag_st);
+    DV_TRY(stream_signal(op.dst, op.slot, op.seq, ctx->flag_st));
+    return note_decoupled_flag(ctx);
   }
-  if (use_flag) DV_TRY(stream_signal(op.dst, op.slot, op.seq, fs));
+  if (use_flag) {
+    if (op.dst->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, fs));
+    DV_TRY(stream_signal(op.dst, op.slot, op.seq, fs));
+  }
   return DV_OK;
 }
 
@@ -856,7 +915,10 @@ static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
           }
         }
     }
-    if (use_flag) DV_TRY(stream_signal(op.signal, op.slot, op.seq, st));
+    if (use_flag) {
+      if (op.signal->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, st));
+      DV_TRY(stream_signal(op.signal, op.slot, op.seq, st));
+    }
     return DV_OK;
   }
   CopyPlan p[2];
@@ -942,11 +1004,12 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
     delete c;
     return s;
   }
-  e = cudaMalloc(&c->tickets, sizeof(unsigned int) * dv_ctx::kTickets);
-  if (e == cudaSuccess) e = cudaMemset(c->tickets, 0, sizeof(unsigned int) * dv_ctx::kTickets);
+  e = cudaMalloc(&c->tickets, sizeof(unsigned int) * (dv_ctx::kTickets + dv_ctx::kGraphTickets));
+  if (e == cudaSuccess) e = cudaMemset(c->tickets, 0, sizeof(unsigned int) * (dv_ctx::kTickets + dv_ctx::kGraphTickets));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dma, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->flag_st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->flag_ev, cudaEventDisableTiming);
   for (int i = 0; e == cudaSuccess && i < 64; ++i) {
     cudaEvent_t ev;
     e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -972,6 +1035,7 @@ dv_status dv_destroy(dv_ctx* ctx) {
     cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->dma);
     cudaStreamDestroy(ctx->flag_st);
+    cudaEventDestroy(ctx->flag_ev);
     for (auto ev : ctx->pipe_ev) cudaEventDestroy(ev);
   }
   delete ctx;
@@ -1176,7 +1240,10 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
                           dst->kind == DV_EP_HOST ? ctx->host_ctas : ctx->max_ctas);
   }
   if (bytes) DV_DMA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyDefault, st));
-  if (use_flag) DV_TRY(stream_signal(dst, flag_slot, seq, st));
+  if (use_flag) {
+    if (dst->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, st));
+    DV_TRY(stream_signal(dst, flag_slot, seq, st));
+  }
   return DV_OK;
 }
 
@@ -1256,12 +1323,23 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
   DV_TRY(check_ep(src, src_off, total, flag_slot, !(xfer & DV_NO_FLAG), "source"));
   DV_ON_DEVICE(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
+  const int64_t row = row_bytes(dst);
+  const uint8_t* wire = (const uint8_t*)src->base + src_off;
+  uint32_t mode = total ? pick_xfer(xfer, src, total, true) : DV_XFER_FUSED;
+  // decided before anything is enqueued (no partial effect), as in gather_run: when one chunk's
+  // staging unit does not fit the pool, AUTO unpacks with the kernel's own loads and an explicit
+  // STAGED request reports DV_ENOMEM
+  if (mode == DV_XFER_STAGED && chunk_bytes > ctx->staging.capacity() / 2 &&
+      !staged_fits(ctx, dst, first, wire, false)) {
+    if (xfer & DV_XFER_STAGED)
+      return fail(DV_ENOMEM, "one layer slab (%llu B) of a chunk exceeds the staging pool; use a "
+                  "larger dv_config.staging_bytes or DV_XFER_FUSED",
+                  (unsigned long long)layer_slab_bytes(&first, row));
+    mode = DV_XFER_FUSED;
+  }
   if (!(xfer & DV_NO_FLAG) && flag_slot >= 0 && wait_seq)
     DV_TRY(stream_wait(src, flag_slot, wait_seq, st));
   if (!total) return DV_OK;
-  const int64_t row = row_bytes(dst);
-  const uint8_t* wire = (const uint8_t*)src->base + src_off;
-  const uint32_t mode = pick_xfer(xfer, src, total, true);
   const Release none{nullptr, 0, nullptr};
   // groups of chunks [k0, k1): the log side is dense over [chunk][l][kv][r][h][s][d]
   auto unpack_group = [&](const uint8_t* base, int32_t k0, int32_t k1) -> dv_status {
@@ -1517,6 +1595,7 @@ dv_status dv_signal(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint6
   DV_TRY(check_ep(ep, 0, 0, flag_slot, true, "endpoint"));
   if (flag_slot < 0) return fail(DV_EINVAL, "negative flag slot");
   DV_ON_DEVICE(ctx->device);
+  if (ep->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, (cudaStream_t)stream));
   return stream_signal(ep, flag_slot, seq, (cudaStream_t)stream);
 }
 

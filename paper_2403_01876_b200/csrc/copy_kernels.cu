@@ -432,6 +432,87 @@ __global__ void __launch_bounds__(THREADS) k_pack_bulk(const KParams p, uint8_t*
   if (p.flag) publish(p, p.pub, p.seq);
 }
 
+// Dense-SOURCE variant for reads over a link (unpacking a wire chunk that sits in pinned host
+// memory, or in a peer GPU's memory): the wire is read with bulk asynchronous copies (the TMA
+// engine, cp.async.bulk global -> shared, SASS UBLKCP.S.G) of `ch` contiguous bytes, completion on
+// an mbarrier per stage, `st` stages in flight per CTA; all threads then scatter the staged bytes
+// into the destination runs with 16/32-byte stores. The per-thread 32-byte zero-copy loads of
+// k_run_copy reach pinned host memory as many small PCIe read requests (ncu: pcie__read_bytes =
+// 2.18 x payload, profiles/r01g_ncu_hbm_kernels.md); a bulk copy lets the copy engine of the SM's
+// TMA unit issue large ones.
+constexpr int kRdStagesMax = 8;
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(b);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_load(uint8_t* smem_dst, const uint8_t* src, uint32_t bytes,
+                                          unsigned long long* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem_dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256) k_unpack_bulk(const KParams p, const uint8_t* src0, uint32_t ch,
+                                                     uint32_t st) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) unsigned long long bar[kRdStagesMax];
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < st; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  const uint64_t total = (uint64_t)p.n_vec * VEC;
+  const uint32_t nchunks = (uint32_t)((total + ch - 1) / ch);
+  if (threadIdx.x == 0)
+    for (uint32_t i = 0; i < st; ++i) {
+      const uint32_t c = blockIdx.x + i * gridDim.x;
+      if (c < nchunks)
+        bulk_load(smem + i * ch, src0 + (uint64_t)c * ch, (uint32_t)(uint32_t)(total - (uint64_t)c * ch < ch ? total - (uint64_t)c * ch : ch),
+                  &bar[i]);
+    }
+  uint32_t it = 0;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const uint32_t s = it % st;
+    mbar_wait(&bar[s], (it / st) & 1);
+    const uint32_t nbytes = (uint32_t)(uint32_t)(total - (uint64_t)c * ch < ch ? total - (uint64_t)c * ch : ch);
+    const uint32_t g0 = (uint32_t)((uint64_t)c * ch / VEC);
+    const uint8_t* buf = smem + s * ch;
+    for (uint32_t v = threadIdx.x; v < nbytes / VEC; v += blockDim.x) {
+      const Vec<VEC> x = *reinterpret_cast<const Vec<VEC>*>(buf + v * VEC);
+      const uint8_t* sp;
+      uint8_t* d;
+      locate<VEC>(p, p.src, p.dst, g0 + v, sp, d);
+      st_vec(d, x);
+    }
+    __syncthreads();  // every thread is done reading stage s
+    if (threadIdx.x == 0) {
+      const uint32_t c2 = c + st * gridDim.x;
+      if (c2 < nchunks)
+        bulk_load(smem + s * ch, src0 + (uint64_t)c2 * ch,
+                  (uint32_t)(total - (uint64_t)c2 * ch < ch ? total - (uint64_t)c2 * ch : ch), &bar[s]);
+    }
+  }
+  if (p.flag) publish(p, p.pub, p.seq);
+}
+
 // 16-byte packet transpose through shared memory (NEXT-1, FasterTransformer's 6-D key layout):
 // inside each slab the packet-major side holds [u][s] (a column of positions per packet, each
 // column contiguous), the position-major side [s][u] (the wire, KV5D). A CTA moves a tile of all
@@ -746,6 +827,9 @@ struct Tune {
   int pk = 16;  // DV_PK: largest packets per register-transpose item (1, 2, 4, 8, 16)
   int cluster = 1;  // DV_CLUSTER: small released copies as one cluster (0 off; 1 gpu-scope releases of
                     // <= 8192 vectors; 2 whenever it fits -- see launch_copy)
+  int rdbulk = 0;     // DV_RDBULK: dense-source copies reading over a link use k_unpack_bulk (2: any source)
+  uint32_t rdch = 8192;  // DV_RDCH: bytes per bulk read
+  uint32_t rdst = 4;     // DV_RDST: bulk reads in flight per CTA (<= kRdStagesMax)
 };
 static const Tune& tune() {
   static Tune t = [] {
@@ -763,6 +847,9 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_TRS")) x.trs = atoi(e);
     if (const char* e = getenv("DV_PK")) x.pk = atoi(e);
     if (const char* e = getenv("DV_CLUSTER")) x.cluster = atoi(e);
+    if (const char* e = getenv("DV_RDBULK")) x.rdbulk = atoi(e);
+    if (const char* e = getenv("DV_RDCH")) x.rdch = (uint32_t)std::max(16, atoi(e) / 16 * 16);
+    if (const char* e = getenv("DV_RDST")) x.rdst = (uint32_t)std::min(kRdStagesMax, std::max(1, atoi(e)));
     return x;
   }();
   return t;
@@ -884,6 +971,44 @@ static bool dense_dst(const CopyPlan& p) {
     expect *= p.n[k];
   }
   return true;
+}
+
+// Is the source of run q at src + q*run_bytes (a dense wire chunk)?
+static bool dense_src(const CopyPlan& p) {
+  int64_t expect = (int64_t)p.run_bytes;
+  for (int k = kDims - 1; k >= 0; --k) {
+    if (p.n[k] == 1) continue;
+    if (p.ss[k] != expect) return false;
+    expect *= p.n[k];
+  }
+  return true;
+}
+
+template <int VEC>
+static cudaError_t launch_unpack_bulk_vec(const KParams& kp, const uint8_t* src0, int max_ctas,
+                                          cudaStream_t st) {
+  const uint32_t ch = std::min<uint32_t>(tune().rdch, 64u << 10);
+  const uint32_t nst = std::max<uint32_t>(1, std::min<uint32_t>(tune().rdst, (200u << 10) / ch));
+  const int smem = (int)(ch * nst);
+  static std::atomic<uint64_t> mask{0};
+  if (first_use_on_device(mask))
+    cudaFuncSetAttribute(k_unpack_bulk<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const uint64_t chunks = ((uint64_t)kp.n_vec * VEC + ch - 1) / ch;
+  const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (uint64_t)max_ctas));
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_unpack_bulk<VEC>, kp, src0, ch, nst);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int VEC>
@@ -1175,6 +1300,7 @@ static void load_vec() {
   load_fn(k_run_copy2<VEC, 1, 128>);
   load_fn(k_run_copy2<VEC, 4, 256>);
   load_fn(k_pack_bulk<VEC, 4, 256>);
+  load_fn(k_unpack_bulk<VEC>);
   load_fn(k_copy_cluster<VEC, 1>);
   load_fn(k_copy_cluster<VEC, 2>);
   load_fn(k_copy_cluster<VEC, 4>);
@@ -1298,7 +1424,11 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
     kp.ticket = rel.ticket;
     kp.ts = last ? rel.ts : nullptr;
     kp.pub = pub_of(rel);
-    cudaError_t e = (tune().bulk && dense_dst(p) && !p.dyn)
+    const bool rd_bulk = tune().rdbulk && !p.dyn && dense_src(p) &&
+                         (tune().rdbulk == 2 || over_link(p.src));
+    cudaError_t e = rd_bulk ? (VEC == 32 ? launch_unpack_bulk_vec<32>(kp, p.src + q0 * p.run_bytes, max_ctas, stream)
+                                         : launch_unpack_bulk_vec<16>(kp, p.src + q0 * p.run_bytes, max_ctas, stream))
+                    : (tune().bulk && dense_dst(p) && !p.dyn)
                         ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
                     : (kp.flag && q0 == 0 && last && use_cluster(kp))
                         ? launch_cluster(kp, VEC, stream)

@@ -153,6 +153,7 @@ struct dv_ctx {
   cudaStream_t aux;       // private stream for dv_query on device flags
   cudaStream_t dma;       // copy-engine stream of the pipelined staged transfers
   cudaStream_t flag_st;   // decoupled transfers' flag stores (off the DMA stream's critical path)
+  cudaEvent_t flag_ev;    // recorded on flag_st after the latest decoupled flag store
   std::vector<cudaEvent_t> pipe_ev;  // event ring for kernel <-> DMA hand-offs
   std::atomic<uint32_t> next_ev{0};
   std::mutex pipe_mu;     // one pipelined transfer enqueued at a time per context
@@ -160,7 +161,15 @@ struct dv_ctx {
   // A ticket is held only while its kernel runs (the last CTA resets it), and tickets are handed
   // out round robin at enqueue, so a ticket is reused only after 65,536 later publishing launches
   // of this context -- far more than can be in flight while one copy kernel is still running.
+  // A launch captured into a CUDA graph keeps its ticket for as long as the graph is replayed, so
+  // captured launches take tickets from a separate range [kTickets, kTickets + kGraphTickets)
+  // that is never recycled (a graph's replays are serialised with each other by CUDA).
   static constexpr uint32_t kTickets = 65536;
+  static constexpr uint32_t kGraphTickets = 65536;  // tickets array: kTickets + kGraphTickets
+  std::atomic<uint32_t> next_graph_ticket{0};
+  // set once a decoupled transfer has published on flag_st: later publishes to pinned-host flags
+  // from other streams are ordered after flag_st so a slot's flag stays monotone across modes
+  std::atomic<bool> decoupled_used{false};
 };
 
 namespace dv {
