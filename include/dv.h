@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define DV_ABI_VERSION 2
+#define DV_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define DV_API __attribute__((visibility("default")))
@@ -66,7 +66,7 @@ typedef enum dv_status {
   DV_EALIGN = 4,  /* a base/offset or head_dim*elem_bytes is not a multiple of 16 bytes        */
   DV_ENOMEM = 5,  /* staging pool or an allocation could not be satisfied                     */
   DV_EPEER = 6,   /* IPC export/open failed or a blob is malformed                            */
-  DV_EBUSY = 7,   /* reserved: inbox without credit                                           */
+  DV_EBUSY = 7,   /* DV_NOWAIT: the inbox ring slot has no credit yet (receiver not done)     */
   DV_ECUDA = 8,   /* a CUDA runtime/driver call failed; its text is in dv_last_error()        */
   DV_ENOTSUP = 9  /* valid request this build does not implement                              */
 } dv_status;
@@ -144,6 +144,21 @@ enum {
   DV_EP_PEER = 2    /* another GPU's memory mapped into this process (CUDA IPC) over NVLink     */
 };
 
+/* An inbox may be a RING of n_slots chunk slots with per-source CREDITS (SURVEY §8(a) A5 "inbox
+ * credits per slot"; the paper's token machines consume a mailbox). Then, for flag
+ * slot f (one per source block) and sequence number s >= 1:
+ *   - the chunk of seq s lives in ring slot s % n_slots: at base + (s % n_slots)*slot_bytes + off,
+ *     and off + chunk bytes must fit slot_bytes;
+ *   - the SENDER (dv_scatter / dv_flush / dv_stream_out with flag slot f and seq s) may overwrite
+ *     that slot only once the receiver has consumed seq s - n_slots: its copy is stream-ordered
+ *     after credits[f] >= s - n_slots (a stream memory-op wait on host or own-GPU memory, a
+ *     one-thread acquire-spin kernel on peer memory), or -- with DV_NOWAIT -- the call returns
+ *     DV_EBUSY without enqueueing anything when the credit is not there yet;
+ *   - the RECEIVER (dv_gather / dv_fetch / dv_stream_in with flag slot f and wait_seq s) reads ring
+ *     slot s % n_slots after flags[f] >= s and, once its copy has read the chunk, releases
+ *     credits[f] = s (the copy kernel's own release store, at the scope the memory needs).
+ * Sequence numbers of one source are consecutive (1, 2, 3, ...). credits == NULL: ring addressing
+ * without flow control. n_slots == 0: a plain buffer (no ring, no credits). */
 typedef struct dv_endpoint {
   int32_t kind;     /* DV_EP_*                                                                  */
   int32_t device;   /* device owning the memory (-1 for host)                                  */
@@ -151,7 +166,9 @@ typedef struct dv_endpoint {
   uint64_t bytes;   /* capacity                                                                */
   uint64_t* flags;  /* n_flags monotone 64-bit sequence words (same accessibility as base), or NULL */
   int32_t n_flags;
-  int32_t reserved;
+  int32_t n_slots;      /* ring depth; 0 = no ring                                             */
+  uint64_t slot_bytes;  /* bytes per ring slot (multiple of 16; n_slots * slot_bytes <= bytes)  */
+  uint64_t* credits;    /* n_flags credit words (consumed seq per source), or NULL               */
 } dv_endpoint;
 
 /* Transfer-method flags for the data calls. DV_XFER_AUTO lets the library pick (DESIGN.md §6
@@ -184,6 +201,9 @@ enum {
                                   stream too), so a slot's seq never runs ahead of a DMA in
                                   flight -- except for launches captured into a CUDA graph, which
                                   the caller orders after earlier decoupled transfers.          */
+  DV_NOWAIT = 1u << 4,      /* senders into a credited ring: DV_EBUSY instead of a stream-ordered
+                               wait when a slot has no credit (checked from the host when called;
+                               reading a device-memory credit is a small synchronous copy)     */
   DV_NO_FLAG = 1u << 8      /* do not publish / wait on sequence flags                           */
 };
 
@@ -249,15 +269,20 @@ DV_API dv_status dv_device_free(void* p);
  * in calls on `device`'s context. DV_EPEER if the pair cannot access each other. */
 DV_API dv_status dv_peer_enable(int32_t device, int32_t peer);
 
-typedef struct dv_ipc_blob { uint8_t bytes[96]; } dv_ipc_blob; /* opaque, copyable between processes */
+typedef struct dv_ipc_blob { uint8_t bytes[128]; } dv_ipc_blob; /* opaque, copyable between processes */
 /* Export device memory at `ptr` (any address inside a cudaMalloc allocation -- legacy CUDA IPC;
  * memory from the virtual-memory API, e.g. PyTorch with expandable_segments, or from
  * cudaMallocAsync pools cannot be exported this way: use dv_device_alloc or plain cudaMalloc for
  * inboxes, replica stores and flags that other processes map). DV_EPEER on failure. */
 DV_API dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out);
 /* Map a blob exported by another process (same or other GPU) into this process; returns the
- * address corresponding to the exported `ptr`. Same-process blobs map to the original pointer. */
+ * address corresponding to the exported `ptr`. Same-process blobs map to the original pointer:
+ * a blob carries a random 64-bit token of its exporting process (not the pid, which another PID
+ * namespace may reuse). The blob records the exported extent (allocation end - ptr); every data
+ * call checks that a cache or endpoint inside an IPC mapping fits the mapped extent (DV_EPEER). */
 DV_API dv_status dv_ipc_open(const dv_ipc_blob* blob, void** out);
+/* The exported extent of a blob in bytes (ptr .. end of its allocation), for sizing descriptors. */
+DV_API dv_status dv_ipc_blob_bytes(const dv_ipc_blob* blob, uint64_t* out);
 DV_API dv_status dv_ipc_close(void* mapped);
 
 /* ---- level 3: flush / fetch ----------------------------------------------- */

@@ -1,8 +1,10 @@
 /*
- * dv_testing.h -- test-only utilities of dvstream. NOT part of the streaming
- * path: a synthetic KV "writer" that fills caches with the seeded generator of kvgen/__init__.py
- * (same counter-based splitmix64 coordinate hash, implemented independently on the device), and a
- * synthetic compute kernel for overlap measurements.
+ * dv_testing.h -- test-only utilities of dvstream, exported by the SEPARATE
+ * library libdvstream_testing.so (which links libdvstream.so); NOT part of the streaming path and
+ * not in the product library: a synthetic KV "writer" that fills caches with the seeded generator
+ * of kvgen/__init__.py (same counter-based splitmix64 coordinate hash, implemented independently
+ * on the device), an on-device verifier, flag watchers / consumers and a spin kernel for latency
+ * and overlap measurements. Errors are reported through libdvstream's dv_last_error().
  */
 #ifndef DV_TESTING_H_
 #define DV_TESTING_H_
@@ -37,19 +39,6 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
 DV_API dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kind, uint64_t seed,
                      const int32_t* box, int32_t valid_begin, int32_t valid_end,
                      const dv_region* region, uint64_t* mismatches, void* stream);
-
-/* Latency tracing: while `ts` (device memory, 4 x uint64) is set, every fused copy of `ctx` that
- * publishes a flag records %globaltimer (ns): ts[0] = right after the release store of the flag,
- * ts[1] = min over CTAs of "resident" (before the programmatic-dependency wait; initialise to
- * UINT64_MAX), ts[2] = min over CTAs of "past the wait" (initialise to UINT64_MAX), ts[3] = max
- * over CTAs of "stores issued". NULL disables. */
-DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
-
-/* Release scope the fused publish of `ctx` would use for a flag at `flag` after stores to
- * `payload`: *gpu_scope = 1 when both are this context's GPU's own device memory (not mapped from
- * another process), 0 otherwise (system scope). Host-only query; DESIGN.md §6 protocols 2/3. */
-DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
-                                   int32_t* gpu_scope);
 
 /* Flag watcher: one GPU thread polls `flag` (device memory, or pinned host memory through its
  * device-mapped address) with system-scope acquire loads and writes %globaltimer to ts[i] (device

@@ -1,0 +1,29 @@
+/*
+ * dv_trace.h -- introspection hooks of libdvstream.so (SURVEY §5 "tracing"): latency tracing of
+ * the fused publish and the release-scope decision. Part of the product library (they read or set
+ * context state); no kernels of their own.
+ */
+#ifndef DV_TRACE_H_
+#define DV_TRACE_H_
+#include "dv.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Latency tracing: while `ts` (device memory, 4 x uint64) is set, every fused copy of `ctx` that
+ * publishes a flag records %globaltimer (ns): ts[0] = right after the release store of the flag,
+ * ts[1] = min over CTAs of "resident" (before the programmatic-dependency wait; initialise to
+ * UINT64_MAX), ts[2] = min over CTAs of "past the wait" (initialise to UINT64_MAX), ts[3] = max
+ * over CTAs of "stores issued". NULL disables. */
+DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
+
+/* Release scope the fused publish of `ctx` would use for a flag at `flag` after stores to
+ * `payload`: *gpu_scope = 1 when both are this context's GPU's own device memory (not mapped from
+ * another process), 0 otherwise (system scope). Host-only query; DESIGN.md §6 protocols 2/3. */
+DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
+                                   int32_t* gpu_scope);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

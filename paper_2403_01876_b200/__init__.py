@@ -16,6 +16,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdvstream.so")
+# test utilities (dvt_fill/verify/watch/consume/spin) and prior-art baselines (dvb_*): a separate
+# library that links libdvstream.so; loaded on first use of one of its functions
+TESTING_LIB_PATH = os.path.join(_HERE, "libdvstream_testing.so")
 
 # ---- constants mirrored from include/dv.h --------------------------------------------------------
 DV_OK, DV_EINVAL, DV_EMAP, DV_ERANGE, DV_EALIGN, DV_ENOMEM, DV_EPEER, DV_EBUSY, DV_ECUDA, \
@@ -24,6 +27,7 @@ DV_LAYOUT_KV5D, DV_LAYOUT_FT6D = 0, 1
 DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
 DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_PUBLISH_STREAMOP, DV_NO_FLAG = 0, 1, 2, 4, 256
 DV_XFER_DECOUPLED = 8
+DV_NOWAIT = 16
 DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
 
 
@@ -57,7 +61,7 @@ class dv_piece(C.Structure):
 class dv_endpoint(C.Structure):
     _fields_ = [("kind", C.c_int32), ("device", C.c_int32), ("base", C.c_void_p),
                 ("bytes", C.c_uint64), ("flags", C.c_void_p), ("n_flags", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("n_slots", C.c_int32), ("slot_bytes", C.c_uint64), ("credits", C.c_void_p)]
 
 
 class dv_config(C.Structure):
@@ -65,7 +69,7 @@ class dv_config(C.Structure):
 
 
 class dv_ipc_blob(C.Structure):
-    _fields_ = [("bytes", C.c_uint8 * 96)]
+    _fields_ = [("bytes", C.c_uint8 * 128)]
 
 
 class DVError(RuntimeError):
@@ -97,6 +101,7 @@ _SIGS = {
     "dv_ipc_export": (C.c_int, [C.c_void_p, P(dv_ipc_blob)]),
     "dv_ipc_open": (C.c_int, [P(dv_ipc_blob), P(C.c_void_p)]),
     "dv_ipc_close": (C.c_int, [C.c_void_p]),
+    "dv_ipc_blob_bytes": (C.c_int, [P(dv_ipc_blob), P(C.c_uint64)]),
     "dv_flush": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(dv_endpoint), C.c_uint64,
                            C.c_int32, C.c_uint64, C.c_uint32, C.c_void_p]),
     "dv_fetch": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_uint64, C.c_int32, C.c_uint64,
@@ -141,7 +146,10 @@ _SIGS = {
                                     P(C.c_uint64)]),
 }
 
+TESTING_SYMBOLS = {"dvt_fill", "dvt_verify", "dvt_spin", "dvt_consume", "dvt_watch", "dvb_per_run_copy",
+                   "dvb_buffered_copy"}
 _lib = None
+_tlib = None
 
 
 def lib() -> C.CDLL:
@@ -152,6 +160,8 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if name in TESTING_SYMBOLS:
+                continue
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
@@ -159,8 +169,29 @@ def lib() -> C.CDLL:
     return _lib
 
 
+def testing_lib() -> C.CDLL:
+    """Load libdvstream_testing.so (test utilities + prior-art baselines; links libdvstream.so)."""
+    global _tlib
+    if _tlib is None:
+        lib()
+        if not os.path.exists(TESTING_LIB_PATH):
+            raise ImportError(f"{TESTING_LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        T = C.CDLL(TESTING_LIB_PATH)
+        for name in TESTING_SYMBOLS:
+            res, args = _SIGS[name]
+            f = getattr(T, name)
+            f.restype = res
+            f.argtypes = args
+        _tlib = T
+    return _tlib
+
+
 def exported_symbols():
-    return list(_SIGS)
+    return [n for n in _SIGS if n not in TESTING_SYMBOLS]
+
+
+def testing_symbols():
+    return sorted(TESTING_SYMBOLS)
 
 
 _fast = None
@@ -205,7 +236,7 @@ _fns = {}
 def _call(name, *args):
     f = _fns.get(name)
     if f is None:
-        f = _fns[name] = getattr(lib(), name)
+        f = _fns[name] = getattr(testing_lib() if name in TESTING_SYMBOLS else lib(), name)
     st = f(*args)
     if st != DV_OK:
         raise DVError(st, name, lib().dv_last_error().decode())
@@ -291,19 +322,24 @@ def cache_raw(k_ptr, v_ptr, device, elem_bytes, layer_begin, n_layers, req_begin
                     req_begin, n_reqs, n_heads, max_seq, head_dim, head_begin)
 
 
-def endpoint(kind, base_ptr, nbytes, flags_ptr=0, n_flags=0, device=-1) -> dv_endpoint:
-    return dv_endpoint(kind, device, base_ptr, nbytes, flags_ptr, n_flags, 0)
+def endpoint(kind, base_ptr, nbytes, flags_ptr=0, n_flags=0, device=-1, n_slots=0, slot_bytes=0,
+             credits_ptr=0) -> dv_endpoint:
+    """Endpoint from raw pointers; n_slots > 0 makes it a ring inbox (credits_ptr: n_flags credit
+    words, include/dv.h)."""
+    return dv_endpoint(kind, device, base_ptr, nbytes, flags_ptr, n_flags, n_slots, slot_bytes, credits_ptr)
 
 
-def endpoint_of(buf, flags=None, kind=None) -> dv_endpoint:
+def endpoint_of(buf, flags=None, kind=None, n_slots=0, slot_bytes=0, credits=None) -> dv_endpoint:
     """Endpoint over a torch buffer (device or pinned host) and an optional uint64/int64 flag
-    tensor in the same kind of memory."""
+    tensor in the same kind of memory; n_slots/slot_bytes/credits (a tensor of n_flags words)
+    make it a ring inbox with flow control."""
     if kind is None:
         kind = DV_EP_DEVICE if buf.is_cuda else DV_EP_HOST
     dev = buf.device.index if buf.is_cuda else -1
     nb = buf.numel() * buf.element_size()
     fp, nf = (flags.data_ptr(), flags.numel()) if flags is not None else (0, 0)
-    return dv_endpoint(kind, dev, buf.data_ptr(), nb, fp, nf, 0)
+    cp = credits.data_ptr() if credits is not None else 0
+    return dv_endpoint(kind, dev, buf.data_ptr(), nb, fp, nf, n_slots, slot_bytes, cp)
 
 
 def endpoint_array(eps):
@@ -436,6 +472,15 @@ def dv_ipc_open(blob: bytes) -> int:
 
 def dv_ipc_close(p):
     _call("dv_ipc_close", C.c_void_p(p))
+
+
+def dv_ipc_blob_bytes(blob: bytes) -> int:
+    """Bytes the exporter shared from its pointer to the end of that allocation."""
+    b = dv_ipc_blob()
+    C.memmove(b.bytes, blob, len(b.bytes))
+    n = C.c_uint64()
+    _call("dv_ipc_blob_bytes", C.byref(b), C.byref(n))
+    return n.value
 
 
 def dv_flush(ctx, src_ptr, nbytes, dst: dv_endpoint, dst_off=0, flag_slot=-1, seq=0, xfer=0, stream=None):

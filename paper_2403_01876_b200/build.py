@@ -7,7 +7,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libdvstream.so")
-SOURCES = ["route.cpp", "api.cu", "copy_kernels.cu", "testing.cu", "baselines.cu"]
+SOURCES = ["route.cpp", "api.cu", "copy_kernels.cu"]
+# test utilities and the paper's prior-art copy methods: a separate library linking the product one
+OUT_TESTING = os.path.join(HERE, "libdvstream_testing.so")
+SOURCES_TESTING = ["testing.cu", "baselines.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("DV_NVCC_EXTRA", "").split()   # experiment hook, e.g. -DDV_MIN_BLOCKS=6
 FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -15,25 +18,36 @@ FLAGS = ["-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidde
          "-I", os.path.join(ROOT, "include"), "-DDV_BUILD"]
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "dv_internal.h"), os.path.join(ROOT, "include", "dv.h"),
-                   os.path.join(ROOT, "include", "dv_testing.h"), os.path.join(ROOT, "include", "dv_device.cuh"),
-                   os.path.join(ROOT, "include", "dv_baselines.h")]
-    if not force and os.path.exists(OUT):
-        t = os.path.getmtime(OUT)
+def _nvcc(srcs, out, deps, extra_link, force, verbose, log):
+    if not force and os.path.exists(out):
+        t = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d)):
-            return OUT
-    cmd = [NVCC] + FLAGS + EXTRA + srcs + ["-o", OUT + ".tmp", "-lrt", "-ldl", "-lpthread"]
+            return out
+    cmd = [NVCC] + FLAGS + EXTRA + srcs + ["-o", out + ".tmp"] + extra_link
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libdvstream.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    os.replace(out + ".tmp", out)
+    with open(os.path.join(HERE, log), "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return out
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    """libdvstream.so (the product: route, API, copy kernels), then libdvstream_testing.so (test
+    utilities + prior-art baselines, linked against it)."""
+    inc = [os.path.join(ROOT, "include", h) for h in ("dv.h", "dv_trace.h", "dv_device.cuh")]
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    _nvcc(srcs, OUT, srcs + [os.path.join(CSRC, "dv_internal.h")] + inc, ["-lrt", "-ldl", "-lpthread"],
+          force, verbose, "build.log")
+    tsrcs = [os.path.join(CSRC, s) for s in SOURCES_TESTING]
+    tinc = [os.path.join(ROOT, "include", h) for h in ("dv_testing.h", "dv_baselines.h")]
+    _nvcc(tsrcs, OUT_TESTING, tsrcs + [OUT, os.path.join(CSRC, "dv_internal.h")] + inc + tinc,
+          ["-L", HERE, "-ldvstream", "-Xlinker", "-rpath,$ORIGIN", "-lrt", "-lpthread"], force, verbose,
+          "build_testing.log")
     return OUT
 
 

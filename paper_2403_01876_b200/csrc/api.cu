@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <limits.h>
 #include <string.h>
+#include <time.h>
 #include <sys/mman.h>
 #include <sys/syscall.h>
 #include <unistd.h>
@@ -13,7 +14,7 @@
 #include <mutex>
 
 #include "dv_internal.h"
-#include "../../include/dv_testing.h"
+#include "../../include/dv_trace.h"
 
 namespace dv {
 
@@ -306,6 +307,10 @@ static uint64_t region_bytes(const dv_region* r, const dv_cache* c) {
 
 static int64_t row_bytes(const dv_cache* c) { return (int64_t)c->head_dim * c->elem_bytes; }
 
+static dv_status check_mapped(const void* p, uint64_t extent, const char* name);
+static dv_status check_cache_mapped(const dv_cache* c, const char* name);
+
+// Endpoint structure and the capacity for `bytes` at `off` (inside one ring slot for a ring).
 static dv_status check_ep(const dv_endpoint* ep, uint64_t off, uint64_t bytes, int32_t slot,
                           bool use_flag, const char* name) {
   if (!ep) return fail(DV_EINVAL, "%s: NULL endpoint", name);
@@ -314,15 +319,91 @@ static dv_status check_ep(const dv_endpoint* ep, uint64_t off, uint64_t bytes, i
   if (!ep->base && bytes) return fail(DV_EINVAL, "%s: NULL endpoint base", name);
   if (((uintptr_t)ep->base | off) % 16)
     return fail(DV_EALIGN, "%s: endpoint base/offset not 16-byte aligned", name);
-  if (off > ep->bytes || bytes > ep->bytes - off)
+  if (ep->n_slots < 0) return fail(DV_EINVAL, "%s: negative n_slots", name);
+  if (ep->n_slots > 0) {
+    if (!ep->slot_bytes || ep->slot_bytes % 16)
+      return fail(DV_EALIGN, "%s: ring slot_bytes %llu not a positive multiple of 16", name,
+                  (unsigned long long)ep->slot_bytes);
+    if ((uint64_t)ep->n_slots > ep->bytes / ep->slot_bytes)
+      return fail(DV_EINVAL, "%s: ring of %d x %llu B exceeds endpoint capacity %llu", name,
+                  ep->n_slots, (unsigned long long)ep->slot_bytes, (unsigned long long)ep->bytes);
+    if (off > ep->slot_bytes || bytes > ep->slot_bytes - off)
+      return fail(DV_EINVAL, "%s: [%llu, +%llu) exceeds the ring slot of %llu B", name,
+                  (unsigned long long)off, (unsigned long long)bytes,
+                  (unsigned long long)ep->slot_bytes);
+    if ((uintptr_t)ep->credits % 8) return fail(DV_EALIGN, "%s: credits not 8-byte aligned", name);
+    if (ep->credits && !ep->flags)
+      return fail(DV_EINVAL, "%s: credits need flags (one credit word per flag slot)", name);
+  } else if (off > ep->bytes || bytes > ep->bytes - off) {
     return fail(DV_EINVAL, "%s: [%llu, +%llu) exceeds endpoint capacity %llu", name,
                 (unsigned long long)off, (unsigned long long)bytes, (unsigned long long)ep->bytes);
+  }
   if (use_flag && slot >= 0) {
     if (!ep->flags || slot >= ep->n_flags)
       return fail(DV_EINVAL, "%s: flag slot %d but endpoint has %d flags", name, slot, ep->n_flags);
     if ((uintptr_t)ep->flags % 8) return fail(DV_EALIGN, "%s: flags not 8-byte aligned", name);
   }
+  if (ep->base) DV_TRY(check_mapped(ep->base, ep->bytes, name));
+  if (ep->flags) DV_TRY(check_mapped(ep->flags, 8ull * (uint64_t)std::max(ep->n_flags, 0), name));
+  if (ep->credits) DV_TRY(check_mapped(ep->credits, 8ull * (uint64_t)std::max(ep->n_flags, 0), name));
   return DV_OK;
+}
+
+// ---- inbox rings and credits (dv.h, dv_endpoint) ----------------------------------------------
+static bool has_ring(const dv_endpoint* ep) { return ep && ep->n_slots > 0; }
+static uint64_t ring_off(const dv_endpoint* ep, uint64_t seq) {
+  return has_ring(ep) ? (seq % (uint64_t)ep->n_slots) * ep->slot_bytes : 0;
+}
+// A data call into / out of a ring needs a flag slot and a sequence number >= 1.
+static dv_status check_ring_use(const dv_endpoint* ep, int32_t slot, uint64_t seq, bool use_flag,
+                                const char* name) {
+  if (!has_ring(ep)) return DV_OK;
+  if (!use_flag || slot < 0 || seq < 1)
+    return fail(DV_EINVAL, "%s: a ring endpoint needs a flag slot and a sequence number >= 1", name);
+  return DV_OK;
+}
+static bool local_vidmem(const dv_ctx* ctx, const void* p);
+// The value of a 64-bit word in host, device or mapped peer memory, read now from the host (a
+// small synchronous copy for device memory).
+static dv_status read_word(dv_ctx* ctx, const uint64_t* p, uint64_t* out) {
+  cudaPointerAttributes at;
+  DV_CUDA(cudaPointerGetAttributes(&at, p));
+  if (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered) {
+    *out = __atomic_load_n(p, __ATOMIC_ACQUIRE);
+    return DV_OK;
+  }
+  DV_CUDA(cudaMemcpyAsync(out, p, 8, cudaMemcpyDefault, ctx->aux));
+  DV_CUDA(cudaStreamSynchronize(ctx->aux));
+  return DV_OK;
+}
+// Sender side, validation time: with DV_NOWAIT a seq whose ring slot has no credit yet -> DV_EBUSY
+// (nothing has been enqueued; the caller retries).
+static dv_status credit_check_nowait(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
+                                     uint32_t xfer) {
+  if (!has_ring(ep) || !ep->credits || !(xfer & DV_NOWAIT) || seq <= (uint64_t)ep->n_slots)
+    return DV_OK;
+  uint64_t c = 0;
+  DV_TRY(read_word(ctx, &ep->credits[slot], &c));
+  if (c + (uint64_t)ep->n_slots < seq)
+    return fail(DV_EBUSY, "inbox ring slot %llu busy: source %d's credit is %llu, seq %llu needs %llu",
+                (unsigned long long)(seq % (uint64_t)ep->n_slots), slot, (unsigned long long)c,
+                (unsigned long long)seq, (unsigned long long)(seq - (uint64_t)ep->n_slots));
+  return DV_OK;
+}
+// Sender side, enqueue time: order the writes of seq s after credits[slot] >= s - n_slots. A
+// stream memory-op wait where the word is pinned host memory or this GPU's own HBM; a one-thread
+// acquire-spin kernel for peer memory (mapped over NVLink).
+static dv_status stream_wait_word(const uint64_t* p, uint64_t v, cudaStream_t st);
+static dv_status credit_wait(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
+                             uint32_t xfer, cudaStream_t st) {
+  if (!has_ring(ep) || !ep->credits || seq <= (uint64_t)ep->n_slots || (xfer & DV_NOWAIT))
+    return DV_OK;   // NOWAIT: the credit was already there at validation (credits only grow)
+  const uint64_t need = seq - (uint64_t)ep->n_slots;
+  const uint64_t* p = &ep->credits[slot];
+  cudaPointerAttributes at;
+  DV_CUDA(cudaPointerGetAttributes(&at, p));
+  if (at.type == cudaMemoryTypeHost || local_vidmem(ctx, p)) return stream_wait_word(p, need, st);
+  return launch_wait_geq(p, need, st);
 }
 
 static dv_status check_ctx(dv_ctx* ctx) {
@@ -348,12 +429,31 @@ static bool local_vidmem(const dv_ctx* ctx, const void* p) {
 // The release of a fused copy: the endpoint's flag, a ticket, and the scope. Payload (the plans'
 // destinations) and flag all in this GPU's HBM -> a gpu-scope release suffices (publish() protocol
 // 3); anything in pinned host or peer memory -> system scope.
+static dv_status word_release(dv_ctx* ctx, uint64_t* word, uint64_t seq, const CopyPlan* p, int np,
+                              cudaStream_t st, Release* out);
 static dv_status ticket_release(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, uint64_t seq,
                                 bool use_flag, const CopyPlan* p, int np, cudaStream_t st,
                                 Release* out) {
+  *out = Release{nullptr, 0, nullptr};
+  if (use_flag && slot >= 0 && ep && ep->flags) return word_release(ctx, &ep->flags[slot], seq, p, np, st, out);
+  return DV_OK;
+}
+// The receiver's credit (dv.h, rings): released by the unpack kernel once it has read the chunk.
+// Its loads completed before its stores, which the release orders; the scope is the credit word's
+// (gpu scope for this GPU's HBM -- peers polling it over NVLink are served by this GPU's L2).
+static dv_status credit_release(dv_ctx* ctx, const dv_endpoint* src, int32_t slot, uint64_t seq,
+                                cudaStream_t st, Release* out) {
+  *out = Release{nullptr, 0, nullptr};
+  if (!has_ring(src) || !src->credits) return DV_OK;
+  return word_release(ctx, &src->credits[slot], seq, nullptr, 0, st, out);
+}
+// A release of `seq` into `word` after a copy kernel's plans `p` (their destinations decide the
+// scope together with the word's memory).
+static dv_status word_release(dv_ctx* ctx, uint64_t* word, uint64_t seq, const CopyPlan* p, int np,
+                              cudaStream_t st, Release* out) {
   Release r{nullptr, 0, nullptr};
-  if (use_flag && slot >= 0 && ep && ep->flags) {
-    r.flag = (unsigned long long*)&ep->flags[slot];
+  {
+    r.flag = (unsigned long long*)word;
     r.seq = seq;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     DV_CUDA(cudaStreamIsCapturing(st, &cs));
@@ -386,14 +486,16 @@ static dv_status stream_signal(const dv_endpoint* ep, int32_t slot, uint64_t seq
   return DV_OK;
 }
 
-static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
-                             cudaStream_t stream) {
+static dv_status stream_wait_word(const uint64_t* p, uint64_t v, cudaStream_t stream) {
   const Driver* d;
   DV_TRY(driver(&d));
-  int r = d->streamWaitValue64(stream, (unsigned long long)(uintptr_t)&ep->flags[slot], seq,
-                               CU_STREAM_WAIT_VALUE_GEQ);
+  int r = d->streamWaitValue64(stream, (unsigned long long)(uintptr_t)p, v, CU_STREAM_WAIT_VALUE_GEQ);
   if (r) return drv_fail(r, "cuStreamWaitValue64");
   return DV_OK;
+}
+static dv_status stream_wait(const dv_endpoint* ep, int32_t slot, uint64_t seq,
+                             cudaStream_t stream) {
+  return stream_wait_word(&ep->flags[slot], seq, stream);
 }
 
 static dv_status hand_off(dv_ctx* ctx, cudaStream_t from, cudaStream_t to);
@@ -490,6 +592,7 @@ static dv_status staged_capacity_check(dv_ctx* ctx, uint32_t xfer, const dv_endp
 static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
   DV_TRY(check_ctx(ctx));
   DV_TRY(check_cache(op.src, "source"));
+  DV_TRY(check_cache_mapped(op.src, "source"));
   DV_TRY(check_region_shape(&op.reg));
   DV_TRY(check_cache_holds(op.src, &op.reg, "source"));
   const bool use_flag = !(op.xfer & DV_NO_FLAG);
@@ -498,7 +601,10 @@ static dv_status scatter_check(dv_ctx* ctx, const ScatterOp& op) {
     return fail(DV_EINVAL, "DV_XFER_DECOUPLED needs a flag: the flag is its only completion signal");
   DV_TRY(check_ep(op.dst, op.dst_off, region_bytes(&op.reg, op.src), op.slot, use_flag,
                   "destination"));
-  return staged_capacity_check(ctx, op.xfer, op.dst, op.src, op.reg, op.dst_off, true);
+  DV_TRY(check_ring_use(op.dst, op.slot, op.seq, use_flag, "destination"));
+  DV_TRY(staged_capacity_check(ctx, op.xfer, op.dst, op.src, op.reg,
+                               op.dst_off + ring_off(op.dst, op.seq), true));
+  return credit_check_nowait(ctx, op.dst, op.slot, op.seq, op.xfer);   // last: DV_EBUSY
 }
 
 // Layer slabs of a region's wire: [l][...] -- slab l starts at (l - l0) * slab bytes.
@@ -759,8 +865,10 @@ static dv_status scatter_run(dv_ctx* ctx, const ScatterOp& op, cudaStream_t st) 
   const uint64_t bytes = region_bytes(&reg, c);
   const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
   uint32_t mode = pick_xfer(op.xfer, op.dst, bytes, false);
-  uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off;
+  uint8_t* wire = (uint8_t*)op.dst->base + op.dst_off + ring_off(op.dst, op.seq);
   const int64_t row = row_bytes(c);
+  // a credited ring slot is overwritten only after the receiver consumed its previous chunk
+  DV_TRY(credit_wait(ctx, op.dst, op.slot, op.seq, op.xfer, st));
   // AUTO picked staging but the pool cannot hold one layer slab of this region: the kernel's own
   // stores move it instead (an explicit STAGED / DECOUPLED request still reports DV_ENOMEM)
   if (mode == DV_XFER_STAGED && !(op.xfer & (DV_XFER_FUSED | DV_XFER_STAGED | DV_XFER_DECOUPLED)) &&
@@ -823,11 +931,14 @@ struct GatherOp {
 static dv_status gather_check(dv_ctx* ctx, const GatherOp& op) {
   DV_TRY(check_ctx(ctx));
   DV_TRY(check_cache(op.dst, "destination"));
+  DV_TRY(check_cache_mapped(op.dst, "destination"));
   DV_TRY(check_region_shape(&op.reg));
   DV_TRY(check_cache_holds(op.dst, &op.reg, "destination"));
   const bool use_flag = !(op.xfer & DV_NO_FLAG);
   DV_TRY(check_ep(op.src, op.src_off, region_bytes(&op.reg, op.dst), op.slot, use_flag, "source"));
-  return staged_capacity_check(ctx, op.xfer, op.src, op.dst, op.reg, op.src_off, false);
+  DV_TRY(check_ring_use(op.src, op.slot, op.wait_seq, use_flag, "source"));
+  return staged_capacity_check(ctx, op.xfer, op.src, op.dst, op.reg,
+                               op.src_off + ring_off(op.src, op.wait_seq), false);
 }
 
 static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
@@ -835,7 +946,7 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
   const dv_region reg = resolve_heads(&op.reg, c);
   const uint64_t bytes = region_bytes(&reg, c);
   uint32_t mode = bytes ? pick_xfer(op.xfer, op.src, bytes, true) : DV_XFER_FUSED;
-  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off;
+  const uint8_t* wire = (const uint8_t*)op.src->base + op.src_off + ring_off(op.src, op.wait_seq);
   // decided before anything is enqueued (no partial effect): AUTO falls back to the kernel's own
   // loads when one layer slab does not fit half the staging pool; explicit STAGED reports it
   if (mode == DV_XFER_STAGED && !staged_fits(ctx, c, reg, wire, false)) {
@@ -845,19 +956,25 @@ static dv_status gather_run(dv_ctx* ctx, const GatherOp& op, cudaStream_t st) {
                   (unsigned long long)layer_slab_bytes(&reg, row_bytes(c)));
     mode = DV_XFER_FUSED;
   }
-  if (!(op.xfer & DV_NO_FLAG) && op.slot >= 0 && op.wait_seq)
-    DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
-  if (!bytes) return DV_OK;
-  if (mode == DV_XFER_STAGED) return staged_unpack(ctx, wire, c, reg, st);
+  const bool use_flag = !(op.xfer & DV_NO_FLAG) && op.slot >= 0;
+  if (use_flag && op.wait_seq) DV_TRY(stream_wait(op.src, op.slot, op.wait_seq, st));
+  // the receiver's credit for this chunk (ring inboxes): released once the chunk has been read
+  Release credit{nullptr, 0, nullptr};
+  if (use_flag) DV_TRY(credit_release(ctx, op.src, op.slot, op.wait_seq, st, &credit));
+  const int ctas = (op.src->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas : ctx->max_ctas;
+  if (!bytes || mode == DV_XFER_STAGED) {
+    if (bytes) DV_TRY(staged_unpack(ctx, wire, c, reg, st));
+    if (!credit.flag) return DV_OK;
+    return launch_copy(CopyPlan{}, 0, 0, credit, ctas, st);   // publish only
+  }
   const int64_t row = row_bytes(c);
   TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
   TView cv[2] = {cache_view(c, 0, &reg), cache_view(c, 1, &reg)};
   CopyPlan p[2];
   const int np = build_plans(wv, cv, &reg, row, ORDER_WIRE, Outer{}, p);
   if (np < 0) return fail(DV_ENOTSUP, "copy not expressible");
-  const int ctas = (op.src->kind == DV_EP_HOST || c->device < 0) ? ctx->host_ctas : ctx->max_ctas;
-  if (np == 2) return launch_copy2(p[0], p[1], Release{nullptr, 0, nullptr}, ctas, st);
-  return launch_copy(p[0], 0, p[0].runs(), Release{nullptr, 0, nullptr}, ctas, st);
+  if (np == 2) return launch_copy2(p[0], p[1], credit, ctas, st);
+  return launch_copy(p[0], 0, p[0].runs(), credit, ctas, st);
 }
 
 struct RemapOp {
@@ -874,6 +991,8 @@ static dv_status remap_check(dv_ctx* ctx, const RemapOp& op) {
   DV_TRY(check_ctx(ctx));
   DV_TRY(check_cache(op.src, "source"));
   DV_TRY(check_cache(op.dst, "destination"));
+  DV_TRY(check_cache_mapped(op.src, "source"));
+  DV_TRY(check_cache_mapped(op.dst, "destination"));
   DV_TRY(check_region_shape(&op.reg));
   const dv_region reg = resolve_heads(&op.reg, op.src);
   DV_TRY(check_cache_holds(op.src, &reg, "source"));
@@ -941,17 +1060,34 @@ static dv_status remap_run(dv_ctx* ctx, const RemapOp& op, cudaStream_t st) {
 struct Blob {
   uint32_t magic;
   uint32_t version;
-  int32_t pid;
+  uint64_t token;             // random per exporting process (same-process fast path; not the pid,
+                              // which two PID namespaces on one host can share)
   int32_t device;
+  int32_t pad;
   cudaIpcMemHandle_t handle;  // 64 bytes
   uint64_t offset;            // ptr - allocation base
   uint64_t ptr;               // exporter's address (same-process fast path)
+  uint64_t extent;            // bytes from ptr to the end of its allocation
 };
 static_assert(sizeof(Blob) <= sizeof(dv_ipc_blob), "blob too large");
 static const uint32_t kBlobMagic = 0x44564950;  // "DVIP"
 static std::mutex g_ipc_mu;
 static std::map<uintptr_t, std::pair<void*, int>> g_ipc_open;  // mapped -> (base, refcount)
 static std::map<uintptr_t, std::pair<uint64_t, int>> g_ipc_ranges;  // base -> (end, refcount)
+
+// This process's blob token: 64 random bits drawn once (getrandom), mixed with the pid and a
+// clock as a fallback.
+static uint64_t process_token() {
+  static const uint64_t tok = [] {
+    uint64_t t = 0;
+    if (syscall(SYS_getrandom, &t, sizeof t, 0) != (long)sizeof t) t = 0;
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    t ^= ((uint64_t)getpid() << 32) ^ (uint64_t)ts.tv_nsec ^ ((uint64_t)ts.tv_sec << 20);
+    return t ? t : 1;
+  }();
+  return tok;
+}
 
 static bool in_ipc_mapping(const void* p) {
   const uintptr_t a = (uintptr_t)p;
@@ -961,6 +1097,31 @@ static bool in_ipc_mapping(const void* p) {
   if (it == g_ipc_ranges.begin()) return false;
   --it;
   return a < it->second.first;
+}
+
+// A descriptor that starts inside an IPC mapping must end inside it too: caches and endpoints
+// built from raw mapped pointers are checked against the mapped allocation's extent.
+static dv_status check_mapped(const void* p, uint64_t extent, const char* name) {
+  const uintptr_t a = (uintptr_t)p;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  if (g_ipc_ranges.empty()) return DV_OK;
+  auto it = g_ipc_ranges.upper_bound(a);
+  if (it == g_ipc_ranges.begin()) return DV_OK;
+  --it;
+  if (a >= it->second.first) return DV_OK;   // not IPC-mapped memory
+  if (extent > it->second.first - a)
+    return fail(DV_EPEER, "%s: %llu bytes at an IPC-mapped address exceed the mapped allocation "
+                "(%llu bytes left): descriptor geometry does not match what the peer exported", name,
+                (unsigned long long)extent, (unsigned long long)(it->second.first - a));
+  return DV_OK;
+}
+
+static uint64_t cache_extent(const dv_cache* c) {
+  return (uint64_t)c->n_layers * c->n_reqs * c->n_heads * c->max_seq * c->head_dim * c->elem_bytes;
+}
+static dv_status check_cache_mapped(const dv_cache* c, const char* name) {
+  DV_TRY(check_mapped(c->k, cache_extent(c), name));
+  return check_mapped(c->v, cache_extent(c), name);
 }
 
 }  // namespace dv
@@ -1147,10 +1308,11 @@ dv_status dv_ipc_export(const void* ptr, dv_ipc_blob* out) {
   Blob b{};
   b.magic = kBlobMagic;
   b.version = DV_ABI_VERSION;
-  b.pid = (int32_t)getpid();
+  b.token = process_token();
   b.device = at.device;
   b.offset = (uint64_t)(uintptr_t)ptr - base;
   b.ptr = (uint64_t)(uintptr_t)ptr;
+  b.extent = base + size - (uint64_t)(uintptr_t)ptr;
   {
     DeviceGuard g(at.device);
     cudaError_t e = cudaIpcGetMemHandle(&b.handle, (void*)(uintptr_t)base);
@@ -1167,7 +1329,7 @@ dv_status dv_ipc_open(const dv_ipc_blob* blob, void** out) {
   memcpy(&b, blob->bytes, sizeof b);
   if (b.magic != kBlobMagic || b.version != DV_ABI_VERSION)
     return fail(DV_EPEER, "malformed IPC blob");
-  if (b.pid == (int32_t)getpid()) {  // same process (loopback peer): the address is valid here
+  if (b.token == process_token()) {  // same process (loopback peer): the address is valid here
     *out = (void*)(uintptr_t)b.ptr;
     return DV_OK;
   }
@@ -1189,6 +1351,15 @@ dv_status dv_ipc_open(const dv_ipc_blob* blob, void** out) {
   ent.first = base;
   ent.second += 1;
   *out = mapped;
+  return DV_OK;
+}
+
+dv_status dv_ipc_blob_bytes(const dv_ipc_blob* blob, uint64_t* out) {
+  if (!blob || !out) return fail(DV_EINVAL, "NULL argument");
+  Blob b;
+  memcpy(&b, blob->bytes, sizeof b);
+  if (b.magic != kBlobMagic || b.version != DV_ABI_VERSION) return fail(DV_EPEER, "malformed IPC blob");
+  *out = b.extent;
   return DV_OK;
 }
 
@@ -1220,9 +1391,12 @@ dv_status dv_flush(dv_ctx* ctx, const void* src, uint64_t bytes, const dv_endpoi
   if (!src && bytes) return fail(DV_EINVAL, "NULL source");
   const bool use_flag = !(xfer & DV_NO_FLAG) && flag_slot >= 0;
   DV_TRY(check_ep(dst, dst_off, bytes, flag_slot, !(xfer & DV_NO_FLAG), "destination"));
+  DV_TRY(check_ring_use(dst, flag_slot, seq, use_flag, "destination"));
+  DV_TRY(credit_check_nowait(ctx, dst, flag_slot, seq, xfer));
   DV_ON_DEVICE(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  uint8_t* d = (uint8_t*)dst->base + dst_off;
+  uint8_t* d = (uint8_t*)dst->base + dst_off + ring_off(dst, seq);
+  DV_TRY(credit_wait(ctx, dst, flag_slot, seq, xfer, st));
   const uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   if (m == DV_XFER_FUSED && bytes % 16 == 0 && (uintptr_t)src % 16 == 0) {
     CopyPlan p{};
@@ -1252,11 +1426,15 @@ dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_
   DV_TRY(check_ctx(ctx));
   if (!dst && bytes) return fail(DV_EINVAL, "NULL destination");
   DV_TRY(check_ep(src, src_off, bytes, flag_slot, !(xfer & DV_NO_FLAG), "source"));
+  const bool use_flag = !(xfer & DV_NO_FLAG) && flag_slot >= 0;
+  DV_TRY(check_ring_use(src, flag_slot, wait_seq, use_flag, "source"));
   DV_ON_DEVICE(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  if (!(xfer & DV_NO_FLAG) && flag_slot >= 0 && wait_seq)
-    DV_TRY(stream_wait(src, flag_slot, wait_seq, st));
-  const uint8_t* s = (const uint8_t*)src->base + src_off;
+  if (use_flag && wait_seq) DV_TRY(stream_wait(src, flag_slot, wait_seq, st));
+  const uint8_t* s = (const uint8_t*)src->base + src_off + ring_off(src, wait_seq);
+  Release credit{nullptr, 0, nullptr};
+  if (use_flag) DV_TRY(credit_release(ctx, src, flag_slot, wait_seq, st, &credit));
+  const int ctas = src->kind == DV_EP_HOST ? ctx->host_ctas : ctx->max_ctas;
   const uint32_t m = xfer & (DV_XFER_FUSED | DV_XFER_STAGED);
   if (m == DV_XFER_FUSED && bytes % 16 == 0 && (uintptr_t)dst % 16 == 0 && bytes) {
     CopyPlan p{};
@@ -1269,10 +1447,10 @@ dv_status dv_fetch(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off, int32_
       p.ss[kDims - 1] = p.ds[kDims - 1] = 1 << 20;
       p.run_bytes = 1u << 20;
     }
-    return launch_copy(p, 0, p.runs(), Release{nullptr, 0, nullptr},
-                       src->kind == DV_EP_HOST ? ctx->host_ctas : ctx->max_ctas, st);
+    return launch_copy(p, 0, p.runs(), credit, ctas, st);
   }
   if (bytes) DV_DMA(cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDefault, st));
+  if (credit.flag) return launch_copy(CopyPlan{}, 0, 0, credit, ctas, st);   // publish only
   return DV_OK;
 }
 
@@ -1321,6 +1499,7 @@ dv_status dv_gather_chunks(dv_ctx* ctx, const dv_endpoint* src, uint64_t src_off
   const uint64_t chunk_bytes = region_bytes(&first, dst);
   const uint64_t total = chunk_bytes * (uint64_t)n_chunks;
   DV_TRY(check_ep(src, src_off, total, flag_slot, !(xfer & DV_NO_FLAG), "source"));
+  if (has_ring(src)) return fail(DV_EINVAL, "dv_gather_chunks reads a log, not a ring inbox");
   DV_ON_DEVICE(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t row = row_bytes(dst);
@@ -1440,6 +1619,7 @@ dv_status dv_scatter_dyn(dv_ctx* ctx, const dv_cache* src, const dv_region* regi
   const dv_region last = shift_pos(reg, max_step);
   DV_TRY(check_cache_holds(src, &last, "source"));
   const uint64_t bytes = region_bytes(&reg, src);
+  if (has_ring(dst)) return fail(DV_EINVAL, "dv_scatter_dyn writes a log, not a ring inbox");
   DV_TRY(check_ep(dst, dst_off, bytes + (uint64_t)max_step * dst_step_bytes, flag_slot, true,
                   "destination"));
   if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
@@ -1597,6 +1777,12 @@ dv_status dv_signal(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint6
   DV_ON_DEVICE(ctx->device);
   if (ep->kind == DV_EP_HOST) DV_TRY(after_decoupled_flags(ctx, (cudaStream_t)stream));
   return stream_signal(ep, flag_slot, seq, (cudaStream_t)stream);
+}
+
+dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts) {
+  if (!ctx) return fail(DV_EINVAL, "NULL context");
+  ctx->trace_ts = (unsigned long long*)ts;
+  return DV_OK;
 }
 
 dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,

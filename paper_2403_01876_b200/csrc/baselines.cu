@@ -48,7 +48,7 @@ extern "C" dv_status dvb_per_run_copy(const dv_cache* src, const dv_region* regi
         for (int r = 0; r < g.nR; ++r)
           for (int h = 0; h < g.H; ++h) {
             const uint8_t* s = (kv ? g.v : g.k) + l * g.sl + r * g.sr + h * g.sh;
-            DV_DMA(cudaMemcpyAsync(w, s, g.run, cudaMemcpyDefault, (cudaStream_t)stream));
+            DV_CUDA(cudaMemcpyAsync(w, s, g.run, cudaMemcpyDefault, (cudaStream_t)stream));
             w += g.run;
             ++calls;
           }
@@ -68,12 +68,12 @@ extern "C" dv_status dvb_buffered_copy(const dv_cache* src, const dv_region* reg
       for (int kv = 0; kv < 2; ++kv)
         for (int r = 0; r < g.nR; ++r) {
           const uint8_t* s = (kv ? g.v : g.k) + l * g.sl + r * g.sr;
-          DV_DMA(cudaMemcpy2DAsync(w, g.run, s, g.sh, g.run, g.H, cudaMemcpyDefault,
+          DV_CUDA(cudaMemcpy2DAsync(w, g.run, s, g.sh, g.run, g.H, cudaMemcpyDefault,
                                     (cudaStream_t)stream));
           w += g.run * g.H;
           ++calls;
         }
-    DV_DMA(cudaMemcpyAsync(dst, staging, total, cudaMemcpyDefault, (cudaStream_t)stream));
+    DV_CUDA(cudaMemcpyAsync(dst, staging, total, cudaMemcpyDefault, (cudaStream_t)stream));
     ++calls;
   }
   if (n_calls) *n_calls = calls;

@@ -774,6 +774,30 @@ __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KP
   }
 }
 
+// Credit wait on peer memory (api.cu credit_wait): thread 0 polls with system-scope acquire loads
+// and backs off; the copy kernel behind it passes its griddepcontrol.wait only once this grid
+// has completed.
+__global__ void k_wait_geq(const unsigned long long* p, unsigned long long v) {
+  if (threadIdx.x != 0) return;
+  unsigned ns = 32;
+  for (;;) {
+    unsigned long long x;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    if (x >= v) break;
+    __nanosleep(ns);
+    if (ns < 1024) ns *= 2;
+  }
+}
+
+dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream) {
+  (void)cudaGetLastError();
+  k_wait_geq<<<1, 32, 0, stream>>>((const unsigned long long*)p, (unsigned long long)v);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "credit wait kernel launch");
+  return DV_OK;
+}
+
 static DevDiv to_dev(const FastDiv& f) { return DevDiv{f.d, f.mul, f.shr}; }
 
 // Per-device "attribute already set" bits (function attributes are per device context).
@@ -1312,6 +1336,7 @@ static void load_vec() {
 void preload_kernels() {
   (void)cluster_ctas();   // decide the cluster size (and set the attribute) outside any capture
   load_fn(k_run_copy<16, 1, 32>);
+  load_fn(k_wait_geq);
   load_vec<16>();
   load_vec<32>();
   for (int pk : {0, 1, 2, 4, 8, 16}) {

@@ -12,11 +12,16 @@
 
 #include "../../include/dv.h"
 
+// Internal helpers the separate test library (libdvstream_testing.so: testing.cu, baselines.cu)
+// calls in libdvstream.so: exported with default visibility, but C++-mangled in namespace dv and
+// declared only here -- not part of the C ABI.
+#define DV_SHARED __attribute__((visibility("default")))
+
 namespace dv {
 
 // ---- error state (thread-local message behind dv_last_error) --------------------------------
-dv_status fail(dv_status s, const char* fmt, ...);
-dv_status cuda_fail(cudaError_t e, const char* what);
+DV_SHARED dv_status fail(dv_status s, const char* fmt, ...);
+DV_SHARED dv_status cuda_fail(cudaError_t e, const char* what);
 #define DV_TRY(expr)                         \
   do {                                       \
     dv_status _s = (expr);                   \
@@ -93,6 +98,9 @@ dv_status launch_copy2(const CopyPlan& a, const CopyPlan& b, const Release& rel,
                        cudaStream_t stream);
 // Load every library kernel on the current device (no lazy loading at first launch).
 void preload_kernels();
+// Stream-ordered wait until *p >= v, by a one-thread kernel polling with system-scope acquire
+// loads (for words in peer memory, where stream memory operations are not used).
+dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream);
 
 // ---- CUDA driver entry points (resolved through the runtime; no -lcuda) --------------------
 struct Driver {
@@ -174,14 +182,14 @@ struct dv_ctx {
 
 namespace dv {
 // Validation + descriptor helpers shared by the API translation units (route.cpp, api.cu).
-dv_status check_setup(const dv_setup* s, const char* name);
-dv_status check_region_shape(const dv_region* r);
-bool all_heads(const dv_region* r);
-bool region_empty(const dv_region* r);
-dv_region resolve_heads(const dv_region* r, const dv_cache* c);  // "all heads" -> the cache's
-uint64_t region_bytes_h(const dv_region* r, int32_t H, int32_t D, int32_t e);
-dv_status check_cache(const dv_cache* c, const char* name);
-dv_status check_cache_holds(const dv_cache* c, const dv_region* r, const char* name);
+DV_SHARED dv_status check_setup(const dv_setup* s, const char* name);
+DV_SHARED dv_status check_region_shape(const dv_region* r);
+DV_SHARED bool all_heads(const dv_region* r);
+DV_SHARED bool region_empty(const dv_region* r);
+DV_SHARED dv_region resolve_heads(const dv_region* r, const dv_cache* c);  // "all heads" -> the cache's
+DV_SHARED uint64_t region_bytes_h(const dv_region* r, int32_t H, int32_t D, int32_t e);
+DV_SHARED dv_status check_cache(const dv_cache* c, const char* name);
+DV_SHARED dv_status check_cache_holds(const dv_cache* c, const dv_region* r, const char* name);
 dv_status route(const dv_setup* src, const dv_setup* dst, const dv_region* region,
                 int32_t n_heads, int32_t head_dim, int32_t elem_bytes,
                 std::vector<dv_piece>* out);

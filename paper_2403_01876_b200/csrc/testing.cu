@@ -240,12 +240,6 @@ extern "C" dv_status dvt_verify(const dv_cache* c, const void* wire, int32_t kin
   return DV_OK;
 }
 
-extern "C" dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts) {
-  if (!ctx) return fail(DV_EINVAL, "NULL context");
-  ctx->trace_ts = (unsigned long long*)ts;
-  return DV_OK;
-}
-
 extern "C" dv_status dvt_watch(const uint64_t* flag, uint64_t seq0, int32_t n, uint64_t* ts,
                                uint64_t timeout_ns, void* stream) {
   if (!flag || !ts || n < 0) return fail(DV_EINVAL, "bad dvt_watch arguments");

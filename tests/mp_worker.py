@@ -146,12 +146,87 @@ def mode_ipc(rank, world, direct):
     ctx.close()
 
 
+def mode_ring(rank, world, n=300):
+    """Rank 1 (receiver) owns a 2-slot ring inbox + flags + credits (dv_device_alloc, exported over
+    CUDA IPC); rank 0 (sender) maps them and streams n token chunks with seq 1..n. The sender's
+    credit waits poll IPC-mapped memory (the acquire-spin kernel path), its DV_NOWAIT call for seq 3
+    before the receiver has started returns DV_EBUSY; the receiver's cache equals kvgen's words."""
+    dev = int(os.environ.get("DV_MP_DEVICE", "0"))
+    torch.cuda.set_device(dev)
+    ctx = dv.dv_create(dev)
+    L, B, Hh, S, Dd, p = 3, 2, 4, 8 + n, 16, 4
+    chunk = 2 * L * B * Hh * Dd * 2
+    info = None
+    if rank == 1:
+        inbox = dv.dv_device_alloc(dev, 2 * chunk)
+        fc = dv.dv_device_alloc(dev, 16)          # flag word, then credit word
+        z = torch.zeros(2, dtype=torch.int64, device="cuda")
+        dv.dv_flush(ctx, z.data_ptr(), 16, dv.endpoint(dv.DV_EP_DEVICE, fc, 16, device=dev), 0, xfer=dv.DV_XFER_STAGED)
+        torch.cuda.synchronize()
+        info = {"inbox": dv.dv_ipc_export(inbox), "fc": dv.dv_ipc_export(fc)}
+    infos = [None] * world
+    dist.all_gather_object(infos, info)
+    seed = 321
+    if rank == 0:
+        K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, Hh, S, Dd, seed=seed)
+        k = torch.from_numpy(K.view(np.int16)).cuda()
+        v = torch.from_numpy(V.view(np.int16)).cuda()
+        src = dv.cache(k, v)
+        ib, fc = dv.dv_ipc_open(infos[1]["inbox"]), dv.dv_ipc_open(infos[1]["fc"])
+        assert dv.dv_ipc_blob_bytes(infos[1]["inbox"]) >= 2 * chunk
+        ep = dv.endpoint(dv.DV_EP_PEER, ib, 2 * chunk, fc, 1, device=dev, n_slots=2, slot_bytes=chunk,
+                         credits_ptr=fc + 8)
+        regs = [dv.region(0, L, 0, B, p + t - 1, p + t) for t in range(1, n + 1)]
+        nw = dv.DV_XFER_FUSED | dv.DV_NOWAIT
+        dv.dv_scatter(ctx, src, regs[0], ep, 0, flag_slot=0, seq=1, xfer=nw)
+        dv.dv_scatter(ctx, src, regs[1], ep, 0, flag_slot=0, seq=2, xfer=nw)
+        try:
+            dv.dv_scatter(ctx, src, regs[2], ep, 0, flag_slot=0, seq=3, xfer=nw)
+            raise AssertionError("expected DV_EBUSY: the receiver has not consumed seq 1")
+        except dv.DVError as e:
+            assert e.status == dv.DV_EBUSY, e
+        dist.barrier()                             # receiver starts consuming
+        for t in range(3, n + 1):                  # blocking: credit waits on IPC-mapped memory
+            dv.dv_scatter(ctx, src, regs[t - 1], ep, 0, flag_slot=0, seq=t)
+        torch.cuda.synchronize()
+        dist.barrier()
+        dv.dv_ipc_close(ib)
+        dv.dv_ipc_close(fc)
+        dist.barrier()
+    else:
+        dk = torch.full((L, B, Hh, S, Dd), -1, dtype=torch.int16, device="cuda")
+        dvv = torch.full_like(dk, -1)
+        dst = dv.cache(dk, dvv)
+        fcp = dv.dv_ipc_open(info["fc"])           # own allocation: maps to itself
+        ibp = dv.dv_ipc_open(info["inbox"])
+        ep = dv.endpoint(dv.DV_EP_DEVICE, ibp, 2 * chunk, fcp, 1, device=dev, n_slots=2, slot_bytes=chunk,
+                         credits_ptr=fcp + 8)
+        dist.barrier()
+        for t in range(1, n + 1):
+            if t % 50 == 0:
+                dv.dvt_spin(300_000, 1)            # a slow receiver now and then
+            dv.dv_gather(ctx, ep, 0, dst, dv.region(0, L, 0, B, p + t - 1, p + t), flag_slot=0, wait_seq=t)
+        torch.cuda.synchronize()
+        dist.barrier()
+        K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, Hh, S, Dd, seed=seed)
+        gk, gv = dk.cpu().numpy().view(np.uint16), dvv.cpu().numpy().view(np.uint16)
+        assert np.array_equal(gk[:, :, :, p:p + n], K[:, :, :, p:p + n]), "K mismatch"
+        assert np.array_equal(gv[:, :, :, p:p + n], V[:, :, :, p:p + n]), "V mismatch"
+        assert np.all(gk[:, :, :, :p] == kvgen.SENTINEL) and np.all(gk[:, :, :, p + n:] == kvgen.SENTINEL)
+        dist.barrier()
+        dv.dv_device_free(ibp)
+        dv.dv_device_free(fcp)
+    ctx.close()
+
+
 def main():
     mode = sys.argv[1]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo", rank=rank, world_size=world)
     if mode == "route":
         mode_route(rank, world)
+    elif mode == "ring":
+        mode_ring(rank, world)
     else:
         mode_ipc(rank, world, direct=(mode == "direct"))
     dist.barrier()

@@ -18,22 +18,44 @@ from oracle import kvstream as ok
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
+PRODUCT_HEADERS = ("dv.h", "dv_trace.h")
+TESTING_HEADERS = ("dv_testing.h", "dv_baselines.h")
+
+
+def declared_symbols(headers=None):
     syms = set()
     for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        if headers is not None and os.path.basename(h) not in headers:
+            continue
         for m in re.finditer(r"DV_API\s+[\w\s\*]+?\b(dv[tb]?_\w+)\s*\(", open(h).read()):
             syms.add(m.group(1))
     return syms
 
 
+def _dynamic_symbols(path):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    return {l.split()[-1] for l in out.splitlines() if " T " in l}
+
+
 def test_library_exports_every_declared_symbol():
+    """libdvstream.so exports exactly the C symbols of dv.h + dv_trace.h (the product); the test
+    utilities and prior-art baselines of dv_testing.h / dv_baselines.h live in the separate
+    libdvstream_testing.so and are NOT in the product library."""
     L = dv.lib()
-    syms = declared_symbols()
-    assert len(syms) >= 29
-    missing = [s for s in syms if not hasattr(L, s)]
+    prod, test = declared_symbols(PRODUCT_HEADERS), declared_symbols(TESTING_HEADERS)
+    assert declared_symbols() == prod | test and not prod & test
+    assert len(prod) >= 30 and len(test) >= 7
+    missing = [s for s in prod if not hasattr(L, s)]
     assert not missing, missing
-    assert set(dv.exported_symbols()) == syms
-    assert dv.dv_abi_version() == 2
+    assert set(dv.exported_symbols()) == prod and set(dv.testing_symbols()) == test
+    T = dv.testing_lib()
+    assert not [s for s in test if not hasattr(T, s)]
+    c_prod = {s for s in _dynamic_symbols(dv.LIB_PATH) if s.startswith(("dv_", "dvt_", "dvb_"))}
+    c_test = {s for s in _dynamic_symbols(dv.TESTING_LIB_PATH) if s.startswith(("dv_", "dvt_", "dvb_"))}
+    assert c_prod == prod, c_prod ^ prod
+    assert c_test == test, c_test ^ test
+    assert dv.dv_abi_version() == 3
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -231,3 +231,163 @@ def test_bulk_host_reads_match_oracle(rdch, rdst):
     r = subprocess.run([sys.executable, "-c", BULK_SCRIPT, ROOT], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------------------------------------
+# Inbox rings with credits (include/dv.h dv_endpoint; SURVEY §8(a) A5 "inbox credits per slot",
+# §8(b) DV_EBUSY; the token machines consume a mailbox)
+def _ring_case(n_steps, seed):
+    L, B, H, S, D, p = 3, 2, 4, 64 + n_steps, 16, 4
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=seed)
+    return (L, B, H, S, D, p), K, V
+
+
+@pytest.mark.parametrize("inbox_host", [False, True])
+def test_ring_credits_stream_1000_chunks_through_two_slots(inbox_host):
+    """1,000 token chunks (one position of every layer each, seq 1..1000) go through an inbox of
+    only TWO ring slots: the sender's stream writes seq s into slot s % 2 only after the receiver
+    released credit s - 2; the receiver (another stream, stalled now and then by spin kernels)
+    waits on the flag, unpacks into its cache and releases the credit. Every position of the
+    receiver's cache equals the oracle's stream of the same region."""
+    n = 1000
+    (L, B, H, S, D, p), K, V = _ring_case(n, 101)
+    k, v = to_dev(K), to_dev(V)
+    src = dv.cache(k, v)
+    chunk = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    if inbox_host:
+        inbox = pinned_u16(2 * chunk // 2)
+        fl, cr = flags(1, pinned=True), flags(1, pinned=True)
+    else:
+        inbox = torch.full((2 * chunk // 2,), -1, dtype=torch.int16, device="cuda")
+        fl, cr = flags(1), flags(1)
+    ep = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk, credits=cr)
+    dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    dst = dv.cache(dk, dvv)
+    cx = ctx()
+    s_send, s_recv = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for t in range(1, n + 1):
+        reg = dv.region(0, L, 0, B, p + t - 1, p + t)
+        dv.dv_scatter(cx, src, reg, ep, 0, flag_slot=0, seq=t, xfer=dv.DV_XFER_FUSED, stream=s_send.cuda_stream)
+        if t % 97 == 0:
+            dv.dvt_spin(200_000, 1, stream=s_recv.cuda_stream)   # a slow receiver
+        if t % 89 == 0:
+            dv.dvt_spin(100_000, 1, stream=s_send.cuda_stream)   # a slow sender
+        dv.dv_gather(cx, ep, 0, dst, reg, flag_slot=0, wait_seq=t, stream=s_recv.cuda_stream)
+    torch.cuda.synchronize()
+    assert int(fl[0]) == n and int(cr[0]) == n
+    o = ok.Cache(*kvgen.sentinel_cache(L, B, H, S, D), 0, 0, H, S, D)
+    ok.stream({(0, 0): ok.Cache(K, V, 0, 0, H, S, D)}, ok.Setup([0, L], [0, B], S), {(0, 0): o},
+              ok.Setup([0, L], [0, B], S), (0, L, 0, B, p, p + n))
+    assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)
+
+
+def test_ring_without_credits_overwrites_unread_slots():
+    """Negative control for the test above: the same 2-slot ring WITHOUT credits lets the sender
+    overwrite slots the (stalled) receiver has not read -- the receiver's cache then differs from
+    the oracle. (Shows the credit test can fail.)"""
+    n = 64
+    (L, B, H, S, D, p), K, V = _ring_case(n, 102)
+    k, v = to_dev(K), to_dev(V)
+    src = dv.cache(k, v)
+    chunk = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    inbox = torch.full((2 * chunk // 2,), -1, dtype=torch.int16, device="cuda")
+    fl = flags(1)
+    ep = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk)   # no credits
+    dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    cx = ctx()
+    s_send, s_recv = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    dv.dvt_spin(5_000_000, 1, stream=s_recv.cuda_stream)          # receiver stalled 5 ms
+    for t in range(1, n + 1):
+        reg = dv.region(0, L, 0, B, p + t - 1, p + t)
+        dv.dv_scatter(cx, src, reg, ep, 0, flag_slot=0, seq=t, stream=s_send.cuda_stream)
+        dv.dv_gather(cx, ep, 0, dv.cache(dk, dvv), reg, flag_slot=0, wait_seq=t, stream=s_recv.cuda_stream)
+    torch.cuda.synchronize()
+    o = ok.Cache(*kvgen.sentinel_cache(L, B, H, S, D), 0, 0, H, S, D)
+    ok.stream({(0, 0): ok.Cache(K, V, 0, 0, H, S, D)}, ok.Setup([0, L], [0, B], S), {(0, 0): o},
+              ok.Setup([0, L], [0, B], S), (0, L, 0, B, p, p + n))
+    assert not (np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V))
+
+
+def test_ring_nowait_returns_ebusy_without_partial_effect():
+    """DV_NOWAIT: a sender whose ring slot still holds an unconsumed chunk gets DV_EBUSY and
+    nothing is enqueued (inbox bytes and flag unchanged); once the receiver has consumed seq 1
+    the same call succeeds. Also the validation of ring descriptors."""
+    (L, B, H, S, D, p), K, V = _ring_case(8, 103)
+    k, v = to_dev(K), to_dev(V)
+    src = dv.cache(k, v)
+    chunk = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    inbox = torch.full((2 * chunk // 2,), -1, dtype=torch.int16, device="cuda")
+    fl, cr = flags(1), flags(1)
+    ep = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk, credits=cr)
+    cx = ctx()
+    regs = [dv.region(0, L, 0, B, p + t, p + t + 1) for t in range(4)]
+    nw = dv.DV_XFER_FUSED | dv.DV_NOWAIT
+    dv.dv_scatter(cx, src, regs[0], ep, 0, flag_slot=0, seq=1, xfer=nw)
+    dv.dv_scatter(cx, src, regs[1], ep, 0, flag_slot=0, seq=2, xfer=nw)
+    torch.cuda.synchronize()
+    before = inbox.clone()
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(cx, src, regs[2], ep, 0, flag_slot=0, seq=3, xfer=nw)
+    assert ei.value.status == dv.DV_EBUSY
+    torch.cuda.synchronize()
+    assert torch.equal(inbox, before) and int(fl[0]) == 2
+    dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    dv.dv_gather(cx, ep, 0, dv.cache(dk, dvv), regs[0], flag_slot=0, wait_seq=1)
+    torch.cuda.synchronize()
+    assert int(cr[0]) == 1
+    dv.dv_scatter(cx, src, regs[2], ep, 0, flag_slot=0, seq=3, xfer=nw)   # slot 1 is free now
+    torch.cuda.synchronize()
+    assert int(fl[0]) == 3
+    w = to_np(inbox)
+    osrc = ok.Cache(K, V, 0, 0, H, S, D)
+    assert np.array_equal(w[chunk // 2:], ok.pack(osrc, (0, L, 0, B, p + 2, p + 3)))   # slot 3 % 2 = 1
+    assert np.array_equal(w[:chunk // 2], ok.pack(osrc, (0, L, 0, B, p + 1, p + 2)))   # slot 0 = seq 2
+    # ring descriptors are validated: chunk larger than a slot, slot not a multiple of 16, no flag
+    bad = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk - 16, credits=cr)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(cx, src, regs[3], bad, 0, flag_slot=0, seq=4)
+    assert ei.value.status == dv.DV_EINVAL
+    bad = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk + 8, credits=cr)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(cx, src, regs[3], bad, 0, flag_slot=0, seq=4)
+    assert ei.value.status == dv.DV_EALIGN
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_scatter(cx, src, regs[3], ep, 0, flag_slot=-1, seq=4)
+    assert ei.value.status == dv.DV_EINVAL
+
+
+def test_ring_stream_out_in_two_sources_one_inbox():
+    """Level 1 with a 2-slot ring inbox: two prompt blocks (layer split [0,3) [3,6)) stream 40
+    token steps each into ONE token block (all 6 layers) through the same ring inbox; each source
+    has its own flag and credit slot. The token cache equals the oracle's disaggregation result
+    (PAPER.md:266)."""
+    L, B, H, S, D, p, n = 6, 2, 3, 64, 16, 8, 40
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=104)
+    ps, ts = dv.Setup([0, 3, 6], [0, B], S), dv.Setup([0, L], [0, B], S)
+    tensors = [(to_dev(K[a:b]), to_dev(V[a:b])) for a, b in ((0, 3), (3, 6))]
+    srcs = [dv.cache(kk, vv, a, 0) for (kk, vv), a in zip(tensors, (0, 3))]   # tensors own the memory
+    chunk = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    inbox = torch.full((2 * chunk // 2,), -1, dtype=torch.int16, device="cuda")
+    fl, cr = flags(2), flags(2)
+    ep = dv.endpoint_of(inbox, fl, n_slots=2, slot_bytes=chunk, credits=cr)
+    dk, dvv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    dst = dv.cache(dk, dvv)
+    cx = ctx()
+    s_send = [torch.cuda.Stream(), torch.cuda.Stream()]
+    s_recv = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for t in range(1, n + 1):
+        reg = dv.region(0, L, 0, B, p + t - 1, p + t)
+        for i in range(2):
+            dv.dv_stream_out(cx, srcs[i], reg, ps, i, 0, ts, [ep], seq=t, stream=s_send[i].cuda_stream)
+        if t % 7 == 0:
+            dv.dvt_spin(150_000, 1, stream=s_recv.cuda_stream)
+        dv.dv_stream_in(cx, dst, reg, ps, ts, 0, 0, ep, t, stream=s_recv.cuda_stream)
+    torch.cuda.synchronize()
+    assert fl.tolist() == [n, n] and cr.tolist() == [n, n]
+    o = ok.Cache(*kvgen.sentinel_cache(L, B, H, S, D), 0, 0, H, S, D)
+    osrc = {(0, 0): ok.Cache(K[:3], V[:3], 0, 0, H, S, D), (1, 0): ok.Cache(K[3:], V[3:], 3, 0, H, S, D)}
+    ok.stream(osrc, ok.Setup([0, 3, 6], [0, B], S), {(0, 0): o}, ok.Setup([0, L], [0, B], S), (0, L, 0, B, p, p + n))
+    assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)

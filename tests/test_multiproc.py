@@ -57,6 +57,14 @@ def test_cross_process_ipc_stream(mode):
 
 
 @pytest.mark.gpu
+def test_cross_process_ring_inbox_with_credits():
+    """A 2-slot ring inbox with credits shared over CUDA IPC between a sender and a receiver
+    process: 300 chunks, DV_EBUSY for a NOWAIT send into an unconsumed slot, blocking credit waits
+    on IPC-mapped memory (the acquire-spin kernel), the receiver's cache == kvgen's words."""
+    _run("ring", 2)
+
+
+@pytest.mark.gpu
 def test_bench_multirank_launch_path():
     """bench.py under torchrun with 2 ranks (both on the one available GPU, gloo plumbing): the
     weak-scaling path runs, takes the max over ranks and rank 0 prints one JSON line."""
