@@ -12,8 +12,11 @@ with its sequence flag published -- all hot-path rows of SURVEY §8(a) for the h
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--xfer auto|fused|staged]
 
 N > 1 (torchrun): every rank is an independent pipeline stage streaming its own C2 cache to its own
-pinned host memory (weak scaling, no data-path collective); time = max over ranks.
-Rank 0 prints ONE JSON line.
+pinned host memory (weak scaling, no data-path collective); time = max over ranks; `value` stays
+this C2 figure at every N. The same line then carries "nvlink": the peer paths of north_star on
+the N GPUs (tools/bench_peer.py nvlink_suite: in-run link peaks, C5 ring replication at P = N,
+C3 N/2 -> N/2 disaggregation, their NCCL send/recv baselines, per-layer put latency with the
+system-scope release, every delivered word verified on the device). Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -40,6 +43,7 @@ CONFIG = {"workload": "C2 OPT-13B shape (L40 H40 D128, fp16 words) b8 p1000 S204
           "l2": "inputs larger than L2: 13.4 GB device cache, every step reads a fresh position "
                 "(new 256-B lines); host log ring 64 steps = 419 MB"}
 METRIC = "KV stream GB/s (token-step stream-out to pinned host)"
+PCIE_NOMINAL_GBS = 64.0   # PCIe Gen5 x16 per direction (nominal)
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -137,6 +141,10 @@ def run_ours(args):
     log = torch.empty(RING * STEP_BYTES // 2, dtype=torch.int16, pin_memory=True)
     fl = torch.zeros(4, dtype=torch.int64, pin_memory=True)
     ep = dv.endpoint_of(log, fl)
+    # the same log as the level-1 destination: a ring inbox of RING step-sized slots (token step t
+    # lands in slot t % RING; include/dv.h rings), read by the host consumer -- no credits
+    ring = dv.endpoint_array([dv.endpoint_of(log, fl, n_slots=RING, slot_bytes=STEP_BYTES)])
+    stage = dv.Setup([0, L], [0, B], S)        # this GPU's stage: all C2 layers, one microbatch
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     npos = S - P
@@ -145,9 +153,10 @@ def run_ours(args):
         return P + (t - 1) % npos
 
     def step(t, xf=xfer):
+        # the whole hot path per token step: route (level 1, A1) -> pack (A2) -> PCIe put (A3b) ->
+        # seq flag (A5), through dv_stream_out into the host log's ring slot t % RING
         q = pos_of(t)
-        dv.dv_scatter(ctx, cache, (0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
-                      flag_slot=0, seq=t, xfer=xf, stream=sp)
+        dv.dv_stream_out(ctx, cache, (0, L, 0, B, q, q + 1), stage, 0, 0, stage, ring, seq=t, xfer=xf, stream=sp)
 
     torch.cuda.synchronize()
     clocks = Clocks(local)
@@ -223,8 +232,8 @@ def run_ours(args):
         e = evs[t % 8]
         e.record(s_in)
         stream.wait_event(e)
-        dv.dv_scatter(ctx, cache, dv.region(0, L, 0, B, q, q + 1), ep, (t % RING) * STEP_BYTES,
-                      flag_slot=0, seq=10_000_000 + t, xfer=xfer, stream=sp)
+        dv.dv_stream_out(ctx, cache, (0, L, 0, B, q, q + 1), stage, 0, 0, stage, ring, seq=10_000_000 + t,
+                         xfer=xfer, stream=sp)
     for t in range(1, args.warmup + 1):
         e2e_step(t)
     torch.cuda.synchronize()
@@ -248,6 +257,16 @@ def run_ours(args):
     extras = {}
     if not args.no_extras and rank == 0:
         extras = run_extras(dv, ctx, cache, stream, args, pos_of)
+    nvlink = None
+    if world > 1 and not args.no_nvlink:
+        # the peer paths of north_star on the N GPUs of this box (tools/bench_peer.py): link peaks,
+        # C5 ring replication, C3 disaggregation, NCCL send/recv baselines, every word verified
+        from tools import bench_peer
+        del k, v
+        torch.cuda.empty_cache()
+        env = bench_peer.Env(backend)
+        env.local, env.dev = local, dev
+        nvlink = bench_peer.nvlink_suite(ctx, env, steps=args.nvlink_steps)
     clk = clocks.stop()
 
     value = world * args.steps * STEP_BYTES / (elapsed_ms * 1e-3) / 1e9
@@ -263,27 +282,25 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     if args.xfer in ("auto", "fused"):
-        dram_traffic, pcie_traffic = _ncu_traffic("final")
-        roof = {"bound": "pcie", "achieved": STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9,
-                "peak": pcie_peak, "unit": "GB/s",
-                "frac": (STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9 / pcie_peak) if pcie_peak else None,
+        dram_traffic, pcie_traffic, tsrc = _ncu_traffic("fused")
+        ach = STEP_BYTES / (mean_kernel_ms * 1e-3) / 1e9
+        roof = {"bound": "pcie", "achieved": ach, "peak": pcie_peak, "unit": "GB/s",
+                "frac": (ach / pcie_peak) if pcie_peak else None,
                 "traffic": dram_traffic, "traffic_pcie_write": pcie_traffic,
-                "traffic_source": "profiles/r01_io_counters_final.csv (ncu dram__bytes_read+write, "
-                                  "pcie__write_bytes per launch, median)",
+                "traffic_source": tsrc + " (ncu dram__bytes_read+write, pcie__write_bytes per launch, median)",
                 "kernel": "k_run_copy (fused pack -> pinned host zero-copy PCIe stores + st.release.sys flag)"}
     else:
         # decoupled / staged: the step's bytes cross PCIe by the copy engine (one cudaMemcpyAsync of
         # the packed step per step, back to back on the library's DMA stream); the pack kernel
         # (k_run_copy, cache -> HBM staging) is a few us of HBM work beside it. achieved = bytes per
         # step / device time per step (a lower bound of the DMA's own rate).
-        dram_traffic, pcie_traffic = _ncu_traffic("decoupled")
+        dram_traffic, pcie_traffic, tsrc = _ncu_traffic("decoupled")
         ach = STEP_BYTES / (elapsed_ms / args.steps * 1e-3) / 1e9
         roof = {"bound": "pcie", "achieved": ach, "peak": pcie_peak, "unit": "GB/s",
                 "frac": ach / pcie_peak if pcie_peak else None,
                 "traffic": dram_traffic,
-                "traffic_source": "profiles/r01g_io_counters.csv: ncu dram__bytes_read+write "
-                                  "per launch of the pack kernel (HBM side; the copy engine's PCIe "
-                                  "bytes are not a kernel counter), median",
+                "traffic_source": tsrc + ": ncu dram__bytes_read+write per launch of the pack kernel (HBM "
+                                  "side; the copy engine's PCIe bytes are not a kernel counter), median",
                 "kernel": "copy-engine D2H of the packed step (cudaMemcpyAsync on the library DMA "
                           "stream), fed by k_run_copy pack (cache -> HBM staging), flag by a stream "
                           "write on the library flag stream",
@@ -292,6 +309,7 @@ def run_ours(args):
     roof.update({
         "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
         "algorithmic_bytes_per_launch": STEP_BYTES,
+        "peak_nominal": PCIE_NOMINAL_GBS, "frac_nominal": roof["achieved"] / PCIE_NOMINAL_GBS,
         "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
                        "PCIe Gen5 x16 nominal 64 GB/s"})
     line = {
@@ -299,8 +317,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
         "data": "synthetic (splitmix64 coordinate-hash fill, seed 20240305)",
-        "config": dict(CONFIG, parallelism=f"independent stages x{world}" if world > 1 else "1 stage",
-                       xfer=args.xfer, cpu_affinity=cpu_affinity),
+        "config": _config(world),
+        "run": {"xfer": args.xfer, "cpu_affinity": cpu_affinity,
+                "api": "dv_stream_out (level 1: route -> pack -> put -> flag) into a 64-slot ring in pinned host memory"},
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": STEP_BYTES,
                 "d2h_bytes_per_step": STEP_BYTES,
                 "how": "per step: dv_gather of the token's K/V from pinned host into the device cache "
@@ -315,6 +334,8 @@ def run_ours(args):
         "us_per_token_layer": (extras.get("token_layer_latency", {}).get("host") or {}).get("p50_us"),
         "extras": extras,
     }
+    if world > 1:
+        line["nvlink"] = nvlink if nvlink is not None else {"skipped": "--no-nvlink"}
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -341,26 +362,40 @@ def _bind_gpu_local_cpus(index):
         return None
 
 
-def _ncu_traffic(name="final"):
-    """DRAM and PCIe bytes per launch of the headline kernel from the committed ncu capture
-    (profiles/r01_io_counters_<name>.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
-    pcie__write_bytes.sum on this same command), median over the captured launches."""
+def _config(world):
+    """The workload's config -- identical in both arms (ours and --impl reference) at every N."""
+    return dict(CONFIG, parallelism=f"independent stages x{world}" if world > 1 else "1 stage")
+
+
+def _ncu_traffic(name="decoupled"):
+    """DRAM and PCIe bytes per launch of the headline kernel from the committed ncu capture of this
+    same command (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,pcie__write_bytes.sum),
+    median over the captured launches of the pack kernel. Returns (dram, pcie, source) where the
+    source names the file and the sha256 of its content (so the line pins the exact capture)."""
     import csv
-    path = os.path.join(ROOT, "profiles", {"decoupled": "r01g_io_counters.csv"}.get(name, f"r01_io_counters_{name}.csv"))
-    try:
-        rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
-    except OSError:
-        return None, None
-    hdr, body = rows[0], rows[1:]
-    per = {}
-    for r in body:
-        d = dict(zip(hdr, r))
-        per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"])
-    dram = sorted(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in per.values())
-    pcie = sorted(v.get("pcie__write_bytes.sum", 0) for v in per.values())
-    if not dram:
-        return None, None
-    return dram[len(dram) // 2], pcie[len(pcie) // 2]
+    import hashlib
+    files = {"decoupled": ["r02_io_counters.csv", "r01g_io_counters.csv"],
+             "fused": ["r02_io_counters_fused.csv", "r01_io_counters_final.csv"]}[name]
+    for fn in files:
+        path = os.path.join(ROOT, "profiles", fn)
+        try:
+            raw = open(path, "rb").read()
+        except OSError:
+            continue
+        rows = [r for r in csv.reader(l for l in raw.decode().splitlines() if l.startswith('"'))]
+        hdr, body = rows[0], rows[1:]
+        per = {}
+        for r in body:
+            d = dict(zip(hdr, r))
+            if "k_run_copy" not in d.get("Kernel Name", "k_run_copy"):
+                continue
+            per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"])
+        dram = sorted(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in per.values())
+        pcie = sorted(v.get("pcie__write_bytes.sum", 0) for v in per.values())
+        if dram:
+            return (dram[len(dram) // 2], pcie[len(pcie) // 2],
+                    f"profiles/{fn} sha256:{hashlib.sha256(raw).hexdigest()[:16]}")
+    return None, None, None
 
 
 def _spot_check(wire, q, seed):
@@ -754,7 +789,8 @@ def run_reference(args):
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u16 (opaque fp16 words)", "data": "synthetic",
-            "config": dict(CONFIG, parallelism="1 stage (CPU oracle)"),
+            "config": _config(int(os.environ.get("WORLD_SIZE", "1"))),
+            "run": {"oracle": "numpy, one host process (rank 0 at N > 1)"},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"{args.steps} timed C2 token steps of the numpy oracle on host cores"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -772,6 +808,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-nvlink", action="store_true", help="N > 1: skip the peer-path suite in the JSON line")
+    ap.add_argument("--nvlink-steps", type=int, default=200, help="N > 1: C5 token steps timed in the peer suite")
     ap.add_argument("--peer-baseline", default="none", choices=["none", "nccl"],
                     help="c3/c5: run the NCCL send/recv baseline (pack -> ncclSend/ncclRecv -> unpack) instead of dvstream's peer stores")
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],

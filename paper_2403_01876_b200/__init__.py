@@ -563,12 +563,22 @@ def dv_remap_dyn(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, d_step_ptr, 
 def dv_stream_out(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
                   dst_setup: Setup, inboxes, seq, xfer=0, stream=None, my_tp=0):
     arr = endpoint_array(inboxes)
+    f = _fast or fast()
+    if f:
+        return _check(f.stream_out(ctx.addr, _addr(src), _reg_fast(reg), _addr(src_setup.c), my_stage, my_micro, my_tp,
+                                   _addr(dst_setup.c), _addr(arr), len(arr), seq, xfer, _sint(stream)),
+                      "dv_stream_out")
     _call("dv_stream_out", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage, my_micro,
-          my_tp, C.byref(dst_setup.c), arr, len(inboxes), seq, xfer, _stream(stream))
+          my_tp, C.byref(dst_setup.c), arr, len(arr), seq, xfer, _stream(stream))
 
 
 def dv_stream_in(ctx, dst: dv_cache, reg: dv_region, src_setup: Setup, dst_setup: Setup, my_stage,
                  my_micro, inbox: dv_endpoint, wait_seq, xfer=0, stream=None, my_tp=0):
+    f = _fast or fast()
+    if f:
+        return _check(f.stream_in(ctx.addr, _addr(dst), _reg_fast(reg), _addr(src_setup.c), _addr(dst_setup.c),
+                                  my_stage, my_micro, my_tp, _addr(inbox), wait_seq, xfer, _sint(stream)),
+                      "dv_stream_in")
     _call("dv_stream_in", ctx.h, C.byref(dst), _reg_ct(reg), C.byref(src_setup.c), C.byref(dst_setup.c),
           my_stage, my_micro, my_tp, C.byref(inbox), wait_seq, xfer, _stream(stream))
 

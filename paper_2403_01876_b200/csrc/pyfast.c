@@ -138,6 +138,47 @@ static PyObject* f_stream_out_direct(PyObject* self, PyObject* const* a, Py_ssiz
   return PyLong_FromLong(s);
 }
 
+/* stream_out(ctx, src*, region*, src_setup*, my_stage, my_micro, my_tp, dst_setup*, inboxes*,
+ *            n_inboxes, seq, xfer, stream) */
+static PyObject* f_stream_out(PyObject* self, PyObject* const* a, Py_ssize_t nargs) {
+  NARGS(13);
+  void *ctx, *src, *reg, *ss, *ds, *ib, *st;
+  dv_region rt;
+  int32_t stage, micro, tp, n;
+  uint64_t seq, xfer;
+  if (get_ptr(a[0], &ctx) || get_ptr(a[1], &src) || get_region(a[2], &rt, &reg) || get_ptr(a[3], &ss) ||
+      get_i32(a[4], &stage) || get_i32(a[5], &micro) || get_i32(a[6], &tp) || get_ptr(a[7], &ds) ||
+      get_ptr(a[8], &ib) || get_i32(a[9], &n) || get_u64(a[10], &seq) || get_u64(a[11], &xfer) ||
+      get_ptr(a[12], &st))
+    return NULL;
+  dv_status s;
+  Py_BEGIN_ALLOW_THREADS
+  s = dv_stream_out((dv_ctx*)ctx, (const dv_cache*)src, (const dv_region*)reg, (const dv_setup*)ss, stage,
+                    micro, tp, (const dv_setup*)ds, (const dv_endpoint*)ib, n, seq, (uint32_t)xfer, st);
+  Py_END_ALLOW_THREADS
+  return PyLong_FromLong(s);
+}
+
+/* stream_in(ctx, dst*, region*, src_setup*, dst_setup*, my_stage, my_micro, my_tp, inbox*, wait_seq,
+ *           xfer, stream) */
+static PyObject* f_stream_in(PyObject* self, PyObject* const* a, Py_ssize_t nargs) {
+  NARGS(12);
+  void *ctx, *dst, *reg, *ss, *ds, *ib, *st;
+  dv_region rt;
+  int32_t stage, micro, tp;
+  uint64_t seq, xfer;
+  if (get_ptr(a[0], &ctx) || get_ptr(a[1], &dst) || get_region(a[2], &rt, &reg) || get_ptr(a[3], &ss) ||
+      get_ptr(a[4], &ds) || get_i32(a[5], &stage) || get_i32(a[6], &micro) || get_i32(a[7], &tp) ||
+      get_ptr(a[8], &ib) || get_u64(a[9], &seq) || get_u64(a[10], &xfer) || get_ptr(a[11], &st))
+    return NULL;
+  dv_status s;
+  Py_BEGIN_ALLOW_THREADS
+  s = dv_stream_in((dv_ctx*)ctx, (const dv_cache*)dst, (const dv_region*)reg, (const dv_setup*)ss,
+                   (const dv_setup*)ds, stage, micro, tp, (const dv_endpoint*)ib, seq, (uint32_t)xfer, st);
+  Py_END_ALLOW_THREADS
+  return PyLong_FromLong(s);
+}
+
 /* wait(ctx, ep*, flag_slot, seq, stream) and signal(...) */
 static PyObject* f_wait_signal(PyObject* const* a, Py_ssize_t nargs, int signal) {
   NARGS(5);
@@ -164,6 +205,8 @@ static PyMethodDef methods[] = {
     {"remap", (PyCFunction)(void (*)(void))f_remap, METH_FASTCALL, "dv_remap"},
     {"stream_out_direct", (PyCFunction)(void (*)(void))f_stream_out_direct, METH_FASTCALL,
      "dv_stream_out_direct"},
+    {"stream_out", (PyCFunction)(void (*)(void))f_stream_out, METH_FASTCALL, "dv_stream_out"},
+    {"stream_in", (PyCFunction)(void (*)(void))f_stream_in, METH_FASTCALL, "dv_stream_in"},
     {"wait", (PyCFunction)(void (*)(void))f_wait, METH_FASTCALL, "dv_wait"},
     {"signal", (PyCFunction)(void (*)(void))f_signal, METH_FASTCALL, "dv_signal"},
     {NULL, NULL, 0, NULL}};

@@ -106,7 +106,7 @@ def test_fast_path_module_builds_and_exports():
     entry points; a malformed call raises instead of reaching the library."""
     f = dv.fast()
     assert f is not None and f.__file__.startswith(os.path.dirname(dv.__file__))
-    for name in ("scatter", "gather", "remap", "stream_out_direct", "wait", "signal"):
+    for name in ("scatter", "gather", "remap", "stream_out", "stream_in", "stream_out_direct", "wait", "signal"):
         assert callable(getattr(f, name))
     with pytest.raises(TypeError):
         f.scatter(0, 0)

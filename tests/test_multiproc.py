@@ -64,23 +64,45 @@ def test_cross_process_ring_inbox_with_credits():
     _run("ring", 2)
 
 
+def _no_errors(d, path="nvlink"):
+    if isinstance(d, dict):
+        assert "error" not in d, f"{path}: {d.get('error')}"
+        for k, v in d.items():
+            _no_errors(v, f"{path}.{k}")
+
+
 @pytest.mark.gpu
-def test_bench_multirank_launch_path():
-    """bench.py under torchrun with 2 ranks (both on the one available GPU, gloo plumbing): the
-    weak-scaling path runs, takes the max over ranks and rank 0 prints one JSON line."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_multirank_launch_path(world):
+    """bench.py under torchrun with N ranks (all on the one available GPU, gloo plumbing; shrunk
+    peer shapes): the weak-scaling C2 path runs, takes the max over ranks, and rank 0 prints ONE
+    JSON line that also carries the peer-path suite ("nvlink": link peaks, C5 ring replication,
+    C3 disaggregation, their send/recv baselines) -- every delivered word verified clean. On an
+    N-GPU box the driver's scaling run executes exactly this path across NVLink."""
     import json
     port = _free_port()
-    env = dict(os.environ, DV_BENCH_SAME_DEVICE="1")
+    env = dict(os.environ, DV_BENCH_SAME_DEVICE="1", DV_BENCH_PEER_SMALL="1")
     root = os.path.dirname(HERE)
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
                         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
-                        "--gpus", "2", "--steps", "20", "--warmup", "3", "--no-extras", "--no-cpu-baseline",
-                        "--dist-backend", "gloo"], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+                        "--gpus", str(world), "--steps", "20", "--warmup", "3", "--no-extras", "--no-cpu-baseline",
+                        "--dist-backend", "gloo", "--nvlink-steps", "16"], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] == 20
+    assert d["n_gpus"] == world and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] == 20
+    nv = d["nvlink"]
+    _no_errors(nv)
+    assert len(nv["devices"]) == world and nv["link"]["peak_gbs"] > 0
+    c5, c3 = nv["c5"], nv["c3"]
+    assert c5["parity"]["mismatches"] == 0 and c5["nccl_baseline"]["parity"]["mismatches"] == 0
+    assert c3["parity"]["mismatches"] == 0 and c3["parity"]["positions_past_prompt_untouched"]
+    assert c3["nccl_baseline"]["parity"]["mismatches"] == 0
+    assert c5["latency_per_layer_put"]["release_scope"] == "system" and c5["latency_per_layer_put"]["p50_us"] > 0
+    assert c5["pingpong"]["rtt_us"] > 0 and c5["token_step"]["gbs_per_gpu"] > 0 and c3["handoff"]["gbs_per_prompt_gpu"] > 0
+    assert d["config"] == json.loads(json.dumps(d["config"])) and "xfer" not in d["config"]
 
 
 @pytest.mark.gpu

@@ -1,20 +1,34 @@
-"""Peer (NVLink) workloads for bench.py: one process per GPU, CUDA-IPC-mapped destinations.
+"""Peer (NVLink) workloads: one process per GPU, CUDA-IPC-mapped destinations.
 
-  C5 ring (BASELINE.json configs[4]): OPT-66B shape (72 heads, head_dim 128), b 16, P = N stages
-     of 64/N layers (8 layers at N = 1, loopback); after the prompt (p = 1024) every token step
-     each stage streams its new K/V (all its layers, one position) into the replica store it
-     keeps at (x+1)%P with dv_stream_out_direct and a seq flag in the successor's
-     memory. One STEP = one token step of every stage.
-  C3 disaggregation (configs[2]): OPT-66B, b 8, p 1000; N/2 prompt GPUs -> N/2 token GPUs with a
-     different layer partition (S 1024 -> 2048); one STEP = one prompt's full hand-off, layer by
-     layer (Opt 2), straight into the token GPUs' caches. N = 1: both sides on one GPU (loopback).
+Used two ways:
+  * `bench.py --gpus N` (N > 1, the driver's scaling run) calls `nvlink_suite()` after the C2
+    headline: every peer path of north_star measured on the N GPUs of the box, with parity, in the
+    SAME JSON line (key "nvlink");
+  * `bench.py --workload c3|c5` prints one line for that workload alone (`run_c3` / `run_c5`).
 
-Both print the same JSON contract line as bench.py's default workload (metric = aggregate GB/s of
-KV bytes delivered, time = max over ranks).
+The measurements (all timed on the device with CUDA events, max over ranks):
+  link    in-run peer peaks: copy-engine (cudaMemcpyAsync into the successor's IPC-mapped buffer)
+          and SM stores (dv_flush FUSED), all ranks sending to (x+1)%N at once (ring) and, for
+          N >= 2, even ranks only (one direction per link) -- the roofline denominators;
+  C5      ring replication (BASELINE.json configs[4], §4.2.3): OPT-66B shape (72 heads,
+          head_dim 128), b 16, P = N stages of 64/N layers. The prompt (p = 1024) is replicated in
+          bulk into the successor's replica store (reading Q13), then token steps (one position of
+          all the stage's layers per step); per-layer put latency (writer end ->
+          system-scope release of the seq flag, %globaltimer) and a ping-pong RTT; NCCL baseline
+          (pack -> ncclSend/ncclRecv -> unpack) for the same token steps and the same prompt
+          replica; every word of every replica store checked on the device (dvt_verify);
+  C3      prompt->token disaggregation (configs[2], §4.2.1): OPT-66B b 8, p 1000;
+          N/2 prompt GPUs (S 1024) hand their prompt KV layer by layer (Opt 2)
+          straight into N/2 token GPUs with a different layer partition (S 2048); NCCL baseline
+          (per layer pack -> send to the owning token rank -> unpack); every word of every token
+          cache checked on the device, and positions >= p still the sentinel.
+At N = 1 the same code runs as loopback (the "peer" is this GPU: HBM-bound).
+DV_BENCH_PEER_SMALL=1 shrinks the shapes (tests with all ranks on one GPU).
 """
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -25,37 +39,88 @@ import torch.distributed as dist  # noqa: E402
 import paper_2403_01876_b200 as dv  # noqa: E402
 
 H, D = 72, 128
+NVLINK_NOMINAL_GBS = 900.0          # per direction per GPU (NVLink 5, 18 links; task statement)
+NVLINK_GUIDE_GBS = 770.0            # measured peer copy in /opt/skills/guides/B200_PROFILING.md
+SEED_C5, SEED_C3 = 20240309, 20240306
 
 
-def _env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("DV_BENCH_SAME_DEVICE") == "1":
-        local = 0
-    return world, rank, local
+def _small():
+    return os.environ.get("DV_BENCH_PEER_SMALL") == "1"
 
 
-def _gather(obj, world):
-    if world == 1:
-        return [obj]
-    out = [None] * world
-    dist.all_gather_object(out, obj)
-    return out
+class Env:
+    """Rank / device / process-group plumbing of one bench process."""
+
+    def __init__(self, backend):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if os.environ.get("DV_BENCH_SAME_DEVICE") == "1":   # test hook: all ranks on cuda:0 (gloo)
+            self.local = 0
+        self.backend = backend
+        self.dev = torch.device("cuda", self.local)
+
+    def init(self):
+        torch.cuda.set_device(self.local)
+        if self.world > 1 and not dist.is_initialized():
+            dist.init_process_group(self.backend, **({"device_id": self.dev} if self.backend == "nccl" else {}))
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev if self.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev if self.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def barrier(self):
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def identity(self):
+        p = torch.cuda.get_device_properties(self.local)
+        return {"rank": self.rank, "device": self.local, "name": p.name,
+                "pci": f"{getattr(p, 'pci_domain_id', 0):04x}:{getattr(p, 'pci_bus_id', 0):02x}:"
+                       f"{getattr(p, 'pci_device_id', 0):02x}", "uuid": str(getattr(p, "uuid", ""))}
 
 
-def _max(x, world, dev, backend):
-    if world == 1:
-        return x
-    t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+def _timed(env, fn, reps=1, head_start_ns=0):
+    """Device time of `reps` calls of fn on the current stream (ms, max over ranks), bracketed by a
+    barrier + synchronize on both sides."""
+    st = torch.cuda.current_stream()
+    env.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if head_start_ns:
+        dv.dvt_spin(head_start_ns, 1, stream=st.cuda_stream)
+    a.record(st)
+    for _ in range(reps):
+        fn()
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = env.max(a.elapsed_time(b))
+    env.barrier()
+    return ms
 
 
-def _sendrecv(args, sbuf, dst, rbuf, src):
+def _sendrecv(backend, sbuf, dst, rbuf, src):
     """The baseline's exchange: NCCL grouped send/recv of device buffers; with the gloo backend
     (multi-process tests on one GPU) the same exchange staged through host copies."""
-    if args.dist_backend == "nccl":
+    if backend == "nccl":
         ops = []
         if sbuf is not None:
             ops.append(dist.P2POp(dist.isend, sbuf, dst))
@@ -77,351 +142,523 @@ def _sendrecv(args, sbuf, dst, rbuf, src):
         rbuf.copy_(rh)
 
 
-def _impl(args, baseline):
-    if not baseline:
-        return "dvstream"
-    return "nccl-baseline" if args.dist_backend == "nccl" else "sendrecv-baseline (gloo, host-staged; tests only)"
+def _roof(achieved, peak, peak_src):
+    return {"bound": "nvlink", "achieved": achieved, "unit": "GB/s", "peak": peak,
+            "frac": achieved / peak if peak else None, "peak_source": peak_src,
+            "peak_nominal": NVLINK_NOMINAL_GBS, "frac_nominal": achieved / NVLINK_NOMINAL_GBS}
 
 
-def run_c5(args, bench):
-    world, rank, local = _env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group(args.dist_backend, **({"device_id": dev} if args.dist_backend == "nccl" else {}))
-    P = world
-    Ls = 64 // P if P > 1 else 8
-    b, S, p = 16, 2048, 1024
-    ctx = dv.dv_create(local)
-    lb = rank * Ls
-    own_k = torch.empty((Ls, b, H, S, D), dtype=torch.int16, device=dev)
-    own_v = torch.empty_like(own_k)
-    own = dv.cache(own_k, own_v, lb, 0)
-    dv.dvt_fill(own, dv.DVT_FILL_HASH, seed=20240309)
-    # replica store for the predecessor's layers, and the flag word the predecessor publishes
-    pred = (rank - 1) % P
-    rep_k = torch.full((Ls, b, H, S, D), -1, dtype=torch.int16, device=dev)
-    rep_v = torch.full_like(rep_k, -1)
-    flags = torch.zeros(P, dtype=torch.int64, device=dev)
-    ack = torch.zeros(1, dtype=torch.int64, device=dev)   # the successor's ping-pong acks land here
-    torch.cuda.synchronize()
-    blob = {"k": dv.dv_ipc_export(rep_k.data_ptr()), "v": dv.dv_ipc_export(rep_v.data_ptr()),
-            "f": dv.dv_ipc_export(flags.data_ptr()), "a": dv.dv_ipc_export(ack.data_ptr()),
-            "layer_begin": pred * Ls}
-    blobs = _gather(blob, world)
-    succ = (rank + 1) % P
-    sb = blobs[succ]
-    kp, vp, fp = dv.dv_ipc_open(sb["k"]), dv.dv_ipc_open(sb["v"]), dv.dv_ipc_open(sb["f"])
-    rep_at_succ = dv.cache_raw(kp, vp, local if world == 1 else succ, 2, sb["layer_begin"], Ls, 0, b, H, S, D)
-    sig = dv.endpoint(dv.DV_EP_PEER, fp, 8 * P, fp, P, device=succ)
-    setup = dv.Setup([rank * Ls, rank * Ls + Ls], [0, b], S)  # this stage as a 1-block "setup"
-    st = torch.cuda.current_stream()
-    sp = st.cuda_stream
+def _pct(xs, q):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, int(len(xs) * q))] if xs else None
 
-    step_bytes = 2 * Ls * b * H * D * 2
-    nccl = getattr(args, "peer_baseline", "none") == "nccl"
-    if nccl:
-        # BASELINE (north_star: "NCCL send/recv kept only as the baseline"): pack the step into a
-        # device buffer, ncclSend it to the successor / ncclRecv the predecessor's, unpack it into
-        # the replica store. Needs >= 2 GPUs and the nccl backend.
-        assert world > 1, "--peer-baseline nccl needs >= 2 ranks"
-        sbuf = torch.empty(step_bytes // 2, dtype=torch.int16, device=dev)
-        rbuf = torch.empty_like(sbuf)
-        rep_local = dv.cache(rep_k, rep_v, pred * Ls, 0)
 
-    dst_arr, sig_arr = dv.cache_array([rep_at_succ]), dv.endpoint_array([sig])   # reused every step
+# =====================================================================================================
+# link probe: the in-run peer peaks
+# =====================================================================================================
+def link_probe(ctx, env, nbytes=None, reps=5):
+    nbytes = nbytes or ((32 << 20) if _small() else (256 << 20))
+    W, r = env.world, env.rank
+    src = dv.dv_device_alloc(env.local, nbytes)
+    dst = dv.dv_device_alloc(env.local, nbytes)
+    blobs = env.gather(dv.dv_ipc_export(dst))
+    succ = (r + 1) % W
+    peer = dv.dv_ipc_open(blobs[succ])
+    ep = dv.endpoint(dv.DV_EP_PEER if W > 1 else dv.DV_EP_DEVICE, peer, nbytes, device=succ if W > 1 else env.local)
+    sp = torch.cuda.current_stream().cuda_stream
+    out = {"bytes": nbytes, "reps": reps, "topology": "ring x -> (x+1)%N, all ranks at once"}
+    for name, xf in (("ce", dv.DV_XFER_STAGED), ("sm", dv.DV_XFER_FUSED)):
+        ms = _timed(env, lambda: dv.dv_flush(ctx, src, nbytes, ep, 0, xfer=xf, stream=sp), reps)
+        out[f"ring_{name}_gbs"] = nbytes * reps / ms / 1e6      # per GPU egress (and ingress)
+    if W >= 2:
+        # one direction per link: even ranks send to their successor, odd ranks only receive
+        send = r % 2 == 0 and succ != r
+        ms = _timed(env, lambda: dv.dv_flush(ctx, src, nbytes, ep, 0, xfer=dv.DV_XFER_STAGED, stream=sp)
+                    if send else None, reps)
+        out["uni_ce_gbs"] = nbytes * reps / ms / 1e6
+    env.barrier()
+    dv.dv_ipc_close(peer)
+    env.barrier()
+    dv.dv_device_free(src)
+    dv.dv_device_free(dst)
+    out["peak_gbs"] = max(out["ring_ce_gbs"], out["ring_sm_gbs"], out.get("uni_ce_gbs", 0.0))
+    out["how"] = ("dv_flush of one contiguous buffer into the successor's IPC-mapped buffer: ce = "
+                  "copy engine (cudaMemcpyAsync), sm = the library's copy kernel storing over the link; "
+                  "device time, max over ranks")
+    return out
 
-    def step(t):
-        q = p + (t - 1) % (S - p)
-        if not nccl:
-            dv.dv_stream_out_direct(ctx, own, (lb, lb + Ls, 0, b, q, q + 1), setup, 0, 0, setup,
-                                    dst_arr, sig_arr, seq=t, stream=sp)
-            return
-        dv.dv_scatter(ctx, own, dv.region(lb, lb + Ls, 0, b, q, q + 1), dv.endpoint_of(sbuf), 0, stream=sp)
-        _sendrecv(args, sbuf, succ, rbuf, pred)
-        dv.dv_gather(ctx, dv.endpoint_of(rbuf), 0, rep_local, dv.region(pred * Ls, pred * Ls + Ls, 0, b, q, q + 1),
-                     stream=sp)
-    # prompt replica first (bulk, Q13), then token steps
-    if not nccl:   # the NCCL baseline times the token steps only
-        dv.dv_stream_out_direct(ctx, own, dv.region(lb, lb + Ls, 0, b, 0, p), setup, 0, 0, setup, [rep_at_succ],
-                                [sig], seq=1, stream=sp)
-    t = 1
-    for _ in range(args.warmup):
-        t += 1
-        step(t)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0, _ = dv.dv_stats()
-    a.record(st)
-    for _ in range(args.steps):
-        t += 1
-        step(t)
-    e.record(st)
-    torch.cuda.synchronize()
-    l1, _ = dv.dv_stats()
-    ms = _max(a.elapsed_time(e), world, dev, args.dist_backend)
-    host_us = None
-    dev_us = None
-    if not nccl:
-        # the same steps queued behind a spin head start: device time per step without the host's
-        # enqueue rate (the timed region above includes it: one dv_stream_out_direct per step)
-        import time as _t
+
+# =====================================================================================================
+# C5 ring replication
+# =====================================================================================================
+class C5:
+    def __init__(self, ctx, env):
+        self.ctx, self.env = ctx, env
+        P = env.world
+        self.P = P
+        self.Ls = 64 // P if P > 1 else 8
+        self.b, self.S, self.p = (2, 256, 64) if _small() else (16, 2048, 1024)
+        r = env.rank
+        self.lb = r * self.Ls
+        self.pred, self.succ = (r - 1) % P, (r + 1) % P
+        shape = (self.Ls, self.b, H, self.S, D)
+        self.own_k = torch.empty(shape, dtype=torch.int16, device=env.dev)
+        self.own_v = torch.empty_like(self.own_k)
+        self.own = dv.cache(self.own_k, self.own_v, self.lb, 0)
+        dv.dvt_fill(self.own, dv.DVT_FILL_HASH, seed=SEED_C5)
+        self.rep_k = torch.full(shape, -1, dtype=torch.int16, device=env.dev)
+        self.rep_v = torch.full_like(self.rep_k, -1)
+        self.rep = dv.cache(self.rep_k, self.rep_v, self.pred * self.Ls, 0)
+        self.flags = torch.zeros(P, dtype=torch.int64, device=env.dev)
+        self.ack = torch.zeros(1, dtype=torch.int64, device=env.dev)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        a2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dv.dvt_spin(max(2_000_000, args.steps * 40_000), 1, stream=sp)
-        a2.record(st)
-        h0 = _t.perf_counter()
-        for _ in range(args.steps):
-            t += 1
-            step(t)
-        host_us = (_t.perf_counter() - h0) / args.steps * 1e6
-        e2.record(st)
-        torch.cuda.synchronize()
-        dev_us = _max(a2.elapsed_time(e2) * 1e3 / args.steps, world, dev, args.dist_backend)
-    graph = None if nccl else _graph_steps(ctx, own, rep_at_succ, sig, lb, Ls, b, p, S, world, dev, args, st)
-    pingpong = None if nccl else _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, blobs[pred]["a"],
-                                           lb, Ls, b, p, S, P, world, dev, args, st)
-    # the predecessor's last step landed in our replica store: sampled parity vs kvgen
-    if world > 1:
-        dist.barrier()
-    q = p + (t - 1) % (S - p)
-    bad = bench.sample_region(rep_k, rep_v, pred * Ls, 0, H, S, D, (pred * Ls, pred * Ls + Ls, 0, b, q, q + 1),
-                              20240309)
-    bad = int(_max(bad, world, dev, args.dist_backend))
-    value = P * args.steps * step_bytes / (ms * 1e-3) / 1e9
-    if rank == 0:
-        print(json.dumps({
-            "metric": "KV stream GB/s (ring replication, token step per stage)", "value": value, "unit": "GB/s",
-            "impl": _impl(args, nccl),
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
-            "data": "synthetic (splitmix64 coordinate-hash fill)",
-            "config": {"workload": f"C5 OPT-66B ring replication b16, {P} stage(s) x {Ls} layers, "
-                                   f"one position per step -> successor's replica store",
-                       "bytes_per_step_per_stage": step_bytes, "parallelism": f"pp{P} ring",
-                       "transport": "CUDA IPC peer stores" if world > 1 else "loopback (same GPU)"},
-            "gpu_launches": int(l1 - l0), "parity_spot_check": {"mismatches": bad}, "pingpong": pingpong,
-            "device_us_per_step": dev_us, "host_enqueue_us_per_step": host_us, "graph": graph,
-            "ideal_us_per_step_at_770GBps": step_bytes / 770e3}), flush=True)
-    for x in (kp, vp, fp):
-        dv.dv_ipc_close(x)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        blob = {"k": dv.dv_ipc_export(self.rep_k.data_ptr()), "v": dv.dv_ipc_export(self.rep_v.data_ptr()),
+                "f": dv.dv_ipc_export(self.flags.data_ptr()), "a": dv.dv_ipc_export(self.ack.data_ptr()),
+                "layer_begin": self.pred * self.Ls}
+        self.blobs = env.gather(blob)
+        sb = self.blobs[self.succ]
+        self.kp, self.vp, self.fp = dv.dv_ipc_open(sb["k"]), dv.dv_ipc_open(sb["v"]), dv.dv_ipc_open(sb["f"])
+        sdev = self.succ if env.world > 1 and os.environ.get("DV_BENCH_SAME_DEVICE") != "1" else env.local
+        self.rep_at_succ = dv.cache_raw(self.kp, self.vp, sdev, 2, sb["layer_begin"], self.Ls, 0, self.b, H,
+                                        self.S, D)
+        self.sig = dv.endpoint(dv.DV_EP_PEER, self.fp, 8 * P, self.fp, P, device=sdev)
+        self.setup = dv.Setup([self.lb, self.lb + self.Ls], [0, self.b], self.S)
+        self.dst_arr, self.sig_arr = dv.cache_array([self.rep_at_succ]), dv.endpoint_array([self.sig])
+        self.sp = torch.cuda.current_stream().cuda_stream
+        self.layer_bytes_tok = 2 * self.b * H * D * 2          # one layer, one position (576 KiB at b 16)
+        self.step_bytes = self.Ls * self.layer_bytes_tok
+        self.prompt_bytes = self.step_bytes * self.p
+        self.seq = 0
+        self.t = 0                                               # token steps streamed so far
 
+    def _next_seq(self):
+        self.seq += 1
+        return self.seq
 
-def _graph_steps(ctx, own, rep_at_succ, sig, lb, Ls, b, p, S, world, dev, args, st):
-    """The token step as a CUDA graph (captured once: a device step counter bump + dv_remap_dyn of
-    this stage's new position into the successor's replica store with its seq flag), replayed
-    per token: device time and host cost per step."""
-    d_step = torch.full((1,), -1, dtype=torch.int32, device=dev)
-    g = torch.cuda.CUDAGraph()
-    gs = torch.cuda.Stream()
-    torch.cuda.synchronize()
-    with torch.cuda.stream(gs):
-        with torch.cuda.graph(g, stream=gs):
-            d_step.add_(1)
-            dv.dv_remap_dyn(ctx, own, rep_at_succ, dv.region(lb, lb + Ls, 0, b, p, p + 1), d_step.data_ptr(),
-                            S - p - 1, signal=sig, flag_slot=0, seq=2 * 10 ** 7, stream=gs.cuda_stream)
-    torch.cuda.synchronize()
-    reps = min(args.steps, S - p - 10)
-    import time as _t
-    with torch.cuda.stream(gs):
-        d_step.fill_(-1)
-        for _ in range(5):
-            g.replay()
-        d_step.fill_(-1)
+    def pos(self, t):                                            # reading Q4: step t writes p + t - 1
+        return self.p + (t - 1) % (self.S - self.p)
+
+    def prompt_replica(self):
+        lb, Ls = self.lb, self.Ls
+        dv.dv_stream_out_direct(self.ctx, self.own, (lb, lb + Ls, 0, self.b, 0, self.p), self.setup, 0, 0,
+                                self.setup, self.dst_arr, self.sig_arr, seq=self._next_seq(), stream=self.sp)
+
+    def token_step(self):
+        self.t += 1
+        q = self.pos(self.t)
+        lb = self.lb
+        dv.dv_stream_out_direct(self.ctx, self.own, (lb, lb + self.Ls, 0, self.b, q, q + 1), self.setup, 0, 0,
+                                self.setup, self.dst_arr, self.sig_arr, seq=self._next_seq(), stream=self.sp)
+
+    def verify(self, n_pos):
+        """Every word of this rank's replica store (the predecessor's layers) on [0, n_pos) against
+        the generator (dvt_verify on the device); returns mismatches (max over ranks) and words."""
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.env.dev)
+        reg = dv.region(self.pred * self.Ls, self.pred * self.Ls + self.Ls, 0, self.b, 0, n_pos)
+        dv.dvt_verify(self.rep, cnt.data_ptr(), seed=SEED_C5, reg=reg, stream=self.sp)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        bad = int(self.env.max(float(cnt.item())))
+        words = 2 * self.Ls * self.b * H * n_pos * D
+        return {"mismatches": bad, "words_per_rank": words, "how": "dvt_verify of every replica word vs the generator"}
+
+    def latency(self, n=300):
+        """Per-layer put latency with the system-scope release: writer (dvt_fill of one layer's new
+        position) ends -> the put's seq flag released into the successor's memory (%globaltimer on
+        the sender, dvt_trace stamps)."""
+        env = self.env
+        te = torch.zeros(n, dtype=torch.int64, device=env.dev)
+        ts = torch.zeros((n, 4), dtype=torch.int64, device=env.dev)
+        ts[:, 1:3] = 2 ** 63 - 1
+        q = self.S - 1
+        env.barrier()
+        dv.dvt_spin(20_000_000, 1, stream=self.sp)
+        for i in range(n):
+            layer = self.lb + i % self.Ls
+            reg = dv.region(layer, layer + 1, 0, self.b, q, q + 1)
+            dv.dvt_fill(self.own, dv.DVT_FILL_HASH, seed=SEED_C5, reg=reg, stream=self.sp, t_end_ptr=te[i].data_ptr())
+            dv.dvt_trace(self.ctx, ts[i].data_ptr())
+            dv.dv_stream_out_direct(self.ctx, self.own, reg, self.setup, 0, 0, self.setup, self.dst_arr,
+                                    self.sig_arr, seq=self._next_seq(), stream=self.sp)
+        dv.dvt_trace(self.ctx, 0)
+        torch.cuda.synchronize()
+        us = ((ts[:, 0] - te).double() / 1e3).tolist()[20:]
+        p50, p99 = env.max(_pct(us, 0.5)), env.max(_pct(us, 0.99))
+        scope = dv.dvt_release_scope(self.ctx, self.fp, self.kp)
+        return {"p50_us": p50, "p99_us": p99, "n": len(us), "bytes": self.layer_bytes_tok,
+                "release_scope": "gpu" if scope else "system",
+                "how": "writer end -> st.release of the seq flag in the successor's memory, sender "
+                       "%globaltimer; p50/p99 max over ranks"}
+
+    def pingpong(self, iters=300):
+        """Put one layer (+ flag) into the successor, wait for the predecessor's put, ack into the
+        predecessor's memory, wait for the successor's ack: RTT per iteration (device time)."""
+        env = self.env
+        pa = dv.dv_ipc_open(self.blobs[self.pred]["a"])
+        pdev = self.pred if env.world > 1 and os.environ.get("DV_BENCH_SAME_DEVICE") != "1" else env.local
+        pred_ack = dv.endpoint(dv.DV_EP_PEER, pa, 8, pa, 1, device=pdev)
+        own_ack = dv.endpoint(dv.DV_EP_DEVICE, self.ack.data_ptr(), 8, self.ack.data_ptr(), 1, device=env.local)
+        inbox = dv.endpoint(dv.DV_EP_DEVICE, self.flags.data_ptr(), 8 * self.P, self.flags.data_ptr(), self.P,
+                            device=env.local)
+        q = self.S - 1
+        env.barrier()
+        base = self.seq + 10        # every rank's flags/acks move in lockstep from here
+        base = int(env.max(base))
+
+        def one(i):
+            layer = self.lb + i % self.Ls
+            dv.dv_stream_out_direct(self.ctx, self.own, dv.region(layer, layer + 1, 0, self.b, q, q + 1), self.setup,
+                                    0, 0, self.setup, self.dst_arr, self.sig_arr, seq=base + i, stream=self.sp)
+            dv.dv_wait(self.ctx, inbox, 0, base + i, stream=self.sp)   # slot 0: the predecessor's 1-block setup
+            dv.dv_signal(self.ctx, pred_ack, 0, base + i, stream=self.sp)
+            dv.dv_wait(self.ctx, own_ack, 0, base + i, stream=self.sp)
+        for i in range(20):
+            one(i)
+        env.barrier()
+        st = torch.cuda.current_stream()
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dv.dvt_spin(max(2_000_000, reps * 20_000), 1, stream=gs.cuda_stream)
-        a.record(gs)
-        h0 = _t.perf_counter()
-        for _ in range(reps):
-            g.replay()
-        host_us = (_t.perf_counter() - h0) / reps * 1e6
-        e.record(gs)
+        dv.dvt_spin(max(4_000_000, iters * 12_000), 1, stream=self.sp)
+        a.record(st)
+        for i in range(20, 20 + iters):
+            one(i)
+        e.record(st)
         torch.cuda.synchronize()
-    dev_us = _max(a.elapsed_time(e) * 1e3 / reps, world, dev, args.dist_backend)
-    return {"device_us_per_step": dev_us, "host_us_per_step": host_us, "steps": reps,
-            "gbs_per_stage": 2 * Ls * b * H * D * 2 / dev_us / 1e3,
-            "how": "one captured graph per token step (step-counter bump + dv_remap_dyn), replayed"}
+        rtt = env.max(a.elapsed_time(e) * 1e3 / iters)
+        self.seq = base + 20 + iters
+        env.barrier()
+        dv.dv_ipc_close(pa)
+        return {"rtt_us": rtt, "one_way_us": rtt / 2, "bytes": self.layer_bytes_tok, "iters": iters,
+                "how": "put+flag -> stream wait on the predecessor's flag -> ack into its memory -> wait own ack"}
+
+    def nccl_baseline(self, steps):
+        """NCCL send/recv baseline (north_star: "NCCL send/recv kept only as the baseline"): the
+        same prompt replica (per layer: pack -> send to the successor / recv from the predecessor ->
+        unpack) and the same token steps (pack the step -> send/recv -> unpack). The replica store
+        is reset first, so the verify after it checks what NCCL delivered."""
+        env = self.env
+        self.rep_k.fill_(-1)
+        self.rep_v.fill_(-1)
+        lb, Ls, b, p = self.lb, self.Ls, self.b, self.p
+        plb = self.pred * Ls
+        lay_b = 2 * b * H * p * D * 2
+        sbuf = torch.empty(lay_b // 2, dtype=torch.int16, device=env.dev)
+        rbuf = torch.empty_like(sbuf)
+        sep, rep_ = dv.endpoint_of(sbuf), dv.endpoint_of(rbuf)
+
+        def prompt():
+            for l in range(Ls):
+                dv.dv_scatter(self.ctx, self.own, (lb + l, lb + l + 1, 0, b, 0, p), sep, 0, stream=self.sp)
+                _sendrecv(env.backend, sbuf, self.succ, rbuf, self.pred)
+                dv.dv_gather(self.ctx, rep_, 0, self.rep, (plb + l, plb + l + 1, 0, b, 0, p), stream=self.sp)
+        ms_prompt = _timed(env, prompt)
+        tb = torch.empty(self.step_bytes // 2, dtype=torch.int16, device=env.dev)
+        trb = torch.empty_like(tb)
+        tep, trep = dv.endpoint_of(tb), dv.endpoint_of(trb)
+        t0 = [0]
+
+        def token():
+            t0[0] += 1
+            q = self.pos(t0[0])
+            dv.dv_scatter(self.ctx, self.own, (lb, lb + Ls, 0, b, q, q + 1), tep, 0, stream=self.sp)
+            _sendrecv(env.backend, tb, self.succ, trb, self.pred)
+            dv.dv_gather(self.ctx, trep, 0, self.rep, (plb, plb + Ls, 0, b, q, q + 1), stream=self.sp)
+        for _ in range(3):
+            token()
+        t0[0] = 0
+        ms_tok = _timed(env, token, steps)
+        out = {"prompt_replica": {"ms": ms_prompt, "gbs_per_gpu": self.prompt_bytes / ms_prompt / 1e6},
+               "token_step": {"us": ms_tok * 1e3 / steps, "gbs_per_gpu": self.step_bytes * steps / ms_tok / 1e6},
+               "parity": self.verify(self.p + min(steps, self.S - self.p)),
+               "impl": "nccl send/recv" if env.backend == "nccl" else "gloo send/recv, host-staged (tests only)"}
+        return out
+
+    def close(self):
+        for x in (self.kp, self.vp, self.fp):
+            dv.dv_ipc_close(x)
 
 
-def _pingpong(ctx, own, setup, rep_at_succ, sig, flags, ack, pred_ack_blob, lb, Ls, b, p, S, P, world, dev,
-              args, st, iters=500):
-    """SURVEY §8(d) peer latency, second form: a ping-pong per token·layer (one layer, one
-    position, b 16 = 589,824 B). Every iteration each stage x (1) puts the layer into the replica
-    store at (x+1)%P with its seq flag (dv_stream_out_direct), (2) waits on the stream for the flag
-    its predecessor puts into its own memory, (3) writes an ack into the predecessor's memory
-    (dv_signal over the peer mapping) and (4) waits for its successor's ack. RTT = device time per
-    iteration (a spin head start hides the host enqueue); one-way ~ RTT / 2. At N = 1 the peer is
-    this GPU (loopback)."""
-    pa = dv.dv_ipc_open(pred_ack_blob)
-    pred_ack = dv.endpoint(dv.DV_EP_PEER, pa, 8, pa, 1)
-    own_ack = dv.endpoint(dv.DV_EP_DEVICE, ack.data_ptr(), 8, ack.data_ptr(), 1)
-    inbox = dv.endpoint(dv.DV_EP_DEVICE, flags.data_ptr(), 8 * P, flags.data_ptr(), P)
-    sp = st.cuda_stream
-    q = S - 1
-    base = 10 ** 7
-
-    def one(i):
-        layer = lb + i % Ls
-        dv.dv_stream_out_direct(ctx, own, dv.region(layer, layer + 1, 0, b, q, q + 1), setup, 0, 0, setup,
-                                [rep_at_succ], [sig], seq=base + i, stream=sp)
-        dv.dv_wait(ctx, inbox, 0, base + i, stream=sp)
-        dv.dv_signal(ctx, pred_ack, 0, base + i, stream=sp)
-        dv.dv_wait(ctx, own_ack, 0, base + i, stream=sp)
-    for i in range(20):
-        one(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dv.dvt_spin(max(4_000_000, iters * 12_000), 1, stream=sp)
-    a.record(st)
-    for i in range(20, 20 + iters):
-        one(i)
-    e.record(st)
-    torch.cuda.synchronize()
-    rtt = _max(a.elapsed_time(e) * 1e3 / iters, world, dev, args.dist_backend)
-    if world > 1:
-        dist.barrier()
-    dv.dv_ipc_close(pa)
-    return {"rtt_us": rtt, "one_way_us": rtt / 2, "bytes": 2 * b * H * D * 2, "iters": iters,
-            "how": "put+flag -> stream wait on the predecessor's flag -> ack into its memory -> wait own ack; "
-                   "device time per iteration, max over ranks"}
+def c5_suite(ctx, env, steps=200, peak=None, peak_src=None, nccl=True):
+    c = C5(ctx, env)
+    out = {"workload": f"C5 OPT-66B ring replication b{c.b}, {c.P} stage(s) x {c.Ls} layers, p {c.p}, S {c.S}",
+           "bytes_prompt_replica_per_gpu": c.prompt_bytes, "bytes_token_step_per_gpu": c.step_bytes}
+    ms = _timed(env, c.prompt_replica)
+    g = c.prompt_bytes / ms / 1e6
+    out["prompt_replica"] = {"ms": ms, "gbs_per_gpu": g, "gbs_aggregate": g * c.P,
+                             "roofline": _roof(g, peak, peak_src)}
+    steps = min(steps, c.S - c.p)
+    for _ in range(3):
+        c.token_step()
+    c.t = 0                                    # timed steps rewrite positions p .. p+steps-1
+    ms = _timed(env, c.token_step, steps, head_start_ns=max(2_000_000, steps * 40_000))
+    g = c.step_bytes * steps / ms / 1e6
+    out["token_step"] = {"us": ms * 1e3 / steps, "gbs_per_gpu": g, "gbs_aggregate": g * c.P, "steps": steps,
+                         "roofline": _roof(g, peak, peak_src),
+                         "how": "one dv_stream_out_direct per step (all the stage's layers, one position) "
+                                "into the successor's replica store + seq flag; spin head start hides the enqueue"}
+    out["parity"] = c.verify(c.p + steps)
+    out["latency_per_layer_put"] = c.latency()
+    out["pingpong"] = c.pingpong()
+    if nccl and env.world > 1:
+        out["nccl_baseline"] = c.nccl_baseline(steps)
+        nb = out["nccl_baseline"]
+        out["dvstream_vs_nccl"] = {
+            "prompt_replica": out["prompt_replica"]["gbs_per_gpu"] / nb["prompt_replica"]["gbs_per_gpu"],
+            "token_step": out["token_step"]["gbs_per_gpu"] / nb["token_step"]["gbs_per_gpu"]}
+    c.close()
+    env.barrier()
+    del c
+    torch.cuda.empty_cache()
+    return out
 
 
+# =====================================================================================================
+# C3 prompt -> token disaggregation
+# =====================================================================================================
 def _token_bounds(n):
     return {1: [0, 64], 2: [0, 29, 64], 4: [0, 13, 30, 47, 64]}.get(n) or \
         [round(64 * k / n) for k in range(n + 1)]
 
 
-def run_c3(args, bench):
-    world, rank, local = _env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group(args.dist_backend, **({"device_id": dev} if args.dist_backend == "nccl" else {}))
-    b, Sp, St = 8, 1024, 2048
-    p = int(os.environ.get("DV_C3_PROMPT", "1000"))   # test hook: shorter prompts (C3 is p = 1000)
-    n_p = max(1, world // 2)
-    n_t = max(1, world - n_p) if world > 1 else 1
-    pb = [round(64 * k / n_p) for k in range(n_p + 1)]
-    tb = _token_bounds(n_t)
-    ps, ts = dv.Setup(pb, [0, b], Sp), dv.Setup(tb, [0, b], St)
-    ctx = dv.dv_create(local)
-    is_prompt = world == 1 or rank < n_p
-    is_token = world == 1 or rank >= n_p
-    mine = {}
-    blob = None
-    if is_token:
-        j = 0 if world == 1 else rank - n_p
-        k = torch.full((tb[j + 1] - tb[j], b, H, St, D), -1, dtype=torch.int16, device=dev)
-        v = torch.full_like(k, -1)
-        f = torch.zeros(n_p, dtype=torch.int64, device=dev)
-        mine.update(tk=k, tv=v, tf=f, j=j)
-        torch.cuda.synchronize()
-        blob = {"k": dv.dv_ipc_export(k.data_ptr()), "v": dv.dv_ipc_export(v.data_ptr()),
-                "f": dv.dv_ipc_export(f.data_ptr()), "j": j}
-    if world == 1:
-        blobs = [blob]
-    else:
-        blobs = [x for x in _gather(blob, world) if x is not None]
-    blobs.sort(key=lambda x: x["j"])
-    if is_prompt:
-        i = 0 if world == 1 else rank
-        pk = torch.empty((pb[i + 1] - pb[i], b, H, Sp, D), dtype=torch.int16, device=dev)
-        pv = torch.empty_like(pk)
-        pc = dv.cache(pk, pv, pb[i], 0)
-        dv.dvt_fill(pc, dv.DVT_FILL_HASH, seed=20240306, valid=(0, p))
-        caches, sigs, opened = [], [], []
-        for bl in blobs:
-            kp, vp, fp = dv.dv_ipc_open(bl["k"]), dv.dv_ipc_open(bl["v"]), dv.dv_ipc_open(bl["f"])
-            opened += [kp, vp, fp]
-            jj = bl["j"]
-            caches.append(dv.cache_raw(kp, vp, local, 2, tb[jj], tb[jj + 1] - tb[jj], 0, b, H, St, D))
-            sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8 * n_p, fp, n_p, device=local))
-        mine.update(pc=pc, i=i, caches=caches, sigs=sigs, opened=opened)
-    st = torch.cuda.current_stream()
-    sp = st.cuda_stream
-    seq = [0]
-    nccl = getattr(args, "peer_baseline", "none") == "nccl"
-    if nccl:
-        # BASELINE (SURVEY §8(d) 3): each prompt layer packed into a device buffer, sent with NCCL
-        # to the token rank that holds the layer, received and unpacked there.
-        assert world > 1, "--peer-baseline nccl needs >= 2 ranks"
-        lbytes = 2 * b * H * p * D * 2
-        xbuf = torch.empty(lbytes // 2, dtype=torch.int16, device=dev)
-        if is_token:
-            j = mine["j"]
-            mine["tc"] = dv.cache(mine["tk"], mine["tv"], tb[j], 0)
+class C3:
+    def __init__(self, ctx, env):
+        self.ctx, self.env = ctx, env
+        W, r = env.world, env.rank
+        self.b, self.Sp, self.St = (2, 64, 128) if _small() else (8, 1024, 2048)
+        self.p = int(os.environ.get("DV_C3_PROMPT", "32" if _small() else "1000"))
+        self.n_p = max(1, W // 2)
+        self.n_t = max(1, W - self.n_p) if W > 1 else 1
+        self.pb = [round(64 * k / self.n_p) for k in range(self.n_p + 1)]
+        self.tb = _token_bounds(self.n_t)
+        self.ps, self.ts = dv.Setup(self.pb, [0, self.b], self.Sp), dv.Setup(self.tb, [0, self.b], self.St)
+        self.is_prompt = W == 1 or r < self.n_p
+        self.is_token = W == 1 or r >= self.n_p
+        self.sp = torch.cuda.current_stream().cuda_stream
+        blob = None
+        if self.is_token:
+            self.j = 0 if W == 1 else r - self.n_p
+            j = self.j
+            self.tk = torch.full((self.tb[j + 1] - self.tb[j], self.b, H, self.St, D), -1, dtype=torch.int16,
+                                 device=env.dev)
+            self.tv = torch.full_like(self.tk, -1)
+            self.tc = dv.cache(self.tk, self.tv, self.tb[j], 0)
+            self.tf = torch.zeros(self.n_p, dtype=torch.int64, device=env.dev)
+            torch.cuda.synchronize()
+            blob = {"k": dv.dv_ipc_export(self.tk.data_ptr()), "v": dv.dv_ipc_export(self.tv.data_ptr()),
+                    "f": dv.dv_ipc_export(self.tf.data_ptr()), "j": j, "rank": r, "device": env.local}
+        blobs = [x for x in env.gather(blob) if x is not None]
+        blobs.sort(key=lambda x: x["j"])
+        self.token_ranks = [x["rank"] for x in blobs]
+        self.opened = []
+        if self.is_prompt:
+            self.i = 0 if W == 1 else r
+            i = self.i
+            self.pk = torch.empty((self.pb[i + 1] - self.pb[i], self.b, H, self.Sp, D), dtype=torch.int16,
+                                  device=env.dev)
+            self.pv = torch.empty_like(self.pk)
+            self.pc = dv.cache(self.pk, self.pv, self.pb[i], 0)
+            dv.dvt_fill(self.pc, dv.DVT_FILL_HASH, seed=SEED_C3, valid=(0, self.p))
+            caches, sigs = [], []
+            for bl in blobs:
+                kp, vp, fp = dv.dv_ipc_open(bl["k"]), dv.dv_ipc_open(bl["v"]), dv.dv_ipc_open(bl["f"])
+                self.opened += [kp, vp, fp]
+                jj = bl["j"]
+                caches.append(dv.cache_raw(kp, vp, bl["device"], 2, self.tb[jj], self.tb[jj + 1] - self.tb[jj], 0,
+                                           self.b, H, self.St, D))
+                sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8 * self.n_p, fp, self.n_p, device=bl["device"]))
+            self.caches, self.sigs = dv.cache_array(caches), dv.endpoint_array(sigs)
+            self.n_dst = len(caches)
+        self.layer_bytes = 2 * self.b * H * self.p * D * 2
+        self.seq = 0
 
-    def owner(bounds, layer):
-        return max(x for x in range(len(bounds) - 1) if bounds[x] <= layer)
+    def my_prompt_bytes(self):
+        return (self.pb[self.i + 1] - self.pb[self.i]) * self.layer_bytes if self.is_prompt else 0
 
-    def handoff():
-        seq[0] += 1
-        if nccl:
-            if is_prompt:
-                i = mine["i"]
-                for layer in range(pb[i], pb[i + 1]):
-                    dv.dv_scatter(ctx, mine["pc"], dv.region(layer, layer + 1, 0, b, 0, p), dv.endpoint_of(xbuf), 0,
-                                  stream=sp)
-                    _sendrecv(args, xbuf, n_p + owner(tb, layer), None, None)
-            else:
-                j = mine["j"]
-                for layer in range(tb[j], tb[j + 1]):
-                    _sendrecv(args, None, None, xbuf, owner(pb, layer))
-                    dv.dv_gather(ctx, dv.endpoint_of(xbuf), 0, mine["tc"], dv.region(layer, layer + 1, 0, b, 0, p),
-                                 stream=sp)
+    def handoff(self):
+        self.seq += 1
+        if not self.is_prompt:
             return
-        if is_prompt:
-            i = mine["i"]
-            for layer in range(pb[i], pb[i + 1]):      # layer by layer (Opt 2, PAPER.md:123)
-                dv.dv_stream_out_direct(ctx, mine["pc"], dv.region(layer, layer + 1, 0, b, 0, p), ps, i, 0, ts,
-                                        mine["caches"], mine["sigs"], seq=seq[0], stream=sp)
-    for _ in range(args.warmup):
-        handoff()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(args.steps):
-        handoff()
-    e.record(st)
-    torch.cuda.synchronize()
-    ms = _max(a.elapsed_time(e), world, dev, args.dist_backend)
-    if world > 1:
-        dist.barrier()
-    bad = 0
-    if is_token:
-        j = mine["j"]
-        bad = bench.sample_region(mine["tk"], mine["tv"], tb[j], 0, H, St, D, (tb[j], tb[j + 1], 0, b, 0, p),
-                                  20240306)
-    bad = int(_max(bad, world, dev, args.dist_backend))
-    total = 64 * 2 * b * H * p * D * 2
-    if rank == 0:
-        print(json.dumps({
-            "metric": "KV stream GB/s (prompt-token disaggregation hand-off)", "value": args.steps * total / (ms * 1e-3) / 1e9,
-            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
-            "data": "synthetic (splitmix64 coordinate-hash fill)",
-            "config": {"workload": f"C3 OPT-66B b8 p1000: {n_p} prompt GPU(s) {pb} -> {n_t} token GPU(s) {tb}, "
-                                   f"S 1024 -> 2048, layer by layer, direct remap",
-                       "bytes_per_step": total, "parallelism": f"pp{n_p} -> pp{n_t}",
-                       "transport": "CUDA IPC peer stores" if world > 1 else "loopback (same GPU, HBM)"},
-            "parity_spot_check": {"mismatches": bad}, "impl": _impl(args, nccl),
-            "ideal_ms_per_step_at_770GBps_per_prompt_gpu": total / n_p / 770e6}), flush=True)
-    for x in mine.get("opened", []):
-        dv.dv_ipc_close(x)
-    if world > 1:
-        dist.barrier()
+        i = self.i
+        for layer in range(self.pb[i], self.pb[i + 1]):       # layer by layer (Opt 2, PAPER.md:123)
+            dv.dv_stream_out_direct(self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), self.ps, i,
+                                    0, self.ts, self.caches, self.sigs, seq=self.seq, stream=self.sp)
+
+    def verify(self):
+        env = self.env
+        bad = 0
+        sentinel_ok = True
+        if self.is_token:
+            j = self.j
+            cnt = torch.zeros(1, dtype=torch.int64, device=env.dev)
+            dv.dvt_verify(self.tc, cnt.data_ptr(), seed=SEED_C3, valid=(0, self.p),
+                          reg=dv.region(self.tb[j], self.tb[j + 1], 0, self.b, 0, self.p), stream=self.sp)
+            torch.cuda.synchronize()
+            bad = int(cnt.item())
+            sentinel_ok = bool((self.tk[:, :, :, self.p:] == -1).all()) and bool((self.tv[:, :, :, self.p:] == -1).all())
+        bad = int(env.max(float(bad)))
+        sentinel_ok = env.max(0.0 if sentinel_ok else 1.0) == 0.0
+        return {"mismatches": bad, "positions_past_prompt_untouched": sentinel_ok,
+                "words": 2 * 64 * self.b * H * self.p * D,
+                "how": "dvt_verify of every token-cache word on [0, p) vs the generator; [p, S) still the sentinel"}
+
+    def nccl_baseline(self, steps):
+        env = self.env
+        if self.is_token:
+            self.tk.fill_(-1)
+            self.tv.fill_(-1)
+        xbuf = torch.empty(self.layer_bytes // 2, dtype=torch.int16, device=env.dev)
+        xep = dv.endpoint_of(xbuf)
+
+        def owner(bounds, layer):
+            return max(x for x in range(len(bounds) - 1) if bounds[x] <= layer)
+
+        def run():
+            if self.is_prompt and self.is_token:       # N = 1: no exchange, pack + unpack
+                return
+            if self.is_prompt:
+                i = self.i
+                for layer in range(self.pb[i], self.pb[i + 1]):
+                    dv.dv_scatter(self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), xep, 0,
+                                  stream=self.sp)
+                    _sendrecv(env.backend, xbuf, self.token_ranks[owner(self.tb, layer)], None, None)
+            else:
+                j = self.j
+                for layer in range(self.tb[j], self.tb[j + 1]):
+                    _sendrecv(env.backend, None, None, xbuf, owner(self.pb, layer))
+                    dv.dv_gather(self.ctx, xep, 0, self.tc, dv.region(layer, layer + 1, 0, self.b, 0, self.p),
+                                 stream=self.sp)
+        ms = _timed(env, run, steps)
+        total = 64 * self.layer_bytes
+        per_gpu = env.max(self.my_prompt_bytes()) * steps / ms / 1e6
+        return {"ms_per_handoff": ms / steps, "gbs_aggregate": total * steps / ms / 1e6, "gbs_per_prompt_gpu": per_gpu,
+                "parity": self.verify(),
+                "impl": "nccl send/recv" if env.backend == "nccl" else "gloo send/recv, host-staged (tests only)"}
+
+    def close(self):
+        for x in self.opened:
+            dv.dv_ipc_close(x)
+
+
+def c3_suite(ctx, env, steps=3, peak=None, peak_src=None, nccl=True):
+    c = C3(ctx, env)
+    total = 64 * c.layer_bytes
+    out = {"workload": f"C3 OPT-66B b{c.b} p{c.p}: {c.n_p} prompt GPU(s) {c.pb} -> {c.n_t} token GPU(s) {c.tb}, "
+                       f"S {c.Sp} -> {c.St}, layer by layer, straight into the token caches",
+           "bytes_per_handoff": total}
+    c.handoff()                                 # warm-up
+    env.barrier()
+    ms = _timed(env, c.handoff, steps)
+    per_gpu = env.max(c.my_prompt_bytes()) * steps / ms / 1e6
+    out["handoff"] = {"ms": ms / steps, "gbs_aggregate": total * steps / ms / 1e6, "gbs_per_prompt_gpu": per_gpu,
+                      "steps": steps, "roofline": _roof(per_gpu, peak, peak_src),
+                      "ideal_ms_at_peak": (env.max(c.my_prompt_bytes()) / peak / 1e6) if peak else None}
+    out["parity"] = c.verify()
+    if nccl and env.world > 1:
+        out["nccl_baseline"] = c.nccl_baseline(steps)
+        out["dvstream_vs_nccl"] = out["handoff"]["gbs_per_prompt_gpu"] / out["nccl_baseline"]["gbs_per_prompt_gpu"]
+    c.close()
+    env.barrier()
+    del c
+    torch.cuda.empty_cache()
+    return out
+
+
+# =====================================================================================================
+def nvlink_suite(ctx, env, steps=200, nccl=True):
+    """Everything above in one pass; returns the dict for rank 0's JSON line (None on other ranks)."""
+    t0 = time.perf_counter()
+    res = {"devices": env.gather(env.identity()), "transport": "CUDA IPC peer stores (one process per GPU)"}
+    if os.environ.get("DV_BENCH_SAME_DEVICE") == "1":
+        res["transport"] = "CUDA IPC between processes on ONE GPU (test mode: HBM, not NVLink)"
+    devs = {d["uuid"] or d["pci"] for d in res["devices"]}
+    res["distinct_gpus"] = len(devs)
+    for name, fn in (("link", lambda: link_probe(ctx, env)),):
+        try:
+            res[name] = fn()
+        except Exception as e:   # noqa: BLE001 -- a failed part is reported, the line still prints
+            res[name] = {"error": f"{type(e).__name__}: {e}"}
+    peak = res["link"].get("peak_gbs")
+    src = "in-run peer copy (link probe: max of copy-engine / SM-store ring and one-direction copies)"
+    for name, fn in (("c5", lambda: c5_suite(ctx, env, steps, peak, src, nccl)),
+                     ("c3", lambda: c3_suite(ctx, env, 3, peak, src, nccl))):
+        try:
+            res[name] = fn()
+        except Exception as e:   # noqa: BLE001
+            res[name] = {"error": f"{type(e).__name__}: {e}"}
+            try:
+                env.barrier()
+            except Exception:   # noqa: BLE001
+                pass
+    res["wall_s"] = time.perf_counter() - t0
+    return res if env.rank == 0 else None
+
+
+# =====================================================================================================
+# stand-alone workloads (bench.py --workload c3 | c5): one JSON line each
+# =====================================================================================================
+def _line(args, env, metric, value, ms_per_step, cfg, extra):
+    return {"metric": metric, "value": value, "unit": "GB/s", "n_gpus": env.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": cfg.pop("scaling", "weak"), "vs_baseline": None, "dtype": "u16 (opaque fp16 words)",
+            "data": "synthetic (splitmix64 coordinate-hash fill)", "config": cfg, **extra}
+
+
+def run_c5(args, bench):
+    env = Env(args.dist_backend)
+    env.init()
+    ctx = dv.dv_create(env.local)
+    nccl = getattr(args, "peer_baseline", "none") == "nccl"
+    link = link_probe(ctx, env) if env.world > 1 else None
+    peak = link["peak_gbs"] if link else None
+    if nccl:
+        assert env.world > 1, "--peer-baseline nccl needs >= 2 ranks"
+        c = C5(ctx, env)
+        c.prompt_replica()
+        nb = c.nccl_baseline(args.steps)
+        c.close()
+        value, msps, extra = nb["token_step"]["gbs_per_gpu"] * env.world, nb["token_step"]["us"] / 1e3, \
+            {"impl": "nccl-baseline" if env.backend == "nccl" else "sendrecv-baseline (gloo, host-staged; tests only)",
+             "parity_spot_check": {"mismatches": nb["parity"]["mismatches"]}, "baseline": nb}
+    else:
+        r = c5_suite(ctx, env, args.steps, peak, "in-run link probe", nccl=False)
+        ts = r["token_step"]
+        value, msps = ts["gbs_aggregate"], ts["us"] / 1e3
+        extra = {"impl": "dvstream", "parity_spot_check": {"mismatches": r["parity"]["mismatches"]}, "c5": r,
+                 "link": link, "gpu_launches": None}
+    if env.rank == 0:
+        print(json.dumps(_line(args, env, "KV stream GB/s (ring replication, token step per stage)", value, msps,
+                               {"workload": f"C5 OPT-66B ring replication, {env.world} stage(s)",
+                                "parallelism": f"pp{env.world} ring"}, extra)), flush=True)
+    env.barrier()
+    ctx.close()
+    if env.world > 1:
+        dist.destroy_process_group()
+
+
+def run_c3(args, bench):
+    env = Env(args.dist_backend)
+    env.init()
+    ctx = dv.dv_create(env.local)
+    nccl = getattr(args, "peer_baseline", "none") == "nccl"
+    link = link_probe(ctx, env) if env.world > 1 else None
+    peak = link["peak_gbs"] if link else None
+    if nccl:
+        assert env.world > 1, "--peer-baseline nccl needs >= 2 ranks"
+        c = C3(ctx, env)
+        nb = c.nccl_baseline(args.steps)
+        c.close()
+        value, msps = nb["gbs_aggregate"], nb["ms_per_handoff"]
+        extra = {"impl": "nccl-baseline" if env.backend == "nccl" else "sendrecv-baseline (gloo, host-staged; tests only)",
+                 "parity_spot_check": {"mismatches": nb["parity"]["mismatches"]}, "baseline": nb}
+    else:
+        r = c3_suite(ctx, env, args.steps, peak, "in-run link probe", nccl=False)
+        value, msps = r["handoff"]["gbs_aggregate"], r["handoff"]["ms"]
+        extra = {"impl": "dvstream", "parity_spot_check": {"mismatches": r["parity"]["mismatches"]}, "c3": r,
+                 "link": link}
+    if env.rank == 0:
+        print(json.dumps(_line(args, env, "KV stream GB/s (prompt-token disaggregation hand-off)", value, msps,
+                               {"workload": "C3 OPT-66B disaggregation hand-off", "scaling": "strong",
+                                "parallelism": f"pp{max(1, env.world // 2)} -> pp{max(1, env.world - env.world // 2)}"},
+                               extra)), flush=True)
+    env.barrier()
+    ctx.close()
+    if env.world > 1:
         dist.destroy_process_group()
