@@ -323,7 +323,7 @@ def run_ours(args):
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": STEP_BYTES,
                 "d2h_bytes_per_step": STEP_BYTES,
                 "how": "per step: dv_gather of the token's K/V from pinned host into the device cache "
-                       "(H2D + unpack, input stream) then dv_scatter to the pinned-host log (pack + D2H, "
+                       "(H2D + unpack, input stream) then dv_stream_out into the pinned-host ring log (route + pack + D2H, "
                        "main stream); step t+1's H2D overlaps step t's D2H (PCIe full duplex)"},
         "gpu_launches": int(launches),
         "copy_engine_dmas": int(dma1 - dma0),   # library cudaMemcpyAsync calls in the timed region

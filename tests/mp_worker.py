@@ -58,9 +58,18 @@ def mode_route(rank, world):
     assert tot == ok.region_bytes(0, 12, 0, 4, 0, P_LEN, H, D, 2)
 
 
+def _device(rank):
+    """cuda:0 for every rank (the one-GPU test box), or rank % device_count with DV_MP_CROSS=1 (a
+    multi-GPU box: the same IPC mappings then cross NVLink)."""
+    if os.environ.get("DV_MP_CROSS") == "1":
+        return rank % torch.cuda.device_count()
+    return 0
+
+
 def mode_ipc(rank, world, direct):
-    torch.cuda.set_device(0)
-    ctx = dv.dv_create(0)
+    dev = _device(rank)
+    torch.cuda.set_device(dev)
+    ctx = dv.dv_create(dev)
     pb, tb = blocks(PSPLIT, PREQ), blocks(TSPLIT, TREQ)
     assert world == len(pb) + len(tb)
     ps, ts = dv.Setup(PSPLIT, PREQ, SP), dv.Setup(TSPLIT, TREQ, ST)
@@ -75,15 +84,15 @@ def mode_ipc(rank, world, direct):
         v = torch.full_like(k, -1)
         mine = {"k": k, "v": v, "cache": dv.cache(k, v, a, c0)}
         words = (b_ - a) * (c1 - c0) * H * P_LEN * D * 2
-        inbox = dv.dv_device_alloc(0, words * 2)
-        flagp = dv.dv_device_alloc(0, 8 * n_src)
+        inbox = dv.dv_device_alloc(dev, words * 2)
+        flagp = dv.dv_device_alloc(dev, 8 * n_src)
         fz = torch.zeros(n_src, dtype=torch.int64, device="cuda")
-        dv.dv_flush(ctx, fz.data_ptr(), 8 * n_src, dv.endpoint(dv.DV_EP_DEVICE, flagp, 8 * n_src, device=0), 0,
+        dv.dv_flush(ctx, fz.data_ptr(), 8 * n_src, dv.endpoint(dv.DV_EP_DEVICE, flagp, 8 * n_src, device=dev), 0,
                     xfer=dv.DV_XFER_STAGED)
         torch.cuda.synchronize()
         info = {"inbox": dv.dv_ipc_export(inbox), "flags": dv.dv_ipc_export(flagp), "words": words,
                 "k": dv.dv_ipc_export(k.data_ptr()), "v": dv.dv_ipc_export(v.data_ptr()),
-                "shape": (b_ - a, c1 - c0, a, c0), "block": (j, w)}
+                "shape": (b_ - a, c1 - c0, a, c0), "block": (j, w), "dev": dev}
         mine.update(inbox=inbox, flagp=flagp, words=words)
     infos = [None] * world
     dist.all_gather_object(infos, info)
@@ -102,13 +111,13 @@ def mode_ipc(rank, world, direct):
             opened += [ib, fp]
             # memory mapped from another process is never "this GPU's own HBM": system-scope release
             assert not dv.dvt_release_scope(ctx, fp, ib) and not dv.dvt_release_scope(ctx, fp + 8, ib + 64)
-            eps.append(dv.endpoint(dv.DV_EP_PEER, ib, inf["words"] * 2, fp, n_src, device=0))
-            sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8, fp, n_src, device=0))
+            eps.append(dv.endpoint(dv.DV_EP_PEER, ib, inf["words"] * 2, fp, n_src, device=inf["dev"]))
+            sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8, fp, n_src, device=inf["dev"]))
             if direct:
                 kp, vp = dv.dv_ipc_open(inf["k"]), dv.dv_ipc_open(inf["v"])
                 opened += [kp, vp]
                 nl, nr, la, ra = inf["shape"]
-                caches.append(dv.cache_raw(kp, vp, 0, 2, la, nl, ra, nr, H, ST, D))
+                caches.append(dv.cache_raw(kp, vp, inf["dev"], 2, la, nl, ra, nr, H, ST, D))
         if direct:
             dv.dv_stream_out_direct(ctx, src, reg, ps, i, u, ts, caches, sigs, seq=5)
         else:
@@ -120,7 +129,7 @@ def mode_ipc(rank, world, direct):
         dist.barrier()   # every mapping closed before the exporters free their memory
     else:                                                   # token block: receive
         j, w = tb[rank - n_src]
-        iep = dv.endpoint(dv.DV_EP_DEVICE, mine["inbox"], mine["words"] * 2, mine["flagp"], n_src, device=0)
+        iep = dv.endpoint(dv.DV_EP_DEVICE, mine["inbox"], mine["words"] * 2, mine["flagp"], n_src, device=dev)
         assert dv.dvt_release_scope(ctx, mine["flagp"], mine["inbox"])   # own allocation: gpu scope
         if direct:
             # wait for every source block that routes to us, then the bytes are already in place
@@ -151,7 +160,7 @@ def mode_ring(rank, world, n=300):
     CUDA IPC); rank 0 (sender) maps them and streams n token chunks with seq 1..n. The sender's
     credit waits poll IPC-mapped memory (the acquire-spin kernel path), its DV_NOWAIT call for seq 3
     before the receiver has started returns DV_EBUSY; the receiver's cache equals kvgen's words."""
-    dev = int(os.environ.get("DV_MP_DEVICE", "0"))
+    dev = _device(rank)
     torch.cuda.set_device(dev)
     ctx = dv.dv_create(dev)
     L, B, Hh, S, Dd, p = 3, 2, 4, 8 + n, 16, 4
@@ -163,7 +172,7 @@ def mode_ring(rank, world, n=300):
         z = torch.zeros(2, dtype=torch.int64, device="cuda")
         dv.dv_flush(ctx, z.data_ptr(), 16, dv.endpoint(dv.DV_EP_DEVICE, fc, 16, device=dev), 0, xfer=dv.DV_XFER_STAGED)
         torch.cuda.synchronize()
-        info = {"inbox": dv.dv_ipc_export(inbox), "fc": dv.dv_ipc_export(fc)}
+        info = {"inbox": dv.dv_ipc_export(inbox), "fc": dv.dv_ipc_export(fc), "dev": dev}
     infos = [None] * world
     dist.all_gather_object(infos, info)
     seed = 321
@@ -174,7 +183,7 @@ def mode_ring(rank, world, n=300):
         src = dv.cache(k, v)
         ib, fc = dv.dv_ipc_open(infos[1]["inbox"]), dv.dv_ipc_open(infos[1]["fc"])
         assert dv.dv_ipc_blob_bytes(infos[1]["inbox"]) >= 2 * chunk
-        ep = dv.endpoint(dv.DV_EP_PEER, ib, 2 * chunk, fc, 1, device=dev, n_slots=2, slot_bytes=chunk,
+        ep = dv.endpoint(dv.DV_EP_PEER, ib, 2 * chunk, fc, 1, device=infos[1]["dev"], n_slots=2, slot_bytes=chunk,
                          credits_ptr=fc + 8)
         regs = [dv.region(0, L, 0, B, p + t - 1, p + t) for t in range(1, n + 1)]
         nw = dv.DV_XFER_FUSED | dv.DV_NOWAIT

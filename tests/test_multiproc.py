@@ -24,12 +24,12 @@ def _free_port():
     return p
 
 
-def _run(mode, world, timeout=240):
+def _run(mode, world, timeout=240, extra_env=None):
     port = _free_port()
     procs = []
     for r in range(world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), LOCAL_RANK="0")
+                   MASTER_PORT=str(port), LOCAL_RANK="0", **(extra_env or {}))
         procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "mp_worker.py"), mode], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     outs = []
@@ -54,6 +54,23 @@ def test_route_agreement_gloo_world2():
 def test_cross_process_ipc_stream(mode):
     # 2 prompt blocks (stages [0,6),[6,12) x 1 microbatch) + 3x2 token blocks -> 8 ranks
     _run(mode, 2 + 6)
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:   # noqa: BLE001
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs: ranks on different devices, IPC over NVLink")
+@pytest.mark.parametrize("mode", ["ipc", "direct", "ring"])
+def test_cross_gpu_processes(mode):
+    """The multi-process IPC tests with rank r on GPU r % device_count (DV_MP_CROSS=1): mappings,
+    stores, system-scope releases, stream waits and credit spins all cross NVLink."""
+    _run(mode, 8 if mode != "ring" else 2, extra_env={"DV_MP_CROSS": "1"})
 
 
 @pytest.mark.gpu
