@@ -678,6 +678,11 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["baseline_buffered_2d_memcpy_us"] = ms * 1e3
     ex["speedup_buffered_vs_per_run"] = ex["baseline_per_run_memcpy_us"] / ex["baseline_buffered_2d_memcpy_us"]
     ex["speedup_ours_vs_buffered"] = ex["baseline_buffered_2d_memcpy_us"] / ex["token_step_host_fused_us"]
+
+    # NEXT-2: token streaming overlapped with a synthetic model step:
+    # paired ABBA trials, step / compute slowdown with a 95 % CI, m, every streamed word verified
+    from tools import bench_overlap
+    ex["overlap"] = bench_overlap.measure(ctx, cache, 20240305)
     return ex
 
 

@@ -391,3 +391,56 @@ def test_ring_stream_out_in_two_sources_one_inbox():
     osrc = {(0, 0): ok.Cache(K[:3], V[:3], 0, 0, H, S, D), (1, 0): ok.Cache(K[3:], V[3:], 3, 0, H, S, D)}
     ok.stream(osrc, ok.Setup([0, 3, 6], [0, B], S), {(0, 0): o}, ok.Setup([0, L], [0, B], S), (0, L, 0, B, p, p + n))
     assert np.array_equal(to_np(dk), o.K) and np.array_equal(to_np(dvv), o.V)
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-2: streaming overlapped with compute (PAPER.md:123-135 Opt 2/3, :310)
+@pytest.mark.parametrize("xfer", [dv.DV_XFER_DECOUPLED, dv.DV_XFER_FUSED])
+def test_streaming_under_concurrent_compute_matches_oracle(xfer):
+    """200 token steps streamed (dv_stream_out into a 16-slot host ring, high-priority stream) while
+    bf16 GEMMs and an HBM copy saturate the GPU on another stream; each step's stream-out is
+    ordered after the previous step's compute (Opt 3). Every chunk, read the moment its flag
+    appears, equals the oracle's pack of that position."""
+    L, B, H, S, D, p, n, R = 8, 8, 16, 256, 128, 24, 200, 16
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=601)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    osrc = ok.Cache(K, V, 0, 0, H, S, D)
+    step = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    log = pinned_u16(R * step // 2)
+    fl = flags(1, pinned=True)
+    ring = dv.endpoint_array([dv.endpoint_of(log, fl, n_slots=R, slot_bytes=step)])
+    stage = dv.Setup([0, L], [0, B], S)
+    cx = ctx()
+    comp, strm = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    big2 = torch.empty_like(big)
+    torch.cuda.synchronize()
+    seq0 = int(fl[0])
+    evs = []
+    bad = []
+    for i in range(n):
+        with torch.cuda.stream(comp):
+            torch.matmul(a, a)
+            big2.copy_(big)
+            e = torch.cuda.Event()
+            e.record(comp)
+            evs.append(e)
+        if i > 0:
+            strm.wait_event(evs[i - 1])
+        q = p + i
+        dv.dv_stream_out(cx, c, (0, L, 0, B, q, q + 1), stage, 0, 0, stage, ring, seq=seq0 + i + 1, xfer=xfer,
+                         stream=strm)
+        # a consumer thread would read each chunk as its flag appears; here: check the chunk the
+        # moment its flag is visible, before the ring slot can be reused (R steps later)
+        if i >= R // 2:
+            t = i - R // 2 + 1
+            while int(fl[0]) < seq0 + t:
+                pass
+            j = seq0 + t
+            w = log[(j % R) * step // 2:((j % R) + 1) * step // 2].numpy().view(np.uint16)
+            if not np.array_equal(w, ok.pack(osrc, (0, L, 0, B, p + t - 1, p + t))):
+                bad.append(t)
+    torch.cuda.synchronize()
+    assert int(fl[0]) == seq0 + n and not bad, bad[:5]
