@@ -376,6 +376,52 @@ DV_API dv_status dv_signal(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot
  * directly; device-memory flags with a small synchronous copy. */
 DV_API dv_status dv_query(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq, int32_t* done);
 
+/* ---- persistent stream engine: the per-layer latency path (DESIGN.md §6 "Persistent engine") -
+ * A few CTAs stay resident (a cooperative grid on the engine's own highest-priority stream) and
+ * run REGISTERED plans when their doorbell rings, so a per-layer stream-out (PAPER.md:123-135,
+ * Opt 2/3) pays no kernel launch, no wait for free SM slots (e.g. behind a GEMM) and no dependency
+ * wait between "the producer wrote layer l's K/V" and the copy. A plan is a dv_scatter_dyn /
+ * dv_remap_dyn shape: at step k its positions move by k (token step t writes p + t - 1, reading
+ * Q4), the destination by k positions (remap) or k*dst_step_bytes (scatter), and it releases
+ * flag seq + k at the scope the memory needs (system for host / peer memory). Ringing the doorbell
+ * of a plan with step k asks for every step of that plan not yet executed up to k, in order.
+ * While an engine runs, cudaDeviceSynchronize() (e.g. torch.cuda.synchronize()) cannot return:
+ * park the engine first (dv_engine_park; the next kick relaunches it) or synchronise streams. */
+typedef struct dv_engine dv_engine;
+/* n_ctas resident CTAs of 256 threads forming ONE thread-block cluster (1 .. 16; 8 saturate PCIe
+ * Gen5 x16): cluster rank 0 polls the doorbells, every CTA copies its static share (1,024-vector
+ * units rank, rank + n_ctas, ...) of each requested (plan, step), cluster barriers order the
+ * shares before rank 0's release of the flag. Jobs run one at a time in the order they are found,
+ * so flags are released in order. While it runs, a kernel that is not yet loaded (CUDA lazy
+ * loading, e.g. a torch op used for the first time) or a new stream cannot start: create streams
+ * and warm every kernel before dv_engine_create / dv_engine_resume, or set CUDA_MODULE_LOADING=EAGER. */
+DV_API dv_status dv_engine_create(dv_ctx* ctx, int32_t n_ctas, dv_engine** out);
+DV_API dv_status dv_engine_destroy(dv_engine* e);   /* parks, then frees */
+/* Stop the resident grid once the jobs already rung are done; blocks until it has exited. */
+DV_API dv_status dv_engine_park(dv_engine* e);
+/* Relaunch a parked engine (no-op if it runs): needed before producer kernels ring doorbells
+ * themselves; dv_engine_kick does it implicitly. */
+DV_API dv_status dv_engine_resume(dv_engine* e);
+/* Register a plan (validated for every step k in [0, max_step], as dv_scatter_dyn / dv_remap_dyn;
+ * K and V must share one copy plan, i.e. no FT6D key transpose) -> *plan. Up to 256 plans. */
+DV_API dv_status dv_engine_plan_scatter(dv_engine* e, const dv_cache* src, const dv_region* region,
+                                        const dv_endpoint* dst, uint64_t dst_off,
+                                        uint64_t dst_step_bytes, int32_t flag_slot, uint64_t seq,
+                                        int32_t max_step, int32_t* plan);
+DV_API dv_status dv_engine_plan_remap(dv_engine* e, const dv_cache* src, const dv_cache* dst,
+                                      const dv_region* region, const dv_endpoint* signal,
+                                      int32_t flag_slot, uint64_t seq, int32_t max_step,
+                                      int32_t* plan);
+/* Ring plan's doorbell with step k after all prior work on `stream` (a stream memory write; the
+ * engine is relaunched first if it was parked). */
+DV_API dv_status dv_engine_kick(dv_engine* e, int32_t plan, int32_t step, void* stream);
+/* The plan's doorbell word in device memory, for a PRODUCER KERNEL to ring itself (lowest
+ * latency; include/dv_device.cuh dv_engine_ring): store step + 1 with a gpu-scope release once all
+ * of the producer's stores are ordered before it. The engine must be running (not parked). */
+DV_API dv_status dv_engine_doorbell(dv_engine* e, int32_t plan, uint64_t** word);
+/* Steps of `plan` the engine has completed (flag released), read now (small synchronous copy). */
+DV_API dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,4 +41,13 @@ static __device__ __forceinline__ int dv_flag_wait(const uint64_t* flag, uint64_
   }
 }
 
+/* Ring a dv_engine doorbell (dv_engine_doorbell) from a producer kernel: ask for every step of the
+ * plan up to `step`. Call it from ONE thread once every store of the producer that the plan reads
+ * is ordered before it (e.g. after a __syncthreads() in the last CTA of a ticket chain, or in a
+ * single-CTA producer): a gpu-scope release max, so the engine's acquire sees the data. */
+static __device__ __forceinline__ void dv_engine_ring(uint64_t* doorbell, uint64_t step) {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(doorbell), "l"(step + 1) : "memory");
+}
+
 #endif

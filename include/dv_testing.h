@@ -30,6 +30,13 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
                    int32_t valid_begin, int32_t valid_end, const dv_region* region,
                    uint64_t* t_end, void* stream);
 
+/* dvt_fill (hash kind, whole positions of `region`) whose LAST CTA then rings a dv_engine doorbell
+ * with `step` (dv_device.cuh dv_engine_ring) once every CTA's stores are ordered before it -- a
+ * producer that starts the engine's copy itself. `ticket` is a device uint32 counter, zero before
+ * the call (the last CTA resets it). */
+DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region* region, uint64_t* t_end,
+                               uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
+
 /* Verifier (the second, on-device parity check of SURVEY §8(c) C-5 at full sizes): adds to
  * *mismatches (device memory, uint64) the number of words of `region` that differ from the
  * generator word dvt_fill would write there (same kind / seed / box / valid range). wire == NULL:

@@ -23,6 +23,13 @@ DV_API dv_status dvt_trace(dv_ctx* ctx, uint64_t* ts);
 DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* payload,
                                    int32_t* gpu_scope);
 
+/* Engine tracing: while `stamps` (device memory, 5 * n uint64) is set, the engine writes, for step
+ * k of plan p, five %globaltimer stamps into stamps[5 * ((k * n_plans + p) % n) + 0..4]: the flag
+ * release, the doorbell found by the poll, past the posting cluster barrier, the copy's stores
+ * issued (rank 0), past the collecting cluster barrier (n_plans = plans registered). Set it while
+ * the engine is parked or idle. */
+DV_API dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -131,8 +131,22 @@ _SIGS = {
     "dv_wait": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
     "dv_signal": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
     "dv_query": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, P(C.c_int32)]),
+    "dv_engine_create": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
+    "dv_engine_destroy": (C.c_int, [C.c_void_p]),
+    "dv_engine_park": (C.c_int, [C.c_void_p]),
+    "dv_engine_resume": (C.c_int, [C.c_void_p]),
+    "dv_engine_plan_scatter": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_endpoint), C.c_uint64,
+                                         C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, P(C.c_int32)]),
+    "dv_engine_plan_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint),
+                                       C.c_int32, C.c_uint64, C.c_int32, P(C.c_int32)]),
+    "dv_engine_kick": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "dv_engine_doorbell": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
+    "dv_engine_done": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
+    "dvt_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
+    "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
+                                C.c_void_p, C.c_void_p]),
     "dvt_verify": (C.c_int, [P(dv_cache), C.c_void_p, C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32,
                              C.c_int32, P(dv_region), C.c_void_p, C.c_void_p]),
     "dvt_trace": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -146,7 +160,7 @@ _SIGS = {
                                     P(C.c_uint64)]),
 }
 
-TESTING_SYMBOLS = {"dvt_fill", "dvt_verify", "dvt_spin", "dvt_consume", "dvt_watch", "dvb_per_run_copy",
+TESTING_SYMBOLS = {"dvt_fill", "dvt_fill_ring", "dvt_verify", "dvt_spin", "dvt_consume", "dvt_watch", "dvb_per_run_copy",
                    "dvb_buffered_copy"}
 _lib = None
 _tlib = None
@@ -404,9 +418,12 @@ class Context:
         self.h = h
         self.addr = h.value   # the dv_ctx* as an int (fast path)
         self.device = device
+        self._engines = []
 
     def close(self):
         if self.h:
+            for e in list(self._engines):
+                e.close()
             _call("dv_destroy", self.h)
             self.h = None
 
@@ -617,12 +634,83 @@ def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
     return bool(d.value)
 
 
+# ---- persistent stream engine (include/dv.h dv_engine_*) -----------------------------------------
+class Engine:
+    """A resident copy engine (dv_engine_create). While it runs, torch.cuda.synchronize() cannot
+    return: call park() first (the next kick relaunches it), or synchronise streams."""
+
+    def __init__(self, ctx, n_ctas=8):
+        self.ctx = ctx
+        h = C.c_void_p()
+        _call("dv_engine_create", ctx.h, n_ctas, C.byref(h))
+        self.h = h
+        ctx._engines.append(self)
+
+    def plan_scatter(self, src: dv_cache, reg, dst: dv_endpoint, dst_off, dst_step_bytes, flag_slot=-1, seq=0,
+                     max_step=0) -> int:
+        p = C.c_int32()
+        _call("dv_engine_plan_scatter", self.h, C.byref(src), _reg_ct(reg), C.byref(dst), dst_off, dst_step_bytes,
+              flag_slot, seq, max_step, C.byref(p))
+        return p.value
+
+    def plan_remap(self, src: dv_cache, dst: dv_cache, reg, signal: dv_endpoint = None, flag_slot=-1, seq=0,
+                   max_step=0) -> int:
+        p = C.c_int32()
+        _call("dv_engine_plan_remap", self.h, C.byref(src), C.byref(dst), _reg_ct(reg), _ref(signal), flag_slot,
+              seq, max_step, C.byref(p))
+        return p.value
+
+    def kick(self, plan, step, stream=None):
+        _call("dv_engine_kick", self.h, plan, step, _stream(stream))
+
+    def doorbell(self, plan) -> int:
+        w = C.c_void_p()
+        _call("dv_engine_doorbell", self.h, plan, C.byref(w))
+        return w.value
+
+    def done(self, plan) -> int:
+        n = C.c_uint64()
+        _call("dv_engine_done", self.h, plan, C.byref(n))
+        return n.value
+
+    def trace(self, stamps_ptr=0, n=0):
+        _call("dvt_engine_trace", self.h, C.c_void_p(stamps_ptr), n)
+
+    def park(self):
+        _call("dv_engine_park", self.h)
+
+    def resume(self):
+        _call("dv_engine_resume", self.h)
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            _call("dv_engine_destroy", self.h)
+            if self in self.ctx._engines:
+                self.ctx._engines.remove(self)
+        self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def dv_engine_create(ctx, n_ctas=8) -> Engine:
+    return Engine(ctx, n_ctas)
+
+
 # ---- test-only utilities (include/dv_testing.h) and baselines (include/dv_baselines.h) -----------
 def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_region = None, stream=None,
              t_end_ptr=0):
     b = (C.c_int32 * 5)(*box) if box is not None else None
     _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], (None if reg is None else _reg_ct(reg)), C.c_void_p(t_end_ptr),
           _stream(stream))
+
+
+def dvt_fill_ring(c: dv_cache, seed, reg, doorbell_ptr, step, ticket_ptr, t_end_ptr=0, stream=None):
+    _call("dvt_fill_ring", C.byref(c), seed, _reg_ct(reg), C.c_void_p(t_end_ptr), C.c_void_p(doorbell_ptr), step,
+          C.c_void_p(ticket_ptr), _stream(stream))
 
 
 def dvt_verify(c: dv_cache, counter_ptr, seed=0, kind=0, reg: dv_region = None, wire_ptr=0, box=None,

@@ -1189,6 +1189,14 @@ dv_status dv_create(int32_t device, const dv_config* cfg, dv_ctx** out) {
 dv_status dv_destroy(dv_ctx* ctx) {
   if (!ctx) return DV_OK;
   {
+    std::vector<dv_engine*> es;
+    {
+      std::lock_guard<std::mutex> lk(ctx->engine_mu);
+      es = ctx->engines;
+    }
+    for (auto* e : es) dv_engine_destroy(e);   // a resident engine would block the device sync
+  }
+  {
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
     ctx->staging.destroy();
@@ -1810,6 +1818,246 @@ dv_status dv_query(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64
     DV_CUDA(cudaStreamSynchronize(ctx->aux));
   }
   *done = v >= seq;
+  return DV_OK;
+}
+
+// ---- persistent stream engine ------------------------------------------------------------------
+}  // extern "C"
+
+struct dv_engine {
+  dv_ctx* ctx;
+  int n_ctas;
+  cudaStream_t st;    // the resident grid (highest priority)
+  cudaStream_t ctl;   // control writes (stop, plan table) while the grid runs
+  void* state;
+  void* plans;
+  int n_plans = 0;
+  int32_t max_step[dv::kEngineMaxPlans];
+  bool running = false;
+  std::mutex mu;
+};
+
+namespace dv {
+static dv_status engine_put(dv_engine* e, size_t off, const void* v, size_t n) {
+  DV_CUDA(cudaMemcpyAsync((uint8_t*)e->state + off, v, n, cudaMemcpyHostToDevice, e->ctl));
+  DV_CUDA(cudaStreamSynchronize(e->ctl));
+  return DV_OK;
+}
+static dv_status engine_start(dv_engine* e) {   // e->mu held
+  if (e->running) return DV_OK;
+  DV_TRY(engine_launch(e->state, e->plans, e->n_ctas, e->st));
+  e->running = true;
+  return DV_OK;
+}
+static dv_status engine_stop(dv_engine* e) {    // e->mu held
+  if (!e->running) return DV_OK;
+  const unsigned int one = 1, zero = 0;
+  DV_TRY(engine_put(e, engine_field_offset(0), &one, sizeof one));
+  DV_CUDA(cudaStreamSynchronize(e->st));
+  DV_TRY(engine_put(e, engine_field_offset(0), &zero, sizeof zero));
+  e->running = false;
+  return DV_OK;
+}
+static dv_status engine_add(dv_engine* e, const CopyPlan& p, const Release& rel, int32_t max_step,
+                            int32_t* plan) {
+  std::lock_guard<std::mutex> lk(e->mu);
+  if (e->n_plans >= kEngineMaxPlans) return fail(DV_ENOMEM, "engine plan table full (%d plans)", kEngineMaxPlans);
+  const int id = e->n_plans;
+  DV_TRY(engine_set_plan(e->plans, id, p, rel, max_step, e->ctl));
+  e->max_step[id] = max_step;
+  const int32_t n = id + 1;
+  DV_TRY(engine_put(e, engine_field_offset(1), &n, sizeof n));   // the dispatcher scans [0, n)
+  e->n_plans = n;
+  *plan = id;
+  return DV_OK;
+}
+}  // namespace dv
+
+extern "C" {
+
+dv_status dv_engine_create(dv_ctx* ctx, int32_t n_ctas, dv_engine** out) {
+  DV_TRY(check_ctx(ctx));
+  if (!out) return fail(DV_EINVAL, "NULL out");
+  if (n_ctas < 1 || n_ctas > 16) return fail(DV_EINVAL, "engine CTAs %d outside [1, 16]", n_ctas);
+  DV_ON_DEVICE(ctx->device);
+  dv_engine* e = new dv_engine();
+  e->ctx = ctx;
+  e->n_ctas = n_ctas;
+  int lo = 0, hi = 0;
+  cudaError_t r = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (r == cudaSuccess) r = cudaStreamCreateWithPriority(&e->st, cudaStreamNonBlocking, hi);
+  if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->ctl, cudaStreamNonBlocking);
+  if (r != cudaSuccess) {
+    delete e;
+    return cuda_fail(r, "engine streams");
+  }
+  dv_status st = engine_alloc(&e->state, &e->plans);
+  if (st == DV_OK) {
+    std::lock_guard<std::mutex> lk(e->mu);
+    st = engine_start(e);
+  }
+  if (st != DV_OK) {
+    cudaFree(e->state);
+    cudaFree(e->plans);
+    delete e;
+    return st;
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->engine_mu);
+    ctx->engines.push_back(e);
+  }
+  *out = e;
+  return DV_OK;
+}
+
+dv_status dv_engine_park(dv_engine* e) {
+  if (!e) return fail(DV_EINVAL, "NULL engine");
+  DV_ON_DEVICE(e->ctx->device);
+  std::lock_guard<std::mutex> lk(e->mu);
+  return engine_stop(e);
+}
+
+dv_status dv_engine_resume(dv_engine* e) {
+  if (!e) return fail(DV_EINVAL, "NULL engine");
+  DV_ON_DEVICE(e->ctx->device);
+  std::lock_guard<std::mutex> lk(e->mu);
+  return engine_start(e);
+}
+
+dv_status dv_engine_destroy(dv_engine* e) {
+  if (!e) return DV_OK;
+  {
+    DeviceGuard g(e->ctx->device);
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      engine_stop(e);
+    }
+    cudaStreamDestroy(e->st);
+    cudaStreamDestroy(e->ctl);
+    cudaFree(e->state);
+    cudaFree(e->plans);
+  }
+  {
+    std::lock_guard<std::mutex> lk(e->ctx->engine_mu);
+    auto& v = e->ctx->engines;
+    v.erase(std::remove(v.begin(), v.end(), e), v.end());
+  }
+  delete e;
+  return DV_OK;
+}
+
+dv_status dv_engine_plan_scatter(dv_engine* e, const dv_cache* src, const dv_region* region,
+                                 const dv_endpoint* dst, uint64_t dst_off, uint64_t dst_step_bytes,
+                                 int32_t flag_slot, uint64_t seq, int32_t max_step, int32_t* plan) {
+  if (!e || !plan) return fail(DV_EINVAL, "NULL engine or plan");
+  dv_ctx* ctx = e->ctx;
+  if (!region) return fail(DV_EINVAL, "NULL region");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  if (dst_step_bytes % 16) return fail(DV_EALIGN, "dst_step_bytes not a multiple of 16");
+  DV_TRY(check_cache(src, "source"));
+  DV_TRY(check_cache_mapped(src, "source"));
+  DV_TRY(check_region_shape(region));
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  DV_TRY(check_cache_holds(src, &reg, "source"));
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  if (has_ring(dst)) return fail(DV_EINVAL, "engine plans write a log, not a ring inbox");
+  const uint64_t bytes = region_bytes(&reg, src);
+  DV_TRY(check_ep(dst, dst_off, bytes + (uint64_t)max_step * dst_step_bytes, flag_slot, true, "destination"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  DV_ON_DEVICE(ctx->device);
+  const int64_t row = row_bytes(src);
+  uint8_t* wire = (uint8_t*)dst->base + dst_off;
+  TView sv[2] = {cache_view(src, 0, &reg), cache_view(src, 1, &reg)};
+  TView wv[2] = {wire_view(wire, 0, &reg, row), wire_view(wire, 1, &reg, row)};
+  CopyPlan p[2];
+  const int np = build_plans(sv, wv, &reg, row, ORDER_WIRE, Outer{}, p);
+  if (np != 1) return fail(DV_ENOTSUP, "engine plans need K and V in one copy plan (no FT6D key)");
+  p[0].dyn_ss = sv[0].st[DS];
+  p[0].dyn_ds = (int64_t)dst_step_bytes;
+  Release rel{nullptr, 0, nullptr};
+  if (flag_slot >= 0 && dst->flags) {
+    rel.flag = (unsigned long long*)&dst->flags[flag_slot];
+    rel.seq = seq;
+    rel.gpu_scope = local_vidmem(ctx, rel.flag) && local_vidmem(ctx, p[0].dst);
+  }
+  return engine_add(e, p[0], rel, max_step, plan);
+}
+
+dv_status dv_engine_plan_remap(dv_engine* e, const dv_cache* src, const dv_cache* dst,
+                               const dv_region* region, const dv_endpoint* signal, int32_t flag_slot,
+                               uint64_t seq, int32_t max_step, int32_t* plan) {
+  if (!e || !plan) return fail(DV_EINVAL, "NULL engine or plan");
+  dv_ctx* ctx = e->ctx;
+  if (!region) return fail(DV_EINVAL, "NULL region");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  RemapOp op{src, dst, *region, signal, flag_slot, seq, DV_XFER_FUSED};
+  DV_TRY(remap_check(ctx, op));
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  DV_TRY(check_cache_holds(dst, &last, "destination"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  DV_ON_DEVICE(ctx->device);
+  const int64_t row = row_bytes(src);
+  TView sv[2] = {cache_view(src, 0, &reg), cache_view(src, 1, &reg)};
+  TView dv_[2] = {cache_view(dst, 0, &reg), cache_view(dst, 1, &reg)};
+  CopyPlan p[2];
+  const int np = build_plans(sv, dv_, &reg, row, ORDER_KV_OUTER, Outer{}, p);
+  if (np != 1) return fail(DV_ENOTSUP, "engine plans need K and V in one copy plan (no FT6D key)");
+  p[0].dyn_ss = sv[0].st[DS];
+  p[0].dyn_ds = dv_[0].st[DS];
+  Release rel{nullptr, 0, nullptr};
+  if (signal && flag_slot >= 0 && signal->flags) {
+    rel.flag = (unsigned long long*)&signal->flags[flag_slot];
+    rel.seq = seq;
+    rel.gpu_scope = local_vidmem(ctx, rel.flag) && local_vidmem(ctx, p[0].dst);
+  }
+  return engine_add(e, p[0], rel, max_step, plan);
+}
+
+dv_status dv_engine_kick(dv_engine* e, int32_t plan, int32_t step, void* stream) {
+  if (!e) return fail(DV_EINVAL, "NULL engine");
+  std::lock_guard<std::mutex> lk(e->mu);
+  if (plan < 0 || plan >= e->n_plans) return fail(DV_EINVAL, "plan %d not registered", plan);
+  if (step < 0 || step > e->max_step[plan])
+    return fail(DV_ERANGE, "step %d outside [0, %d] (max_step of plan %d)", step, e->max_step[plan], plan);
+  DV_ON_DEVICE(e->ctx->device);
+  DV_TRY(engine_start(e));   // relaunch a parked engine first (its stream orders it after the old one)
+  const Driver* d;
+  DV_TRY(driver(&d));
+  int r = d->streamWriteValue64(stream, (unsigned long long)(uintptr_t)engine_word(e->state, 0, plan),
+                                (unsigned long long)step + 1, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r) return drv_fail(r, "cuStreamWriteValue64 (engine doorbell)");
+  return DV_OK;
+}
+
+dv_status dv_engine_doorbell(dv_engine* e, int32_t plan, uint64_t** word) {
+  if (!e || !word) return fail(DV_EINVAL, "NULL engine or word");
+  std::lock_guard<std::mutex> lk(e->mu);
+  if (plan < 0 || plan >= e->n_plans) return fail(DV_EINVAL, "plan %d not registered", plan);
+  *word = (uint64_t*)engine_word(e->state, 0, plan);
+  return DV_OK;
+}
+
+dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps) {
+  if (!e || !steps) return fail(DV_EINVAL, "NULL engine or steps");
+  if (plan < 0 || plan >= e->n_plans) return fail(DV_EINVAL, "plan %d not registered", plan);
+  DV_ON_DEVICE(e->ctx->device);
+  DV_CUDA(cudaMemcpyAsync(steps, engine_word(e->state, 1, plan), 8, cudaMemcpyDeviceToHost, e->ctl));
+  DV_CUDA(cudaStreamSynchronize(e->ctl));
+  return DV_OK;
+}
+
+dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n) {
+  if (!e) return fail(DV_EINVAL, "NULL engine");
+  if (stamps && !n) return fail(DV_EINVAL, "zero stamps");
+  DV_ON_DEVICE(e->ctx->device);
+  std::lock_guard<std::mutex> lk(e->mu);
+  DV_TRY(engine_put(e, engine_field_offset(3), &n, sizeof n));
+  DV_TRY(engine_put(e, engine_field_offset(2), &stamps, sizeof stamps));
   return DV_OK;
 }
 

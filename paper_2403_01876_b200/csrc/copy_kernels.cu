@@ -1304,6 +1304,249 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
   return DV_OK;
 }
 
+// ---- persistent stream engine (dv_engine_*, DESIGN.md §6 "Persistent engine") -----------------
+// ONE thread-block cluster of W <= 16 CTAs stays resident on its own highest-priority stream.
+// Registered plans (a run copy whose source and destination move by k positions / k*step bytes at
+// step k, and the flag it releases with seq + k) are triggered by doorbells: want[plan] = k + 1 (a
+// stream memory write after the producer, or a release by the producer kernel itself). Warp 0 of
+// cluster rank 0 polls the doorbells (one L2 round trip per scan: every lane's loads in flight at
+// once) and posts the next (plan, step) in its shared memory; a cluster barrier hands it to every
+// CTA (read through distributed shared memory), each CTA copies its static share (1,024-vector
+// units rank, rank + W, ...), a second cluster barrier (release / acquire) collects every CTA's
+// stores, and rank 0 releases the flag at the scope the memory needs. Jobs run in lockstep, so
+// every flag is released in step order. No launch, no SM-slot wait, no dependency wait and no
+// global-memory ticket sit between the producer's doorbell and the copy. The plans' parameters
+// live in every CTA's shared memory.
+constexpr int kEngineMaxCtas = 16;   // the non-portable cluster size (8 where refused)
+struct EPlan {
+  KParams kp;        // whole plan at step 0 (q_begin 0); dyn_ss / dyn_ds: bytes per step
+  int32_t vec;       // 16 or 32
+  int32_t max_step;
+};
+struct EState {
+  unsigned long long want[kEngineMaxPlans];    // doorbells (steps requested + 1)
+  unsigned long long done[kEngineMaxPlans];    // steps completed (flag released)
+  unsigned long long issued[kEngineMaxPlans];  // rank 0's progress, kept across park / relaunch
+  unsigned int stop;
+  int32_t n_plans;                             // registered plans (polled: [0, n_plans))
+  unsigned long long* stamps;                  // optional: %globaltimer after (plan, step)'s release
+  unsigned long long n_stamps;                 // stamps[(step * n_plans + plan) % n_stamps]
+};
+
+__device__ __forceinline__ unsigned long long ld_rlx_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Warp 0 of rank 0: the next pending plan (lowest index), or -1 (stop requested, nothing pending);
+// *np_out = the registered plans seen by the scan.
+__device__ __forceinline__ int engine_poll(EState* s, const unsigned long long* issued, int* np_out) {
+  const int lane = threadIdx.x;
+  bool stopping = false;
+  for (;;) {
+    const int np = *(volatile int32_t*)&s->n_plans;   // plans registered while the engine runs
+    *np_out = np;
+    // one round trip per scan: every lane's doorbell loads and the stop word in flight together
+    const unsigned st = *(volatile unsigned int*)&s->stop;
+    unsigned long long w[kEngineMaxPlans / 32];
+#pragma unroll
+    for (int i = 0; i < kEngineMaxPlans / 32; ++i) {
+      const int p = lane + 32 * i;
+      w[i] = p < np ? ld_rlx_gpu(&s->want[p]) : 0ull;
+    }
+#pragma unroll
+    for (int i = 0; i < kEngineMaxPlans / 32; ++i) {
+      const int p = lane + 32 * i;
+      const unsigned m = __ballot_sync(0xffffffffu, p < np && w[i] > issued[p]);
+      if (m) return 32 * i + __ffs(m) - 1;
+    }
+    if (stopping) return -1;   // stop seen, and a full scan after it found nothing pending
+    if (st) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");   // every doorbell released before the stop
+      stopping = true;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_engine(EState* s, const EPlan* plans) {
+  extern __shared__ __align__(16) uint8_t esm[];
+  KParams* sp = reinterpret_cast<KParams*>(esm);                                   // [kEngineMaxPlans]
+  int32_t* svec = reinterpret_cast<int32_t*>(sp + kEngineMaxPlans);
+  __shared__ unsigned long long issued[kEngineMaxPlans];   // rank 0 only
+  __shared__ __align__(16) int32_t job[4];                   // rank 0's copy is the broadcast
+  uint32_t rank, W;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(W));
+  uint32_t job_addr;   // rank 0's `job` in the cluster's shared window
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(job_addr) : "r"((uint32_t)__cvta_generic_to_shared(job)));
+  if (rank == 0)
+    for (int p = threadIdx.x; p < kEngineMaxPlans; p += blockDim.x) issued[p] = s->issued[p];
+  __syncthreads();
+  int loaded = 0;
+  __shared__ unsigned long long t_found;
+  for (;;) {
+    if (rank == 0 && threadIdx.x < 32) {
+      int np = 0;
+      const int plan = engine_poll(s, issued, &np);
+      if (threadIdx.x == 0) {
+        if (plan >= 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");   // the producer's data
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_found));
+        job[0] = plan;
+        job[1] = plan >= 0 ? (int32_t)issued[plan] : 0;
+        job[2] = np;
+      }
+    }
+    cluster_sync_all();   // B1: the job is posted
+    unsigned long long t_b1 = 0, t_copied = 0, t_b2 = 0;
+    if (rank == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b1));
+    int32_t plan, k, np, pad_;
+    asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(plan), "=r"(k), "=r"(np), "=r"(pad_) : "r"(job_addr) : "memory");
+    if (plan < 0) {       // park: rank 0 keeps its progress for the relaunch
+      if (rank == 0)
+        for (int p = threadIdx.x; p < kEngineMaxPlans; p += blockDim.x) s->issued[p] = issued[p];
+      cluster_sync_all();   // nobody leaves while a peer may still read rank 0's shared memory
+      return;
+    }
+    if (np > loaded) {    // newly registered plans' parameters into shared memory
+      for (int p = loaded; p < np; ++p) {
+        const int* from = reinterpret_cast<const int*>(&plans[p].kp);
+        int* to = reinterpret_cast<int*>(&sp[p]);
+        for (int i = threadIdx.x; i < (int)(sizeof(KParams) / sizeof(int)); i += blockDim.x) to[i] = from[i];
+        if (threadIdx.x == 0) svec[p] = plans[p].vec;
+      }
+      loaded = np;
+      __syncthreads();
+    }
+    const KParams& kp = sp[plan];
+    if (svec[plan] == 32)
+      run_chunks<32, 4, 256>(kp, kp.src + (int64_t)k * kp.dyn_ss, kp.dst + (int64_t)k * kp.dyn_ds, rank, W);
+    else
+      run_chunks<16, 4, 256>(kp, kp.src + (int64_t)k * kp.dyn_ss, kp.dst + (int64_t)k * kp.dyn_ds, rank, W);
+    if (rank == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_copied));
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this thread's stores, performed at gpu scope
+    cluster_sync_all();   // B2: every CTA's stores are in rank 0's causality past
+    if (rank == 0 && threadIdx.x == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b2));
+      if (kp.flag) {
+        const unsigned long long seq = kp.seq + (unsigned long long)k;
+        if (kp.pub == 3)
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(kp.flag), "l"(seq) : "memory");
+        else
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(kp.flag), "l"(seq) : "memory");
+      }
+      unsigned long long* stamps = s->stamps;
+      const unsigned long long n_stamps = s->n_stamps;
+      if (stamps && n_stamps) {   // [flag released, job found, past B1, copy issued, past B2]
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        unsigned long long* r = stamps + 5 * (((unsigned long long)k * (unsigned long long)np + plan) % n_stamps);
+        r[0] = t;
+        r[1] = t_found;
+        r[2] = t_b1;
+        r[3] = t_copied;
+        r[4] = t_b2;
+      }
+      issued[plan] = (unsigned long long)k + 1;
+      st_rel_gpu(&s->done[plan], (unsigned long long)k + 1);
+    }
+  }
+}
+
+int engine_smem() { return (int)(kEngineMaxPlans * (sizeof(KParams) + sizeof(int32_t))); }
+
+// Cluster size of the engine: n_ctas when the device accepts it (> 8 needs the non-portable
+// attribute), else an error.
+static dv_status engine_cfg(int n_ctas) {
+  static std::atomic<uint64_t> mask{0};
+  if (first_use_on_device(mask)) {
+    cudaFuncSetAttribute(k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, engine_smem());
+    cudaFuncSetAttribute(k_engine, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    (void)cudaGetLastError();
+  }
+  if (n_ctas < 1 || n_ctas > kEngineMaxCtas) return fail(DV_EINVAL, "engine CTAs %d outside [1, %d]", n_ctas, kEngineMaxCtas);
+  return DV_OK;
+}
+
+dv_status engine_alloc(void** state, void** plans) {
+  DV_CUDA(cudaMalloc(state, sizeof(EState)));
+  DV_CUDA(cudaMalloc(plans, sizeof(EPlan) * kEngineMaxPlans));
+  DV_CUDA(cudaMemset(*state, 0, sizeof(EState)));
+  DV_CUDA(cudaMemset(*plans, 0, sizeof(EPlan) * kEngineMaxPlans));
+  return DV_OK;
+}
+
+dv_status engine_launch(void* state, const void* plans, int n_ctas, cudaStream_t st) {
+  DV_TRY(engine_cfg(n_ctas));
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_ctas);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = engine_smem();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;   // the whole grid is ONE cluster
+  at[0].val.clusterDim.x = n_ctas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_engine, (EState*)state, (const EPlan*)plans);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "engine kernel launch");
+  return DV_OK;
+}
+
+unsigned long long* engine_word(void* state, int which, int plan) {
+  EState* s = (EState*)state;
+  switch (which) {
+    case 0: return &s->want[plan];
+    case 1: return &s->done[plan];
+    case 2: return nullptr;
+    default: return nullptr;
+  }
+}
+size_t engine_field_offset(int which) {
+  switch (which) {
+    case 0: return offsetof(EState, stop);
+    case 1: return offsetof(EState, n_plans);
+    case 2: return offsetof(EState, stamps);
+    default: return offsetof(EState, n_stamps);
+  }
+}
+
+// Plan `id` := the whole run plan p (one launch's worth; at most 2^31 vectors), released into
+// `flag` with seq + k at step k.
+dv_status engine_set_plan(void* plans, int id, const CopyPlan& p, const Release& rel, int32_t max_step,
+                          cudaStream_t st) {
+  if (p.kind != kRun) return fail(DV_ENOTSUP, "engine plans are run copies (no packet transpose)");
+  uint64_t orall = (uint64_t)(uintptr_t)p.src | (uint64_t)(uintptr_t)p.dst | p.run_bytes;
+  for (int k = 0; k < kDims; ++k) orall |= (uint64_t)p.ss[k] | (uint64_t)p.ds[k];
+  orall |= (uint64_t)p.dyn_ss | (uint64_t)p.dyn_ds;
+  if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
+  const int VEC = (orall % 32 == 0) ? 32 : 16;
+  if (p.runs() * (p.run_bytes / VEC) >= (1ull << 31)) return fail(DV_ENOTSUP, "engine plan too large");
+  EPlan e{};
+  fill_kparams(p, VEC, &e.kp);
+  e.kp.dyn = nullptr;
+  e.kp.flag = rel.flag;
+  e.kp.seq = rel.seq;
+  e.kp.pub = pub_of(rel) >= 2 ? pub_of(rel) : 2;
+  e.vec = VEC;
+  e.max_step = max_step;
+  DV_CUDA(cudaMemcpyAsync((EPlan*)plans + id, &e, sizeof e, cudaMemcpyHostToDevice, st));
+  DV_CUDA(cudaStreamSynchronize(st));
+  return DV_OK;
+}
+
 // Load every kernel of the library on the current device now (cudaFuncGetAttributes needs the
 // loaded function). Under CUDA lazy loading a kernel is otherwise loaded at its first launch, and
 // that load waits for the device: a consumer kernel already spinning on one of our flags would
@@ -1337,6 +1580,7 @@ void preload_kernels() {
   (void)cluster_ctas();   // decide the cluster size (and set the attribute) outside any capture
   load_fn(k_run_copy<16, 1, 32>);
   load_fn(k_wait_geq);
+  load_fn(k_engine);
   load_vec<16>();
   load_vec<32>();
   for (int pk : {0, 1, 2, 4, 8, 16}) {

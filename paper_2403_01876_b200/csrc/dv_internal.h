@@ -102,6 +102,17 @@ void preload_kernels();
 // loads (for words in peer memory, where stream memory operations are not used).
 dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream);
 
+// ---- persistent stream engine (copy_kernels.cu k_engine; C API dv_engine_* in api.cu) --------
+constexpr int kEngineMaxPlans = 256;
+dv_status engine_alloc(void** state, void** plans);
+dv_status engine_launch(void* state, const void* plans, int n_ctas, cudaStream_t st);
+// which: 0 = want[plan] (the doorbell), 1 = done[plan], 2 = completed jobs
+unsigned long long* engine_word(void* state, int which, int plan);
+// which: 0 = stop, 1 = n_plans, 2 = stamps pointer, 3 = n_stamps -- byte offsets in the state
+size_t engine_field_offset(int which);
+dv_status engine_set_plan(void* plans, int id, const CopyPlan& p, const Release& rel, int32_t max_step,
+                          cudaStream_t st);
+
 // ---- CUDA driver entry points (resolved through the runtime; no -lcuda) --------------------
 struct Driver {
   int (*streamWaitValue64)(void* stream, unsigned long long addr, unsigned long long value,
@@ -166,6 +177,8 @@ struct dv_ctx {
   std::atomic<uint32_t> next_ev{0};
   std::mutex pipe_mu;     // one pipelined transfer enqueued at a time per context
   unsigned long long* trace_ts = nullptr;  // dvt_trace: publish timestamps land here
+  std::vector<dv_engine*> engines;        // live persistent engines (parked by dv_destroy)
+  std::mutex engine_mu;
   // A ticket is held only while its kernel runs (the last CTA resets it), and tickets are handed
   // out round robin at enqueue, so a ticket is reused only after 65,536 later publishing launches
   // of this context -- far more than can be in flight while one copy kernel is still running.

@@ -26,6 +26,9 @@ struct FillParams {
   int32_t box[5];
   int32_t vlo, vhi;
   unsigned long long* t_end;  // optional: max over CTAs of %globaltimer after their stores
+  uint64_t* ring;             // optional: a dv_engine doorbell the last CTA rings (dvt_fill_ring)
+  uint64_t ring_step;
+  unsigned int* ticket;       // CTA counter for the last-CTA ring (zero between uses)
 };
 
 // The generator's word at global coordinate (kv, l, r, h, s, d) (kvgen.hash_words / uid / const).
@@ -74,6 +77,18 @@ __global__ void k_fill(const FillParams p) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       atomicMax(p.t_end, t);
+    }
+  }
+  if (p.ring) {   // a producer ringing the engine itself: the last CTA, after every CTA's stores
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      const unsigned prev = atomicAdd(p.ticket, 1u);
+      if (prev == gridDim.x * gridDim.y - 1) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        *p.ticket = 0u;
+        dv_engine_ring(p.ring, p.ring_step);
+      }
     }
   }
 }
@@ -219,6 +234,28 @@ extern "C" dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, co
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)slabs, 2);
   cfg.blockDim = dim3(threads);
+  cfg.stream = (cudaStream_t)stream;
+  DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill, p));
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region* region,
+                                   uint64_t* t_end, uint64_t* doorbell, uint64_t step,
+                                   uint32_t* ticket, void* stream) {
+  if (!doorbell || !ticket) return fail(DV_EINVAL, "NULL doorbell or ticket");
+  FillParams p;
+  uint64_t slabs;
+  DV_TRY(fill_params(c, DVT_FILL_HASH, seed, nullptr, 0, 1 << 30, region, &p, &slabs));
+  p.t_end = (unsigned long long*)t_end;
+  p.ring = doorbell;
+  p.ring_step = step;
+  p.ticket = ticket;
+  if (!slabs) return fail(DV_EINVAL, "empty region");
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)slabs, 2);
+  cfg.blockDim = dim3(p.n * p.D >= 256 ? 256 : 128);
   cfg.stream = (cudaStream_t)stream;
   DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill, p));
   DV_CUDA(cudaGetLastError());

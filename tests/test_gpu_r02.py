@@ -444,3 +444,140 @@ def test_streaming_under_concurrent_compute_matches_oracle(xfer):
                 bad.append(t)
     torch.cuda.synchronize()
     assert int(fl[0]) == seq0 + n and not bad, bad[:5]
+
+
+# ------------------------------------------------------------------------------------------------
+# Persistent stream engine (include/dv.h dv_engine_*; the per-layer latency path).
+# While an engine runs, a kernel that is not loaded yet (CUDA lazy loading) or a new stream cannot
+# start: every test creates its streams and warms the kernels it uses before the engine runs.
+def _engine_case(seed, L=4, B=2, H=4, S=48, D=32, p=8):
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=seed)
+    return (L, B, H, S, D, p), K, V
+
+
+def _wait_done(eng, plans, n, timeout=10.0):
+    t0 = time.time()
+    while any(eng.done(pl) < n for pl in plans):
+        assert time.time() - t0 < timeout, [eng.done(pl) for pl in plans]
+
+
+@pytest.mark.parametrize("dst_host", [False, True])
+def test_engine_per_layer_plans_match_oracle(dst_host):
+    """One engine plan per layer (a dyn scatter into a host / device log: token step k of layer l
+    lands at k*step + l*layer bytes), kicked per layer per token step from a stream; each layer's
+    flag word reaches seq + k; the log equals the oracle's packs. Then park ->
+    torch.cuda.synchronize() returns -> a kick relaunches the engine for a new plan."""
+    (L, B, H, S, D, p), K, V = _engine_case(701)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    osrc = ok.Cache(K, V, 0, 0, H, S, D)
+    T = S - p
+    lay = ok.region_bytes(0, 1, 0, B, 0, 1, H, D, 2)
+    stepb = L * lay
+    log = pinned_u16(T * stepb // 2) if dst_host else torch.full((T * stepb // 2,), -1, dtype=torch.int16, device="cuda")
+    fl = flags(L, pinned=dst_host)
+    ep = dv.endpoint_of(log, fl)
+    log2 = torch.full((stepb // 2,), -1, dtype=torch.int16, device="cuda")
+    fl2 = flags(1)
+    st = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    cx = ctx()
+    eng = dv.Engine(cx, 4)
+    try:
+        plans = [eng.plan_scatter(c, (l, l + 1, 0, B, p, p + 1), ep, l * lay, stepb, flag_slot=l, seq=1, max_step=T - 1)
+                 for l in range(L)]
+        for t in range(T):
+            for l in range(L):
+                eng.kick(plans[l], t, stream=st)
+        _wait_done(eng, plans, T)
+        eng.park()
+        torch.cuda.synchronize()                 # returns: the engine is parked
+        assert fl.tolist() == [T] * L
+        got = to_np(log)
+        for t in range(T):
+            for l in range(L):
+                o = (t * stepb + l * lay) // 2
+                assert np.array_equal(got[o:o + lay // 2], ok.pack(osrc, (l, l + 1, 0, B, p + t, p + t + 1))), (t, l)
+        # a kick relaunches the parked engine; a plan registered while parked runs
+        pl2 = eng.plan_scatter(c, (0, L, 0, B, p, p + 1), dv.endpoint_of(log2, fl2), 0, 0, flag_slot=0, seq=5, max_step=0)
+        eng.kick(pl2, 0, stream=st)
+        _wait_done(eng, [pl2], 1)
+        eng.park()
+        torch.cuda.synchronize()
+        assert int(fl2[0]) == 5 and np.array_equal(to_np(log2), ok.pack(osrc, (0, L, 0, B, p, p + 1)))
+        assert [eng.done(pl) for pl in plans] == [T] * L   # parking kept every plan's progress
+    finally:
+        eng.close()
+
+
+def test_engine_producer_rings_doorbell_remap_matches_oracle():
+    """A producer kernel rings the engine itself (dvt_fill_ring: its last CTA releases the doorbell
+    after every CTA's stores): each token step rewrites position p + k of every layer with a new
+    seed, then the engine remaps that position into a second cache (a C5 replica store shape) and
+    releases the flag -- a consumer stream waiting on the flag copies the replica's position out
+    before the next step; every copy equals the generator for that step's seed."""
+    (L, B, H, S, D, p), K, V = _engine_case(702)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    rk, rv = sentinel_like((L, B, H, S, D)), sentinel_like((L, B, H, S, D))
+    rep = dv.cache(rk, rv)
+    fl = flags(1)
+    sig = dv.endpoint_of(fl, fl)
+    cx = ctx()
+    T = 16
+    ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dummy = torch.zeros(1, dtype=torch.int64, device="cuda")
+    prod, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [(torch.empty((L, B, H, D), dtype=torch.int16, device="cuda"),
+             torch.empty((L, B, H, D), dtype=torch.int16, device="cuda")) for _ in range(T)]
+    # warm every kernel used while the engine runs
+    dv.dvt_fill_ring(c, 1, (0, L, 0, B, 0, 1), dummy.data_ptr(), 0, ticket.data_ptr(), stream=prod)
+    with torch.cuda.stream(cons):
+        outs[0][0].copy_(rk[:, :, :, p])
+    torch.cuda.synchronize()
+    eng = dv.Engine(cx, 4)
+    try:
+        pl = eng.plan_remap(c, rep, (0, L, 0, B, p, p + 1), sig, flag_slot=0, seq=1, max_step=T - 1)
+        db = eng.doorbell(pl)
+        for t in range(T):
+            dv.dvt_fill_ring(c, 1000 + t, (0, L, 0, B, p + t, p + t + 1), db, t, ticket.data_ptr(), stream=prod)
+            dv.dv_wait(cx, sig, 0, 1 + t, stream=cons)
+            with torch.cuda.stream(cons):
+                outs[t][0].copy_(rk[:, :, :, p + t])
+                outs[t][1].copy_(rv[:, :, :, p + t])
+        prod.synchronize()
+        cons.synchronize()
+        eng.park()
+        torch.cuda.synchronize()
+        assert int(fl[0]) == T
+        for t, (ok_, ov_) in enumerate(outs):
+            Kt, Vt = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=1000 + t)
+            assert np.array_equal(to_np(ok_), Kt[:, :, :, p + t]) and np.array_equal(to_np(ov_), Vt[:, :, :, p + t]), t
+    finally:
+        eng.close()
+
+
+def test_engine_validation():
+    (L, B, H, S, D, p), K, V = _engine_case(703)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    cx = ctx()
+    buf = torch.empty(1 << 16, dtype=torch.int16, device="cuda")
+    with pytest.raises(dv.DVError) as ei:
+        dv.Engine(cx, 17)                            # one cluster: at most 16 CTAs
+    assert ei.value.status == dv.DV_EINVAL
+    eng = dv.Engine(cx, 2)
+    try:
+        with pytest.raises(dv.DVError) as ei:       # step S - p would run past max_seq
+            eng.plan_scatter(c, (0, L, 0, B, p, p + 1), dv.endpoint_of(buf), 0, 0, max_step=S - p)
+        assert ei.value.status == dv.DV_ERANGE
+        pl = eng.plan_scatter(c, (0, 1, 0, B, p, p + 1), dv.endpoint_of(buf), 0, 0, max_step=3)
+        with pytest.raises(dv.DVError) as ei:
+            eng.kick(pl, 4)
+        assert ei.value.status == dv.DV_ERANGE
+        with pytest.raises(dv.DVError) as ei:
+            eng.kick(pl + 1, 0)
+        assert ei.value.status == dv.DV_EINVAL
+    finally:
+        eng.close()
+    torch.cuda.synchronize()
