@@ -17,6 +17,8 @@ The measurements (all timed on the device with CUDA events, max over ranks):
           system-scope release of the seq flag, %globaltimer) and a ping-pong RTT; NCCL baseline
           (pack -> ncclSend/ncclRecv -> unpack) for the same token steps and the same prompt
           replica; every word of every replica store checked on the device (dvt_verify);
+  C4      microbatch swapping on every rank at once (configs[3]): the shared
+          host PCIe fabric, per-GPU vs alone, NUMA-local pinned logs;
   C3      prompt->token disaggregation (configs[2], PAPER.md:266 §4.2.1): OPT-66B b 8, p 1000;
           N/2 prompt GPUs (S 1024) hand their prompt KV layer by layer (Opt 2)
           straight into N/2 token GPUs with a different layer partition (S 2048); NCCL baseline
@@ -562,6 +564,73 @@ def c3_suite(ctx, env, steps=3, peak=None, peak_src=None, nccl=True):
 
 
 # =====================================================================================================
+# C4 concurrent swapping: the shared host PCIe fabric (BASELINE.json configs[3])
+# =====================================================================================================
+def c4_concurrent(ctx, env, steps=4):
+    """Every rank is one BLOOM-176B pipeline stage (9 layers, b 4, S 2048) swapping microbatches
+    with its own NUMA-local pinned host log (dv_host_alloc_near): per step, the step delta of the
+    running microbatch out (2.06 MB, decoupled) and the whole i = 1024 prefix of the next one in
+    (2.11 GB, copy engine; PAPER.md:572 transf_i = i*B*C). Rank 0 alone first, then all ranks at
+    once: per-GPU and aggregate PCIe GB/s. Every swapped-in word verified on the device."""
+    Hc, nL, b, S, i_pref = 112, 9, 4, 2048, (128 if _small() else 1024)
+    seed = 20240307
+    step_b = 2 * nL * b * Hc * D * 2
+    nb_in = i_pref * step_b
+    run_k = torch.empty((nL, b, Hc, S, D), dtype=torch.int16, device=env.dev)
+    run_v = torch.empty_like(run_k)
+    run = dv.cache(run_k, run_v)
+    dv.dvt_fill(run, dv.DVT_FILL_HASH, seed=seed)
+    free_k = torch.full_like(run_k, -1)
+    free_v = torch.full_like(run_v, -1)
+    free = dv.cache(free_k, free_v)
+    hp, node = dv.dv_host_alloc_near(env.local, nb_in + 64 * step_b)
+    try:
+        log = dv.endpoint(dv.DV_EP_HOST, hp, nb_in)
+        out_fl = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        out = dv.endpoint(dv.DV_EP_HOST, hp + nb_in, 64 * step_b, out_fl.data_ptr(), 1)
+        sp = torch.cuda.current_stream().cuda_stream
+        dv.dv_scatter(ctx, run, (0, nL, 0, b, 0, i_pref), log, 0, stream=sp)   # the microbatch's swap-out
+        seq = [0]
+
+        def step():
+            seq[0] += 1
+            q = i_pref + seq[0] % (S - i_pref)
+            dv.dv_scatter(ctx, run, (0, nL, 0, b, q, q + 1), out, (seq[0] % 64) * step_b, flag_slot=0, seq=seq[0],
+                          xfer=dv.DV_XFER_DECOUPLED, stream=sp)
+            dv.dv_gather(ctx, log, 0, free, (0, nL, 0, b, 0, i_pref), stream=sp)
+
+        def timed(active):
+            def body():
+                if active:
+                    for _ in range(steps):
+                        step()
+                    dv.dv_wait(ctx, out, 0, seq[0], stream=sp)
+            return _timed(env, body)
+        step()
+        env.barrier()
+        moved = steps * (nb_in + step_b)
+        ms_alone = timed(env.rank == 0)
+        ms_all = timed(True)
+        cnt = torch.zeros(1, dtype=torch.int64, device=env.dev)
+        dv.dvt_verify(free, cnt.data_ptr(), seed=seed, reg=dv.region(0, nL, 0, b, 0, i_pref), stream=sp)
+        torch.cuda.synchronize()
+        bad = int(env.max(float(cnt.item())))
+        per_all = moved / ms_all / 1e6
+        return {"workload": f"C4 BLOOM-176B stage (9 layers, b4, S2048) per rank: swap-out of a step delta "
+                            f"({step_b} B, decoupled) + swap-in of the i = {i_pref} prefix ({nb_in} B) per step",
+                "steps": steps, "numa_node": node,
+                "alone_gbs_rank0": moved / ms_alone / 1e6,
+                "concurrent_gbs_per_gpu": per_all, "concurrent_gbs_aggregate": per_all * env.world,
+                "concurrent_vs_alone": (moved / ms_all) / (moved / ms_alone),
+                "parity": {"mismatches": bad, "how": "dvt_verify of every swapped-in word vs the generator"},
+                "how": "per-GPU = bytes moved / device time (max over ranks); aggregate = per-GPU x N"}
+    finally:
+        torch.cuda.synchronize()
+        dv.dv_host_free(hp)
+        del run_k, run_v, free_k, free_v
+        torch.cuda.empty_cache()
+
+
 def nvlink_suite(ctx, env, steps=200, nccl=True):
     """Everything above in one pass; returns the dict for rank 0's JSON line (None on other ranks)."""
     t0 = time.perf_counter()
@@ -578,7 +647,8 @@ def nvlink_suite(ctx, env, steps=200, nccl=True):
     peak = res["link"].get("peak_gbs")
     src = "in-run peer copy (link probe: max of copy-engine / SM-store ring and one-direction copies)"
     for name, fn in (("c5", lambda: c5_suite(ctx, env, steps, peak, src, nccl)),
-                     ("c3", lambda: c3_suite(ctx, env, 3, peak, src, nccl))):
+                     ("c3", lambda: c3_suite(ctx, env, 3, peak, src, nccl)),
+                     ("c4_pcie_concurrent", lambda: c4_concurrent(ctx, env))):
         try:
             res[name] = fn()
         except Exception as e:   # noqa: BLE001
