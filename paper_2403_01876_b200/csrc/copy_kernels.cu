@@ -710,13 +710,77 @@ __device__ __forceinline__ void transpose_tiles(const TParams& p, uint4* tile, c
   }
 }
 
+// Two-position register form (PK packets x 2 adjacent positions per item, DV_PP=2): the
+// packet-major side moves 32-byte vectors (positions s, s+1 of one packet are adjacent there), the
+// position-major side two PK*16-byte row pieces. Items = slabs x (U / PK) x (N / 2); N even.
+template <int DIR, int PK>
+__device__ __forceinline__ void transpose_regs2(const TParams& p, const uint8_t* src0, uint8_t* dst0,
+                                                uint32_t bid, uint32_t nb) {
+  for (uint32_t i = bid * 256 + threadIdx.x; i < p.n_items; i += nb * 256) {
+    uint32_t rest, s2, slab, g;
+    p.fN.divmod(i, rest, s2);   // fN = N / 2
+    p.fG.divmod(rest, slab, g);
+    int64_t so = 0, dof = 0;
+    uint32_t q = slab;
+#pragma unroll
+    for (int k = 3; k >= 1; --k) {
+      uint32_t x;
+      p.fd[k].divmod(q, q, x);
+      so += (int64_t)x * p.ss[k];
+      dof += (int64_t)x * p.ds[k];
+    }
+    so += (int64_t)q * p.ss[0];
+    dof += (int64_t)q * p.ds[0];
+    const uint32_t u0 = g * PK, s = 2 * s2;
+    Vec<32> v[PK];   // v[k]: packet u0 + k at positions s (words 0..3) and s + 1 (words 4..7)
+    if (DIR == 0) {  // packet-major source
+      const uint8_t* a = src0 + so + (int64_t)u0 * p.su + (int64_t)s * 16;
+#pragma unroll
+      for (int k = 0; k < PK; ++k) ld_vec(v[k], a + (int64_t)k * p.su);
+      uint8_t* d = dst0 + dof + (int64_t)s * p.sps + (int64_t)u0 * 16;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < PK; k += 2) {
+          Vec<32> x;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            x.w[c] = v[k].w[4 * r + c];
+            x.w[4 + c] = v[k + 1].w[4 * r + c];
+          }
+          st_vec(d + (int64_t)r * p.sps + 16 * k, x);
+        }
+    } else {         // position-major source
+      const uint8_t* a = src0 + so + (int64_t)s * p.sps + (int64_t)u0 * 16;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k < PK; k += 2) {
+          Vec<32> x;
+          ld_vec(x, a + (int64_t)r * p.sps + 16 * k);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            v[k].w[4 * r + c] = x.w[c];
+            v[k + 1].w[4 * r + c] = x.w[4 + c];
+          }
+        }
+      uint8_t* d = dst0 + dof + (int64_t)u0 * p.su + (int64_t)s * 16;
+#pragma unroll
+      for (int k = 0; k < PK; ++k) st_vec(d + (int64_t)k * p.su, v[k]);
+    }
+  }
+}
+
 // PK is a template parameter of the kernels (not a runtime branch): the register budget of each
 // instantiation is that of its own form (59-64 registers at PK <= 4, 1024 threads per SM).
+// PK > 32 selects the two-position form with PK - 32 packets per item.
 template <int DIR, int PK>
 __device__ __forceinline__ void transpose_any(const TParams& p, uint4* tile, const uint8_t* src0,
                                               uint8_t* dst0, uint32_t bid, uint32_t nb) {
   if constexpr (PK == 0)
     transpose_tiles<DIR>(p, tile, src0, dst0, bid, nb);
+  else if constexpr (PK > 32)
+    transpose_regs2<DIR, PK - 32>(p, src0, dst0, bid, nb);
   else
     transpose_regs<DIR, PK>(p, src0, dst0, bid, nb);
 }
@@ -849,6 +913,7 @@ struct Tune {
   uint64_t small = 148ull * 128 * 4;  // DV_SMALL: copies up to this many vectors use U=1, 128 thr
   int trs = 0;  // DV_TRS: packet transpose form (0 registers PK<=pk; 1 shared-memory tiles; 2 PK=1; 3 PK<=2)
   int pk = 16;  // DV_PK: largest packets per register-transpose item (1, 2, 4, 8, 16)
+  int pp = 1;       // DV_PP: positions per register-transpose item (1, or 2 = the two-position form)
   int cluster = 1;  // DV_CLUSTER: small released copies as one cluster (0 off; 1 gpu-scope releases of
                     // <= 8192 vectors; 2 whenever it fits -- see launch_copy)
   int rdbulk = 0;     // DV_RDBULK: dense-source copies reading over a link use k_unpack_bulk (2: any source)
@@ -871,6 +936,7 @@ static const Tune& tune() {
     if (const char* e = getenv("DV_TRS")) x.trs = atoi(e);
     if (const char* e = getenv("DV_PK")) x.pk = atoi(e);
     if (const char* e = getenv("DV_CLUSTER")) x.cluster = atoi(e);
+    if (const char* e = getenv("DV_PP")) x.pp = atoi(e);
     if (const char* e = getenv("DV_RDBULK")) x.rdbulk = atoi(e);
     if (const char* e = getenv("DV_RDCH")) x.rdch = (uint32_t)std::max(16, atoi(e) / 16 * 16);
     if (const char* e = getenv("DV_RDST")) x.rdst = (uint32_t)std::min(kRdStagesMax, std::max(1, atoi(e)));
@@ -1138,7 +1204,18 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
         break;
       }
   }
-  if (tp.pk) {
+  // DV_PP=2: the two-position form, when N is even and the packet-major side's 32-byte vectors
+  // are aligned too (base, packet stride, slab strides, step stride)
+  uint64_t km = p.t_su | (uint64_t)(p.tdir == 0 ? p.dyn_ss : p.dyn_ds) |
+                (uint64_t)(uintptr_t)(p.tdir == 0 ? p.src : p.dst);
+  for (int d = 0; d < 4; ++d) km |= (uint64_t)(p.tdir == 0 ? tp.ss[d] : tp.ds[d]);
+  if (tune().pp == 2 && (tp.pk == 16 || tp.pk == 8 || tp.pk == 4) && p.tN % 2 == 0 && km % 32 == 0) {
+    const int pk2 = tp.pk == 4 ? 4 : 8;
+    tp.n_items = (uint32_t)(items1 / pk2 / 2);
+    tp.fN = to_dev(make_fastdiv(p.tN / 2));
+    tp.fG = to_dev(make_fastdiv(p.tU / pk2));
+    tp.pk = 32 + pk2;
+  } else if (tp.pk) {
     tp.n_items = (uint32_t)(items1 / tp.pk);
     tp.fN = to_dev(make_fastdiv(p.tN));
     tp.fG = to_dev(make_fastdiv(p.tU / tp.pk));
@@ -1173,6 +1250,8 @@ using TrFn = void (*)(TParams, KParams, uint32_t);
 template <int DIR>
 static PtFn pt_fn(int pk) {
   switch (pk) {
+    case 40: return k_packet_transpose<DIR, 40>;
+    case 36: return k_packet_transpose<DIR, 36>;
     case 16: return k_packet_transpose<DIR, 16>;
     case 8: return k_packet_transpose<DIR, 8>;
     case 4: return k_packet_transpose<DIR, 4>;
@@ -1184,6 +1263,8 @@ static PtFn pt_fn(int pk) {
 template <int DIR, int VEC>
 static TrFn tr_fn(int pk) {
   switch (pk) {
+    case 40: return k_transpose_run<DIR, VEC, 40>;
+    case 36: return k_transpose_run<DIR, VEC, 36>;
     case 16: return k_transpose_run<DIR, VEC, 16>;
     case 8: return k_transpose_run<DIR, VEC, 8>;
     case 4: return k_transpose_run<DIR, VEC, 4>;
@@ -1571,7 +1652,7 @@ static void load_vec() {
   load_fn(k_copy_cluster<VEC, 1>);
   load_fn(k_copy_cluster<VEC, 2>);
   load_fn(k_copy_cluster<VEC, 4>);
-  for (int pk : {0, 1, 2, 4, 8, 16}) {
+  for (int pk : {0, 1, 2, 4, 8, 16, 36, 40}) {
     load_fn(tr_fn<0, VEC>(pk));
     load_fn(tr_fn<1, VEC>(pk));
   }
@@ -1583,7 +1664,7 @@ void preload_kernels() {
   load_fn(k_engine);
   load_vec<16>();
   load_vec<32>();
-  for (int pk : {0, 1, 2, 4, 8, 16}) {
+  for (int pk : {0, 1, 2, 4, 8, 16, 36, 40}) {
     load_fn(pt_fn<0>(pk));
     load_fn(pt_fn<1>(pk));
   }

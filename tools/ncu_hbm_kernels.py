@@ -66,7 +66,7 @@ def main():
         dv.dv_scatter(ctx, c6, dv.region(1, 2, 0, B, P, P + 1), dv.endpoint_of(host, hfl), 0, flag_slot=0,
                       seq=1 + i)
     torch.cuda.synchronize()
-    reg7 = (0, 2, 0, B, 1000, 1064)                       # 2 layers x 64 positions = 10.5 MB
+    reg7 = (0, 2, 0, B, 1000, 1064)                       # 2 layers x 64 positions = 20.97 MB (K and V)
     nb7 = 2 * 2 * B * H * 64 * D * 2
     hlog = torch.zeros(nb7 // 2, dtype=torch.int16, pin_memory=True)
     for _ in range(2):

@@ -13,7 +13,7 @@ KEYS = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum", "dra
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread"]
 LABELS = ["C2 token step -> HBM wire", "C2 prompt layer -> HBM wire", "C3 prompt layer remap S1024->2048",
           "FT6D prompt layer pack, K transpose + V run copy", "token-layer 160 KiB -> HBM + flag",
-          "token-layer 160 KiB -> pinned host + flag", "10.5 MB gather FROM pinned host (kernel loads)"]
+          "token-layer 160 KiB -> pinned host + flag", "20.97 MB gather FROM pinned host (kernel loads)"]
 
 
 def main(rep):
