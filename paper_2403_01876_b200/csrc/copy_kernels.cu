@@ -1482,6 +1482,8 @@ __global__ void __launch_bounds__(256) k_engine(EState* s, const EPlan* plans) {
         job[0] = plan;
         job[1] = plan >= 0 ? (int32_t)issued[plan] : 0;
         job[2] = np;
+        // taken: the next poll (after the barriers below) must not see this step as pending
+        if (plan >= 0) issued[plan] += 1;
       }
     }
     cluster_sync_all();   // B1: the job is posted
@@ -1535,7 +1537,6 @@ __global__ void __launch_bounds__(256) k_engine(EState* s, const EPlan* plans) {
         r[3] = t_copied;
         r[4] = t_b2;
       }
-      issued[plan] = (unsigned long long)k + 1;
       st_rel_gpu(&s->done[plan], (unsigned long long)k + 1);
     }
   }
