@@ -190,3 +190,71 @@ def test_random_stream_out_in_against_oracle(block):
             assert np.array_equal(to_np(k), odst[kk].K) and np.array_equal(to_np(v), odst[kk].V), \
                 (block, it, form, xf, sl, dl, sr, dr, sh, dh, kk)
     cx.close()
+
+
+@pytest.mark.parametrize("block", list(range(6)) + list(range(1000, 1000 + 6 * (_SCALE - 1))))
+def test_random_ring_pipelines_against_oracle(block):
+    """Random pipelines streaming T token rounds (one position each) through RING inboxes of random
+    depth (1..3 slots, include/dv.h) with per-source credits in device or pinned-host memory;
+    every source block sends on its own stream, the receivers on another, with random stalls on
+    both sides (the credits must hold the senders back). The final token caches equal the
+    oracle's stream of the whole region."""
+    rng = random.Random(4242 + block)
+    cx = dv.dv_create(0)
+    for it in range(3):
+        D = rng.choice([16, 64])
+        L, R, Hn = rng.randint(1, 6), rng.randint(1, 3), rng.randint(1, 4)
+        sl, dl = _bounds(rng, 0, L, rng.randint(1, min(L, 3))), _bounds(rng, 0, L, rng.randint(1, min(L, 3)))
+        sr, dr = _bounds(rng, 0, R, rng.randint(1, min(R, 2))), _bounds(rng, 0, R, rng.randint(1, min(R, 2)))
+        T, p = rng.randint(4, 12), rng.randint(0, 4)
+        S = p + T + rng.randint(0, 3)
+        ps, ts = ok.Setup(sl, sr, S), ok.Setup(dl, dr, S)
+        dps, dts = dv.Setup(sl, sr, S), dv.Setup(dl, dr, S)
+        seed = rng.randint(0, 1 << 30)
+        depth = rng.randint(1, 3)
+        host = rng.random() < 0.5
+        xf = rng.choice([dv.DV_XFER_FUSED, dv.DV_XFER_AUTO, dv.DV_XFER_DECOUPLED] if host else
+                        [dv.DV_XFER_FUSED, dv.DV_XFER_AUTO])
+        src, osrc, dst, odst = {}, {}, {}, {}
+        for i in range(len(sl) - 1):
+            for u in range(len(sr) - 1):
+                k, v, c, o = mk_cache(rng, sl[i], sl[i + 1] - sl[i], sr[u], sr[u + 1] - sr[u], 0, Hn, S, D,
+                                      rng.choice([0, 1]), seed)
+                src[(i, u)], osrc[(i, u)] = (k, v, c), o
+        for j in range(len(dl) - 1):
+            for w in range(len(dr) - 1):
+                k, v, c, o = mk_cache(rng, dl[j], dl[j + 1] - dl[j], dr[w], dr[w + 1] - dr[w], 0, Hn, S, D,
+                                      rng.choice([0, 1]), 0, sentinel=True)
+                dst[(j, w)], odst[(j, w)] = (k, v, c), o
+        nsrc = len(src)
+        eps, keep = {}, []
+        for (j, w), (k, v, c) in dst.items():
+            slot = c.n_layers * 2 * c.n_reqs * Hn * D * 2          # one position of this block
+            mk = (lambda n, dt: torch.zeros(n, dtype=dt, pin_memory=True)) if host else \
+                 (lambda n, dt: torch.zeros(n, dtype=dt, device="cuda"))
+            buf, fl, cr = mk(depth * slot // 2, torch.int16), mk(nsrc, torch.int64), mk(nsrc, torch.int64)
+            keep += [buf, fl, cr]
+            eps[(j, w)] = dv.endpoint_of(buf, fl, n_slots=depth, slot_bytes=slot, credits=cr)
+        dorder = sorted(dst, key=lambda kk: dts.flat(*kk))
+        ep_list = [eps[kk] for kk in dorder]
+        s_send = {key: torch.cuda.Stream() for key in src}
+        s_recv = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        for t in range(1, T + 1):
+            reg = dv.region(0, L, 0, R, p + t - 1, p + t)
+            for (i, u), (k, v, c) in src.items():
+                if rng.random() < 0.15:
+                    dv.dvt_spin(rng.randint(20_000, 200_000), 1, stream=s_send[(i, u)].cuda_stream)
+                dv.dv_stream_out(cx, c, reg, dps, i, u, dts, ep_list, seq=t, xfer=xf,
+                                 stream=s_send[(i, u)].cuda_stream)
+            if rng.random() < 0.3:
+                dv.dvt_spin(rng.randint(20_000, 300_000), 1, stream=s_recv.cuda_stream)
+            for (j, w) in dorder:
+                dv.dv_stream_in(cx, dst[(j, w)][2], reg, dps, dts, j, w, eps[(j, w)], t, stream=s_recv.cuda_stream)
+        torch.cuda.synchronize()
+        ok.stream(osrc, ps, odst, ts, (0, L, 0, R, p, p + T))
+        for kk in dst:
+            k, v = dst[kk][0], dst[kk][1]
+            assert np.array_equal(to_np(k), odst[kk].K) and np.array_equal(to_np(v), odst[kk].V), \
+                (block, it, depth, host, xf, sl, dl, sr, dr, kk)
+    cx.close()
