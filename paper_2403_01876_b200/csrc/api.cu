@@ -398,12 +398,8 @@ static dv_status credit_wait(dv_ctx* ctx, const dv_endpoint* ep, int32_t slot, u
                              uint32_t xfer, cudaStream_t st) {
   if (!has_ring(ep) || !ep->credits || seq <= (uint64_t)ep->n_slots || (xfer & DV_NOWAIT))
     return DV_OK;   // NOWAIT: the credit was already there at validation (credits only grow)
-  const uint64_t need = seq - (uint64_t)ep->n_slots;
-  const uint64_t* p = &ep->credits[slot];
-  cudaPointerAttributes at;
-  DV_CUDA(cudaPointerGetAttributes(&at, p));
-  if (at.type == cudaMemoryTypeHost || local_vidmem(ctx, p)) return stream_wait_word(p, need, st);
-  return launch_wait_geq(p, need, st);
+  (void)ctx;
+  return stream_wait_word(&ep->credits[slot], seq - (uint64_t)ep->n_slots, st);
 }
 
 static dv_status check_ctx(dv_ctx* ctx) {
@@ -476,17 +472,36 @@ static dv_status word_release(dv_ctx* ctx, uint64_t* word, uint64_t seq, const C
   return DV_OK;
 }
 
+// Stream memory operations serve words in pinned host memory and in the calling GPU's own HBM;
+// a word in peer memory (another GPU's, or mapped from another process) is written / waited on by
+// a one-thread kernel instead (system-scope release / acquire over the link).
+static bool memop_ok(const void* p) {
+  if (in_ipc_mapping(p)) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  if (at.type == cudaMemoryTypeHost) return true;
+  int dev = -1;
+  cudaGetDevice(&dev);
+  return at.type == cudaMemoryTypeDevice && at.device == dev;
+}
+
 static dv_status stream_signal(const dv_endpoint* ep, int32_t slot, uint64_t seq,
                                cudaStream_t stream) {
+  uint64_t* p = &ep->flags[slot];
+  if (!memop_ok(p)) return launch_store_release(p, seq, stream);
   const Driver* d;
   DV_TRY(driver(&d));
-  int r = d->streamWriteValue64(stream, (unsigned long long)(uintptr_t)&ep->flags[slot], seq,
+  int r = d->streamWriteValue64(stream, (unsigned long long)(uintptr_t)p, seq,
                                 CU_STREAM_WRITE_VALUE_DEFAULT);
   if (r) return drv_fail(r, "cuStreamWriteValue64");
   return DV_OK;
 }
 
 static dv_status stream_wait_word(const uint64_t* p, uint64_t v, cudaStream_t stream) {
+  if (!memop_ok(p)) return launch_wait_geq(p, v, stream);
   const Driver* d;
   DV_TRY(driver(&d));
   int r = d->streamWaitValue64(stream, (unsigned long long)(uintptr_t)p, v, CU_STREAM_WAIT_VALUE_GEQ);

@@ -853,6 +853,23 @@ __global__ void k_wait_geq(const unsigned long long* p, unsigned long long v) {
   }
 }
 
+// Stream-ordered release of a word in peer memory (api.cu stream_signal): every earlier grid of the
+// stream has completed; one thread fences at system scope and releases the value.
+__global__ void k_store_release(unsigned long long* p, unsigned long long v) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+dv_status launch_store_release(uint64_t* p, uint64_t v, cudaStream_t stream) {
+  (void)cudaGetLastError();
+  k_store_release<<<1, 32, 0, stream>>>((unsigned long long*)p, (unsigned long long)v);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "release kernel launch");
+  return DV_OK;
+}
+
 dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream) {
   (void)cudaGetLastError();
   k_wait_geq<<<1, 32, 0, stream>>>((const unsigned long long*)p, (unsigned long long)v);
@@ -1662,6 +1679,7 @@ void preload_kernels() {
   (void)cluster_ctas();   // decide the cluster size (and set the attribute) outside any capture
   load_fn(k_run_copy<16, 1, 32>);
   load_fn(k_wait_geq);
+  load_fn(k_store_release);
   load_fn(k_engine);
   load_vec<16>();
   load_vec<32>();

@@ -101,6 +101,8 @@ void preload_kernels();
 // Stream-ordered wait until *p >= v, by a one-thread kernel polling with system-scope acquire
 // loads (for words in peer memory, where stream memory operations are not used).
 dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream);
+// Stream-ordered *p = v with a system-scope release, by a one-thread kernel (peer memory).
+dv_status launch_store_release(uint64_t* p, uint64_t v, cudaStream_t stream);
 
 // ---- persistent stream engine (copy_kernels.cu k_engine; C API dv_engine_* in api.cu) --------
 constexpr int kEngineMaxPlans = 256;
