@@ -143,6 +143,7 @@ _SIGS = {
     "dv_engine_doorbell": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
     "dv_engine_done": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "dvt_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
     "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
@@ -632,6 +633,11 @@ def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
     d = C.c_int32()
     _call("dv_query", ctx.h, C.byref(ep), flag_slot, seq, C.byref(d))
     return bool(d.value)
+
+
+def dvt_tune(name: str, value: int):
+    """Change one experiment knob of the copy kernels at run time (include/dv_trace.h)."""
+    _call("dvt_tune", name.encode(), value)
 
 
 # ---- persistent stream engine (include/dv.h dv_engine_*) -----------------------------------------

@@ -2066,6 +2066,8 @@ dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps) {
   return DV_OK;
 }
 
+dv_status dvt_tune(const char* name, int64_t value) { return set_tune(name, value); }
+
 dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n) {
   if (!e) return fail(DV_EINVAL, "NULL engine");
   if (stamps && !n) return fail(DV_EINVAL, "zero stamps");

@@ -937,7 +937,7 @@ struct Tune {
   uint32_t rdch = 8192;  // DV_RDCH: bytes per bulk read
   uint32_t rdst = 4;     // DV_RDST: bulk reads in flight per CTA (<= kRdStagesMax)
 };
-static const Tune& tune() {
+static Tune& tune_mut() {
   static Tune t = [] {
     Tune x;
     if (const char* e = getenv("DV_U")) x.u = atoi(e);
@@ -960,6 +960,21 @@ static const Tune& tune() {
     return x;
   }();
   return t;
+}
+static const Tune& tune() { return tune_mut(); }
+
+// dvt_tune (dv_trace.h): change one experiment knob at run time (same names as the environment).
+dv_status set_tune(const char* name, int64_t value) {
+  Tune& t = tune_mut();
+  const std::string n = name ? name : "";
+  if (n == "DV_TRS") t.trs = (int)value;
+  else if (n == "DV_PK") t.pk = (int)value;
+  else if (n == "DV_PP") t.pp = (int)value;
+  else if (n == "DV_RDBULK") t.rdbulk = (int)value;
+  else if (n == "DV_BULK") t.bulk = (int)value;
+  else if (n == "DV_CLUSTER") t.cluster = (int)value;
+  else return fail(DV_EINVAL, "unknown tunable '%s'", n.c_str());
+  return DV_OK;
 }
 
 // Publish protocol of a release: the environment's (default 2, system scope), narrowed to gpu
@@ -1211,6 +1226,7 @@ static dv_status fill_tparams(const CopyPlan& p, const Release& rel, TParams* ou
   // (tiles), tools/probe_ft6d_host_ctas.py. In HBM the register form is the faster one. A peer
   // GPU's memory is treated like the host's (NVLink is packetised like PCIe; not measurable on
   // one GPU -- memory IPC-mapped from another process on the SAME GPU stays on the register form).
+  // (DV_TRS=4: the register form even over a link -- the peer-memory experiment of bench_peer)
   const bool host_side = tune().trs == 0 && (over_link(p.src) || over_link(p.dst));
   tp.pk = 0;
   if (tune().trs != 1 && !host_side && items1 < (1ull << 31)) {

@@ -104,6 +104,9 @@ dv_status launch_wait_geq(const uint64_t* p, uint64_t v, cudaStream_t stream);
 // Stream-ordered *p = v with a system-scope release, by a one-thread kernel (peer memory).
 dv_status launch_store_release(uint64_t* p, uint64_t v, cudaStream_t stream);
 
+// Run-time change of an experiment knob (dvt_tune).
+dv_status set_tune(const char* name, int64_t value);
+
 // ---- persistent stream engine (copy_kernels.cu k_engine; C API dv_engine_* in api.cu) --------
 constexpr int kEngineMaxPlans = 256;
 dv_status engine_alloc(void** state, void** plans);

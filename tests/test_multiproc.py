@@ -117,6 +117,8 @@ def test_bench_multirank_launch_path(world):
     assert c5["parity"]["mismatches"] == 0 and c5["nccl_baseline"]["parity"]["mismatches"] == 0
     assert c3["parity"]["mismatches"] == 0 and c3["parity"]["positions_past_prompt_untouched"]
     assert c3["nccl_baseline"]["parity"]["mismatches"] == 0
+    ft = c3["ft6d_token_caches"]
+    assert ft["tile_form_auto"]["mismatches"] == 0 and ft["register_form"]["mismatches"] == 0
     c4 = nv["c4_pcie_concurrent"]
     assert c4["parity"]["mismatches"] == 0 and c4["concurrent_gbs_per_gpu"] > 0 and c4["alone_gbs_rank0"] > 0
     assert c5["latency_per_layer_put"]["release_scope"] == "system" and c5["latency_per_layer_put"]["p50_us"] > 0

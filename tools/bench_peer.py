@@ -478,15 +478,19 @@ class C3:
             self.pv = torch.empty_like(self.pk)
             self.pc = dv.cache(self.pk, self.pv, self.pb[i], 0)
             dv.dvt_fill(self.pc, dv.DVT_FILL_HASH, seed=SEED_C3, valid=(0, self.p))
-            caches, sigs = [], []
+            caches, sigs, ft6d = [], [], []
             for bl in blobs:
                 kp, vp, fp = dv.dv_ipc_open(bl["k"]), dv.dv_ipc_open(bl["v"]), dv.dv_ipc_open(bl["f"])
                 self.opened += [kp, vp, fp]
                 jj = bl["j"]
                 caches.append(dv.cache_raw(kp, vp, bl["device"], 2, self.tb[jj], self.tb[jj + 1] - self.tb[jj], 0,
                                            self.b, H, self.St, D))
+                # the same memory seen as FasterTransformer caches (6-D key, NEXT-1): the FT6D probe
+                ft6d.append(dv.cache_raw(kp, vp, bl["device"], 2, self.tb[jj], self.tb[jj + 1] - self.tb[jj], 0,
+                                         self.b, H, self.St, D, layout=dv.DV_LAYOUT_FT6D))
                 sigs.append(dv.endpoint(dv.DV_EP_PEER, fp, 8 * self.n_p, fp, self.n_p, device=bl["device"]))
             self.caches, self.sigs = dv.cache_array(caches), dv.endpoint_array(sigs)
+            self.caches_ft6d = dv.cache_array(ft6d)
             self.n_dst = len(caches)
         self.layer_bytes = 2 * self.b * H * self.p * D * 2
         self.seq = 0
@@ -494,14 +498,48 @@ class C3:
     def my_prompt_bytes(self):
         return (self.pb[self.i + 1] - self.pb[self.i]) * self.layer_bytes if self.is_prompt else 0
 
-    def handoff(self):
+    def handoff(self, ft6d=False):
         self.seq += 1
         if not self.is_prompt:
             return
         i = self.i
+        dst = self.caches_ft6d if ft6d else self.caches
         for layer in range(self.pb[i], self.pb[i + 1]):       # layer by layer (Opt 2)
             dv.dv_stream_out_direct(self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), self.ps, i,
-                                    0, self.ts, self.caches, self.sigs, seq=self.seq, stream=self.sp)
+                                    0, self.ts, dst, self.sigs, seq=self.seq, stream=self.sp)
+
+    def ft6d_forms(self, steps=2):
+        """NEXT-1 over the link: the hand-off into FasterTransformer token caches (6-D key: every
+        key packet transposed on the way), with the shared-memory tile transpose (the automatic
+        choice for memory reached over a link, DV_TRS=0) and with the register transpose forced
+        (DV_TRS=4) -- which is faster over NVLink settles DESIGN §6's reading. Each form's token
+        caches are reset and verified word by word."""
+        env = self.env
+        out = {}
+        for name, trs in (("tile_form_auto", 0), ("register_form", 4)):
+            if self.is_token:
+                self.tk.fill_(-1)
+                self.tv.fill_(-1)
+            dv.dvt_tune("DV_TRS", trs)
+            try:
+                self.handoff(True)                         # warm-up
+                ms = _timed(env, lambda: self.handoff(True), steps)
+            finally:
+                dv.dvt_tune("DV_TRS", 0)
+            per_gpu = env.max(self.my_prompt_bytes()) * steps / ms / 1e6
+            bad = 0
+            if self.is_token:
+                j = self.j
+                c6 = dv.cache_raw(self.tk.data_ptr(), self.tv.data_ptr(), env.local, 2, self.tb[j],
+                                  self.tb[j + 1] - self.tb[j], 0, self.b, H, self.St, D, layout=dv.DV_LAYOUT_FT6D)
+                cnt = torch.zeros(1, dtype=torch.int64, device=env.dev)
+                dv.dvt_verify(c6, cnt.data_ptr(), seed=SEED_C3, valid=(0, self.p),
+                              reg=dv.region(self.tb[j], self.tb[j + 1], 0, self.b, 0, self.p), stream=self.sp)
+                torch.cuda.synchronize()
+                bad = int(cnt.item())
+            out[name] = {"ms_per_handoff": ms / steps, "gbs_per_prompt_gpu": per_gpu,
+                         "mismatches": int(env.max(float(bad)))}
+        return out
 
     def verify(self):
         env = self.env
@@ -573,6 +611,11 @@ def c3_suite(ctx, env, steps=3, peak=None, peak_src=None, nccl=True):
                       "steps": steps, "roofline": _roof(per_gpu, peak, peak_src, env),
                       "ideal_ms_at_peak": (env.max(c.my_prompt_bytes()) / peak / 1e6) if peak else None}
     out["parity"] = c.verify()
+    try:
+        out["ft6d_token_caches"] = c.ft6d_forms()
+    except Exception as e:   # noqa: BLE001
+        out["ft6d_token_caches"] = {"error": f"{type(e).__name__}: {e}"}
+        env.barrier()
     if nccl and env.world > 1:
         out["nccl_baseline"] = c.nccl_baseline(steps)
         out["dvstream_vs_nccl"] = out["handoff"]["gbs_per_prompt_gpu"] / out["nccl_baseline"]["gbs_per_prompt_gpu"]
