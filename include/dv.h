@@ -417,7 +417,8 @@ DV_API dv_status dv_engine_plan_remap(dv_engine* e, const dv_cache* src, const d
 DV_API dv_status dv_engine_kick(dv_engine* e, int32_t plan, int32_t step, void* stream);
 /* The plan's doorbell word in device memory, for a PRODUCER KERNEL to ring itself (lowest
  * latency; include/dv_device.cuh dv_engine_ring): store step + 1 with a gpu-scope release once all
- * of the producer's stores are ordered before it. The engine must be running (not parked). */
+ * of the producer's stores are ordered before it. The engine must be running (not parked). Steps
+ * beyond the plan's max_step are never run (the engine stops the plan there). */
 DV_API dv_status dv_engine_doorbell(dv_engine* e, int32_t plan, uint64_t** word);
 /* Steps of `plan` the engine has completed (flag released), read now (small synchronous copy). */
 DV_API dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps);

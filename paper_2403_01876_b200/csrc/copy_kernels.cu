@@ -1461,7 +1461,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 // Warp 0 of rank 0: the next pending plan (lowest index), or -1 (stop requested, nothing pending);
 // *np_out = the registered plans seen by the scan.
-__device__ __forceinline__ int engine_poll(EState* s, const unsigned long long* issued, int* np_out) {
+__device__ __forceinline__ int engine_poll(EState* s, const EPlan* plans, const unsigned long long* issued,
+                                           int* np_out) {
   const int lane = threadIdx.x;
   bool stopping = false;
   for (;;) {
@@ -1478,7 +1479,9 @@ __device__ __forceinline__ int engine_poll(EState* s, const unsigned long long* 
 #pragma unroll
     for (int i = 0; i < kEngineMaxPlans / 32; ++i) {
       const int p = lane + 32 * i;
-      const unsigned m = __ballot_sync(0xffffffffu, p < np && w[i] > issued[p]);
+      // a step beyond the plan's validated max_step (a producer ringing too far) is never run
+      const bool pend = p < np && w[i] > issued[p] && issued[p] <= (unsigned long long)plans[p].max_step;
+      const unsigned m = __ballot_sync(0xffffffffu, pend);
       if (m) return 32 * i + __ffs(m) - 1;
     }
     if (stopping) return -1;   // stop seen, and a full scan after it found nothing pending
@@ -1508,7 +1511,7 @@ __global__ void __launch_bounds__(256) k_engine(EState* s, const EPlan* plans) {
   for (;;) {
     if (rank == 0 && threadIdx.x < 32) {
       int np = 0;
-      const int plan = engine_poll(s, issued, &np);
+      const int plan = engine_poll(s, plans, issued, &np);
       if (threadIdx.x == 0) {
         if (plan >= 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");   // the producer's data
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_found));

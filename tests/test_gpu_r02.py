@@ -581,3 +581,37 @@ def test_engine_validation():
     finally:
         eng.close()
     torch.cuda.synchronize()
+
+
+def test_engine_never_runs_past_max_step():
+    """A producer ringing a doorbell beyond the plan's validated max_step must not make the engine
+    copy out of range: steps 0..max_step run, the rest never do."""
+    (L, B, H, S, D, p), K, V = _engine_case(704)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    osrc = ok.Cache(K, V, 0, 0, H, S, D)
+    lay = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    buf = torch.full((6 * lay // 2,), -1, dtype=torch.int16, device="cuda")
+    fl = flags(1)
+    word = torch.tensor([6, 0], dtype=torch.int64, device="cuda")   # "step 5" for the doorbell (+ the next word)
+    cx = ctx()
+    torch.cuda.synchronize()
+    eng = dv.Engine(cx, 2)
+    try:
+        pl = eng.plan_scatter(c, (0, L, 0, B, p, p + 1), dv.endpoint_of(buf, fl), 0, lay, flag_slot=0, seq=1,
+                              max_step=3)
+        db = eng.doorbell(pl)
+        # ring "step 5" straight into the doorbell word (as a runaway producer would) with the
+        # library's own copy kernel (loaded: nothing new may load while the engine runs)
+        dv.dv_flush(cx, word.data_ptr(), 16, dv.endpoint(dv.DV_EP_DEVICE, db, 16, device=0), 0, xfer=dv.DV_XFER_FUSED)
+        _wait_done(eng, [pl], 4)
+        time.sleep(0.05)
+        assert eng.done(pl) == 4
+        eng.park()
+        torch.cuda.synchronize()
+        got = to_np(buf)
+        for t in range(4):
+            assert np.array_equal(got[t * lay // 2:(t + 1) * lay // 2], ok.pack(osrc, (0, L, 0, B, p + t, p + t + 1)))
+        assert np.all(got[4 * lay // 2:] == kvgen.SENTINEL) and int(fl[0]) == 4
+    finally:
+        eng.close()
