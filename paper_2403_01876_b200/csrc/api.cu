@@ -372,6 +372,7 @@ static dv_status read_word(dv_ctx* ctx, const uint64_t* p, uint64_t* out) {
     *out = __atomic_load_n(p, __ATOMIC_ACQUIRE);
     return DV_OK;
   }
+  DV_ON_DEVICE(ctx->device);   // validation may run before the caller switched to ctx's device
   DV_CUDA(cudaMemcpyAsync(out, p, 8, cudaMemcpyDefault, ctx->aux));
   DV_CUDA(cudaStreamSynchronize(ctx->aux));
   return DV_OK;
