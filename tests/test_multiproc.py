@@ -117,6 +117,7 @@ def test_bench_multirank_launch_path(world):
     assert c5["parity"]["mismatches"] == 0 and c5["nccl_baseline"]["parity"]["mismatches"] == 0
     assert c3["parity"]["mismatches"] == 0 and c3["parity"]["positions_past_prompt_untouched"]
     assert c3["nccl_baseline"]["parity"]["mismatches"] == 0
+    assert c3["handoff_copy_engine"]["parity"]["mismatches"] == 0 and c5["prompt_replica_copy_engine"]["gbs_per_gpu"] > 0
     ft = c3["ft6d_token_caches"]
     assert ft["tile_form_auto"]["mismatches"] == 0 and ft["register_form"]["mismatches"] == 0
     c4 = nv["c4_pcie_concurrent"]

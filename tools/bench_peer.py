@@ -256,10 +256,11 @@ class C5:
     def pos(self, t):                                            # reading Q4: step t writes p + t - 1
         return self.p + (t - 1) % (self.S - self.p)
 
-    def prompt_replica(self):
+    def prompt_replica(self, xfer=0):
         lb, Ls = self.lb, self.Ls
         dv.dv_stream_out_direct(self.ctx, self.own, (lb, lb + Ls, 0, self.b, 0, self.p), self.setup, 0, 0,
-                                self.setup, self.dst_arr, self.sig_arr, seq=self._next_seq(), stream=self.sp)
+                                self.setup, self.dst_arr, self.sig_arr, seq=self._next_seq(), xfer=xfer,
+                                stream=self.sp)
 
     def token_step(self):
         self.t += 1
@@ -402,6 +403,13 @@ def c5_suite(ctx, env, steps=200, peak=None, peak_src=None, nccl=True):
     g = c.prompt_bytes / ms / 1e6
     out["prompt_replica"] = {"ms": ms, "gbs_per_gpu": g, "gbs_aggregate": g * c.P,
                              "roofline": _roof(g, peak, peak_src, env)}
+    try:   # the same bulk replica by the copy engine (2-D DMAs of p*D*e-byte runs)
+        ms2 = _timed(env, lambda: c.prompt_replica(dv.DV_XFER_STAGED))
+        g2 = c.prompt_bytes / ms2 / 1e6
+        out["prompt_replica_copy_engine"] = {"ms": ms2, "gbs_per_gpu": g2, "roofline": _roof(g2, peak, peak_src, env)}
+    except Exception as e:   # noqa: BLE001
+        out["prompt_replica_copy_engine"] = {"error": f"{type(e).__name__}: {e}"}
+        env.barrier()
     steps = min(steps, c.S - c.p)
     for _ in range(3):
         c.token_step()
@@ -498,7 +506,7 @@ class C3:
     def my_prompt_bytes(self):
         return (self.pb[self.i + 1] - self.pb[self.i]) * self.layer_bytes if self.is_prompt else 0
 
-    def handoff(self, ft6d=False):
+    def handoff(self, ft6d=False, xfer=0):
         self.seq += 1
         if not self.is_prompt:
             return
@@ -506,7 +514,7 @@ class C3:
         dst = self.caches_ft6d if ft6d else self.caches
         for layer in range(self.pb[i], self.pb[i + 1]):       # layer by layer (Opt 2)
             dv.dv_stream_out_direct(self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), self.ps, i,
-                                    0, self.ts, dst, self.sigs, seq=self.seq, stream=self.sp)
+                                    0, self.ts, dst, self.sigs, seq=self.seq, xfer=xfer, stream=self.sp)
 
     def ft6d_forms(self, steps=2):
         """NEXT-1 over the link: the hand-off into FasterTransformer token caches (6-D key: every
@@ -611,6 +619,21 @@ def c3_suite(ctx, env, steps=3, peak=None, peak_src=None, nccl=True):
                       "steps": steps, "roofline": _roof(per_gpu, peak, peak_src, env),
                       "ideal_ms_at_peak": (env.max(c.my_prompt_bytes()) / peak / 1e6) if peak else None}
     out["parity"] = c.verify()
+    try:
+        # the same hand-off by the copy engine (DV_XFER_STAGED: one 2-D DMA per (K or V, layer,
+        # request) over the heads, runs of p*D*e bytes) -- SM stores vs copy engine over the link
+        if c.is_token:
+            c.tk.fill_(-1)
+            c.tv.fill_(-1)
+        c.handoff(xfer=dv.DV_XFER_STAGED)
+        env.barrier()
+        ms2 = _timed(env, lambda: c.handoff(xfer=dv.DV_XFER_STAGED), steps)
+        pg2 = env.max(c.my_prompt_bytes()) * steps / ms2 / 1e6
+        out["handoff_copy_engine"] = {"ms": ms2 / steps, "gbs_per_prompt_gpu": pg2,
+                                      "roofline": _roof(pg2, peak, peak_src, env), "parity": c.verify()}
+    except Exception as e:   # noqa: BLE001
+        out["handoff_copy_engine"] = {"error": f"{type(e).__name__}: {e}"}
+        env.barrier()
     try:
         out["ft6d_token_caches"] = c.ft6d_forms()
     except Exception as e:   # noqa: BLE001
