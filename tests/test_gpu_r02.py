@@ -615,3 +615,53 @@ def test_engine_never_runs_past_max_step():
         assert np.all(got[4 * lay // 2:] == kvgen.SENTINEL) and int(fl[0]) == 4
     finally:
         eng.close()
+
+
+def test_ring_host_consumer_releases_credits():
+    """A HOST consumer drains a pinned-host ring (the paper's token machines check their local CPU
+    memory for KV caches): the GPU producer streams 2,000 token chunks into a 3-slot
+    ring whose credit words live in pinned host memory; a host thread reads each chunk the moment
+    its flag appears, checks it against the oracle's pack, and releases the credit with a plain
+    host store -- the producer's stream-ordered credit waits (cuStreamWaitValue64 on host memory)
+    hold it back. No chunk is ever overwritten before it was read."""
+    import threading
+    L, B, H, S, D, p, n, R = 2, 2, 8, 64, 64, 0, 2000, 3
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=801)
+    k, v = to_dev(K), to_dev(V)
+    c = dv.cache(k, v)
+    osrc = ok.Cache(K, V, 0, 0, H, S, D)
+    step = ok.region_bytes(0, L, 0, B, 0, 1, H, D, 2)
+    exp = [ok.pack(osrc, (0, L, 0, B, q, q + 1)) for q in range(S)]
+    ring = pinned_u16(R * step // 2)
+    fl, cr = flags(1, pinned=True), flags(1, pinned=True)
+    ep = dv.endpoint_of(ring, fl, n_slots=R, slot_bytes=step, credits=cr)
+    cx = ctx()
+    bad, seen = [], [0]
+
+    def consumer():
+        view = ring.numpy().view(np.uint16)
+        for s_ in range(1, n + 1):
+            t0 = time.time()
+            while int(fl[0]) < s_:
+                if time.time() - t0 > 20:
+                    bad.append(("timeout", s_))
+                    return
+            o = (s_ % R) * step // 2
+            if not np.array_equal(view[o:o + step // 2], exp[(s_ - 1) % S]):
+                bad.append(s_)
+            cr[0] = s_        # the credit: the slot may be reused
+            seen[0] = s_
+    import sys
+    old_si = sys.getswitchinterval()
+    sys.setswitchinterval(0.0002)
+    th = threading.Thread(target=consumer)
+    th.start()
+    st = torch.cuda.Stream()
+    for s_ in range(1, n + 1):
+        q = (s_ - 1) % S
+        dv.dv_scatter(cx, c, (0, L, 0, B, q, q + 1), ep, 0, flag_slot=0, seq=s_, stream=st)
+    st.synchronize()
+    th.join(timeout=60)
+    sys.setswitchinterval(old_si)
+    assert not bad, bad[:5]
+    assert seen[0] == n and int(fl[0]) == n
