@@ -30,10 +30,16 @@ DV_API dv_status dvt_release_scope(dv_ctx* ctx, const void* flag, const void* pa
  * the engine is parked or idle. */
 DV_API dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n);
 
+/* Launches so far (all contexts of this process) of one kernel form: "tma_transpose" = the FT6D
+ * key transpose whose packet-major side is moved by TMA tensor copies (DESIGN.md §6 "FT6D keys");
+ * "all" = every library kernel (as dv_stats). DV_EINVAL for an unknown name. */
+DV_API dv_status dvt_launch_count(const char* form, uint64_t* n);
+
 /* Change one experiment knob of the copy kernels at run time (names as the environment variables
  * read at load: "DV_TRS" packet-transpose form -- 0 automatic, 1 shared-memory tiles, 2 / 3
  * registers with PK 1 / <= 2, 4 registers even over a link; "DV_PK", "DV_PP", "DV_RDBULK",
- * "DV_BULK", "DV_CLUSTER"). Not thread-safe against concurrent data calls; DV_EINVAL for an unknown
+ * "DV_BULK", "DV_CLUSTER"; "DV_TMA" 1 / 0 = FT6D key transposes by TMA rows on / off, "DV_TMA_TS"
+ * positions per TMA tile). Not thread-safe against concurrent data calls; DV_EINVAL for an unknown
  * name. For measurements that compare forms in one process. */
 DV_API dv_status dvt_tune(const char* name, int64_t value);
 

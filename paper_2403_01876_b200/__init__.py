@@ -27,6 +27,7 @@ DV_LAYOUT_KV5D, DV_LAYOUT_FT6D = 0, 1
 DV_EP_DEVICE, DV_EP_HOST, DV_EP_PEER = 0, 1, 2
 DV_XFER_AUTO, DV_XFER_FUSED, DV_XFER_STAGED, DV_PUBLISH_STREAMOP, DV_NO_FLAG = 0, 1, 2, 4, 256
 DV_XFER_DECOUPLED = 8
+TMA_DEFAULT = 0   # library default of the DV_TMA knob (FT6D key transposes by TMA rows; dvt_tune)
 DV_NOWAIT = 16
 DVT_FILL_HASH, DVT_FILL_UID, DVT_FILL_CONST = 0, 1, 2
 
@@ -144,6 +145,7 @@ _SIGS = {
     "dv_engine_done": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "dvt_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
+    "dvt_launch_count": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
     "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
@@ -638,6 +640,13 @@ def dv_query(ctx, ep: dv_endpoint, flag_slot, seq) -> bool:
 def dvt_tune(name: str, value: int):
     """Change one experiment knob of the copy kernels at run time (include/dv_trace.h)."""
     _call("dvt_tune", name.encode(), value)
+
+
+def dvt_launch_count(form: str) -> int:
+    """Launches so far of one kernel form ("tma_transpose", "all") -- include/dv_trace.h."""
+    n = C.c_uint64()
+    _call("dvt_launch_count", form.encode(), C.byref(n))
+    return n.value
 
 
 # ---- persistent stream engine (include/dv.h dv_engine_*) -----------------------------------------

@@ -2069,6 +2069,15 @@ dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps) {
 
 dv_status dvt_tune(const char* name, int64_t value) { return set_tune(name, value); }
 
+dv_status dvt_launch_count(const char* form, uint64_t* n) {
+  if (!form || !n) return fail(DV_EINVAL, "dvt_launch_count: NULL argument");
+  const std::string f = form;
+  if (f == "tma_transpose") *n = g_tma_launches.load();
+  else if (f == "all") *n = g_kernel_launches.load();
+  else return fail(DV_EINVAL, "dvt_launch_count: unknown form '%s'", form);
+  return DV_OK;
+}
+
 dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n) {
   if (!e) return fail(DV_EINVAL, "NULL engine");
   if (stamps && !n) return fail(DV_EINVAL, "zero stamps");

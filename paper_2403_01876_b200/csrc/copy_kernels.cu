@@ -20,6 +20,7 @@
 //   * optional fused publish: after its stores each CTA fences at system scope and bumps a
 //     ticket; the last CTA stores the 64-bit sequence flag with st.release.sys (peer / host
 //     observers then see the payload before the flag).
+#include <cuda.h>
 #include <stdlib.h>
 
 #include <mutex>
@@ -32,6 +33,7 @@ namespace dv {
 
 std::atomic<uint64_t> g_kernel_launches{0};
 std::atomic<uint64_t> g_dma_calls{0};
+std::atomic<uint64_t> g_tma_launches{0};
 
 struct DevDiv {
   uint32_t d, mul, shr;
@@ -542,6 +544,14 @@ struct TParams {
   uint32_t n_items;
   DevDiv fN, fG;
   int32_t pk;    // packets per thread item (1, 2, 4, 8, 16); 0 = shared-memory tiles
+  // TMA-row form (transpose_tma): the packet-major side through a 5-D tensor map (16-byte words
+  // of a packet row, packet, up to 3 slab dims); slab dim d contributes i_d * tm_mul[d] to map
+  // coordinate tm_dim[d] (2..4; -1 = unit dim)
+  int32_t tm_nst;          // stages in flight per CTA (0 = not this form)
+  int32_t tm_dim[4];
+  uint32_t tm_mul[4];
+  uint32_t tm_tps;         // tiles per slab
+  DevDiv fTm;              // division by tm_tps
 };
 
 // Register form of the packet transpose: no shared memory, no barrier. A thread item is PK
@@ -838,6 +848,193 @@ __global__ void __launch_bounds__(256) k_transpose_run(const TParams t, const KP
   }
 }
 
+// TMA-row form of the packet transpose (NEXT-1; DESIGN.md §6 "FT6D keys"). The packet-major
+// side (the FT6D key cache, in this GPU's HBM) is moved by the TMA engine, one 2-D box per packet
+// row of TS positions (TS*16 contiguous bytes), through a tensor map whose position extent ends at
+// the region's end (stores past it are clipped by the hardware: bytes outside the region are never
+// written); shared memory holds a tile as [u][s][16 B]. The position-major side is moved by the
+// CTA's threads as 32-byte vectors (two packets of one position; a warp's lanes walk 32 positions
+// of one packet pair: conflict-free 16-byte shared-memory accesses, whole 32-byte sectors in HBM).
+//   DIR 0 (pack / FT6D -> KV5D): thread 0 keeps tm_nst tile loads in flight (mbarrier
+//     complete_tx per stage); all threads store the staged tile.
+//   DIR 1 (unpack / KV5D -> FT6D): all threads load a tile into shared memory, a proxy fence and a
+//     barrier hand it to thread 0, which stores the U packet rows by TMA (bulk async-group); a
+//     stage is refilled only after its stores have read it (cp.async.bulk.wait_group.read).
+// Measured against the register form (PK = 16) on the C2 prompt layer: DESIGN.md §6.
+__device__ __forceinline__ void tma_row_load(const CUtensorMap* m, uint8_t* sdst, unsigned long long* bar,
+                                             const int32_t c[5]) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(sdst)),
+      "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+      "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_row_store(const CUtensorMap* m, const uint8_t* ssrc, const int32_t c[5]) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(m),
+               "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read(int n) {   // at most n bulk groups still reading shared memory
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+  }
+}
+constexpr int kTmaStagesMax = 4;
+
+// tile t -> map coordinates of its first packet row (c[1] = packet 0) and the position-major
+// side's byte offset of its first position
+__device__ __forceinline__ void tma_tile(const TParams& p, uint32_t t, int TS, int32_t c[5], int64_t& pos_off,
+                                         uint32_t& ns, int DIR) {
+  uint32_t slab, ti;
+  p.fTm.divmod(t, slab, ti);
+  const uint32_t s0 = ti * TS;
+  ns = min((uint32_t)TS, p.N - s0);
+  c[0] = (int32_t)(s0 * 4);
+  c[1] = 0;
+  c[2] = c[3] = c[4] = 0;
+  int64_t off = 0;
+  uint32_t q = slab;
+#pragma unroll
+  for (int d = 3; d >= 0; --d) {
+    uint32_t i;
+    if (d > 0)
+      p.fd[d].divmod(q, q, i);
+    else
+      i = q;
+    off += (int64_t)i * (DIR == 0 ? p.ds[d] : p.ss[d]);
+    const int32_t v = (int32_t)(i * p.tm_mul[d]);   // (register-resident: no dynamic index into c)
+    c[2] += p.tm_dim[d] == 2 ? v : 0;
+    c[3] += p.tm_dim[d] == 3 ? v : 0;
+    c[4] += p.tm_dim[d] == 4 ? v : 0;
+  }
+  pos_off = off + (int64_t)s0 * p.sps;
+}
+
+template <int DIR, int TS>
+__device__ __forceinline__ void transpose_tma(const TParams& p, const CUtensorMap* map, uint8_t* sm,
+                                              unsigned long long* bar, uint32_t bid, uint32_t nb) {
+  const int nst = p.tm_nst;
+  const uint32_t U = p.U;
+  const uint32_t stage = U * TS * 16;
+  const uint32_t mine = bid < p.n_tiles ? (p.n_tiles - bid + nb - 1) / nb : 0;
+  const uint32_t items = TS * (U / 2);   // (position, packet pair) items of a tile
+  if (DIR == 0) {
+    auto issue = [&](uint32_t j) {
+      int32_t c[5];
+      int64_t po;
+      uint32_t ns;
+      tma_tile(p, bid + j * nb, TS, c, po, ns, 0);
+      uint8_t* buf = sm + (j % nst) * stage;
+      unsigned long long* b = &bar[j % nst];
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(b)),
+                   "r"(stage)
+                   : "memory");
+      for (uint32_t u = 0; u < U; ++u) {
+        c[1] = (int32_t)u;
+        tma_row_load(map, buf + u * TS * 16, b, c);
+      }
+    };
+    if (threadIdx.x == 0)
+      for (uint32_t j = 0; j < (uint32_t)nst && j < mine; ++j) issue(j);
+    for (uint32_t j = 0; j < mine; ++j) {
+      int32_t c[5];
+      int64_t po;
+      uint32_t ns;
+      tma_tile(p, bid + j * nb, TS, c, po, ns, 0);
+      mbar_wait(&bar[j % nst], (j / nst) & 1);
+      const uint8_t* buf = sm + (j % nst) * stage;
+      uint8_t* out = p.dst + po;
+      for (uint32_t i = threadIdx.x; i < items; i += 256) {
+        const uint32_t s = i % TS, pr = i / TS;
+        if (s < ns) {
+          Vec<32> x;
+          *reinterpret_cast<uint4*>(&x.w[0]) = *reinterpret_cast<const uint4*>(buf + (2 * pr) * TS * 16 + s * 16);
+          *reinterpret_cast<uint4*>(&x.w[4]) = *reinterpret_cast<const uint4*>(buf + (2 * pr + 1) * TS * 16 + s * 16);
+          st_vec(out + (int64_t)s * p.sps + pr * 32, x);
+        }
+      }
+      __syncthreads();   // every thread is done reading this stage
+      if (threadIdx.x == 0 && j + nst < mine) issue(j + nst);
+    }
+  } else {
+    for (uint32_t j = 0; j < mine; ++j) {
+      int32_t c[5];
+      int64_t po;
+      uint32_t ns;
+      tma_tile(p, bid + j * nb, TS, c, po, ns, 1);
+      uint8_t* buf = sm + (j % nst) * stage;
+      if (j >= (uint32_t)nst) {   // the stores issued from this stage nst tiles ago have read it
+        if (threadIdx.x == 0) bulk_wait_read(nst - 1);
+        __syncthreads();
+      }
+      const uint8_t* in = p.src + po;
+      for (uint32_t i0 = threadIdx.x; i0 < items; i0 += 512) {   // two items in flight per thread
+        Vec<32> x[2];
+        bool ok[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t i = i0 + k * 256, s = i % TS, pr = i / TS;
+          ok[k] = i < items && s < ns;
+          if (ok[k]) ld_vec(x[k], in + (int64_t)s * p.sps + pr * 32);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t i = i0 + k * 256, s = i % TS, pr = i / TS;
+          if (ok[k]) {
+            *reinterpret_cast<uint4*>(buf + (2 * pr) * TS * 16 + s * 16) = *reinterpret_cast<const uint4*>(&x[k].w[0]);
+            *reinterpret_cast<uint4*>(buf + (2 * pr + 1) * TS * 16 + s * 16) =
+                *reinterpret_cast<const uint4*>(&x[k].w[4]);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (uint32_t u = 0; u < U; ++u) {
+          c[1] = (int32_t)u;
+          tma_row_store(map, buf + u * TS * 16, c);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // stores complete (before any release)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+  }
+}
+
+// The TMA-row transpose and the value's run copy in ONE launch (CTAs [0, t_blocks) transpose; with
+// t_blocks == gridDim.x it is the transpose alone). The tensor map is a __grid_constant__ parameter.
+template <int DIR, int VEC, int TS>
+__global__ void __launch_bounds__(256) k_transpose_tma_run(const TParams t, const KParams r, uint32_t t_blocks,
+                                                           const __grid_constant__ CUtensorMap map) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  __shared__ __align__(8) unsigned long long bar[kTmaStagesMax];
+  if (blockIdx.x < t_blocks && threadIdx.x == 0) {
+    for (int i = 0; i < t.tm_nst; ++i) mbar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  if (blockIdx.x < t_blocks)
+    transpose_tma<DIR, TS>(t, &map, tsm, bar, blockIdx.x, t_blocks);
+  else
+    run_chunks<VEC, 4, 256>(r, r.src, r.dst, blockIdx.x - t_blocks, gridDim.x - t_blocks);
+  if (t.flag) {
+    KParams kp{};
+    kp.flag = t.flag;
+    kp.ticket = t.ticket;
+    kp.ts = t.ts;
+    publish(kp, t.pub, t.seq);
+  }
+}
+
 // Credit wait on peer memory (api.cu credit_wait): thread 0 polls with system-scope acquire loads
 // and backs off; the copy kernel behind it passes its griddepcontrol.wait only once this grid
 // has completed.
@@ -936,6 +1133,9 @@ struct Tune {
   int rdbulk = 0;     // DV_RDBULK: dense-source copies reading over a link use k_unpack_bulk (2: any source)
   uint32_t rdch = 8192;  // DV_RDCH: bytes per bulk read
   uint32_t rdst = 4;     // DV_RDST: bulk reads in flight per CTA (<= kRdStagesMax)
+  int tma = 0;           // DV_TMA: FT6D key transposes with the packet-major side moved by TMA rows
+  int tma_ts = 0;        // DV_TMA_TS: positions per TMA tile (32 / 64; 0 = per direction)
+  double tma_split = 1.0;  // DV_TMA_TSPLIT: transpose CTAs' share weight (x their byte share)
 };
 static Tune& tune_mut() {
   static Tune t = [] {
@@ -957,6 +1157,9 @@ static Tune& tune_mut() {
     if (const char* e = getenv("DV_RDBULK")) x.rdbulk = atoi(e);
     if (const char* e = getenv("DV_RDCH")) x.rdch = (uint32_t)std::max(16, atoi(e) / 16 * 16);
     if (const char* e = getenv("DV_RDST")) x.rdst = (uint32_t)std::min(kRdStagesMax, std::max(1, atoi(e)));
+    if (const char* e = getenv("DV_TMA")) x.tma = atoi(e);
+    if (const char* e = getenv("DV_TMA_TS")) x.tma_ts = atoi(e);
+    if (const char* e = getenv("DV_TMA_TSPLIT")) x.tma_split = atof(e);
     return x;
   }();
   return t;
@@ -973,6 +1176,8 @@ dv_status set_tune(const char* name, int64_t value) {
   else if (n == "DV_RDBULK") t.rdbulk = (int)value;
   else if (n == "DV_BULK") t.bulk = (int)value;
   else if (n == "DV_CLUSTER") t.cluster = (int)value;
+  else if (n == "DV_TMA") t.tma = (int)value;
+  else if (n == "DV_TMA_TS") t.tma_ts = (int)value;
   else return fail(DV_EINVAL, "unknown tunable '%s'", n.c_str());
   return DV_OK;
 }
@@ -1307,10 +1512,190 @@ static TrFn tr_fn(int pk) {
   }
 }
 
+static void fill_kparams(const CopyPlan& p, int VEC, KParams* kp);
+static uint64_t align_bits(const CopyPlan& p);
+
+// ---- TMA-row transpose: the tensor map of the packet-major side ------------------------------
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encode() {
+  static const TmapEncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      f = nullptr;
+    }
+    return (TmapEncodeFn)f;
+  }();
+  return fn;
+}
+static bool own_hbm(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return at.type == cudaMemoryTypeDevice && at.device == dev;
+}
+static int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 148;
+  }
+  return n;
+}
+constexpr int kTmaSmem = 64 * 1024;   // dynamic shared memory budget of a TMA-row transpose CTA
+
+// The TMA-row form applies when DV_TMA is on, the packet-major side is this GPU's HBM (not a step-
+// shifted graph plan), the position-major side is in HBM too and 32-byte aligned, U is even, and
+// the slab dims fit the map's three remaining dims (unit dims dropped, nested ones merged).
+// Fills tp's tm_* fields, *map and *ts_out; false = use the other forms.
+static bool tma_rows_setup(const CopyPlan& p, TParams& tp, CUtensorMap* map, int* ts_out) {
+  if (!tune().tma || p.dyn || p.tU % 2 || p.tU > 128 || !tmap_encode()) return false;
+  const uint8_t* pm = p.tdir == 0 ? p.src : p.dst;   // packet-major side
+  const uint8_t* ps = p.tdir == 0 ? p.dst : p.src;   // position-major side
+  if ((uintptr_t)pm % 16 || p.t_su % 16 || p.t_su <= 0) return false;
+  uint64_t al = (uint64_t)p.t_ss | (uint64_t)(uintptr_t)ps;
+  for (int d = 0; d < 4; ++d) al |= (uint64_t)(p.tdir == 0 ? tp.ds[d] : tp.ss[d]);
+  if (al % 32) return false;
+  if (!own_hbm(pm) || !own_hbm(ps)) return false;
+  int TS = tune().tma_ts ? tune().tma_ts : (p.tdir == 0 ? 32 : 64);
+  while (TS > 8 && (uint64_t)p.tU * TS * 16 * 2 > (uint64_t)kTmaSmem) TS /= 2;
+  if (TS != 8 && TS != 16 && TS != 32 && TS != 64) return false;
+  const uint32_t stage = p.tU * TS * 16;
+  const int nst = std::min(kTmaStagesMax, (int)(kTmaSmem / stage));
+  if (nst < 2) return false;
+  // slab dims (inner -> outer) -> map dims 2..4
+  uint64_t gn[3] = {1, 1, 1};
+  int64_t gs[3] = {16, 16, 16};
+  int ng = 0;
+  uint64_t slabs = 1;
+  for (int d = 3; d >= 0; --d) {
+    const int k = kDims - 4 + d;
+    const uint64_t n = p.n[k];
+    const int64_t st = p.tdir == 0 ? p.ss[k] : p.ds[k];
+    slabs *= n;
+    if (n == 1) {
+      tp.tm_dim[d] = -1;
+      tp.tm_mul[d] = 0;
+      continue;
+    }
+    if (st <= 0 || st % 16 || st >= (1ll << 40)) return false;
+    if (ng > 0 && st == gs[ng - 1] * (int64_t)gn[ng - 1] && gn[ng - 1] * n < (1ull << 31)) {
+      tp.tm_dim[d] = 2 + ng - 1;   // nests outside the current map dim
+      tp.tm_mul[d] = (uint32_t)gn[ng - 1];
+      gn[ng - 1] *= n;
+      continue;
+    }
+    if (ng == 3) return false;
+    tp.tm_dim[d] = 2 + ng;
+    tp.tm_mul[d] = 1;
+    gn[ng] = n;
+    gs[ng] = st;
+    ++ng;
+  }
+  const uint64_t tps = (p.tN + TS - 1) / TS;
+  if (slabs * tps >= (1ull << 31)) return false;
+  const cuuint64_t dims[5] = {(cuuint64_t)p.tN * 4, p.tU, gn[0], gn[1], gn[2]};
+  const cuuint64_t strides[4] = {(cuuint64_t)p.t_su, (cuuint64_t)gs[0], (cuuint64_t)gs[1], (cuuint64_t)gs[2]};
+  const cuuint32_t box[5] = {(cuuint32_t)TS * 4, 1, 1, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  if (tmap_encode()(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, (void*)pm, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  tp.tm_nst = nst;
+  tp.tm_tps = (uint32_t)tps;
+  tp.fTm = to_dev(make_fastdiv((uint32_t)tps));
+  tp.n_tiles = (uint32_t)(slabs * tps);
+  *ts_out = TS;
+  return true;
+}
+
+using TmFn = void (*)(TParams, KParams, uint32_t, CUtensorMap);
+template <int DIR, int VEC>
+static TmFn tm_fn(int ts) {
+  switch (ts) {
+    case 8: return k_transpose_tma_run<DIR, VEC, 8>;
+    case 16: return k_transpose_tma_run<DIR, VEC, 16>;
+    case 32: return k_transpose_tma_run<DIR, VEC, 32>;
+    default: return k_transpose_tma_run<DIR, VEC, 64>;
+  }
+}
+static void set_tma_smem() {
+  static std::atomic<uint64_t> mask{0};
+  if (first_use_on_device(mask))
+    for (int ts : {8, 16, 32, 64}) {
+      cudaFuncSetAttribute(tm_fn<0, 16>(ts), cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(tm_fn<1, 16>(ts), cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(tm_fn<0, 32>(ts), cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(tm_fn<1, 32>(ts), cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    }
+}
+
+// One launch: the TMA-row transpose of `t` (+ the run copy `r` when given). Every CTA is resident
+// at once (grid = SMs x CTAs per SM that the shared memory allows, <= max_ctas); the transpose
+// CTAs get DV_TMA_TSPLIT x their byte share.
+static dv_status launch_tma_run(const CopyPlan& t, const TParams& tp, const CUtensorMap& map, int TS,
+                                const CopyPlan* r, int max_ctas, cudaStream_t stream) {
+  const int smem = tp.tm_nst * (int)tp.U * TS * 16;
+  const int per_sm = std::max(1, std::min(8, (int)((227u * 1024) / (uint32_t)(smem + 1024))));
+  KParams kr{};
+  int VEC = 32;
+  uint64_t grid, t_blocks;
+  if (r) {
+    const uint64_t orall = align_bits(*r);
+    if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
+    VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
+    fill_kparams(*r, VEC, &kr);
+    grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, (uint64_t)sm_count() * per_sm));
+    const double tb = (double)t.runs() * t.tN * t.tU * 16, rb = (double)r->runs() * r->run_bytes, w = tune().tma_split;
+    t_blocks = (uint64_t)(grid * w * tb / (w * tb + rb) + 0.5);
+    t_blocks = std::min(std::max<uint64_t>(1, t_blocks), grid - 1);
+  } else {
+    grid = std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)max_ctas, (uint64_t)sm_count() * per_sm,
+                                                     (uint64_t)tp.n_tiles}));
+    t_blocks = grid;
+  }
+  set_tma_smem();
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const TmFn fn = t.tdir == 0 ? (VEC == 32 ? tm_fn<0, 32>(TS) : tm_fn<0, 16>(TS))
+                              : (VEC == 32 ? tm_fn<1, 32>(TS) : tm_fn<1, 16>(TS));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, tp, kr, (uint32_t)t_blocks, map);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  g_tma_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "TMA transpose kernel launch");
+  return DV_OK;
+}
+
 static dv_status launch_transpose(const CopyPlan& p, const Release& rel, int max_ctas,
                                   cudaStream_t stream) {
   TParams tp;
   DV_TRY(fill_tparams(p, rel, &tp));
+  {
+    CUtensorMap map;
+    int TS = 0;
+    if (tma_rows_setup(p, tp, &map, &TS)) return launch_tma_run(p, tp, map, TS, nullptr, max_ctas, stream);
+  }
   const int smem = transpose_smem(tp);
   set_transpose_smem();
   (void)cudaGetLastError();
@@ -1379,6 +1764,11 @@ static dv_status launch_transpose_run(const CopyPlan& t, const CopyPlan& r, cons
                                       int max_ctas, cudaStream_t stream) {
   TParams tp;
   DV_TRY(fill_tparams(t, rel, &tp));
+  {
+    CUtensorMap map;
+    int TS = 0;
+    if (tma_rows_setup(t, tp, &map, &TS)) return launch_tma_run(t, tp, map, TS, &r, max_ctas, stream);
+  }
   const uint64_t orall = align_bits(r);
   if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
   const int VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
@@ -1705,6 +2095,12 @@ void preload_kernels() {
   for (int pk : {0, 1, 2, 4, 8, 16, 36, 40}) {
     load_fn(pt_fn<0>(pk));
     load_fn(pt_fn<1>(pk));
+  }
+  for (int ts : {8, 16, 32, 64}) {
+    load_fn(tm_fn<0, 16>(ts));
+    load_fn(tm_fn<1, 16>(ts));
+    load_fn(tm_fn<0, 32>(ts));
+    load_fn(tm_fn<1, 32>(ts));
   }
   (void)cudaGetLastError();
 }

@@ -133,6 +133,7 @@ dv_status driver(const Driver** out);
 // ---- counters (dv_stats) ---------------------------------------------------------------------
 extern std::atomic<uint64_t> g_kernel_launches;
 extern std::atomic<uint64_t> g_dma_calls;
+extern std::atomic<uint64_t> g_tma_launches;   // TMA-row FT6D transposes (dvt_launch_count)
 // A copy-engine call, counted for dv_stats.
 #define DV_DMA(expr)                                         \
   do {                                                       \
