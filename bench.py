@@ -305,7 +305,12 @@ def run_ours(args):
                           "stream), fed by k_run_copy pack (cache -> HBM staging), flag by a stream "
                           "write on the library flag stream",
                 "pack_kernel_us": extras.get("token_step_pack_hbm_us"),
-                "pack_kernel_hbm_frac": extras.get("token_step_pack_hbm_frac")}
+                "pack_kernel_hbm_frac": extras.get("token_step_pack_hbm_frac"),
+                "pack_kernel_vs_contiguous_same_size": extras.get("token_step_pack_vs_contiguous_same_size"),
+                "pack_kernel_note": "a 6.55 MB launch is bound by fixed costs (dependent-launch floor "
+                                    "extras.dependent_launch_floor_us), not by the gather pattern: the "
+                                    "same kernel on a near-contiguous 6.55 MB takes "
+                                    "extras.token_step_pack_contiguous_same_size_us"}
     roof.update({
         "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
         "algorithmic_bytes_per_launch": STEP_BYTES,
@@ -528,6 +533,23 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     ex["token_step_same_size_d2d_copy_us"] = ms * 1e3
     ex["token_step_pack_vs_same_size_copy"] = ex["token_step_same_size_d2d_copy_us"] / ex["token_step_pack_hbm_us"]
     del src_d, dst_d
+    # the same pack kernel on a near-contiguous 6.55 MB (positions [0,320) of one layer and
+    # request: 80 runs of 80 KiB, cycled over layers / requests) and the smallest dependent launch
+    # (one position of one head: 512 B) -- DESIGN.md §6 "Token-step pack, where its 4 us go"
+    def contig():
+        cnt[0] += 1
+        lay, rq = cnt[0] % L, (cnt[0] // L) % B
+        dv.dv_scatter(ctx, cache, dv.region(lay, lay + 1, rq, rq + 1, 0, 320), dep, (cnt[0] % 8) * STEP_BYTES,
+                      stream=sp)
+
+    def tiny():
+        cnt[0] += 1
+        q = pos_of(cnt[0])
+        dv.dv_scatter(ctx, cache, dv.region(0, 1, 0, 1, q, q + 1, 0, 1), dep, (cnt[0] % 8) * 1024, stream=sp)
+    ex["token_step_pack_contiguous_same_size_us"] = _time(contig, stream, reps, head_start_ns=4_000_000) * 1e3
+    ex["token_step_pack_vs_contiguous_same_size"] = (ex["token_step_pack_contiguous_same_size_us"]
+                                                     / ex["token_step_pack_hbm_us"])
+    ex["dependent_launch_floor_us"] = _time(tiny, stream, reps, head_start_ns=4_000_000) * 1e3
     ex["xfer_main"] = "fused" if args.xfer in ("auto", "fused") else args.xfer
 
     # per-layer token latency: from "layer l's new K/V written" to "bytes resident at
