@@ -379,7 +379,7 @@ def _ncu_traffic(name="decoupled"):
     source names the file and the sha256 of its content (so the line pins the exact capture)."""
     import csv
     import hashlib
-    files = {"decoupled": ["r02_io_counters.csv", "r01g_io_counters.csv"],
+    files = {"decoupled": ["r02b_io_counters.csv", "r02_io_counters.csv", "r01g_io_counters.csv"],
              "fused": ["r02_io_counters_fused.csv", "r01_io_counters_final.csv"]}[name]
     for fn in files:
         path = os.path.join(ROOT, "profiles", fn)

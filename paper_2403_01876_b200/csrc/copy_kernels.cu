@@ -1647,7 +1647,6 @@ static void set_tma_smem() {
 static dv_status launch_tma_run(const CopyPlan& t, const TParams& tp, const CUtensorMap& map, int TS,
                                 const CopyPlan* r, int max_ctas, cudaStream_t stream) {
   const int smem = tp.tm_nst * (int)tp.U * TS * 16;
-  const int per_sm = std::max(1, std::min(8, (int)((227u * 1024) / (uint32_t)(smem + 1024))));
   KParams kr{};
   int VEC = 32;
   uint64_t grid, t_blocks;
@@ -1656,6 +1655,16 @@ static dv_status launch_tma_run(const CopyPlan& t, const TParams& tp, const CUte
     if (orall % 16) return fail(DV_EALIGN, "copy plan not 16-byte aligned");
     VEC = (orall % 32 == 0 && tune().vec != 16) ? 32 : 16;
     fill_kparams(*r, VEC, &kr);
+  }
+  const TmFn fn = t.tdir == 0 ? (VEC == 32 ? tm_fn<0, 32>(TS) : tm_fn<0, 16>(TS))
+                              : (VEC == 32 ? tm_fn<1, 32>(TS) : tm_fn<1, 16>(TS));
+  set_tma_smem();
+  int per_sm = 1;   // resident CTAs per SM (registers, threads and shared memory together)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) {
+    (void)cudaGetLastError();
+    per_sm = 1;
+  }
+  if (r) {
     grid = std::max<uint64_t>(2, std::min<uint64_t>((uint64_t)max_ctas, (uint64_t)sm_count() * per_sm));
     const double tb = (double)t.runs() * t.tN * t.tU * 16, rb = (double)r->runs() * r->run_bytes, w = tune().tma_split;
     t_blocks = (uint64_t)(grid * w * tb / (w * tb + rb) + 0.5);
@@ -1665,7 +1674,6 @@ static dv_status launch_tma_run(const CopyPlan& t, const TParams& tp, const CUte
                                                      (uint64_t)tp.n_tiles}));
     t_blocks = grid;
   }
-  set_tma_smem();
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1677,8 +1685,6 @@ static dv_status launch_tma_run(const CopyPlan& t, const TParams& tp, const CUte
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  const TmFn fn = t.tdir == 0 ? (VEC == 32 ? tm_fn<0, 32>(TS) : tm_fn<0, 16>(TS))
-                              : (VEC == 32 ? tm_fn<1, 32>(TS) : tm_fn<1, 16>(TS));
   cudaError_t e = cudaLaunchKernelEx(&cfg, fn, tp, kr, (uint32_t)t_blocks, map);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   g_tma_launches.fetch_add(1, std::memory_order_relaxed);
