@@ -280,30 +280,44 @@ class C5:
         words = 2 * self.Ls * self.b * H * n_pos * D
         return {"mismatches": bad, "words_per_rank": words, "how": "dvt_verify of every replica word vs the generator"}
 
-    def latency(self, n=300):
+    def latency(self, n=300, loaded=False):
         """Per-layer put latency with the system-scope release: writer (dvt_fill of one layer's new
         position) ends -> the put's seq flag released into the successor's memory (%globaltimer on
-        the sender, dvt_trace stamps)."""
+        the sender, dvt_trace stamps). loaded: while a bf16 GEMM loop (8192^3) keeps every SM of
+        this GPU busy on a low-priority stream, the writer and the put run on a high-priority one
+        (NEXT-2: the streaming beside the model's compute)."""
         env = self.env
         te = torch.zeros(n, dtype=torch.int64, device=env.dev)
         ts = torch.zeros((n, 4), dtype=torch.int64, device=env.dev)
         ts[:, 1:3] = 2 ** 63 - 1
         q = self.S - 1
+        sp = self.sp
+        if loaded:
+            lo, hi = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+            ga = torch.randn(8192, 8192, device=env.dev, dtype=torch.bfloat16)
+            gb = torch.randn(8192, 8192, device=env.dev, dtype=torch.bfloat16)
+            torch.matmul(ga, gb)
+            torch.cuda.synchronize()
+            sp = hi.cuda_stream
         env.barrier()
-        dv.dvt_spin(20_000_000, 1, stream=self.sp)
+        if loaded:
+            with torch.cuda.stream(lo):
+                for _ in range(60):          # ~40 ms of GEMMs: longer than the spin + n puts
+                    torch.matmul(ga, gb)
+        dv.dvt_spin(20_000_000, 1, stream=sp)
         for i in range(n):
             layer = self.lb + i % self.Ls
             reg = dv.region(layer, layer + 1, 0, self.b, q, q + 1)
-            dv.dvt_fill(self.own, dv.DVT_FILL_HASH, seed=SEED_C5, reg=reg, stream=self.sp, t_end_ptr=te[i].data_ptr())
+            dv.dvt_fill(self.own, dv.DVT_FILL_HASH, seed=SEED_C5, reg=reg, stream=sp, t_end_ptr=te[i].data_ptr())
             dv.dvt_trace(self.ctx, ts[i].data_ptr())
             dv.dv_stream_out_direct(self.ctx, self.own, reg, self.setup, 0, 0, self.setup, self.dst_arr,
-                                    self.sig_arr, seq=self._next_seq(), stream=self.sp)
+                                    self.sig_arr, seq=self._next_seq(), stream=sp)
         dv.dvt_trace(self.ctx, 0)
         torch.cuda.synchronize()
         us = ((ts[:, 0] - te).double() / 1e3).tolist()[20:]
         p50, p99 = env.max(_pct(us, 0.5)), env.max(_pct(us, 0.99))
         scope = dv.dvt_release_scope(self.ctx, self.fp, self.kp)
-        return {"p50_us": p50, "p99_us": p99, "n": len(us), "bytes": self.layer_bytes_tok,
+        return {"p50_us": p50, "p99_us": p99, "n": len(us), "bytes": self.layer_bytes_tok, "loaded": loaded,
                 "release_scope": "gpu" if scope else "system",
                 "how": "writer end -> st.release of the seq flag in the successor's memory, sender "
                        "%globaltimer; p50/p99 max over ranks"}
@@ -423,7 +437,9 @@ def c5_suite(ctx, env, steps=200, peak=None, peak_src=None, nccl=True):
                          "how": "one dv_stream_out_direct per step (all the stage's layers, one position) "
                                 "into the successor's replica store + seq flag; spin head start hides the enqueue"}
     out["parity"] = c.verify(c.p + steps)
-    for name, fn in (("latency_per_layer_put", c.latency), ("pingpong", c.pingpong)):
+    for name, fn in (("latency_per_layer_put", c.latency),
+                     ("latency_per_layer_put_under_gemm", lambda: c.latency(loaded=True)),
+                     ("pingpong", c.pingpong)):
         try:
             out[name] = fn()
         except Exception as e:   # noqa: BLE001 -- reported; the other C5 numbers still print
