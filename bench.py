@@ -462,6 +462,66 @@ def _time(fn, stream, reps, warm=2, tail=None, head_start_ns=0):
     return a.elapsed_time(b) / reps
 
 
+def _latency_under_gemm(dv, ctx, cache, lep, pos_of, n=400, n_gemm=60):
+    """Per-layer token latency to pinned host (writer end -> flag, C2 layer of 160 KiB) while a bf16
+    GEMM loop (8192^3) saturates the GPU -- NEXT-2's concurrent compute -- in two arrangements:
+    'priority': GEMM on a low-priority stream, writer + stream-out on a high-priority one (all SMs
+    shared); 'partition_<k>': dv_partition_create -- GEMM on the compute partition's stream,
+    writer + stream-out on the k-SM streaming partition's stream (DESIGN.md §6 "SM partitions").
+    Also the GEMM's TFLOP/s during each run (the partition's price)."""
+    import torch
+    lo_pr, hi_pr = torch.cuda.Stream.priority_range()
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    bm = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    out = {}
+    seq = [4 * 10 ** 8]
+    part = dv.dv_partition_create(torch.cuda.current_device(), 16, hi_pr)
+    try:
+        arr = {"priority": (torch.cuda.Stream(priority=hi_pr), torch.cuda.Stream(priority=lo_pr)),
+               f"partition_{part.sms_streaming}": (torch.cuda.ExternalStream(part.streaming),
+                                                    torch.cuda.ExternalStream(part.compute))}
+        for name, (cs, gs) in arr.items():
+            sp = cs.cuda_stream
+            with torch.cuda.stream(gs):
+                torch.matmul(a, bm)
+            for i in range(2 * L):   # warm the kernels on these streams
+                reg = dv.region(i % L, i % L + 1, 0, B, P, P + 1)
+                dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp)
+                seq[0] += 1
+                dv.dv_scatter(ctx, cache, reg, lep, (i % L) * LAYER_BYTES, flag_slot=0, seq=seq[0],
+                              xfer=dv.DV_XFER_FUSED, stream=sp)
+            te = torch.zeros(n, dtype=torch.int64, device="cuda")
+            ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
+            ts[:, 1:3] = 2 ** 63 - 1
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(gs)
+            with torch.cuda.stream(gs):
+                for _ in range(n_gemm):
+                    torch.matmul(a, bm)
+            g1.record(gs)
+            dv.dvt_spin(20_000_000, 1, stream=sp)
+            for i in range(n):
+                layer = i % L
+                q = pos_of(2 + i // L)
+                reg = dv.region(layer, layer + 1, 0, B, q, q + 1)
+                dv.dvt_fill(cache, dv.DVT_FILL_HASH, seed=20240305, reg=reg, stream=sp, t_end_ptr=te[i].data_ptr())
+                dv.dvt_trace(ctx, ts[i].data_ptr())
+                seq[0] += 1
+                dv.dv_scatter(ctx, cache, reg, lep, layer * LAYER_BYTES, flag_slot=0, seq=seq[0],
+                              xfer=dv.DV_XFER_FUSED, stream=sp)
+            dv.dvt_trace(ctx, 0)
+            torch.cuda.synchronize()
+            d = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
+            out[name] = {"p50_us": d[len(d) // 2], "p99_us": d[int(len(d) * 0.99)], "n": len(d),
+                         "gemm_tflops_during": n_gemm * 2 * 8192 ** 3 / (g0.elapsed_time(g1) * 1e-3) / 1e12}
+        out["sms"] = {"streaming": part.sms_streaming, "compute": part.sms_compute}
+    finally:
+        torch.cuda.synchronize()
+        part.destroy()
+    return out
+
+
 def run_extras(dv, ctx, cache, stream, args, pos_of):
     """Secondary measurements reported beside the headline (same run, same box)."""
     import torch
@@ -638,6 +698,10 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     lat["host_enqueue_us_per_call"] = (time.perf_counter() - t0) / L * 1e6
     torch.cuda.synchronize()
     ex["token_layer_latency"] = lat
+    try:
+        ex["token_layer_latency_under_gemm"] = _latency_under_gemm(dv, ctx, cache, lep, pos_of)
+    except Exception as e:   # noqa: BLE001 -- reported; the rest of the line stands
+        ex["token_layer_latency_under_gemm"] = {"error": f"{type(e).__name__}: {e}"}
 
     # CUDA graph of one token step's 40 per-layer stream-outs (captured once, replayed per token
     # with a device-side step counter): host cost per step and device time per step

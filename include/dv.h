@@ -423,6 +423,31 @@ DV_API dv_status dv_engine_doorbell(dv_engine* e, int32_t plan, uint64_t** word)
 /* Steps of `plan` the engine has completed (flag released), read now (small synchronous copy). */
 DV_API dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps);
 
+/* ---- SM partitions: an SM budget for streaming (NEXT-2; DESIGN.md §6
+ * "SM partitions") ----------------------------------------------------------------------------
+ * Splits device `device`'s SMs into two green contexts (disjoint SM sets): a STREAMING partition
+ * of at least `streaming_sms` SMs (rounded up by the driver to its granularity: 8 on sm_100) and a
+ * COMPUTE partition of the rest, and creates one non-blocking stream in each (`priority` for the
+ * streaming one, 0 for the compute one; stream priorities as cudaStreamCreateWithPriority). Work
+ * launched on *streaming_stream runs only on the streaming SMs and work on *compute_stream only on
+ * the others, so a per-layer stream-out never waits for a GEMM's CTAs to retire (measured under a
+ * saturating bf16 GEMM loop: DESIGN.md §6). Work on any OTHER stream of the device (e.g. a
+ * framework's default stream) is not confined and may still occupy the streaming SMs: run the
+ * model's compute on *compute_stream for the isolation to hold. The price is the compute
+ * partition's smaller SM count (compute-bound kernels slow down; HBM-bound ones barely).
+ * Streams are returned as cudaStream_t values (void*); the caller must not destroy them -- they
+ * live until dv_partition_destroy, which must come after all work on them has completed.
+ * *sms_streaming / *sms_compute (optional, may be NULL) receive the SM counts actually assigned.
+ * Errors: DV_EINVAL (NULL outputs, streaming_sms < 1, or no SMs left for the compute partition),
+ * DV_ENOTSUP (the driver has no green contexts), DV_ECUDA (driver failure; nothing is left
+ * allocated). */
+typedef struct dv_partition dv_partition;
+DV_API dv_status dv_partition_create(int32_t device, int32_t streaming_sms, int32_t priority,
+                                     dv_partition** out, void** streaming_stream,
+                                     void** compute_stream, int32_t* sms_streaming,
+                                     int32_t* sms_compute);
+DV_API dv_status dv_partition_destroy(dv_partition* p);
+
 #ifdef __cplusplus
 }
 #endif

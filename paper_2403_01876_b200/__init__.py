@@ -133,6 +133,9 @@ _SIGS = {
     "dv_signal": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, C.c_void_p]),
     "dv_query": (C.c_int, [C.c_void_p, P(dv_endpoint), C.c_int32, C.c_uint64, P(C.c_int32)]),
     "dv_engine_create": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
+    "dv_partition_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, P(C.c_void_p), P(C.c_void_p),
+                                      P(C.c_void_p), P(C.c_int32), P(C.c_int32)]),
+    "dv_partition_destroy": (C.c_int, [C.c_void_p]),
     "dv_engine_destroy": (C.c_int, [C.c_void_p]),
     "dv_engine_park": (C.c_int, [C.c_void_p]),
     "dv_engine_resume": (C.c_int, [C.c_void_p]),
@@ -713,6 +716,30 @@ class Engine:
 
 def dv_engine_create(ctx, n_ctas=8) -> Engine:
     return Engine(ctx, n_ctas)
+
+
+class Partition:
+    """An SM partition (dv_partition_create, include/dv.h): `streaming` and `compute` are the raw
+    cudaStream_t handles (ints) of its two green contexts; wrap them with
+    torch.cuda.ExternalStream to run work there. Destroy after all work on them has completed."""
+
+    def __init__(self, device, streaming_sms, priority=0):
+        h, s0, s1 = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        n0, n1 = C.c_int32(), C.c_int32()
+        _call("dv_partition_create", device, streaming_sms, priority, C.byref(h), C.byref(s0), C.byref(s1),
+              C.byref(n0), C.byref(n1))
+        self.h = h
+        self.streaming, self.compute = s0.value, s1.value
+        self.sms_streaming, self.sms_compute = n0.value, n1.value
+
+    def destroy(self):
+        if self.h:
+            _call("dv_partition_destroy", self.h)
+            self.h = None
+
+
+def dv_partition_create(device, streaming_sms, priority=0) -> Partition:
+    return Partition(device, streaming_sms, priority)
 
 
 # ---- test-only utilities (include/dv_testing.h) and baselines (include/dv_baselines.h) -----------

@@ -2089,3 +2089,132 @@ dv_status dvt_engine_trace(dv_engine* e, uint64_t* stamps, uint64_t n) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// SM partitions (green contexts): dv_partition_create / dv_partition_destroy
+// ---------------------------------------------------------------------------------------------
+namespace dv {
+struct GreenDriver {
+  CUresult (*deviceGet)(CUdevice*, int) = nullptr;
+  CUresult (*deviceGetDevResource)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*smResourceSplitByCount)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*,
+                                     unsigned int, unsigned int) = nullptr;
+  CUresult (*resourceGenerateDesc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
+  CUresult (*greenCtxCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+  CUresult (*greenCtxDestroy)(CUgreenCtx) = nullptr;
+  CUresult (*greenCtxStreamCreate)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
+  CUresult (*streamDestroy)(CUstream) = nullptr;
+};
+static GreenDriver g_green;
+static std::once_flag g_green_once;
+static bool g_green_ok = false;
+static std::string g_green_missing;
+
+static dv_status green_driver(const GreenDriver** out) {
+  std::call_once(g_green_once, [] {
+    struct E {
+      const char* name;
+      void** slot;
+    } es[] = {
+        {"cuDeviceGet", (void**)&g_green.deviceGet},
+        {"cuDeviceGetDevResource", (void**)&g_green.deviceGetDevResource},
+        {"cuDevSmResourceSplitByCount", (void**)&g_green.smResourceSplitByCount},
+        {"cuDevResourceGenerateDesc", (void**)&g_green.resourceGenerateDesc},
+        {"cuGreenCtxCreate", (void**)&g_green.greenCtxCreate},
+        {"cuGreenCtxDestroy", (void**)&g_green.greenCtxDestroy},
+        {"cuGreenCtxStreamCreate", (void**)&g_green.greenCtxStreamCreate},
+        {"cuStreamDestroy", (void**)&g_green.streamDestroy},
+    };
+    bool ok = true;
+    for (auto& e : es) {   // cuGreenCtxStreamCreate: CUDA 12.5
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t r = cudaGetDriverEntryPointByVersion(e.name, e.slot, 12050, cudaEnableDefault, &q);
+      if (r != cudaSuccess || q != cudaDriverEntryPointSuccess || !*e.slot) {
+        (void)cudaGetLastError();
+        if (ok) g_green_missing = e.name;
+        ok = false;
+      }
+    }
+    g_green_ok = ok;
+  });
+  if (!g_green_ok)
+    return fail(DV_ENOTSUP, "this driver has no green contexts (SM partitions): %s unresolved",
+                g_green_missing.c_str());
+  *out = &g_green;
+  return DV_OK;
+}
+
+}  // namespace dv
+
+struct dv_partition {
+  CUgreenCtx g[2] = {nullptr, nullptr};   // [0] streaming, [1] compute
+  CUstream s[2] = {nullptr, nullptr};
+};
+
+namespace dv {
+static void partition_free(const GreenDriver* gd, dv_partition* p) {
+  for (int i = 0; i < 2; ++i) {
+    if (p->s[i]) gd->streamDestroy(p->s[i]);
+    if (p->g[i]) gd->greenCtxDestroy(p->g[i]);
+  }
+  delete p;
+}
+}  // namespace dv
+
+extern "C" {
+dv_status dv_partition_create(int32_t device, int32_t streaming_sms, int32_t priority, dv_partition** out,
+                              void** streaming_stream, void** compute_stream, int32_t* sms_streaming,
+                              int32_t* sms_compute) {
+  using namespace dv;
+  if (!out || !streaming_stream || !compute_stream)
+    return fail(DV_EINVAL, "dv_partition_create: NULL output");
+  if (streaming_sms < 1) return fail(DV_EINVAL, "dv_partition_create: streaming_sms %d < 1", streaming_sms);
+  const GreenDriver* gd = nullptr;
+  DV_TRY(green_driver(&gd));
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+  DV_CUDA(cudaFree(nullptr));   // the device's primary context exists
+  CUdevice dev;
+  CUresult r = gd->deviceGet(&dev, device);
+  if (r != CUDA_SUCCESS) return drv_fail(r, "cuDeviceGet");
+  CUdevResource all, grp, rest;
+  memset(&all, 0, sizeof all);
+  memset(&grp, 0, sizeof grp);
+  memset(&rest, 0, sizeof rest);
+  if ((r = gd->deviceGetDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM)) != CUDA_SUCCESS)
+    return drv_fail(r, "cuDeviceGetDevResource");
+  unsigned int ng = 1;
+  if ((r = gd->smResourceSplitByCount(&grp, &ng, &all, &rest, 0, (unsigned)streaming_sms)) != CUDA_SUCCESS)
+    return drv_fail(r, "cuDevSmResourceSplitByCount");
+  if (ng < 1 || rest.sm.smCount == 0)
+    return fail(DV_EINVAL, "dv_partition_create: %d of the device's %u SMs leave no compute partition",
+                streaming_sms, all.sm.smCount);
+  dv_partition* p = new dv_partition;
+  CUdevResource* parts[2] = {&grp, &rest};
+  for (int i = 0; i < 2; ++i) {
+    CUdevResourceDesc desc;
+    if ((r = gd->resourceGenerateDesc(&desc, parts[i], 1)) != CUDA_SUCCESS ||
+        (r = gd->greenCtxCreate(&p->g[i], desc, dev, CU_GREEN_CTX_DEFAULT_STREAM)) != CUDA_SUCCESS ||
+        (r = gd->greenCtxStreamCreate(&p->s[i], p->g[i], CU_STREAM_NON_BLOCKING, i == 0 ? priority : 0)) !=
+            CUDA_SUCCESS) {
+      partition_free(gd, p);
+      return drv_fail(r, "creating a green context / its stream");
+    }
+  }
+  *out = p;
+  *streaming_stream = (void*)p->s[0];
+  *compute_stream = (void*)p->s[1];
+  if (sms_streaming) *sms_streaming = (int32_t)grp.sm.smCount;
+  if (sms_compute) *sms_compute = (int32_t)rest.sm.smCount;
+  return DV_OK;
+}
+
+dv_status dv_partition_destroy(dv_partition* p) {
+  using namespace dv;
+  if (!p) return DV_OK;
+  const GreenDriver* gd = nullptr;
+  DV_TRY(green_driver(&gd));
+  partition_free(gd, p);
+  return DV_OK;
+}
+}  // extern "C"

@@ -1256,8 +1256,9 @@ static cudaError_t go_cluster(const KParams& kp, int threads, cudaStream_t st) {
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_copy_cluster<VEC, U>, kp);
-  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-  return e != cudaSuccess ? e : cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
 }
 static bool cluster_fits(uint64_t n_vec) { return n_vec <= (uint64_t)cluster_ctas() * 1024 * 4; }
 // Measured (tools/probe_latency.py, C2 layer 160 KiB = 5,120 vectors): into HBM (gpu-scope
@@ -2223,6 +2224,12 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
                     : (kp.flag && q0 == 0 && last && use_cluster(kp))
                         ? launch_cluster(kp, VEC, stream)
                         : launch_cfg(kp, VEC, max_ctas, stream);
+    if (e == cudaErrorInvalidClusterSize) {
+      // a stream of a green context with fewer SMs than the cluster (e.g. an 8-SM streaming
+      // partition, DESIGN.md §6 "SM partitions"): nothing was launched; the ticket form instead
+      (void)cudaGetLastError();
+      e = launch_cfg(kp, VEC, max_ctas, stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");
   }
   return DV_OK;

@@ -68,6 +68,22 @@ def test_no_cpu_fallback_without_gpu():
     assert ei.value.status == dv.DV_ECUDA
 
 
+def test_partition_validates_before_touching_the_device():
+    """dv_partition_create (include/dv.h SM partitions): argument errors are DV_EINVAL before any
+    driver call; without a GPU a valid request fails loudly (never a silent no-op)."""
+    import torch
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_partition_create(0, 0)
+    assert ei.value.status == dv.DV_EINVAL
+    st = dv.lib().dv_partition_create(0, 8, 0, None, None, None, None, None)
+    assert st == dv.DV_EINVAL and "NULL output" in dv.dv_last_error()
+    assert dv.lib().dv_partition_destroy(None) == dv.DV_OK
+    if not torch.cuda.is_available():
+        with pytest.raises(dv.DVError) as ei:
+            dv.dv_partition_create(0, 8)
+        assert ei.value.status in (dv.DV_ECUDA, dv.DV_ENOTSUP)
+
+
 def test_oracle_used_only_by_tests_smoke_and_cpu_baseline():
     """The oracle is test infrastructure: the package, kvgen and tools/ never import it, and
     bench.py imports it only inside its CPU-oracle arm (OracleStep: cpu_baseline, --impl reference)."""
