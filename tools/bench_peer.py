@@ -280,7 +280,7 @@ class C5:
         words = 2 * self.Ls * self.b * H * n_pos * D
         return {"mismatches": bad, "words_per_rank": words, "how": "dvt_verify of every replica word vs the generator"}
 
-    def latency(self, n=300, loaded=False):
+    def latency(self, n=300, loaded=False, partition=0):
         """Per-layer put latency with the system-scope release: writer (dvt_fill of one layer's new
         position) ends -> the put's seq flag released into the successor's memory (%globaltimer on
         the sender, dvt_trace stamps). loaded: while a bf16 GEMM loop (8192^3) keeps every SM of
@@ -292,11 +292,16 @@ class C5:
         ts[:, 1:3] = 2 ** 63 - 1
         q = self.S - 1
         sp = self.sp
+        part = None
         if loaded:
             lo, hi = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+            if partition:   # SM partition (dv_partition_create): put on `partition` SMs, GEMM on the rest
+                part = dv.dv_partition_create(env.local, partition, torch.cuda.Stream.priority_range()[1])
+                hi, lo = torch.cuda.ExternalStream(part.streaming), torch.cuda.ExternalStream(part.compute)
             ga = torch.randn(8192, 8192, device=env.dev, dtype=torch.bfloat16)
             gb = torch.randn(8192, 8192, device=env.dev, dtype=torch.bfloat16)
-            torch.matmul(ga, gb)
+            with torch.cuda.stream(lo):
+                torch.matmul(ga, gb)
             torch.cuda.synchronize()
             sp = hi.cuda_stream
         env.barrier()
@@ -314,10 +319,13 @@ class C5:
                                     self.sig_arr, seq=self._next_seq(), stream=sp)
         dv.dvt_trace(self.ctx, 0)
         torch.cuda.synchronize()
+        if part is not None:
+            part.destroy()
         us = ((ts[:, 0] - te).double() / 1e3).tolist()[20:]
         p50, p99 = env.max(_pct(us, 0.5)), env.max(_pct(us, 0.99))
         scope = dv.dvt_release_scope(self.ctx, self.fp, self.kp)
         return {"p50_us": p50, "p99_us": p99, "n": len(us), "bytes": self.layer_bytes_tok, "loaded": loaded,
+                "sm_partition": partition or None,
                 "release_scope": "gpu" if scope else "system",
                 "how": "writer end -> st.release of the seq flag in the successor's memory, sender "
                        "%globaltimer; p50/p99 max over ranks"}
@@ -439,6 +447,7 @@ def c5_suite(ctx, env, steps=200, peak=None, peak_src=None, nccl=True):
     out["parity"] = c.verify(c.p + steps)
     for name, fn in (("latency_per_layer_put", c.latency),
                      ("latency_per_layer_put_under_gemm", lambda: c.latency(loaded=True)),
+                     ("latency_per_layer_put_under_gemm_sm_partition_16", lambda: c.latency(loaded=True, partition=16)),
                      ("pingpong", c.pingpong)):
         try:
             out[name] = fn()
