@@ -126,14 +126,30 @@ def _copy(st):
             big_dst.copy_(big_src)
 
 
+import ctypes  # noqa: E402
+_cublas = ctypes.CDLL("libcublas.so.12")
+
+
+def sm_target(st, n):
+    """cublasSetSmCountTarget on torch's cuBLAS handle for stream st (0 = the device's count)."""
+    with torch.cuda.stream(st):
+        h = torch.cuda.current_blas_handle()
+        assert _cublas.cublasSetSmCountTarget(ctypes.c_void_p(h), ctypes.c_int(n)) == 0
+
+
 for rep in range(2):
-    for name, st in (("all_sms", plain_lo), ("green_big", s_big)):
+    for name, st, tgt in (("all_sms", plain_lo, 0), ("green_big", s_big, 0),
+                          ("green_big_cublas_sm_target", s_big, rest.sm.smCount)):
+        sm_target(st, tgt)
         ms = timed(st, lambda st=st: gemm_loop(st))
         ms_copy = timed(st, lambda st=st: _copy(st))
         print(json.dumps({"rep": rep, "compute_on": name,
                           "gemm_tflops": round(N_GEMM * 2 * 8192 ** 3 / (ms * 1e-3) / 1e12, 1),
                           "hbm_copy_gbs_2R": round(10 * 2 * big_src.numel() * 2 / (ms_copy * 1e-3) / 1e9, 1)}),
               flush=True)
+        sm_target(st, 0)
+    if os.environ.get("GEMM_ONLY"):
+        continue
     for mode, cs, gs in (("priority", plain_hi, plain_lo), ("green", s_small, s_big), ("green_copy", s_small, plain_lo)):
         for loaded in (False, True):
             r = latency(cs, gs, loaded)
