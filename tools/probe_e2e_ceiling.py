@@ -8,6 +8,11 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+import bench  # noqa: E402
+
+# pinned buffers on the GPU's NUMA node, as bench.py's e2e loop has them (first touch after binding)
+AFFINITY = bench._bind_gpu_local_cpus(0)
+
 N = 6_553_600
 K = 300
 hsrc = torch.empty(64 * N // 2, dtype=torch.int16, pin_memory=True)
@@ -55,7 +60,7 @@ def run(mode):
 
 if __name__ == "__main__" and len(sys.argv) == 1:
     for m in ("independent", "chained", "kernel"):
-        print(json.dumps(run(m)))
+        print(json.dumps(dict(run(m), cpu_affinity=AFFINITY)))
 
 
 def trace(mode="kernel", n=60):
