@@ -6,7 +6,9 @@
  *
  *   build:  gcc -O2 -I include tests/c/abi_smoke.c -L paper_2403_01876_b200 -ldvstream
  *           -Wl,-rpath,paper_2403_01876_b200 -o tests/c/abi_smoke   (done by __graft_entry__.build)
- *   run:    tests/c/abi_smoke [--route-only | --enqueue-bench | --token-bench]
+ *   run:    tests/c/abi_smoke [--route-only | --enqueue-bench | --token-bench | --partition]
+ *           (--partition: the same stream check on the streaming stream of an 8-SM partition,
+ *           dv_partition_create, then dv_partition_destroy)
  * Exit code 0 = pass.
  */
 #define _POSIX_C_SOURCE 199309L
@@ -65,7 +67,7 @@ static uint16_t word(int kv, int l, int r, int h, int s, int d) {
   return (uint16_t)(((((kv * 7 + l) * 13 + r) * 11 + h) * 101 + s) * 17 + d);
 }
 
-static int stream_check(void) {
+static int stream_check(void* st) {
   const int L = 2, B = 2, H = 4, S = 40, S2 = 64, D = 16, P = 40;
   dv_ctx* ctx;
   CHECK(dv_create(0, NULL, &ctx));
@@ -99,25 +101,25 @@ static int stream_check(void) {
   dv_endpoint ev = {DV_EP_DEVICE, 0, dvv, n5 * 2, NULL, 0, 0};
   dv_endpoint ek2 = {DV_EP_DEVICE, 0, dk2, n6 * 2, NULL, 0, 0};
   dv_endpoint ev2 = {DV_EP_DEVICE, 0, dv2, n6 * 2, NULL, 0, 0};
-  CHECK(dv_flush(ctx, hk, n5 * 2, &ek, 0, -1, 0, DV_XFER_STAGED, NULL));
-  CHECK(dv_flush(ctx, hv, n5 * 2, &ev, 0, -1, 0, DV_XFER_STAGED, NULL));
-  CHECK(dv_flush(ctx, ok2, n6 * 2, &ek2, 0, -1, 0, DV_XFER_STAGED, NULL));
-  CHECK(dv_flush(ctx, ov2, n6 * 2, &ev2, 0, -1, 0, DV_XFER_STAGED, NULL));
+  CHECK(dv_flush(ctx, hk, n5 * 2, &ek, 0, -1, 0, DV_XFER_STAGED, st));
+  CHECK(dv_flush(ctx, hv, n5 * 2, &ev, 0, -1, 0, DV_XFER_STAGED, st));
+  CHECK(dv_flush(ctx, ok2, n6 * 2, &ek2, 0, -1, 0, DV_XFER_STAGED, st));
+  CHECK(dv_flush(ctx, ov2, n6 * 2, &ev2, 0, -1, 0, DV_XFER_STAGED, st));
   dv_cache src = {dk, dvv, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S, D, 0};
   dv_cache dst = {dk2, dv2, 0, DV_LAYOUT_KV5D, 2, 0, L, 0, B, H, S2, D, 0};
   const int32_t lb[] = {0, 2}, rb[] = {0, 2};
   dv_setup one = {1, lb, 1, rb, S, 0, NULL}, big = {1, lb, 1, rb, S2, 0, NULL};
   dv_region reg = {0, L, 0, B, 0, P, 0, 0};
   dv_endpoint inbox = {DV_EP_HOST, -1, log, n5 * 4, flags, 1, 0};
-  CHECK(dv_stream_out(ctx, &src, &reg, &one, 0, 0, 0, &big, &inbox, 1, 1, DV_XFER_AUTO, NULL));
-  CHECK(dv_stream_in(ctx, &dst, &reg, &one, &big, 0, 0, 0, &inbox, 1, DV_XFER_AUTO, NULL));
+  CHECK(dv_stream_out(ctx, &src, &reg, &one, 0, 0, 0, &big, &inbox, 1, 1, DV_XFER_AUTO, st));
+  CHECK(dv_stream_in(ctx, &dst, &reg, &one, &big, 0, 0, 0, &inbox, 1, DV_XFER_AUTO, st));
   /* download with level-3 fetches, then wait for everything */
   dv_endpoint hk_ep = {DV_EP_HOST, -1, ok2, n6 * 2, NULL, 0, 0};
-  CHECK(dv_fetch(ctx, &ek2, 0, -1, 0, ok2, n6 * 2, DV_XFER_STAGED, NULL));
-  CHECK(dv_fetch(ctx, &ev2, 0, -1, 0, ov2, n6 * 2, DV_XFER_STAGED, NULL));
+  CHECK(dv_fetch(ctx, &ek2, 0, -1, 0, ok2, n6 * 2, DV_XFER_STAGED, st));
+  CHECK(dv_fetch(ctx, &ev2, 0, -1, 0, ov2, n6 * 2, DV_XFER_STAGED, st));
   (void)hk_ep;
   dv_endpoint fl = {DV_EP_HOST, -1, flags, 64, flags, 8, 0};
-  CHECK(dv_signal(ctx, &fl, 1, 42, NULL));
+  CHECK(dv_signal(ctx, &fl, 1, 42, st));
   int32_t done = 0;
   for (long spin = 0; spin < 2000000000L && !done; ++spin) CHECK(dv_query(ctx, &fl, 1, 42, &done));
   if (!done || flags[0] != 1) {
@@ -258,5 +260,19 @@ int main(int argc, char** argv) {
   if (argc > 1 && !strcmp(argv[1], "--route-only")) return 0;
   if (argc > 1 && !strcmp(argv[1], "--enqueue-bench")) return enqueue_bench();
   if (argc > 1 && !strcmp(argv[1], "--token-bench")) return token_bench();
-  return stream_check();
+  if (argc > 1 && !strcmp(argv[1], "--partition")) {
+    dv_partition* part;
+    void *st_stream, *st_compute;
+    int32_t n0 = 0, n1 = 0;
+    CHECK(dv_partition_create(0, 8, 0, &part, &st_stream, &st_compute, &n0, &n1));
+    if (n0 < 8 || n1 < 1) {
+      fprintf(stderr, "partition %d + %d SMs\n", n0, n1);
+      return 1;
+    }
+    const int rc = stream_check(st_stream);   /* ends with dv_destroy: the device is idle after it */
+    CHECK(dv_partition_destroy(part));
+    if (!rc) printf("partition ok (%d + %d SMs)\n", n0, n1);
+    return rc;
+  }
+  return stream_check(NULL);
 }

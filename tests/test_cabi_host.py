@@ -237,6 +237,16 @@ def test_c_program_streams_through_the_abi():
 
 
 @pytest.mark.gpu
+def test_c_program_streams_on_an_sm_partition():
+    """The same C stream check with every call on the streaming stream of an 8-SM partition made
+    by dv_partition_create (green contexts), from plain C."""
+    import subprocess
+    exe = os.path.join(ROOT, "tests", "c", "abi_smoke")
+    r = subprocess.run([exe, "--partition"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "stream ok" in r.stdout and "partition ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
 def test_c_program_runs_the_headline_token_steps():
     """The headline workload driven from plain C through the ABI alone (decoupled C2 token steps to
     pinned host, completion by the flags): it runs to the last flag and reports its rate."""
