@@ -1260,6 +1260,8 @@ static cudaError_t go_cluster(const KParams& kp, int threads, cudaStream_t st) {
   if (e == cudaSuccess) g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return e;
 }
+// The last stream on which a cluster launch was refused (a small green-context partition).
+static std::atomic<uintptr_t> g_no_cluster_stream{UINTPTR_MAX};   // none yet
 static bool cluster_fits(uint64_t n_vec) { return n_vec <= (uint64_t)cluster_ctas() * 1024 * 4; }
 // Measured (tools/probe_latency.py, C2 layer 160 KiB = 5,120 vectors): into HBM (gpu-scope
 // release) writer end -> flag 3.55 (ticket) -> 3.20 (8-CTA cluster) -> 2.78 us (16-CTA cluster); to
@@ -2221,13 +2223,16 @@ dv_status launch_copy(const CopyPlan& p, uint64_t q_first, uint64_t q_last, cons
                                          : launch_unpack_bulk_vec<16>(kp, p.src + q0 * p.run_bytes, max_ctas, stream))
                     : (tune().bulk && dense_dst(p) && !p.dyn)
                         ? launch_bulk(kp, VEC, p.dst + q0 * p.run_bytes, max_ctas, stream)
-                    : (kp.flag && q0 == 0 && last && use_cluster(kp))
+                    : (kp.flag && q0 == 0 && last && use_cluster(kp) &&
+                       (uintptr_t)stream != g_no_cluster_stream.load())
                         ? launch_cluster(kp, VEC, stream)
                         : launch_cfg(kp, VEC, max_ctas, stream);
     if (e == cudaErrorInvalidClusterSize) {
       // a stream of a green context with fewer SMs than the cluster (e.g. an 8-SM streaming
-      // partition, DESIGN.md §6 "SM partitions"): nothing was launched; the ticket form instead
+      // partition, DESIGN.md §6 "SM partitions"): nothing was launched; the ticket form instead,
+      // and for this stream from now on (one remembered stream: no failed launch per call)
       (void)cudaGetLastError();
+      g_no_cluster_stream.store((uintptr_t)stream);
       e = launch_cfg(kp, VEC, max_ctas, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "copy kernel launch");

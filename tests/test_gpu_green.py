@@ -35,11 +35,13 @@ def test_streaming_on_an_8_sm_green_context_stream():
     c = dv.cache(k, v)
     o = ok.Cache(K, V, 0, 0, H, S, D)
     cx = ctx()
+    torch.cuda.synchronize()
     for dst_host in (False, True):
         reg = (1, 2, 0, B, 70, 71)               # one layer, one position: 160 KiB
         exp = ok.pack(o, reg)
         buf = sentinel_like((exp.size,), pinned=dst_host)
         fl = flags(1, pinned=dst_host)
+        torch.cuda.synchronize()   # buffers made on torch's stream; the partition stream is non-blocking
         dv.dv_scatter(cx, c, dv.region(*reg), dv.endpoint_of(buf, fl), 0, flag_slot=0, seq=7, stream=sp)
         st.synchronize()
         assert np.array_equal(to_np(buf), exp) and int(fl[0]) == 7
@@ -49,16 +51,17 @@ def test_streaming_on_an_8_sm_green_context_stream():
     exp = ok.pack(o, reg)
     inbox = sentinel_like((exp.size,))
     ifl = flags(1)
-    dv.dv_stream_out(cx, c, reg, setup, 0, 0, setup, dv.endpoint_array([dv.endpoint_of(inbox, ifl)]), seq=3,
-                     stream=sp)
     Ks, Vs = kvgen.sentinel_cache(L, B, H, S, D)
     dk, dvv = to_dev(Ks), to_dev(Vs)
     dc = dv.cache(dk, dvv)
     do = ok.Cache(Ks.copy(), Vs.copy(), 0, 0, H, S, D)
     rreg = (0, L, 0, B, 0, 64)
-    dv.dv_remap(cx, c, dc, dv.region(*rreg), stream=sp)
     pexp = ok.pack(o, rreg)
     pbuf = sentinel_like((pexp.size,))
+    torch.cuda.synchronize()
+    dv.dv_stream_out(cx, c, reg, setup, 0, 0, setup, dv.endpoint_array([dv.endpoint_of(inbox, ifl)]), seq=3,
+                     stream=sp)
+    dv.dv_remap(cx, c, dc, dv.region(*rreg), stream=sp)
     dv.dv_scatter(cx, c, dv.region(*rreg), dv.endpoint_of(pbuf), 0, stream=sp)
     st.synchronize()
     assert np.array_equal(to_np(inbox), exp) and int(ifl[0]) == 3
