@@ -462,6 +462,61 @@ def _time(fn, stream, reps, warm=2, tail=None, head_start_ns=0):
     return a.elapsed_time(b) / reps
 
 
+def _latency_fused_producer(dv, ctx, cache, stream, n=440):
+    """Per-layer token latency with the stream-out FUSED INTO THE PRODUCER (device plans,
+    include/dv.h dv_dplan_*) vs the separate stream-out kernel behind it (dv_scatter, PDL): the
+    same vectorised producer (dvt_fill_rows) writes one layer's new K/V (C2: 160 KiB); stamps at the
+    producer's start, its end and the flag release. start -> flag = "write the layer's K/V and make
+    it visible at the destination" (tools/probe_fused_latency.py has the loaded variant)."""
+    import torch
+    sp = stream.cuda_stream
+    out = {}
+    for dst_host in (True, False):
+        dev = "cpu" if dst_host else "cuda"
+        log = torch.empty(L * LAYER_BYTES // 2, dtype=torch.int16, device=dev, pin_memory=dst_host)
+        fl = torch.zeros(L, dtype=torch.int64, device=dev, pin_memory=dst_host)
+        ep = dv.endpoint_of(log, fl)
+        plans = [dv.dv_dplan_scatter(ctx, cache, dv.region(l, l + 1, 0, B, P, P + 1), ep, l * LAYER_BYTES, 0,
+                                     flag_slot=l, seq=1, max_step=S - P - 1) for l in range(L)]
+        res = {}
+        seq = [10 ** 6]
+        for arm in ("fused", "separate"):
+            t0 = torch.full((n,), 2 ** 63 - 1, dtype=torch.int64, device="cuda")
+            te = torch.zeros(n, dtype=torch.int64, device="cuda")
+            ts = torch.zeros((n, 4), dtype=torch.int64, device="cuda")
+            ts[:, 1:3] = 2 ** 63 - 1
+
+            def one(i, arm=arm, t0=t0, te=te, ts=ts):
+                layer, step = i % L, i // L
+                reg = dv.region(layer, layer + 1, 0, B, P + step, P + step + 1)
+                if arm == "fused":
+                    plans[layer].trace = ts[i].data_ptr()
+                    dv.dvt_fill_rows(cache, 20240305, reg, plans[layer], step, t_start_ptr=t0[i].data_ptr(),
+                                     t_end_ptr=te[i].data_ptr(), stream=sp)
+                else:
+                    dv.dvt_fill_rows(cache, 20240305, reg, None, 0, t_start_ptr=t0[i].data_ptr(),
+                                     t_end_ptr=te[i].data_ptr(), stream=sp)
+                    dv.dvt_trace(ctx, ts[i].data_ptr())
+                    seq[0] += 1
+                    dv.dv_scatter(ctx, cache, reg, ep, layer * LAYER_BYTES, flag_slot=layer, seq=seq[0],
+                                  xfer=dv.DV_XFER_FUSED, stream=sp)
+            for i in range(L):
+                one(i)
+            dv.dvt_trace(ctx, 0)
+            torch.cuda.synchronize()
+            dv.dvt_spin(20_000_000, 1, stream=sp)
+            for i in range(n):
+                one(i)
+            dv.dvt_trace(ctx, 0)
+            torch.cuda.synchronize()
+            a = sorted(((ts[:, 0] - t0).double() / 1e3).tolist()[L:])
+            b = sorted(((ts[:, 0] - te).double() / 1e3).tolist()[L:])
+            res[arm] = {"start_to_flag_p50_us": a[len(a) // 2], "start_to_flag_p99_us": a[int(len(a) * 0.99)],
+                        "producer_end_to_flag_p50_us": b[len(b) // 2], "n": len(a)}
+        out["host" if dst_host else "hbm"] = res
+    return out
+
+
 def _latency_under_gemm(dv, ctx, cache, lep, pos_of, n=400, n_gemm=60):
     """Per-layer token latency to pinned host (writer end -> flag, C2 layer of 160 KiB) while a bf16
     GEMM loop (8192^3) saturates the GPU -- NEXT-2's concurrent compute -- in two arrangements:
@@ -698,6 +753,10 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     lat["host_enqueue_us_per_call"] = (time.perf_counter() - t0) / L * 1e6
     torch.cuda.synchronize()
     ex["token_layer_latency"] = lat
+    try:
+        ex["token_layer_latency_fused_producer"] = _latency_fused_producer(dv, ctx, cache, stream)
+    except Exception as e:   # noqa: BLE001 -- reported; the rest of the line stands
+        ex["token_layer_latency_fused_producer"] = {"error": f"{type(e).__name__}: {e}"}
     try:
         ex["token_layer_latency_under_gemm"] = _latency_under_gemm(dv, ctx, cache, lep, pos_of)
     except Exception as e:   # noqa: BLE001 -- reported; the rest of the line stands

@@ -423,6 +423,44 @@ DV_API dv_status dv_engine_doorbell(dv_engine* e, int32_t plan, uint64_t** word)
 /* Steps of `plan` the engine has completed (flag released), read now (small synchronous copy). */
 DV_API dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps);
 
+/* ---- device plans: the stream-out fused into the PRODUCER kernel (Opt 2/3) --
+ * The per-layer stream-out as a separate kernel waits for the producer (the kernel that writes the
+ * layer's new K/V) to finish, then reads the K/V back. A device plan lets the producer itself store
+ * each K/V row it computes both into its cache and straight to the destination -- pinned host
+ * memory over PCIe, a peer GPU's memory over NVLink (IPC-mapped), or this GPU's HBM -- and release
+ * the flag from its own last CTA (include/dv_device.cuh: dv_dplan_row, dv_dplan_release). There is
+ * no second kernel, no dependency wait and no re-read. A plan covers a region at step 0; at step k
+ * (the producer's argument) the positions move by k (token step t writes p + t - 1, reading Q4)
+ * and, for a wire destination, the destination by k * dst_step_bytes; the flag becomes seq + k.
+ * Validation (as dv_scatter_dyn / dv_remap_dyn for every k in [0, max_step]) happens here; the
+ * plan is a plain struct the caller passes to its kernel by value. The release takes a ticket
+ * owned by the plan: one producer launch per plan at a time (stream-ordered launches are fine).
+ * Only KV5D destinations (a row of D*e bytes must be contiguous there). */
+typedef struct dv_dplan {
+  uint8_t* dst[2];          /* K and V destination of (layer o_l, request o_r, head o_h, pos o_s) */
+  int64_t st_l, st_r, st_h, st_s; /* destination byte strides per layer / request / head / position */
+  int64_t step_bytes;       /* destination shift per step (wire destinations; 0 for caches) */
+  int32_t o_l, o_r, o_h, o_s; /* global ids at the destination origin (step 0)                   */
+  int32_t pos_shift;        /* 1: o_s moves with the step (wire); 0: absolute positions (caches) */
+  int32_t l0, l1, r0, r1, h0, h1, s0, s1; /* the region at step 0 (global ids, half-open)        */
+  int32_t row_bytes;        /* head_dim * elem_bytes                                           */
+  int32_t sys_scope;        /* 1: release at system scope (host / peer memory), 0: gpu scope    */
+  uint64_t* flag;           /* NULL: no release                                                 */
+  uint64_t seq;
+  uint32_t* ticket;         /* the plan's own CTA counter (zero between launches)               */
+  uint64_t* trace;          /* optional (dvt): %globaltimer right after the release             */
+} dv_dplan;
+/* Plan rows of `region` of cache `src` (its geometry and head range) into the canonical wire at
+ * dst + dst_off (+ k * dst_step_bytes at step k), releasing flag slot `flag_slot` (-1: none). */
+DV_API dv_status dv_dplan_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                                  const dv_endpoint* dst, uint64_t dst_off, uint64_t dst_step_bytes,
+                                  int32_t flag_slot, uint64_t seq, int32_t max_step, dv_dplan* out);
+/* Plan rows of `region` into cache `dst` (KV5D, e.g. the successor's replica mapped with
+ * dv_ipc_open: PAPER.md:286), same positions, releasing signal's flag slot (signal may be NULL). */
+DV_API dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
+                                const dv_region* region, const dv_endpoint* signal,
+                                int32_t flag_slot, uint64_t seq, int32_t max_step, dv_dplan* out);
+
 /* ---- SM partitions: an SM budget for streaming (NEXT-2; DESIGN.md §6
  * "SM partitions") ----------------------------------------------------------------------------
  * Splits device `device`'s SMs into two green contexts (disjoint SM sets): a STREAMING partition

@@ -16,6 +16,8 @@
 #define DV_DEVICE_CUH
 #include <stdint.h>
 
+#include "dv.h"
+
 /* One system-scope acquire load of the flag. */
 static __device__ __forceinline__ uint64_t dv_flag_load(const uint64_t* flag) {
   uint64_t v;
@@ -48,6 +50,49 @@ static __device__ __forceinline__ int dv_flag_wait(const uint64_t* flag, uint64_
 static __device__ __forceinline__ void dv_engine_ring(uint64_t* doorbell, uint64_t step) {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
   asm volatile("red.release.gpu.global.max.u64 [%0], %1;" ::"l"(doorbell), "l"(step + 1) : "memory");
+}
+
+/* ---- device plans (include/dv.h dv_dplan_*): the stream-out inside the producer kernel ------
+ * Destination of the row (kv, l, r, h, s) -- global ids, D*e bytes -- at step k, or NULL when the
+ * row is outside the plan's region at that step. Store the row there (16- or 32-byte vectors: the
+ * row is 16-byte aligned) in addition to the producer's own cache store. */
+static __device__ __forceinline__ uint8_t* dv_dplan_row(const dv_dplan* p, int32_t k, int kv, int32_t l,
+                                                        int32_t r, int32_t h, int32_t s) {
+  const int32_t sk = s - k;   /* the position at step 0 */
+  if (l < p->l0 || l >= p->l1 || r < p->r0 || r >= p->r1 || h < p->h0 || h >= p->h1 || sk < p->s0 ||
+      sk >= p->s1)
+    return (uint8_t*)0;
+  const int32_t os = p->o_s + (p->pos_shift ? k : 0);
+  return p->dst[kv] + (int64_t)k * p->step_bytes + (int64_t)(l - p->o_l) * p->st_l +
+         (int64_t)(r - p->o_r) * p->st_r + (int64_t)(h - p->o_h) * p->st_h + (int64_t)(s - os) * p->st_s;
+}
+
+/* Release of step k, called by EVERY thread of EVERY CTA of the producer grid once the CTA's row
+ * stores are issued (n_ctas = the grid's CTA count): each CTA orders its stores at gpu scope and
+ * takes a ticket; the last CTA releases flag = seq + k with ONE release at the plan's scope
+ * (st.release.sys for host / peer memory: causality order is cumulative, so every CTA's rows are
+ * visible to any observer of the flag). Contains a __syncthreads(). */
+static __device__ __forceinline__ void dv_dplan_release(const dv_dplan* p, int32_t k, uint32_t n_ctas) {
+  __syncthreads();
+  if (!p->flag) return;
+  if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const uint32_t prev = atomicAdd(p->ticket, 1u);
+    if (prev == n_ctas - 1) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      *(volatile uint32_t*)p->ticket = 0u;
+      const uint64_t v = p->seq + (uint64_t)k;
+      if (p->sys_scope)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
+      else
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
+      if (p->trace) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        *p->trace = t;
+      }
+    }
+  }
 }
 
 #endif

@@ -37,6 +37,17 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
 DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region* region, uint64_t* t_end,
                                uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
 
+/* A vectorised synthetic PRODUCER (kind HASH words of `region` of KV5D cache `c`, 16-byte stores,
+ * one CTA of 128 threads per (layer, request, head) slab and kv). With `plan` (include/dv.h
+ * dv_dplan_*) it also stores every row inside the plan's region at step `step` to the plan's
+ * destination and releases the plan's flag from its last CTA -- the stream-out fused into the
+ * producer (include/dv_device.cuh dv_dplan_row / dv_dplan_release). t_start / t_end (optional,
+ * device uint64, preset by the caller): min over CTAs of %globaltimer at kernel start / max after
+ * the CTA's stores. Triggers programmatic dependent launch at its start. */
+DV_API dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
+                               const dv_dplan* plan, int32_t step, uint64_t* t_start, uint64_t* t_end,
+                               void* stream);
+
 /* Verifier (the second, on-device parity check of SURVEY §8(c) C-5 at full sizes): adds to
  * *mismatches (device memory, uint64) the number of words of `region` that differ from the
  * generator word dvt_fill would write there (same kind / seed / box / valid range). wire == NULL:

@@ -65,6 +65,14 @@ class dv_endpoint(C.Structure):
                 ("n_slots", C.c_int32), ("slot_bytes", C.c_uint64), ("credits", C.c_void_p)]
 
 
+class dv_dplan(C.Structure):
+    """include/dv.h dv_dplan (a device plan: the stream-out fused into the producer kernel)."""
+    _fields_ = [("dst", C.c_void_p * 2)] + [(n, C.c_int64) for n in ("st_l", "st_r", "st_h", "st_s", "step_bytes")] + \
+               [(n, C.c_int32) for n in ("o_l", "o_r", "o_h", "o_s", "pos_shift", "l0", "l1", "r0", "r1", "h0", "h1",
+                                         "s0", "s1", "row_bytes", "sys_scope")] + \
+               [("flag", C.c_void_p), ("seq", C.c_uint64), ("ticket", C.c_void_p), ("trace", C.c_void_p)]
+
+
 class dv_config(C.Structure):
     _fields_ = [("staging_bytes", C.c_uint64), ("max_ctas", C.c_int32), ("host_ctas", C.c_int32)]
 
@@ -147,10 +155,16 @@ _SIGS = {
     "dv_engine_doorbell": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
     "dv_engine_done": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "dvt_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "dv_dplan_scatter": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_endpoint), C.c_uint64, C.c_uint64,
+                                   C.c_int32, C.c_uint64, C.c_int32, P(dv_dplan)]),
+    "dv_dplan_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint), C.c_int32,
+                                 C.c_uint64, C.c_int32, P(dv_dplan)]),
     "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
     "dvt_launch_count": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
+    "dvt_fill_rows": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), P(dv_dplan), C.c_int32, C.c_void_p,
+                                C.c_void_p, C.c_void_p]),
     "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
     "dvt_verify": (C.c_int, [P(dv_cache), C.c_void_p, C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32,
@@ -166,7 +180,7 @@ _SIGS = {
                                     P(C.c_uint64)]),
 }
 
-TESTING_SYMBOLS = {"dvt_fill", "dvt_fill_ring", "dvt_verify", "dvt_spin", "dvt_consume", "dvt_watch", "dvb_per_run_copy",
+TESTING_SYMBOLS = {"dvt_fill", "dvt_fill_ring", "dvt_fill_rows", "dvt_verify", "dvt_spin", "dvt_consume", "dvt_watch", "dvb_per_run_copy",
                    "dvb_buffered_copy"}
 _lib = None
 _tlib = None
@@ -576,6 +590,22 @@ def dv_scatter_dyn(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off
           seq, C.c_void_p(d_step_ptr), max_step, _stream(stream))
 
 
+def dv_dplan_scatter(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_off=0, dst_step_bytes=0, flag_slot=-1,
+                     seq=0, max_step=0) -> dv_dplan:
+    p = dv_dplan()
+    _call("dv_dplan_scatter", ctx.h, C.byref(src), _reg_ct(reg), C.byref(dst), dst_off, dst_step_bytes, flag_slot, seq,
+          max_step, C.byref(p))
+    return p
+
+
+def dv_dplan_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpoint = None, flag_slot=-1, seq=0,
+                   max_step=0) -> dv_dplan:
+    p = dv_dplan()
+    _call("dv_dplan_remap", ctx.h, C.byref(src), C.byref(dst), _reg_ct(reg), _ref(signal), flag_slot, seq, max_step,
+          C.byref(p))
+    return p
+
+
 def dv_remap_dyn(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, d_step_ptr, max_step, signal: dv_endpoint = None,
                  flag_slot=-1, seq=0, stream=None):
     _call("dv_remap_dyn", ctx.h, C.byref(src), C.byref(dst), _reg_ct(reg), _ref(signal), flag_slot, seq,
@@ -748,6 +778,11 @@ def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_re
     b = (C.c_int32 * 5)(*box) if box is not None else None
     _call("dvt_fill", C.byref(c), kind, seed, b, valid[0], valid[1], (None if reg is None else _reg_ct(reg)), C.c_void_p(t_end_ptr),
           _stream(stream))
+
+
+def dvt_fill_rows(c: dv_cache, seed, reg, plan: dv_dplan = None, step=0, t_start_ptr=0, t_end_ptr=0, stream=None):
+    _call("dvt_fill_rows", C.byref(c), seed, _reg_ct(reg), None if plan is None else C.byref(plan), step,
+          C.c_void_p(t_start_ptr), C.c_void_p(t_end_ptr), _stream(stream))
 
 
 def dvt_fill_ring(c: dv_cache, seed, reg, doorbell_ptr, step, ticket_ptr, t_end_ptr=0, stream=None):

@@ -1661,6 +1661,126 @@ dv_status dv_scatter_dyn(dv_ctx* ctx, const dv_cache* src, const dv_region* regi
                         (dst->kind == DV_EP_HOST || src->device < 0) ? ctx->host_ctas : ctx->max_ctas);
 }
 
+// ---- device plans (dv.h dv_dplan_*): the stream-out fused into the producer -------------------
+}  // extern "C"
+namespace dv {
+// The plan's own ticket: taken from the never-recycled range (like a graph-captured launch).
+static dv_status dplan_ticket(dv_ctx* ctx, uint32_t** out) {
+  const uint32_t g = ctx->next_graph_ticket.fetch_add(1);
+  if (g >= dv_ctx::kGraphTickets)
+    return fail(DV_ENOMEM, "more than %u device plans / captured publishing launches in this context",
+                dv_ctx::kGraphTickets);
+  *out = ctx->tickets + dv_ctx::kTickets + g;
+  return DV_OK;
+}
+static void dplan_region(dv_dplan* p, const dv_region& reg, const dv_cache* src) {
+  p->l0 = reg.layer_begin;
+  p->l1 = reg.layer_end;
+  p->r0 = reg.req_begin;
+  p->r1 = reg.req_end;
+  p->h0 = reg.head_begin;
+  p->h1 = reg.head_end;
+  p->s0 = reg.pos_begin;
+  p->s1 = reg.pos_end;
+  p->row_bytes = (int32_t)row_bytes(src);
+}
+}  // namespace dv
+extern "C" {
+
+dv_status dv_dplan_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* region, const dv_endpoint* dst,
+                           uint64_t dst_off, uint64_t dst_step_bytes, int32_t flag_slot, uint64_t seq,
+                           int32_t max_step, dv_dplan* out) {
+  DV_TRY(check_ctx(ctx));
+  if (!region || !out) return fail(DV_EINVAL, "NULL region or plan");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  if (dst_step_bytes % 16) return fail(DV_EALIGN, "dst_step_bytes not a multiple of 16");
+  DV_TRY(check_cache(src, "source"));
+  DV_TRY(check_region_shape(region));
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  DV_TRY(check_cache_holds(src, &reg, "source"));
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  const uint64_t bytes = region_bytes(&reg, src);
+  if (has_ring(dst)) return fail(DV_EINVAL, "a device plan writes a log, not a ring inbox");
+  DV_TRY(check_ep(dst, dst_off, bytes + (uint64_t)max_step * dst_step_bytes, flag_slot, true, "destination"));
+  DV_ON_DEVICE(ctx->device);
+  dv_dplan p;
+  memset(&p, 0, sizeof p);
+  const int64_t row = row_bytes(src);
+  uint8_t* wire = (uint8_t*)dst->base + dst_off;
+  const TView w0 = wire_view(wire, 0, &reg, row), w1 = wire_view(wire, 1, &reg, row);
+  p.dst[0] = (uint8_t*)w0.base;
+  p.dst[1] = (uint8_t*)w1.base;
+  p.st_l = w0.st[DL];
+  p.st_r = w0.st[DR];
+  p.st_h = w0.st[DH];
+  p.st_s = w0.st[DS];
+  p.step_bytes = (int64_t)dst_step_bytes;
+  p.o_l = reg.layer_begin;
+  p.o_r = reg.req_begin;
+  p.o_h = reg.head_begin;
+  p.o_s = reg.pos_begin;
+  p.pos_shift = 1;
+  dplan_region(&p, reg, src);
+  if (flag_slot >= 0 && dst->flags) {
+    p.flag = &dst->flags[flag_slot];
+    p.seq = seq;
+    DV_TRY(dplan_ticket(ctx, &p.ticket));
+    p.sys_scope = !(local_vidmem(ctx, p.flag) && local_vidmem(ctx, wire));
+  }
+  *out = p;
+  return DV_OK;
+}
+
+dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, const dv_region* region,
+                         const dv_endpoint* signal, int32_t flag_slot, uint64_t seq, int32_t max_step,
+                         dv_dplan* out) {
+  if (!region || !out) return fail(DV_EINVAL, "NULL region or plan");
+  if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
+  RemapOp op{src, dst, *region, signal, flag_slot, seq, DV_XFER_FUSED};
+  DV_TRY(remap_check(ctx, op));
+  if (dst->layout != DV_LAYOUT_KV5D) return fail(DV_ENOTSUP, "device plans write KV5D caches only");
+  if (dst->device < 0 && !dst->k) return fail(DV_EINVAL, "NULL destination cache");
+  const dv_region reg = resolve_heads(region, src);
+  if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
+  const dv_region last = shift_pos(reg, max_step);
+  DV_TRY(check_cache_holds(src, &last, "source"));
+  DV_TRY(check_cache_holds(dst, &last, "destination"));
+  if (region_empty(&reg)) return fail(DV_EINVAL, "empty region");
+  DV_ON_DEVICE(ctx->device);
+  dv_dplan p;
+  memset(&p, 0, sizeof p);
+  // the destination cache's origin: (layer_begin, req_begin, head_begin, position 0)
+  dv_region o = reg;
+  o.layer_begin = dst->layer_begin;
+  o.req_begin = dst->req_begin;
+  o.head_begin = dst->head_begin;
+  o.pos_begin = 0;
+  const TView c0 = cache_view(dst, 0, &o), c1 = cache_view(dst, 1, &o);
+  p.dst[0] = (uint8_t*)c0.base;
+  p.dst[1] = (uint8_t*)c1.base;
+  p.st_l = c0.st[DL];
+  p.st_r = c0.st[DR];
+  p.st_h = c0.st[DH];
+  p.st_s = c0.st[DS];
+  p.o_l = dst->layer_begin;
+  p.o_r = dst->req_begin;
+  p.o_h = dst->head_begin;
+  p.o_s = 0;
+  p.pos_shift = 0;
+  dplan_region(&p, reg, src);
+  if (signal && flag_slot >= 0) {
+    p.flag = &signal->flags[flag_slot];
+    p.seq = seq;
+    DV_TRY(dplan_ticket(ctx, &p.ticket));
+    p.sys_scope = !(local_vidmem(ctx, p.flag) && local_vidmem(ctx, dst->k) && local_vidmem(ctx, dst->v));
+  }
+  *out = p;
+  return DV_OK;
+}
+
 dv_status dv_remap_dyn(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
                        const dv_region* region, const dv_endpoint* signal, int32_t flag_slot,
                        uint64_t seq, const int32_t* d_step, int32_t max_step, void* stream) {

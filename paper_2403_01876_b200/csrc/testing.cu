@@ -93,6 +93,62 @@ __global__ void k_fill(const FillParams p) {
   }
 }
 
+// Vectorised producer (dvt_fill_rows): the generator's words of the region with 16-byte stores,
+// one CTA per (slab, kv); with a device plan it also stores every row of the plan's region to the
+// plan's destination and releases the plan's flag from its last CTA (the stream-out fused into
+// the producer, include/dv_device.cuh).
+struct RowsParams {
+  FillParams f;
+  dv_dplan plan;
+  int32_t use_plan;
+  int32_t step;
+  unsigned long long* t_start;
+};
+__global__ void k_fill_rows(const RowsParams rp) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const FillParams& p = rp.f;
+  if (rp.t_start && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(rp.t_start, t);
+  }
+  uint32_t slab = blockIdx.x;
+  const int h = p.h0 + (int)(slab % p.H);
+  slab /= p.H;
+  const int r = p.r0 + (int)(slab % p.nR);
+  const int l = p.l0 + (int)(slab / p.nR);
+  const int kv = blockIdx.y;
+  uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
+                   (int64_t)(h - p.hb) * p.s_h;
+  const int cpr = p.D / 8;   // 16-byte chunks per row
+  const int64_t chunks = (int64_t)p.n * cpr;
+  for (int64_t i = threadIdx.x; i < chunks; i += blockDim.x) {
+    const int s = p.s0 + (int)(i / cpr);
+    const int d0 = (int)(i % cpr) * 8;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = (uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j) |
+             ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
+    const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(base + (int64_t)s * p.D + d0) = v;
+    if (rp.use_plan) {
+      uint8_t* dst = dv_dplan_row(&rp.plan, rp.step, kv, l, r, h, s);
+      if (dst) *reinterpret_cast<uint4*>(dst + (int64_t)d0 * 2) = v;
+    }
+  }
+  if (p.t_end) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p.t_end, t);
+    }
+  }
+  if (rp.use_plan) dv_dplan_release(&rp.plan, rp.step, gridDim.x * gridDim.y);
+}
+
 // Verifier: counts the words of a region that differ from the generator. Cache form (wire == NULL):
 // the same slab walk and addressing as k_fill. Wire form: the canonical wire [l][kv][r][h][s][d]
 // of the region, dense, at `wire` (device or mapped pinned host memory).
@@ -258,6 +314,33 @@ extern "C" dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_re
   cfg.blockDim = dim3(p.n * p.D >= 256 ? 256 : 128);
   cfg.stream = (cudaStream_t)stream;
   DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill, p));
+  DV_CUDA(cudaGetLastError());
+  return DV_OK;
+}
+
+extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
+                                   const dv_dplan* plan, int32_t step, uint64_t* t_start, uint64_t* t_end,
+                                   void* stream) {
+  RowsParams rp{};
+  uint64_t slabs;
+  DV_TRY(fill_params(c, DVT_FILL_HASH, seed, nullptr, 0, 1 << 30, region, &rp.f, &slabs));
+  if (c->layout != DV_LAYOUT_KV5D) return fail(DV_ENOTSUP, "dvt_fill_rows writes KV5D caches only");
+  if (c->head_dim % 8) return fail(DV_EALIGN, "dvt_fill_rows needs head_dim %% 8 == 0");
+  if (!slabs) return fail(DV_EINVAL, "empty region");
+  rp.f.t_end = (unsigned long long*)t_end;
+  rp.t_start = (unsigned long long*)t_start;
+  if (plan) {
+    if (plan->row_bytes != c->head_dim * 2) return fail(DV_EMAP, "plan row size differs from the cache's");
+    rp.plan = *plan;
+    rp.use_plan = 1;
+    rp.step = step;
+  }
+  (void)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)slabs, 2);
+  cfg.blockDim = dim3(128);
+  cfg.stream = (cudaStream_t)stream;
+  DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill_rows, rp));
   DV_CUDA(cudaGetLastError());
   return DV_OK;
 }

@@ -1,0 +1,130 @@
+"""GPU parity of device plans (include/dv.h dv_dplan_*, include/dv_device.cuh): the stream-out
+fused into the producer kernel. The producer is the test library's vectorised writer
+(dvt_fill_rows): it writes kvgen's words into its cache and, through the plan, every row of the
+plan's region straight to the destination, then releases the flag from its last CTA. Everything is
+compared with the CPU oracle (pack / remap of the kvgen cache), and the destination bytes outside
+the plan stay untouched."""
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import paper_2403_01876_b200 as dv
+from oracle import kvstream as ok
+
+from gpu_util import ctx, flags, sentinel_like, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+SEED = 20240311
+
+
+def _cache(L, B, H, S, D, lb=0, rb=0, hb=0):
+    K, V = kvgen.kv5d_cache("hash", lb, L, rb, B, H, S, D, seed=SEED, head_begin=hb)
+    k, v = to_dev(K), to_dev(V)
+    return k, v, dv.cache(k, v, lb, rb, head_begin=hb), ok.Cache(K, V, lb, rb, H, S, D, ok.LAYOUT_KV5D, hb)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_fused_producer_streams_a_token_step_per_step(host):
+    """A plan over (layers 3..7, all requests, all heads) x one position, 6 steps into a log of 6
+    slots (host or HBM): the producer writes position p + k at step k for ALL layers; each slot ==
+    oracle.pack of the plan's region shifted by k, flags seq + k, the cache == kvgen's words."""
+    L, B, H, S, D, p = 10, 3, 4, 64, 128, 20
+    k, v, c, o = _cache(L, B, H, S, D)
+    k.fill_(0)   # the producer must rewrite its region of the cache
+    v.fill_(0)
+    reg = (3, 8, 0, B, p, p + 1)
+    slot = ok.region_bytes(*reg, H, D, 2)
+    log = sentinel_like((6 * slot // 2,), pinned=host)
+    fl = flags(1, pinned=host)
+    ep = dv.endpoint_of(log, fl)
+    plan = dv.dv_dplan_scatter(ctx(), c, dv.region(*reg), ep, 0, slot, flag_slot=0, seq=100, max_step=5)
+    assert plan.sys_scope == (1 if host else 0)
+    torch.cuda.synchronize()
+    for step in range(6):
+        dv.dvt_fill_rows(c, SEED, dv.region(0, L, 0, B, p + step, p + step + 1), plan, step)
+    torch.cuda.synchronize()
+    assert int(fl[0]) == 105
+    got = to_np(log)
+    for step in range(6):
+        exp = ok.pack(o, ok.shifted(reg, step))
+        assert np.array_equal(got[step * slot // 2:(step + 1) * slot // 2], exp), step
+    kk = to_np(k)
+    assert np.array_equal(kk[:, :, :, p:p + 6], o.K[:, :, :, p:p + 6])
+
+
+def test_fused_producer_plan_subset_and_offsets():
+    """Cache with layer / request / head offsets; the plan covers a sub-range of its heads and
+    requests; the producer writes more rows than the plan: only the plan's rows reach the
+    destination (dst_off inside a larger buffer), every other byte stays the sentinel."""
+    L, B, H, S, D = 4, 4, 6, 48, 64
+    lb, rb, hb = 7, 2, 3
+    k, v, c, o = _cache(L, B, H, S, D, lb, rb, hb)
+    reg = (lb + 1, lb + 3, rb + 1, rb + 3, 10, 14, hb + 2, hb + 5)
+    nb = ok.region_bytes(*reg[:6], reg[7] - reg[6], D, 2)   # 3 of the cache's heads
+    buf = sentinel_like((nb // 2 + 4096,))
+    fl = flags(1)
+    plan = dv.dv_dplan_scatter(ctx(), c, dv.region(*reg), dv.endpoint_of(buf, fl), 4096, flag_slot=0, seq=9)
+    torch.cuda.synchronize()
+    dv.dvt_fill_rows(c, SEED, dv.region(lb, lb + L, rb, rb + B, 8, 16), plan, 0)
+    torch.cuda.synchronize()
+    got = to_np(buf)
+    assert np.all(got[:2048] == 0xFFFF)
+    assert np.array_equal(got[2048:2048 + nb // 2], ok.pack(o, reg))
+    assert np.all(got[2048 + nb // 2:] == 0xFFFF)
+    assert int(fl[0]) == 9
+
+
+def test_fused_producer_remap_into_a_cache_then_consumer_stream():
+    """A remap plan into another KV5D cache (other max_seq, its own layer/request origin) releasing
+    a device flag: a consumer stream waits for the flag and copies the destination cache -- it sees
+    every row of the step (20 steps, each compared with oracle.remap)."""
+    L, B, H, S, D = 3, 2, 4, 40, 128
+    k, v, c, o = _cache(L, B, H, S, D, lb=2)
+    Ks, Vs = kvgen.sentinel_cache(L, B, H, 64, D)
+    dk, dvv = to_dev(Ks), to_dev(Vs)
+    dc = dv.cache(dk, dvv, 2, 0)
+    do = ok.Cache(Ks.copy(), Vs.copy(), 2, 0, H, 64, D)
+    fl = flags(1)
+    sig = dv.endpoint_of(torch.empty(64, dtype=torch.int16, device="cuda"), fl)
+    reg = (2, 5, 0, B, 10, 11)
+    plan = dv.dv_dplan_remap(ctx(), c, dc, dv.region(*reg), sig, flag_slot=0, seq=1, max_step=19)
+    assert plan.sys_scope == 0
+    cons = torch.cuda.Stream()
+    snap = torch.empty_like(dk)
+    torch.cuda.synchronize()
+    for step in range(20):
+        dv.dvt_fill_rows(c, SEED, dv.region(2, 5, 0, B, 10 + step, 11 + step), plan, step)
+        dv.dv_wait(ctx(), sig, 0, 1 + step, stream=cons.cuda_stream)
+        with torch.cuda.stream(cons):
+            snap.copy_(dk)
+        cons.synchronize()
+        ok.remap(o, do, ok.shifted(reg, step))
+        assert np.array_equal(to_np(snap), do.K), step
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(dvv), do.V)
+
+
+def test_dplan_validation():
+    """Errors before anything is planned: FT6D destination (rows not contiguous), a log too small
+    for max_step, positions past the source max_seq at max_step, a ring inbox."""
+    L, B, H, S, D = 2, 2, 2, 16, 64
+    k, v, c, o = _cache(L, B, H, S, D)
+    reg = dv.region(0, L, 0, B, 4, 5)
+    nb = ok.region_bytes(0, L, 0, B, 4, 5, H, D, 2)
+    buf = sentinel_like((nb // 2 * 2,))
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_dplan_scatter(ctx(), c, reg, dv.endpoint_of(buf), 0, nb, max_step=2)
+    assert ei.value.status in (dv.DV_ERANGE, dv.DV_EINVAL)
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_dplan_scatter(ctx(), c, reg, dv.endpoint_of(buf), 0, 0, max_step=S)
+    assert ei.value.status == dv.DV_ERANGE
+    k6 = torch.empty((L, B, H, D // 8, S, 8), dtype=torch.int16, device="cuda")
+    c6 = dv.cache(k6, torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda"))
+    with pytest.raises(dv.DVError) as ei:
+        dv.dv_dplan_remap(ctx(), c, c6, reg)
+    assert ei.value.status == dv.DV_ENOTSUP
+    ring = dv.endpoint_of(buf, flags(1), n_slots=2, slot_bytes=nb)
+    with pytest.raises(dv.DVError):
+        dv.dv_dplan_scatter(ctx(), c, reg, ring, 0)

@@ -330,6 +330,48 @@ class C5:
                 "how": "writer end -> st.release of the seq flag in the successor's memory, sender "
                        "%globaltimer; p50/p99 max over ranks"}
 
+    def latency_fused(self, n=300):
+        """Per-layer put with the put FUSED INTO THE PRODUCER (dv_dplan_remap into the successor's
+        IPC-mapped replica, include/dv.h device plans): the vectorised producer (dvt_fill_rows)
+        writes one layer's new K/V into its own cache and the successor's replica and releases the
+        successor's flag. Reported beside the separate path (producer, then dv_stream_out_direct):
+        producer start -> flag release, p50/p99 max over ranks."""
+        env = self.env
+        q = self.S - 1
+        plans = [dv.dv_dplan_remap(self.ctx, self.own, self.rep_at_succ,
+                                   dv.region(self.lb + j, self.lb + j + 1, 0, self.b, q, q + 1), self.sig,
+                                   flag_slot=0, seq=self.seq + 1) for j in range(self.Ls)]
+        out = {}
+        for arm in ("fused", "separate"):
+            t0 = torch.full((n,), 2 ** 63 - 1, dtype=torch.int64, device=env.dev)
+            te = torch.zeros(n, dtype=torch.int64, device=env.dev)
+            ts = torch.zeros((n, 4), dtype=torch.int64, device=env.dev)
+            ts[:, 1:3] = 2 ** 63 - 1
+            env.barrier()
+            dv.dvt_spin(20_000_000, 1, stream=self.sp)
+            for i in range(n):
+                j = i % self.Ls
+                reg = dv.region(self.lb + j, self.lb + j + 1, 0, self.b, q, q + 1)
+                if arm == "fused":
+                    plans[j].trace = ts[i].data_ptr()
+                    plans[j].seq = self._next_seq()
+                    dv.dvt_fill_rows(self.own, SEED_C5, reg, plans[j], 0, t_start_ptr=t0[i].data_ptr(),
+                                     t_end_ptr=te[i].data_ptr(), stream=self.sp)
+                else:
+                    dv.dvt_fill_rows(self.own, SEED_C5, reg, None, 0, t_start_ptr=t0[i].data_ptr(),
+                                     t_end_ptr=te[i].data_ptr(), stream=self.sp)
+                    dv.dvt_trace(self.ctx, ts[i].data_ptr())
+                    dv.dv_stream_out_direct(self.ctx, self.own, reg, self.setup, 0, 0, self.setup, self.dst_arr,
+                                            self.sig_arr, seq=self._next_seq(), stream=self.sp)
+            dv.dvt_trace(self.ctx, 0)
+            torch.cuda.synchronize()
+            us = ((ts[:, 0] - t0).double() / 1e3).tolist()[20:]
+            out[arm] = {"start_to_flag_p50_us": env.max(_pct(us, 0.5)), "start_to_flag_p99_us": env.max(_pct(us, 0.99)),
+                        "n": len(us)}
+        out["bytes"] = self.layer_bytes_tok
+        out["release_scope"] = "system" if plans[0].sys_scope else "gpu"
+        return out
+
     def pingpong(self, iters=300):
         """Put one layer (+ flag) into the successor, wait for the predecessor's put, ack into the
         predecessor's memory, wait for the successor's ack: RTT per iteration (device time)."""
@@ -448,6 +490,7 @@ def c5_suite(ctx, env, steps=200, peak=None, peak_src=None, nccl=True):
     for name, fn in (("latency_per_layer_put", c.latency),
                      ("latency_per_layer_put_under_gemm", lambda: c.latency(loaded=True)),
                      ("latency_per_layer_put_under_gemm_sm_partition_16", lambda: c.latency(loaded=True, partition=16)),
+                     ("latency_per_layer_put_fused_producer", c.latency_fused),
                      ("pingpong", c.pingpong)):
         try:
             out[name] = fn()
