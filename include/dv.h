@@ -435,10 +435,14 @@ DV_API dv_status dv_engine_done(dv_engine* e, int32_t plan, uint64_t* steps);
  * Validation (as dv_scatter_dyn / dv_remap_dyn for every k in [0, max_step]) happens here; the
  * plan is a plain struct the caller passes to its kernel by value. The release takes a ticket
  * owned by the plan: one producer launch per plan at a time (stream-ordered launches are fine).
- * Only KV5D destinations (a row of D*e bytes must be contiguous there). */
+ * Destination caches may be KV5D or FasterTransformer 6-D (the key's 16-byte packets lie S*16
+ * bytes apart there: producers store packets through dv_dplan_packet, or whole rows through
+ * dv_dplan_row where dv_dplan_row_contiguous holds). */
 typedef struct dv_dplan {
   uint8_t* dst[2];          /* K and V destination of (layer o_l, request o_r, head o_h, pos o_s) */
-  int64_t st_l, st_r, st_h, st_s; /* destination byte strides per layer / request / head / position */
+  int64_t st_l, st_r, st_h;  /* destination byte strides per layer / request / head              */
+  int64_t st_s[2], st_u[2];  /* K / V: byte stride per position and per 16-byte packet of a row
+                                (KV5D: row bytes and 16; FasterTransformer's 6-D key: 16 and S*16) */
   int64_t step_bytes;       /* destination shift per step (wire destinations; 0 for caches) */
   int32_t o_l, o_r, o_h, o_s; /* global ids at the destination origin (step 0)                   */
   int32_t pos_shift;        /* 1: o_s moves with the step (wire); 0: absolute positions (caches) */
@@ -455,7 +459,7 @@ typedef struct dv_dplan {
 DV_API dv_status dv_dplan_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                                   const dv_endpoint* dst, uint64_t dst_off, uint64_t dst_step_bytes,
                                   int32_t flag_slot, uint64_t seq, int32_t max_step, dv_dplan* out);
-/* Plan rows of `region` into cache `dst` (KV5D, e.g. the successor's replica mapped with
+/* Plan rows of `region` into cache `dst` (KV5D or FT6D, e.g. the successor's replica mapped with
  * dv_ipc_open: PAPER.md:286), same positions, releasing signal's flag slot (signal may be NULL). */
 DV_API dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst,
                                 const dv_region* region, const dv_endpoint* signal,

@@ -53,18 +53,29 @@ static __device__ __forceinline__ void dv_engine_ring(uint64_t* doorbell, uint64
 }
 
 /* ---- device plans (include/dv.h dv_dplan_*): the stream-out inside the producer kernel ------
- * Destination of the row (kv, l, r, h, s) -- global ids, D*e bytes -- at step k, or NULL when the
- * row is outside the plan's region at that step. Store the row there (16- or 32-byte vectors: the
- * row is 16-byte aligned) in addition to the producer's own cache store. */
-static __device__ __forceinline__ uint8_t* dv_dplan_row(const dv_dplan* p, int32_t k, int kv, int32_t l,
-                                                        int32_t r, int32_t h, int32_t s) {
+ * Destination of the 16-byte packet u of the row (kv, l, r, h, s) -- global ids -- at step k, or
+ * NULL when the row is outside the plan's region at that step. The producer stores each packet it
+ * computes there in addition to its own cache store (16-byte aligned). */
+static __device__ __forceinline__ uint8_t* dv_dplan_packet(const dv_dplan* p, int32_t k, int kv, int32_t l,
+                                                           int32_t r, int32_t h, int32_t s, int32_t u) {
   const int32_t sk = s - k;   /* the position at step 0 */
   if (l < p->l0 || l >= p->l1 || r < p->r0 || r >= p->r1 || h < p->h0 || h >= p->h1 || sk < p->s0 ||
       sk >= p->s1)
     return (uint8_t*)0;
   const int32_t os = p->o_s + (p->pos_shift ? k : 0);
   return p->dst[kv] + (int64_t)k * p->step_bytes + (int64_t)(l - p->o_l) * p->st_l +
-         (int64_t)(r - p->o_r) * p->st_r + (int64_t)(h - p->o_h) * p->st_h + (int64_t)(s - os) * p->st_s;
+         (int64_t)(r - p->o_r) * p->st_r + (int64_t)(h - p->o_h) * p->st_h + (int64_t)(s - os) * p->st_s[kv] +
+         (int64_t)u * p->st_u[kv];
+}
+/* Whether rows of kv are contiguous at the destination (every wire; KV5D caches; the V half of an
+ * FT6D cache): then dv_dplan_row gives the row's start and the producer may store it with wider
+ * vectors. */
+static __device__ __forceinline__ int dv_dplan_row_contiguous(const dv_dplan* p, int kv) {
+  return p->st_u[kv] == 16;
+}
+static __device__ __forceinline__ uint8_t* dv_dplan_row(const dv_dplan* p, int32_t k, int kv, int32_t l,
+                                                        int32_t r, int32_t h, int32_t s) {
+  return dv_dplan_packet(p, k, kv, l, r, h, s, 0);
 }
 
 /* Release of step k, called by EVERY thread of EVERY CTA of the producer grid once the CTA's row

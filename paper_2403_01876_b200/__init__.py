@@ -67,7 +67,8 @@ class dv_endpoint(C.Structure):
 
 class dv_dplan(C.Structure):
     """include/dv.h dv_dplan (a device plan: the stream-out fused into the producer kernel)."""
-    _fields_ = [("dst", C.c_void_p * 2)] + [(n, C.c_int64) for n in ("st_l", "st_r", "st_h", "st_s", "step_bytes")] + \
+    _fields_ = [("dst", C.c_void_p * 2)] + [(n, C.c_int64) for n in ("st_l", "st_r", "st_h")] + \
+               [("st_s", C.c_int64 * 2), ("st_u", C.c_int64 * 2), ("step_bytes", C.c_int64)] + \
                [(n, C.c_int32) for n in ("o_l", "o_r", "o_h", "o_s", "pos_shift", "l0", "l1", "r0", "r1", "h0", "h1",
                                          "s0", "s1", "row_bytes", "sys_scope")] + \
                [("flag", C.c_void_p), ("seq", C.c_uint64), ("ticket", C.c_void_p), ("trace", C.c_void_p)]

@@ -1716,7 +1716,8 @@ dv_status dv_dplan_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* re
   p.st_l = w0.st[DL];
   p.st_r = w0.st[DR];
   p.st_h = w0.st[DH];
-  p.st_s = w0.st[DS];
+  p.st_s[0] = p.st_s[1] = w0.st[DS];
+  p.st_u[0] = p.st_u[1] = 16;
   p.step_bytes = (int64_t)dst_step_bytes;
   p.o_l = reg.layer_begin;
   p.o_r = reg.req_begin;
@@ -1741,7 +1742,6 @@ dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, 
   if (max_step < 0) return fail(DV_EINVAL, "negative max_step");
   RemapOp op{src, dst, *region, signal, flag_slot, seq, DV_XFER_FUSED};
   DV_TRY(remap_check(ctx, op));
-  if (dst->layout != DV_LAYOUT_KV5D) return fail(DV_ENOTSUP, "device plans write KV5D caches only");
   if (dst->device < 0 && !dst->k) return fail(DV_EINVAL, "NULL destination cache");
   const dv_region reg = resolve_heads(region, src);
   if ((int64_t)reg.pos_end + max_step > INT32_MAX) return fail(DV_ERANGE, "positions overflow");
@@ -1764,7 +1764,10 @@ dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache* dst, 
   p.st_l = c0.st[DL];
   p.st_r = c0.st[DR];
   p.st_h = c0.st[DH];
-  p.st_s = c0.st[DS];
+  p.st_s[0] = c0.st[DS];
+  p.st_s[1] = c1.st[DS];
+  p.st_u[0] = c0.st[DU];
+  p.st_u[1] = c1.st[DU];
   p.o_l = dst->layer_begin;
   p.o_r = dst->req_begin;
   p.o_h = dst->head_begin;

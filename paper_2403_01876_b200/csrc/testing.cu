@@ -132,9 +132,9 @@ __global__ void k_fill_rows(const RowsParams rp) {
              ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
     const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
     *reinterpret_cast<uint4*>(base + (int64_t)s * p.D + d0) = v;
-    if (rp.use_plan) {
-      uint8_t* dst = dv_dplan_row(&rp.plan, rp.step, kv, l, r, h, s);
-      if (dst) *reinterpret_cast<uint4*>(dst + (int64_t)d0 * 2) = v;
+    if (rp.use_plan) {   // packet d0/8 of the row (FT6D-key destinations: packets S*16 bytes apart)
+      uint8_t* dst = dv_dplan_packet(&rp.plan, rp.step, kv, l, r, h, s, d0 / 8);
+      if (dst) *reinterpret_cast<uint4*>(dst) = v;
     }
   }
   if (p.t_end) {

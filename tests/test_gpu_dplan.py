@@ -106,9 +106,34 @@ def test_fused_producer_remap_into_a_cache_then_consumer_stream():
     assert np.array_equal(to_np(dvv), do.V)
 
 
+def test_fused_producer_remap_into_an_ft6d_cache():
+    """A remap plan into a FasterTransformer 6-D cache (the key's packets S*16 bytes apart; the
+    producer stores packets through dv_dplan_packet) over 8 steps == oracle.remap into FT6D; the
+    rest of the destination keeps the sentinel."""
+    L, B, H, S, D = 2, 3, 4, 32, 64
+    k, v, c, o = _cache(L, B, H, S, D)
+    Ks, Vs = kvgen.sentinel_cache(L, B, H, 48, D)
+    K6 = kvgen.as_ft6d_key(Ks)
+    dk, dvv = to_dev(K6), to_dev(Vs)
+    dc = dv.cache(dk, dvv)
+    do = ok.Cache(K6.copy(), Vs.copy(), 0, 0, H, 48, D, ok.LAYOUT_FT6D, 0)
+    fl = flags(1)
+    sig = dv.endpoint_of(torch.empty(64, dtype=torch.int16, device="cuda"), fl)
+    reg = (0, L, 1, B, 5, 7, 1, 3)
+    plan = dv.dv_dplan_remap(ctx(), c, dc, dv.region(*reg), sig, flag_slot=0, seq=1, max_step=7)
+    assert list(plan.st_u) == [48 * 16, 16] and list(plan.st_s) == [16, D * 2]
+    torch.cuda.synchronize()
+    for step in range(8):
+        dv.dvt_fill_rows(c, SEED, dv.region(0, L, 0, B, 5 + step, 7 + step), plan, step)
+        ok.remap(o, do, ok.shifted(reg, step))
+    torch.cuda.synchronize()
+    assert int(fl[0]) == 8
+    assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
+
+
 def test_dplan_validation():
-    """Errors before anything is planned: FT6D destination (rows not contiguous), a log too small
-    for max_step, positions past the source max_seq at max_step, a ring inbox."""
+    """Errors before anything is planned: a log too small for max_step, positions past the source
+    max_seq at max_step, a ring inbox."""
     L, B, H, S, D = 2, 2, 2, 16, 64
     k, v, c, o = _cache(L, B, H, S, D)
     reg = dv.region(0, L, 0, B, 4, 5)
@@ -120,11 +145,6 @@ def test_dplan_validation():
     with pytest.raises(dv.DVError) as ei:
         dv.dv_dplan_scatter(ctx(), c, reg, dv.endpoint_of(buf), 0, 0, max_step=S)
     assert ei.value.status == dv.DV_ERANGE
-    k6 = torch.empty((L, B, H, D // 8, S, 8), dtype=torch.int16, device="cuda")
-    c6 = dv.cache(k6, torch.empty((L, B, H, S, D), dtype=torch.int16, device="cuda"))
-    with pytest.raises(dv.DVError) as ei:
-        dv.dv_dplan_remap(ctx(), c, c6, reg)
-    assert ei.value.status == dv.DV_ENOTSUP
     ring = dv.endpoint_of(buf, flags(1), n_slots=2, slot_bytes=nb)
     with pytest.raises(dv.DVError):
         dv.dv_dplan_scatter(ctx(), c, reg, ring, 0)

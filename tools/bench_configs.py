@@ -30,23 +30,39 @@ st = torch.cuda.current_stream()
 sp = st.cuda_stream
 
 
+LAST = {}   # spread of the last timed(): min / p90 of its batch means (SURVEY §8(d) protocol)
+
+
 def emit(**kw):
+    if "us" in kw and LAST:
+        kw.update(LAST)
+    LAST.clear()
     print(json.dumps(kw), flush=True)
 
 
 def timed(fn, reps=5, warm=2, tail=None):
+    """Median over batches of the mean device time per call (us); >= 20 timed calls in >= 3
+    batches of `reps` back-to-back calls (median, min and p90 reported)."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(st)
-    for _ in range(reps):
-        fn()
-    if tail:     # e.g. the consumer's flag wait after decoupled transfers
-        tail()
-    b.record(st)
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps * 1e3   # us
+    batches = max(3, -(-20 // reps))
+    out = []
+    for _ in range(batches):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        if tail:     # e.g. the consumer's flag wait after decoupled transfers
+            tail()
+        b.record(st)
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) / reps * 1e3)   # us
+    out.sort()
+    LAST.clear()
+    LAST.update({"us_min": out[0], "us_p90": out[min(len(out) - 1, int(0.9 * len(out)))], "batches": batches,
+                 "calls_per_batch": reps})
+    return out[len(out) // 2]
 
 
 def new_cache(nL, nR, H, S, D, lb, rb, fill_seed=None, pinned=False, valid=None):
