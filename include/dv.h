@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define DV_ABI_VERSION 3
+#define DV_ABI_VERSION 4   /* 4: device plans (dv_dplan_*), SM partitions (dv_partition_*) */
 
 #if defined(__GNUC__)
 #define DV_API __attribute__((visibility("default")))

@@ -55,7 +55,7 @@ def test_library_exports_every_declared_symbol():
     c_test = {s for s in _dynamic_symbols(dv.TESTING_LIB_PATH) if s.startswith(("dv_", "dvt_", "dvb_"))}
     assert c_prod == prod, c_prod ^ prod
     assert c_test == test, c_test ^ test
-    assert dv.dv_abi_version() == 3
+    assert dv.dv_abi_version() == 4
 
 
 def test_no_cpu_fallback_without_gpu():
