@@ -465,6 +465,25 @@ DV_API dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache
                                 const dv_region* region, const dv_endpoint* signal,
                                 int32_t flag_slot, uint64_t seq, int32_t max_step, dv_dplan* out);
 
+/* Level 1 as device plans (dv_stream_out_direct fused into the producer; §4.2.1 the
+ * prompt -> token hand-off, :286 ring replication): route `region` out of block (my_stage,
+ * my_micro, my_tp) of src_setup into dst_setup's caches, one remap plan per route piece leaving
+ * this block, each releasing signals[destination block] slot = this block's flat index with seq
+ * (+ k at step k). The producer stores every packet through dv_dplan_set_packet (the pieces are
+ * disjoint: at most one plan takes a packet) and ends with dv_dplan_set_release. At most
+ * DV_DPLAN_SET_MAX pieces (DV_ENOTSUP beyond); n == 0 when no piece leaves this block. */
+#define DV_DPLAN_SET_MAX 8
+typedef struct dv_dplan_set {
+  int32_t n;
+  int32_t reserved;
+  dv_dplan plan[DV_DPLAN_SET_MAX];
+} dv_dplan_set;
+DV_API dv_status dv_dplan_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                                            const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
+                                            int32_t my_tp, const dv_setup* dst_setup,
+                                            const dv_cache* dst_caches, const dv_endpoint* signals,
+                                            int32_t n_dst, uint64_t seq, int32_t max_step, dv_dplan_set* out);
+
 /* ---- SM partitions: an SM budget for streaming (NEXT-2; DESIGN.md §6
  * "SM partitions") ----------------------------------------------------------------------------
  * Splits device `device`'s SMs into two green contexts (disjoint SM sets): a STREAMING partition

@@ -83,27 +83,46 @@ static __device__ __forceinline__ uint8_t* dv_dplan_row(const dv_dplan* p, int32
  * takes a ticket; the last CTA releases flag = seq + k with ONE release at the plan's scope
  * (st.release.sys for host / peer memory: causality order is cumulative, so every CTA's rows are
  * visible to any observer of the flag). Contains a __syncthreads(). */
-static __device__ __forceinline__ void dv_dplan_release(const dv_dplan* p, int32_t k, uint32_t n_ctas) {
-  __syncthreads();
+static __device__ __forceinline__ void dv_dplan_release_cta(const dv_dplan* p, int32_t k, uint32_t n_ctas) {
+  /* the part after the CTA's barrier: one thread of the CTA */
   if (!p->flag) return;
-  if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  const uint32_t prev = atomicAdd(p->ticket, 1u);
+  if (prev == n_ctas - 1) {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    const uint32_t prev = atomicAdd(p->ticket, 1u);
-    if (prev == n_ctas - 1) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      *(volatile uint32_t*)p->ticket = 0u;
-      const uint64_t v = p->seq + (uint64_t)k;
-      if (p->sys_scope)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
-      else
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
-      if (p->trace) {
-        uint64_t t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        *p->trace = t;
-      }
+    *(volatile uint32_t*)p->ticket = 0u;
+    const uint64_t v = p->seq + (uint64_t)k;
+    if (p->sys_scope)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
+    else
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p->flag), "l"(v) : "memory");
+    if (p->trace) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      *p->trace = t;
     }
   }
+}
+static __device__ __forceinline__ void dv_dplan_release(const dv_dplan* p, int32_t k, uint32_t n_ctas) {
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) dv_dplan_release_cta(p, k, n_ctas);
+}
+
+/* Plan sets (dv_dplan_stream_out_direct): the destination of a packet is the one plan whose piece
+ * holds it (NULL if none); the release runs every plan's ticket chain after ONE barrier. */
+static __device__ __forceinline__ uint8_t* dv_dplan_set_packet(const dv_dplan_set* s, int32_t k, int kv,
+                                                               int32_t l, int32_t r, int32_t h, int32_t pos,
+                                                               int32_t u) {
+  for (int i = 0; i < s->n; ++i) {
+    uint8_t* d = dv_dplan_packet(&s->plan[i], k, kv, l, r, h, pos, u);
+    if (d) return d;
+  }
+  return (uint8_t*)0;
+}
+static __device__ __forceinline__ void dv_dplan_set_release(const dv_dplan_set* s, int32_t k, uint32_t n_ctas) {
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0)
+    for (int i = 0; i < s->n; ++i) dv_dplan_release_cta(&s->plan[i], k, n_ctas);
 }
 
 #endif

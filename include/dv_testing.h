@@ -38,15 +38,16 @@ DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region
                                uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
 
 /* A vectorised synthetic PRODUCER (kind HASH words of `region` of KV5D cache `c`, 16-byte stores,
- * one CTA of 128 threads per (layer, request, head) slab and kv). With `plan` (include/dv.h
- * dv_dplan_*) it also stores every row inside the plan's region at step `step` to the plan's
- * destination and releases the plan's flag from its last CTA -- the stream-out fused into the
- * producer (include/dv_device.cuh dv_dplan_row / dv_dplan_release). t_start / t_end (optional,
+ * one CTA of 128 threads per (layer, request, head) slab and kv). With `n_plans` plans (include/dv.h
+ * dv_dplan_*; <= DV_DPLAN_SET_MAX, disjoint regions, e.g. a dv_dplan_set) it also stores every
+ * packet inside a plan's region at step `step` to that plan's destination and releases every
+ * plan's flag from its last CTA -- the stream-out fused into the producer (include/dv_device.cuh
+ * dv_dplan_set_packet / dv_dplan_set_release). t_start / t_end (optional,
  * device uint64, preset by the caller): min over CTAs of %globaltimer at kernel start / max after
  * the CTA's stores. Triggers programmatic dependent launch at its start. */
 DV_API dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
-                               const dv_dplan* plan, int32_t step, uint64_t* t_start, uint64_t* t_end,
-                               void* stream);
+                               const dv_dplan* plans, int32_t n_plans, int32_t step, uint64_t* t_start,
+                               uint64_t* t_end, void* stream);
 
 /* Verifier (the second, on-device parity check of SURVEY §8(c) C-5 at full sizes): adds to
  * *mismatches (device memory, uint64) the number of words of `region` that differ from the

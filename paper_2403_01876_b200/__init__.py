@@ -74,6 +74,13 @@ class dv_dplan(C.Structure):
                [("flag", C.c_void_p), ("seq", C.c_uint64), ("ticket", C.c_void_p), ("trace", C.c_void_p)]
 
 
+DV_DPLAN_SET_MAX = 8
+
+
+class dv_dplan_set(C.Structure):
+    _fields_ = [("n", C.c_int32), ("reserved", C.c_int32), ("plan", dv_dplan * DV_DPLAN_SET_MAX)]
+
+
 class dv_config(C.Structure):
     _fields_ = [("staging_bytes", C.c_uint64), ("max_ctas", C.c_int32), ("host_ctas", C.c_int32)]
 
@@ -158,14 +165,17 @@ _SIGS = {
     "dvt_engine_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "dv_dplan_scatter": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_endpoint), C.c_uint64, C.c_uint64,
                                    C.c_int32, C.c_uint64, C.c_int32, P(dv_dplan)]),
+    "dv_dplan_stream_out_direct": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
+                                             C.c_int32, C.c_int32, P(dv_setup), P(dv_cache), P(dv_endpoint),
+                                             C.c_int32, C.c_uint64, C.c_int32, P(dv_dplan_set)]),
     "dv_dplan_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint), C.c_int32,
                                  C.c_uint64, C.c_int32, P(dv_dplan)]),
     "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
     "dvt_launch_count": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
-    "dvt_fill_rows": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), P(dv_dplan), C.c_int32, C.c_void_p,
-                                C.c_void_p, C.c_void_p]),
+    "dvt_fill_rows": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), P(dv_dplan), C.c_int32, C.c_int32,
+                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
     "dvt_verify": (C.c_int, [P(dv_cache), C.c_void_p, C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32,
@@ -651,6 +661,17 @@ def dv_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, m
           my_micro, my_tp, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, xfer, _stream(stream))
 
 
+def dv_dplan_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro,
+                               dst_setup: Setup, dst_caches, signals=None, seq=0, max_step=0, my_tp=0) -> dv_dplan_set:
+    """Level 1 as device plans (include/dv.h): one remap plan per route piece leaving this block."""
+    carr = cache_array(dst_caches)
+    sarr = endpoint_array(signals) if signals is not None else None
+    out = dv_dplan_set()
+    _call("dv_dplan_stream_out_direct", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage, my_micro,
+          my_tp, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, max_step, C.byref(out))
+    return out
+
+
 def dv_wait(ctx, ep: dv_endpoint, flag_slot, seq, stream=None):
     f = _fast or fast()
     if f:
@@ -781,9 +802,18 @@ def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_re
           _stream(stream))
 
 
-def dvt_fill_rows(c: dv_cache, seed, reg, plan: dv_dplan = None, step=0, t_start_ptr=0, t_end_ptr=0, stream=None):
-    _call("dvt_fill_rows", C.byref(c), seed, _reg_ct(reg), None if plan is None else C.byref(plan), step,
-          C.c_void_p(t_start_ptr), C.c_void_p(t_end_ptr), _stream(stream))
+def dvt_fill_rows(c: dv_cache, seed, reg, plan=None, step=0, t_start_ptr=0, t_end_ptr=0, stream=None):
+    """plan: None, a dv_dplan, a dv_dplan_set or a list of dv_dplan."""
+    if plan is None:
+        arr, n = None, 0
+    elif isinstance(plan, dv_dplan):
+        arr, n = C.byref(plan), 1
+    elif isinstance(plan, dv_dplan_set):
+        arr, n = (plan.plan if plan.n else None), plan.n
+    else:
+        arr, n = (dv_dplan * len(plan))(*plan), len(plan)
+    _call("dvt_fill_rows", C.byref(c), seed, _reg_ct(reg), arr, n, step, C.c_void_p(t_start_ptr),
+          C.c_void_p(t_end_ptr), _stream(stream))
 
 
 def dvt_fill_ring(c: dv_cache, seed, reg, doorbell_ptr, step, ticket_ptr, t_end_ptr=0, stream=None):

@@ -99,8 +99,7 @@ __global__ void k_fill(const FillParams p) {
 // the producer, include/dv_device.cuh).
 struct RowsParams {
   FillParams f;
-  dv_dplan plan;
-  int32_t use_plan;
+  dv_dplan_set plans;   // n == 0: no plan
   int32_t step;
   unsigned long long* t_start;
 };
@@ -132,8 +131,8 @@ __global__ void k_fill_rows(const RowsParams rp) {
              ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
     const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
     *reinterpret_cast<uint4*>(base + (int64_t)s * p.D + d0) = v;
-    if (rp.use_plan) {   // packet d0/8 of the row (FT6D-key destinations: packets S*16 bytes apart)
-      uint8_t* dst = dv_dplan_packet(&rp.plan, rp.step, kv, l, r, h, s, d0 / 8);
+    if (rp.plans.n) {   // packet d0/8 of the row (FT6D-key destinations: packets S*16 bytes apart)
+      uint8_t* dst = dv_dplan_set_packet(&rp.plans, rp.step, kv, l, r, h, s, d0 / 8);
       if (dst) *reinterpret_cast<uint4*>(dst) = v;
     }
   }
@@ -146,7 +145,7 @@ __global__ void k_fill_rows(const RowsParams rp) {
       atomicMax(p.t_end, t);
     }
   }
-  if (rp.use_plan) dv_dplan_release(&rp.plan, rp.step, gridDim.x * gridDim.y);
+  if (rp.plans.n) dv_dplan_set_release(&rp.plans, rp.step, gridDim.x * gridDim.y);
 }
 
 // Verifier: counts the words of a region that differ from the generator. Cache form (wire == NULL):
@@ -319,8 +318,8 @@ extern "C" dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_re
 }
 
 extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
-                                   const dv_dplan* plan, int32_t step, uint64_t* t_start, uint64_t* t_end,
-                                   void* stream) {
+                                   const dv_dplan* plans, int32_t n_plans, int32_t step, uint64_t* t_start,
+                                   uint64_t* t_end, void* stream) {
   RowsParams rp{};
   uint64_t slabs;
   DV_TRY(fill_params(c, DVT_FILL_HASH, seed, nullptr, 0, 1 << 30, region, &rp.f, &slabs));
@@ -329,12 +328,14 @@ extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_re
   if (!slabs) return fail(DV_EINVAL, "empty region");
   rp.f.t_end = (unsigned long long*)t_end;
   rp.t_start = (unsigned long long*)t_start;
-  if (plan) {
-    if (plan->row_bytes != c->head_dim * 2) return fail(DV_EMAP, "plan row size differs from the cache's");
-    rp.plan = *plan;
-    rp.use_plan = 1;
-    rp.step = step;
+  if (n_plans < 0 || n_plans > DV_DPLAN_SET_MAX || (n_plans && !plans))
+    return fail(DV_EINVAL, "dvt_fill_rows: %d plans (0 .. %d)", n_plans, DV_DPLAN_SET_MAX);
+  for (int i = 0; i < n_plans; ++i) {
+    if (plans[i].row_bytes != c->head_dim * 2) return fail(DV_EMAP, "plan row size differs from the cache's");
+    rp.plans.plan[i] = plans[i];
   }
+  rp.plans.n = n_plans;
+  rp.step = step;
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)slabs, 2);

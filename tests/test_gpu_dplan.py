@@ -11,6 +11,7 @@ import torch
 import kvgen
 import paper_2403_01876_b200 as dv
 from oracle import kvstream as ok
+from oracle import scenarios
 
 from gpu_util import ctx, flags, sentinel_like, to_dev, to_np
 
@@ -129,6 +130,60 @@ def test_fused_producer_remap_into_an_ft6d_cache():
     torch.cuda.synchronize()
     assert int(fl[0]) == 8
     assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
+
+
+def _blocks(setup):
+    for i in range(setup.n_stages):
+        for u in range(setup.n_micro):
+            yield i, u, setup.layer_bounds[i], setup.layer_bounds[i + 1], setup.req_bounds[u], setup.req_bounds[u + 1]
+
+
+@pytest.mark.parametrize("psplit,tsplit,preq,treq", [
+    ([0, 16, 32, 48, 64], [0, 13, 30, 47, 64], [0, 4], [0, 4]),        # C3 partitions (7 pieces)
+    ([0, 16, 32, 48, 64], [0, 13, 30, 47, 64], [0, 4], [0, 2, 4]),     # + batch split (14 pieces)
+    ([0, 9, 18, 27, 36, 45, 54, 62, 70], [0, 35, 70], [0, 2, 4], [0, 4]),  # merge
+])
+def test_fused_producer_disaggregation(psplit, tsplit, preq, treq):
+    """C3 through plan sets (dv_dplan_stream_out_direct): every prompt block's PRODUCER writes its
+    prompt K/V (positions [0, p)) and, through one plan per route piece, straight into the token
+    blocks' caches (other layer partition, max_seq, batch split) with one release per piece;
+    token caches == oracle.disaggregate, every signal at seq."""
+    H, D, p, Sp, St = 3, 16, 12, 16, 24
+    ps, ts = ok.Setup(psplit, preq, Sp), ok.Setup(tsplit, treq, St)
+    dps, dts = dv.Setup(psplit, preq, Sp), dv.Setup(tsplit, treq, St)
+    prompt, oprompt = {}, {}
+    for i, u, a, b, c0, c1 in _blocks(ps):
+        K, V = kvgen.kv5d_cache("hash", a, b - a, c0, c1 - c0, H, Sp, D, seed=SEED, valid_pos=(0, p))
+        k = torch.full((b - a, c1 - c0, H, Sp, D), -2, dtype=torch.int16, device="cuda")   # the producer writes [0, p)
+        v = torch.full_like(k, -2)
+        prompt[(i, u)] = (k, v, dv.cache(k, v, a, c0))
+        oprompt[(i, u)] = ok.Cache(K, V, a, c0, H, Sp, D)
+    token, otoken = {}, {}
+    for j, w, a, b, c0, c1 in _blocks(ts):
+        k = sentinel_like((b - a, c1 - c0, H, St, D))
+        v = sentinel_like((b - a, c1 - c0, H, St, D))
+        token[(j, w)] = (k, v, dv.cache(k, v, a, c0))
+        otoken[(j, w)] = ok.Cache(*kvgen.sentinel_cache(b - a, c1 - c0, H, St, D), a, c0, H, St, D)
+    reg = dv.region(psplit[0], psplit[-1], preq[0], preq[-1], 0, p)
+    dcs = [token[(j, w)][2] for j, w, *_ in _blocks(ts)]
+    nblk_p, nblk_t = ps.n_stages * ps.n_micro, ts.n_stages * ts.n_micro
+    sigf = flags(nblk_t * nblk_p)
+    sig = [dv.endpoint_of(sigf[:1], sigf[kk * nblk_p:(kk + 1) * nblk_p]) for kk in range(nblk_t)]
+    torch.cuda.synchronize()
+    n_pieces = 0
+    for i, u, a, b, c0, c1 in _blocks(ps):
+        pset = dv.dv_dplan_stream_out_direct(ctx(), prompt[(i, u)][2], reg, dps, i, u, dts, dcs, sig, seq=1)
+        n_pieces += pset.n
+        dv.dvt_fill_rows(prompt[(i, u)][2], SEED, dv.region(a, b, c0, c1, 0, p), pset, 0)
+    torch.cuda.synchronize()
+    assert n_pieces == len(ok.route(ps, ts, (psplit[0], psplit[-1], preq[0], preq[-1], 0, p), H, D, 2))
+    scenarios.disaggregate(oprompt, ps, otoken, ts, p)
+    for key, (k, v, _) in token.items():
+        assert np.array_equal(to_np(k), otoken[key].K) and np.array_equal(to_np(v), otoken[key].V), key
+    # every (token block, prompt block) pair that shares a piece got its release
+    for pc in ok.route(ps, ts, (psplit[0], psplit[-1], preq[0], preq[-1], 0, p), H, D, 2):
+        kk = pc.dst_stage * ts.n_micro + pc.dst_micro
+        assert int(sigf[kk * nblk_p + pc.src_stage * ps.n_micro + pc.src_micro]) == 1
 
 
 def test_dplan_validation():

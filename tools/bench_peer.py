@@ -586,6 +586,54 @@ class C3:
             dv.dv_stream_out_direct(self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), self.ps, i,
                                     0, self.ts, dst, self.sigs, seq=self.seq, xfer=xfer, stream=self.sp)
 
+    def producer_forms(self, steps=2):
+        """The hand-off with the PRODUCER in the loop (the prompt pass writing each layer's K/V --
+        here the test library's vectorised writer dvt_fill_rows): 'separate' = producer, then
+        dv_stream_out_direct per layer; 'fused' = the producer stores every row into its own cache
+        AND, through a plan set per layer (dv_dplan_stream_out_direct: one plan per route piece),
+        into the token GPUs' caches, releasing their flags itself (include/dv.h device plans).
+        Token caches reset before and verified word by word after each form."""
+        env = self.env
+        out = {}
+        sets = {}
+        if self.is_prompt:
+            i = self.i
+            for layer in range(self.pb[i], self.pb[i + 1]):
+                sets[layer] = dv.dv_dplan_stream_out_direct(
+                    self.ctx, self.pc, dv.region(layer, layer + 1, 0, self.b, 0, self.p), self.ps, i, 0, self.ts,
+                    self.caches, self.sigs, seq=1)
+
+        def run(fused):
+            self.seq += 1
+            if not self.is_prompt:
+                return
+            for layer in range(self.pb[self.i], self.pb[self.i + 1]):
+                reg = dv.region(layer, layer + 1, 0, self.b, 0, self.p)
+                if fused:
+                    st = sets[layer]
+                    for q in range(st.n):
+                        st.plan[q].seq = self.seq
+                    dv.dvt_fill_rows(self.pc, SEED_C3, reg, st, 0, stream=self.sp)
+                else:
+                    dv.dvt_fill_rows(self.pc, SEED_C3, reg, None, 0, stream=self.sp)
+                    dv.dv_stream_out_direct(self.ctx, self.pc, reg, self.ps, self.i, 0, self.ts, self.caches, self.sigs,
+                                            seq=self.seq, stream=self.sp)
+        for name, fused in (("separate", False), ("fused", True)):
+            if self.is_token:
+                self.tk.fill_(-1)
+                self.tv.fill_(-1)
+            env.barrier()
+            run(fused)                                    # warm-up
+            ms = _timed(env, lambda fused=fused: run(fused), steps)
+            out[name] = {"ms_per_handoff_with_producer": ms / steps,
+                         "gbs_per_prompt_gpu": env.max(self.my_prompt_bytes()) * steps / ms / 1e6,
+                         "parity": self.verify()}
+        out["how"] = ("prompt layer by layer: producer + dv_stream_out_direct vs the producer fused with the "
+                      "hand-off through plan sets; device time per hand-off, max over ranks. The test producer "
+                      "hashes every word (ALU-bound), so it dominates both arms; the difference is the hand-off "
+                      "the fused form no longer runs as its own pass")
+        return out
+
     def ft6d_forms(self, steps=2):
         """NEXT-1 over the link: the hand-off into FasterTransformer token caches (6-D key: every
         key packet transposed on the way), with the shared-memory tile transpose (the automatic
@@ -689,6 +737,11 @@ def c3_suite(ctx, env, steps=3, peak=None, peak_src=None, nccl=True):
                       "steps": steps, "roofline": _roof(per_gpu, peak, peak_src, env),
                       "ideal_ms_at_peak": (env.max(c.my_prompt_bytes()) / peak / 1e6) if peak else None}
     out["parity"] = c.verify()
+    try:
+        out["producer_fused_vs_separate"] = c.producer_forms()
+    except Exception as e:   # noqa: BLE001 -- reported; the other C3 numbers still print
+        out["producer_fused_vs_separate"] = {"error": f"{type(e).__name__}: {e}"}
+        env.barrier()
     try:
         # the same hand-off by the copy engine (DV_XFER_STAGED: one 2-D DMA per (K or V, layer,
         # request) over the heads, runs of p*D*e bytes) -- SM stores vs copy engine over the link
