@@ -473,6 +473,10 @@ DV_API dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache
  * disjoint: at most one plan takes a packet) and ends with dv_dplan_set_release. At most
  * DV_DPLAN_SET_MAX pieces (DV_ENOTSUP beyond); n == 0 when no piece leaves this block. */
 #define DV_DPLAN_SET_MAX 8
+/* (dv_dplan_stream_out: the inbox form of the same -- each piece's rows go to inboxes[destination
+ * block] at the piece's wire offset, releasing slot = this block's flat index, as dv_stream_out;
+ * the receiver runs dv_stream_in. Ring inboxes are refused (DV_EINVAL): a producer cannot wait for
+ * a credit.) */
 typedef struct dv_dplan_set {
   int32_t n;
   int32_t reserved;
@@ -483,6 +487,10 @@ DV_API dv_status dv_dplan_stream_out_direct(dv_ctx* ctx, const dv_cache* src, co
                                             int32_t my_tp, const dv_setup* dst_setup,
                                             const dv_cache* dst_caches, const dv_endpoint* signals,
                                             int32_t n_dst, uint64_t seq, int32_t max_step, dv_dplan_set* out);
+DV_API dv_status dv_dplan_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                                     const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
+                                     int32_t my_tp, const dv_setup* dst_setup, const dv_endpoint* inboxes,
+                                     int32_t n_inboxes, uint64_t seq, dv_dplan_set* out);
 
 /* ---- SM partitions: an SM budget for streaming (NEXT-2; DESIGN.md §6
  * "SM partitions") ----------------------------------------------------------------------------

@@ -168,6 +168,9 @@ _SIGS = {
     "dv_dplan_stream_out_direct": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32,
                                              C.c_int32, C.c_int32, P(dv_setup), P(dv_cache), P(dv_endpoint),
                                              C.c_int32, C.c_uint64, C.c_int32, P(dv_dplan_set)]),
+    "dv_dplan_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32, C.c_int32,
+                                      C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32, C.c_uint64,
+                                      P(dv_dplan_set)]),
     "dv_dplan_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint), C.c_int32,
                                  C.c_uint64, C.c_int32, P(dv_dplan)]),
     "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
@@ -669,6 +672,16 @@ def dv_dplan_stream_out_direct(ctx, src: dv_cache, reg: dv_region, src_setup: Se
     out = dv_dplan_set()
     _call("dv_dplan_stream_out_direct", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage, my_micro,
           my_tp, C.byref(dst_setup.c), carr, sarr, len(dst_caches), seq, max_step, C.byref(out))
+    return out
+
+
+def dv_dplan_stream_out(ctx, src: dv_cache, reg: dv_region, src_setup: Setup, my_stage, my_micro, dst_setup: Setup,
+                        inboxes, seq=0, my_tp=0) -> dv_dplan_set:
+    """Level 1 as device plans, inbox form (include/dv.h): one scatter plan per route piece."""
+    arr = endpoint_array(inboxes)
+    out = dv_dplan_set()
+    _call("dv_dplan_stream_out", ctx.h, C.byref(src), _reg_ct(reg), C.byref(src_setup.c), my_stage, my_micro, my_tp,
+          C.byref(dst_setup.c), arr, len(inboxes), seq, C.byref(out))
     return out
 
 

@@ -1934,6 +1934,33 @@ dv_status dv_dplan_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_
   return DV_OK;
 }
 
+dv_status dv_dplan_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
+                              const dv_setup* src_setup, int32_t my_stage, int32_t my_micro, int32_t my_tp,
+                              const dv_setup* dst_setup, const dv_endpoint* inboxes, int32_t n_inboxes,
+                              uint64_t seq, dv_dplan_set* out) {
+  DV_TRY(check_ctx(ctx));
+  if (!out) return fail(DV_EINVAL, "NULL plan set");
+  std::vector<dv_piece> ps;
+  DV_TRY(my_pieces(src_setup, dst_setup, region, src, my_stage, my_micro, my_tp, true, &ps));
+  if (!inboxes && !ps.empty()) return fail(DV_EINVAL, "NULL inboxes");
+  if (ps.size() > DV_DPLAN_SET_MAX)
+    return fail(DV_ENOTSUP, "%zu route pieces leave this block (a plan set holds %d)", ps.size(),
+                DV_DPLAN_SET_MAX);
+  const int32_t slot = flat_block(src_setup, my_stage, my_micro, my_tp);
+  dv_dplan_set set;
+  memset(&set, 0, sizeof set);
+  for (auto& p : ps) {
+    const int32_t k = flat_block(dst_setup, p.dst_stage, p.dst_micro, p.dst_tp);
+    if (k >= n_inboxes) return fail(DV_EINVAL, "inbox %d missing (n_inboxes %d)", k, n_inboxes);
+    if (has_ring(&inboxes[k])) return fail(DV_EINVAL, "device plans do not write ring inboxes (credits)");
+    const dv_region pr = piece_region(p);
+    DV_TRY(dv_dplan_scatter(ctx, src, &pr, &inboxes[k], p.dst_wire_off, 0, slot, seq, 0, &set.plan[set.n]));
+    ++set.n;
+  }
+  *out = set;
+  return DV_OK;
+}
+
 // ---- completion -----------------------------------------------------------------------------
 dv_status dv_wait(dv_ctx* ctx, const dv_endpoint* ep, int32_t flag_slot, uint64_t seq,
                   void* stream) {

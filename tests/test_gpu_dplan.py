@@ -143,7 +143,8 @@ def _blocks(setup):
     ([0, 16, 32, 48, 64], [0, 13, 30, 47, 64], [0, 4], [0, 2, 4]),     # + batch split (14 pieces)
     ([0, 9, 18, 27, 36, 45, 54, 62, 70], [0, 35, 70], [0, 2, 4], [0, 4]),  # merge
 ])
-def test_fused_producer_disaggregation(psplit, tsplit, preq, treq):
+@pytest.mark.parametrize("form", ["direct", "inbox"])
+def test_fused_producer_disaggregation(psplit, tsplit, preq, treq, form):
     """C3 through plan sets (dv_dplan_stream_out_direct): every prompt block's PRODUCER writes its
     prompt K/V (positions [0, p)) and, through one plan per route piece, straight into the token
     blocks' caches (other layer partition, max_seq, batch split) with one release per piece;
@@ -171,19 +172,31 @@ def test_fused_producer_disaggregation(psplit, tsplit, preq, treq):
     sig = [dv.endpoint_of(sigf[:1], sigf[kk * nblk_p:(kk + 1) * nblk_p]) for kk in range(nblk_t)]
     torch.cuda.synchronize()
     n_pieces = 0
+    if form == "inbox":   # the paper's mailbox form: plans into inboxes, receivers run dv_stream_in
+        eps, keep = [], []
+        for j, w, a, b, c0, c1 in _blocks(ts):
+            keep.append((sentinel_like(((b - a) * (c1 - c0) * H * p * D * 2,)), flags(nblk_p)))
+            eps.append(dv.endpoint_of(*keep[-1]))
+        torch.cuda.synchronize()
     for i, u, a, b, c0, c1 in _blocks(ps):
-        pset = dv.dv_dplan_stream_out_direct(ctx(), prompt[(i, u)][2], reg, dps, i, u, dts, dcs, sig, seq=1)
+        if form == "direct":
+            pset = dv.dv_dplan_stream_out_direct(ctx(), prompt[(i, u)][2], reg, dps, i, u, dts, dcs, sig, seq=1)
+        else:
+            pset = dv.dv_dplan_stream_out(ctx(), prompt[(i, u)][2], reg, dps, i, u, dts, eps, seq=1)
         n_pieces += pset.n
         dv.dvt_fill_rows(prompt[(i, u)][2], SEED, dv.region(a, b, c0, c1, 0, p), pset, 0)
+    if form == "inbox":
+        for kk, (j, w, *_r) in enumerate(_blocks(ts)):
+            dv.dv_stream_in(ctx(), token[(j, w)][2], reg, dps, dts, j, w, eps[kk], 1)
     torch.cuda.synchronize()
     assert n_pieces == len(ok.route(ps, ts, (psplit[0], psplit[-1], preq[0], preq[-1], 0, p), H, D, 2))
     scenarios.disaggregate(oprompt, ps, otoken, ts, p)
     for key, (k, v, _) in token.items():
         assert np.array_equal(to_np(k), otoken[key].K) and np.array_equal(to_np(v), otoken[key].V), key
-    # every (token block, prompt block) pair that shares a piece got its release
-    for pc in ok.route(ps, ts, (psplit[0], psplit[-1], preq[0], preq[-1], 0, p), H, D, 2):
-        kk = pc.dst_stage * ts.n_micro + pc.dst_micro
-        assert int(sigf[kk * nblk_p + pc.src_stage * ps.n_micro + pc.src_micro]) == 1
+    if form == "direct":   # every (token block, prompt block) pair that shares a piece got its release
+        for pc in ok.route(ps, ts, (psplit[0], psplit[-1], preq[0], preq[-1], 0, p), H, D, 2):
+            kk = pc.dst_stage * ts.n_micro + pc.dst_micro
+            assert int(sigf[kk * nblk_p + pc.src_stage * ps.n_micro + pc.src_micro]) == 1
 
 
 def test_dplan_validation():
