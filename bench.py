@@ -275,7 +275,7 @@ def run_ours(args):
     # achieved figure below is a lower bound)
     mean_kernel_ms = elapsed_ms / max(1, launches)
     peaks = _peaks()
-    pcie_peak = extras.get("pcie_dma_d2h_gbs")
+    pcie_peak = extras.get("pcie_dma_d2h_peak_gbs")
     if rank != 0:
         dv.dv_destroy(ctx)
         if world > 1:
@@ -315,8 +315,8 @@ def run_ours(args):
         "peak_same_size_dma": extras.get("pcie_dma_d2h_same_size_gbs"),
         "algorithmic_bytes_per_launch": STEP_BYTES,
         "peak_nominal": PCIE_NOMINAL_GBS, "frac_nominal": roof["achieved"] / PCIE_NOMINAL_GBS,
-        "peak_source": "in-run cudaMemcpyAsync D2H of 256 MiB pinned (copy engine), this box; "
-                       "PCIe Gen5 x16 nominal 64 GB/s"})
+        "peak_source": "in-run copy-engine D2H into pinned memory, this box: the best of 3 trials of 256 MiB "
+                       "copies and of back-to-back step-sized (6.55 MB) copies; PCIe Gen5 x16 nominal 64 GB/s"})
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -379,7 +379,7 @@ def _ncu_traffic(name="decoupled"):
     source names the file and the sha256 of its content (so the line pins the exact capture)."""
     import csv
     import hashlib
-    files = {"decoupled": ["r02b_io_counters.csv", "r02_io_counters.csv", "r01g_io_counters.csv"],
+    files = {"decoupled": ["r02d_io_counters.csv", "r02b_io_counters.csv", "r02_io_counters.csv", "r01g_io_counters.csv"],
              "fused": ["r02_io_counters_fused.csv", "r01_io_counters_final.csv"]}[name]
     for fn in files:
         path = os.path.join(ROOT, "profiles", fn)
@@ -586,13 +586,18 @@ def run_extras(dv, ctx, cache, stream, args, pos_of):
     n = 256 << 20
     hb = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     db = torch.empty(n, dtype=torch.uint8, device="cuda")
-    ms = _time(lambda: hb.copy_(db, non_blocking=True), stream, 5)
+    # best of 3 trials of 5 copies each: the link's rate varies by a few % run to run under the
+    # power cap, and a peak is the best observed, not one sample
+    ms = min(_time(lambda: hb.copy_(db, non_blocking=True), stream, 5) for _ in range(3))
     ex["pcie_dma_d2h_gbs"] = n / ms / 1e6
-    ms = _time(lambda: db.copy_(hb, non_blocking=True), stream, 5)
+    ms = min(_time(lambda: db.copy_(hb, non_blocking=True), stream, 5) for _ in range(3))
     ex["pcie_dma_h2d_gbs"] = n / ms / 1e6
     # the same 6.55 MB per transfer as one token step, back to back (fixed costs included)
-    ms = _time(lambda: hb[:STEP_BYTES].copy_(db[:STEP_BYTES], non_blocking=True), stream, 100)
+    ms = min(_time(lambda: hb[:STEP_BYTES].copy_(db[:STEP_BYTES], non_blocking=True), stream, 100)
+             for _ in range(3))
     ex["pcie_dma_d2h_same_size_gbs"] = STEP_BYTES / ms / 1e6
+    # the roofline's denominator: the best D2H rate the copy engine showed in this run (either size)
+    ex["pcie_dma_d2h_peak_gbs"] = max(ex["pcie_dma_d2h_gbs"], ex["pcie_dma_d2h_same_size_gbs"])
     del hb, db
 
     # token step: fused vs staged (host), and pack-only into HBM

@@ -38,7 +38,8 @@ DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region
                                uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
 
 /* A vectorised synthetic PRODUCER (kind HASH words of `region` of KV5D cache `c`, 16-byte stores,
- * one CTA of 128 threads per (layer, request, head) slab and kv). With `n_plans` plans (include/dv.h
+ * one thread per 16-byte chunk in a grid-stride loop of at most 4 x SMs CTAs of 256 threads -- the
+ * shape of a producer's grid, so few CTAs join the plans' release). With `n_plans` plans (include/dv.h
  * dv_dplan_*; <= DV_DPLAN_SET_MAX, disjoint regions, e.g. a dv_dplan_set) it also stores every
  * packet inside a plan's region at step `step` to that plan's destination and releases every
  * plan's flag from its last CTA -- the stream-out fused into the producer (include/dv_device.cuh

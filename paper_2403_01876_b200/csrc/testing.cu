@@ -3,6 +3,8 @@
 #include "../../include/dv_testing.h"
 #include "dv_internal.h"
 
+#include <algorithm>
+
 namespace dv {
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -101,6 +103,7 @@ struct RowsParams {
   FillParams f;
   dv_dplan_set plans;   // n == 0: no plan
   int32_t step;
+  int64_t slabs;        // (layer, request, head) slabs of the region
   unsigned long long* t_start;
 };
 __global__ void k_fill_rows(const RowsParams rp) {
@@ -111,19 +114,23 @@ __global__ void k_fill_rows(const RowsParams rp) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(rp.t_start, t);
   }
-  uint32_t slab = blockIdx.x;
-  const int h = p.h0 + (int)(slab % p.H);
-  slab /= p.H;
-  const int r = p.r0 + (int)(slab % p.nR);
-  const int l = p.l0 + (int)(slab / p.nR);
-  const int kv = blockIdx.y;
-  uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
-                   (int64_t)(h - p.hb) * p.s_h;
+  // grid-stride over every 16-byte chunk of the region: (kv, slab, position, chunk), chunk fastest
   const int cpr = p.D / 8;   // 16-byte chunks per row
-  const int64_t chunks = (int64_t)p.n * cpr;
-  for (int64_t i = threadIdx.x; i < chunks; i += blockDim.x) {
-    const int s = p.s0 + (int)(i / cpr);
-    const int d0 = (int)(i % cpr) * 8;
+  const int64_t per_slab = (int64_t)p.n * cpr;
+  const int64_t total = 2 * rp.slabs * per_slab;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ks = i / per_slab;              // kv * slabs + slab
+    const int64_t in_slab = i - ks * per_slab;
+    const int kv = (int)(ks / rp.slabs);
+    uint32_t slab = (uint32_t)(ks - (int64_t)kv * rp.slabs);
+    const int h = p.h0 + (int)(slab % p.H);
+    slab /= p.H;
+    const int r = p.r0 + (int)(slab % p.nR);
+    const int l = p.l0 + (int)(slab / p.nR);
+    const int s = p.s0 + (int)(in_slab / cpr);
+    const int d0 = (int)(in_slab % cpr) * 8;
+    uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
+                     (int64_t)(h - p.hb) * p.s_h;
     uint32_t w[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -145,7 +152,7 @@ __global__ void k_fill_rows(const RowsParams rp) {
       atomicMax(p.t_end, t);
     }
   }
-  if (rp.plans.n) dv_dplan_set_release(&rp.plans, rp.step, gridDim.x * gridDim.y);
+  if (rp.plans.n) dv_dplan_set_release(&rp.plans, rp.step, gridDim.x);
 }
 
 // Verifier: counts the words of a region that differ from the generator. Cache form (wire == NULL):
@@ -336,10 +343,18 @@ extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_re
   }
   rp.plans.n = n_plans;
   rp.step = step;
+  rp.slabs = (int64_t)slabs;
+  // one thread per 16-byte chunk, 256-thread CTAs, at most 4 CTAs per SM (a producer's grid):
+  // few CTAs take part in the plans' release ticket chains
+  const int64_t chunks = 2 * (int64_t)slabs * rp.f.n * (c->head_dim / 8);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, 4 * (int64_t)nsm));
   (void)cudaGetLastError();
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)slabs, 2);
-  cfg.blockDim = dim3(128);
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
   cfg.stream = (cudaStream_t)stream;
   DV_CUDA(cudaLaunchKernelEx(&cfg, k_fill_rows, rp));
   DV_CUDA(cudaGetLastError());
