@@ -6,7 +6,9 @@ Both arms use the same vectorised producer (dvt_fill_rows). Stamps (%globaltimer
 first CTA start (t_start), its last CTA's stores done (t_end), the flag release (library trace /
 the plan's trace). Reported per arm: start -> flag (the whole "write the layer's K/V and make it
 visible at the destination") and, for the separate arm, end -> flag (the usual writer-end metric).
-LOADED=1: a bf16 GEMM loop on a low-priority stream, producer + stream-out on a high-priority one."""
+LOADED=1: a bf16 GEMM loop on a low-priority stream, producer + stream-out on a high-priority one;
+PART=k: the producer and the stream-out on a k-SM partition (dv_partition_create), the GEMM on the
+rest."""
 import json
 import os
 import sys
@@ -26,8 +28,13 @@ SEED = 20240305
 N = 1040
 LOADED = os.environ.get("LOADED") == "1"
 lo_pr, hi_pr = torch.cuda.Stream.priority_range()
-st = torch.cuda.Stream(priority=hi_pr)
-gst = torch.cuda.Stream(priority=lo_pr)
+PART = int(os.environ.get("PART", "0"))   # PART=k: producer + stream-out on a k-SM partition, GEMM on the rest
+if PART:
+    part = dv.dv_partition_create(0, PART, hi_pr)
+    st, gst = torch.cuda.ExternalStream(part.streaming), torch.cuda.ExternalStream(part.compute)
+else:
+    st = torch.cuda.Stream(priority=hi_pr)
+    gst = torch.cuda.Stream(priority=lo_pr)
 sp = st.cuda_stream
 if LOADED:
     ga = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
@@ -96,4 +103,5 @@ def run(dst_host):
 
 for rep in range(2):
     for host in (True, False):
-        print(json.dumps({"rep": rep, "dst": "host" if host else "hbm", "loaded": LOADED, **run(host)}), flush=True)
+        print(json.dumps({"rep": rep, "dst": "host" if host else "hbm", "loaded": LOADED, "sm_partition": PART or None,
+                          **run(host)}), flush=True)
