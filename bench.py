@@ -514,6 +514,9 @@ def _latency_fused_producer(dv, ctx, cache, stream, n=440):
             res[arm] = {"start_to_flag_p50_us": a[len(a) // 2], "start_to_flag_p99_us": a[int(len(a) * 0.99)],
                         "producer_end_to_flag_p50_us": b[len(b) // 2], "n": len(a)}
         out["host" if dst_host else "hbm"] = res
+        torch.cuda.synchronize()
+        for pl in plans:
+            dv.dv_dplan_free(ctx, pl)
     return out
 
 

@@ -465,6 +465,11 @@ DV_API dv_status dv_dplan_remap(dv_ctx* ctx, const dv_cache* src, const dv_cache
                                 const dv_region* region, const dv_endpoint* signal,
                                 int32_t flag_slot, uint64_t seq, int32_t max_step, dv_dplan* out);
 
+/* Hand a plan's ticket back to the context (the plan then releases nothing): after the last
+ * producer launch using it has completed. Plans never freed keep their tickets until dv_destroy;
+ * a context has 65,536 plan / captured-launch tickets (DV_ENOMEM beyond). */
+DV_API dv_status dv_dplan_free(dv_ctx* ctx, dv_dplan* plan);
+
 /* Level 1 as device plans (dv_stream_out_direct fused into the producer; §4.2.1 the
  * prompt -> token hand-off, :286 ring replication): route `region` out of block (my_stage,
  * my_micro, my_tp) of src_setup into dst_setup's caches, one remap plan per route piece leaving
@@ -487,6 +492,7 @@ DV_API dv_status dv_dplan_stream_out_direct(dv_ctx* ctx, const dv_cache* src, co
                                             int32_t my_tp, const dv_setup* dst_setup,
                                             const dv_cache* dst_caches, const dv_endpoint* signals,
                                             int32_t n_dst, uint64_t seq, int32_t max_step, dv_dplan_set* out);
+DV_API dv_status dv_dplan_set_free(dv_ctx* ctx, dv_dplan_set* set);   /* dv_dplan_free of every plan */
 DV_API dv_status dv_dplan_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region* region,
                                      const dv_setup* src_setup, int32_t my_stage, int32_t my_micro,
                                      int32_t my_tp, const dv_setup* dst_setup, const dv_endpoint* inboxes,

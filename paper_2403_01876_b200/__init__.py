@@ -171,6 +171,8 @@ _SIGS = {
     "dv_dplan_stream_out": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_region), P(dv_setup), C.c_int32, C.c_int32,
                                       C.c_int32, P(dv_setup), P(dv_endpoint), C.c_int32, C.c_uint64,
                                       P(dv_dplan_set)]),
+    "dv_dplan_free": (C.c_int, [C.c_void_p, P(dv_dplan)]),
+    "dv_dplan_set_free": (C.c_int, [C.c_void_p, P(dv_dplan_set)]),
     "dv_dplan_remap": (C.c_int, [C.c_void_p, P(dv_cache), P(dv_cache), P(dv_region), P(dv_endpoint), C.c_int32,
                                  C.c_uint64, C.c_int32, P(dv_dplan)]),
     "dvt_tune": (C.c_int, [C.c_char_p, C.c_int64]),
@@ -610,6 +612,14 @@ def dv_dplan_scatter(ctx, src: dv_cache, reg: dv_region, dst: dv_endpoint, dst_o
     _call("dv_dplan_scatter", ctx.h, C.byref(src), _reg_ct(reg), C.byref(dst), dst_off, dst_step_bytes, flag_slot, seq,
           max_step, C.byref(p))
     return p
+
+
+def dv_dplan_free(ctx, plan):
+    """Hand back a plan's (dv_dplan) or a plan set's (dv_dplan_set) tickets: after its last launch."""
+    if isinstance(plan, dv_dplan_set):
+        _call("dv_dplan_set_free", ctx.h, C.byref(plan))
+    else:
+        _call("dv_dplan_free", ctx.h, C.byref(plan))
 
 
 def dv_dplan_remap(ctx, src: dv_cache, dst: dv_cache, reg: dv_region, signal: dv_endpoint = None, flag_slot=-1, seq=0,

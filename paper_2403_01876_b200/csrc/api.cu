@@ -1666,6 +1666,14 @@ dv_status dv_scatter_dyn(dv_ctx* ctx, const dv_cache* src, const dv_region* regi
 namespace dv {
 // The plan's own ticket: taken from the never-recycled range (like a graph-captured launch).
 static dv_status dplan_ticket(dv_ctx* ctx, uint32_t** out) {
+  {
+    std::lock_guard<std::mutex> lk(ctx->dplan_mu);
+    if (!ctx->dplan_free.empty()) {
+      *out = ctx->dplan_free.back();
+      ctx->dplan_free.pop_back();
+      return DV_OK;
+    }
+  }
   const uint32_t g = ctx->next_graph_ticket.fetch_add(1);
   if (g >= dv_ctx::kGraphTickets)
     return fail(DV_ENOMEM, "more than %u device plans / captured publishing launches in this context",
@@ -1686,6 +1694,29 @@ static void dplan_region(dv_dplan* p, const dv_region& reg, const dv_cache* src)
 }
 }  // namespace dv
 extern "C" {
+
+dv_status dv_dplan_free(dv_ctx* ctx, dv_dplan* plan) {
+  DV_TRY(check_ctx(ctx));
+  if (!plan) return fail(DV_EINVAL, "NULL plan");
+  if (plan->ticket) {
+    const uint32_t* lo = ctx->tickets + dv_ctx::kTickets;
+    if (plan->ticket < lo || plan->ticket >= lo + dv_ctx::kGraphTickets)
+      return fail(DV_EINVAL, "the plan's ticket is not one of this context's plan tickets");
+    std::lock_guard<std::mutex> lk(ctx->dplan_mu);
+    ctx->dplan_free.push_back(plan->ticket);
+  }
+  plan->ticket = nullptr;
+  plan->flag = nullptr;   // a freed plan releases nothing
+  return DV_OK;
+}
+
+dv_status dv_dplan_set_free(dv_ctx* ctx, dv_dplan_set* set) {
+  DV_TRY(check_ctx(ctx));
+  if (!set) return fail(DV_EINVAL, "NULL plan set");
+  for (int i = 0; i < set->n && i < DV_DPLAN_SET_MAX; ++i) DV_TRY(dv_dplan_free(ctx, &set->plan[i]));
+  set->n = 0;
+  return DV_OK;
+}
 
 dv_status dv_dplan_scatter(dv_ctx* ctx, const dv_cache* src, const dv_region* region, const dv_endpoint* dst,
                            uint64_t dst_off, uint64_t dst_step_bytes, int32_t flag_slot, uint64_t seq,
@@ -1926,8 +1957,13 @@ dv_status dv_dplan_stream_out_direct(dv_ctx* ctx, const dv_cache* src, const dv_
     const int32_t k = flat_block(dst_setup, p.dst_stage, p.dst_micro, p.dst_tp);
     if (k >= n_dst) return fail(DV_EINVAL, "destination %d missing (n_dst %d)", k, n_dst);
     const dv_region pr = piece_region(p);
-    DV_TRY(dv_dplan_remap(ctx, src, &dst_caches[k], &pr, signals ? &signals[k] : nullptr, slot, seq, max_step,
-                          &set.plan[set.n]));
+    const dv_status st = dv_dplan_remap(ctx, src, &dst_caches[k], &pr, signals ? &signals[k] : nullptr, slot, seq,
+                                        max_step, &set.plan[set.n]);
+    if (st != DV_OK) {   // hand back the tickets of the plans made so far (the error message stays)
+      const std::string msg = dv_last_error();
+      (void)dv_dplan_set_free(ctx, &set);
+      return fail(st, "%s", msg.c_str());
+    }
     ++set.n;
   }
   *out = set;
@@ -1954,7 +1990,13 @@ dv_status dv_dplan_stream_out(dv_ctx* ctx, const dv_cache* src, const dv_region*
     if (k >= n_inboxes) return fail(DV_EINVAL, "inbox %d missing (n_inboxes %d)", k, n_inboxes);
     if (has_ring(&inboxes[k])) return fail(DV_EINVAL, "device plans do not write ring inboxes (credits)");
     const dv_region pr = piece_region(p);
-    DV_TRY(dv_dplan_scatter(ctx, src, &pr, &inboxes[k], p.dst_wire_off, 0, slot, seq, 0, &set.plan[set.n]));
+    const dv_status st = dv_dplan_scatter(ctx, src, &pr, &inboxes[k], p.dst_wire_off, 0, slot, seq, 0,
+                                          &set.plan[set.n]);
+    if (st != DV_OK) {
+      const std::string msg = dv_last_error();
+      (void)dv_dplan_set_free(ctx, &set);
+      return fail(st, "%s", msg.c_str());
+    }
     ++set.n;
   }
   *out = set;

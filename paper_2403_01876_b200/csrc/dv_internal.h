@@ -194,6 +194,9 @@ struct dv_ctx {
   static constexpr uint32_t kTickets = 65536;
   static constexpr uint32_t kGraphTickets = 65536;  // tickets array: kTickets + kGraphTickets
   std::atomic<uint32_t> next_graph_ticket{0};
+  // device plans' tickets handed back by dv_dplan_free (reused before the range grows)
+  std::mutex dplan_mu;
+  std::vector<uint32_t*> dplan_free;
   // set once a decoupled transfer has published on flag_st: later publishes to pinned-host flags
   // from other streams are ordered after flag_st so a slot's flag stays monotone across modes
   std::atomic<bool> decoupled_used{false};

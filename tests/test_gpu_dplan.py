@@ -216,3 +216,30 @@ def test_dplan_validation():
     ring = dv.endpoint_of(buf, flags(1), n_slots=2, slot_bytes=nb)
     with pytest.raises(dv.DVError):
         dv.dv_dplan_scatter(ctx(), c, reg, ring, 0)
+
+
+def test_dplan_free_returns_tickets():
+    """dv_dplan_free hands the plan's ticket back: the next plan reuses it, 70,000 make / free cycles
+    stay inside the context's 65,536 plan tickets, and a freed plan's producer releases nothing
+    (its rows still land)."""
+    L, B, H, S, D = 1, 1, 2, 16, 64
+    k, v, c, o = _cache(L, B, H, S, D)
+    reg = (0, 1, 0, 1, 3, 4)
+    nb = ok.region_bytes(*reg, H, D, 2)
+    buf = sentinel_like((nb // 2,))
+    fl = flags(1)
+    ep = dv.endpoint_of(buf, fl)
+    p1 = dv.dv_dplan_scatter(ctx(), c, dv.region(*reg), ep, 0, flag_slot=0, seq=5)
+    t1 = p1.ticket
+    dv.dv_dplan_free(ctx(), p1)
+    assert not p1.ticket and not p1.flag
+    p2 = dv.dv_dplan_scatter(ctx(), c, dv.region(*reg), ep, 0, flag_slot=0, seq=5)
+    assert p2.ticket == t1
+    for _ in range(70_000):
+        q = dv.dv_dplan_scatter(ctx(), c, dv.region(*reg), ep, 0, flag_slot=0, seq=5)
+        dv.dv_dplan_free(ctx(), q)
+    dv.dv_dplan_free(ctx(), p2)
+    torch.cuda.synchronize()
+    dv.dvt_fill_rows(c, SEED, dv.region(*reg), p2, 0)   # freed: rows land, no release
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(buf), ok.pack(o, reg)) and int(fl[0]) == 0

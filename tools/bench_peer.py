@@ -370,6 +370,8 @@ class C5:
                         "n": len(us)}
         out["bytes"] = self.layer_bytes_tok
         out["release_scope"] = "system" if plans[0].sys_scope else "gpu"
+        for pl in plans:
+            dv.dv_dplan_free(self.ctx, pl)
         return out
 
     def pingpong(self, iters=300):
@@ -628,6 +630,9 @@ class C3:
             out[name] = {"ms_per_handoff_with_producer": ms / steps,
                          "gbs_per_prompt_gpu": env.max(self.my_prompt_bytes()) * steps / ms / 1e6,
                          "parity": self.verify()}
+        torch.cuda.synchronize()
+        for st in sets.values():
+            dv.dv_dplan_free(self.ctx, st)
         out["how"] = ("prompt layer by layer: producer + dv_stream_out_direct vs the producer fused with the "
                       "hand-off through plan sets; device time per hand-off, max over ranks. The test producer "
                       "hashes every word (ALU-bound), so it dominates both arms; the difference is the hand-off "
