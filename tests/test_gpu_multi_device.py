@@ -100,6 +100,60 @@ def test_peer_stream_two_devices(ctxs, form):
     assert int(flags.max()) == 7
 
 
+def test_fused_producer_into_the_other_gpu(ctxs):
+    """Device plans across GPUs: the producer on GPU 0 (dvt_fill_rows) stores its rows into its
+    own cache and, through plan sets (dv_dplan_stream_out_direct), straight into GPU 1's caches of
+    another layer partition and max_seq over NVLink, releasing GPU 1's flags (system scope); GPU 1's
+    stream waits for every piece, then its caches == oracle.stream."""
+    L, B, H, S, D, S2, p = 6, 2, 4, 40, 32, 64, 33
+    seed = 503
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=seed, valid_pos=(0, p))
+    ps, ts = dv.Setup([0, 3, 6], [0, B], S), dv.Setup([0, 2, 4, 6], [0, B], S2)
+    reg = dv.region(0, L, 0, B, 0, p)
+    src = []
+    for i, (a, b) in enumerate(((0, 3), (3, 6))):
+        k = torch.full((b - a, B, H, S, D), -2, dtype=torch.int16, device="cuda:0")
+        v = torch.full_like(k, -2)
+        src.append((k, v, dv.cache(k, v, a, 0)))
+    dst = []
+    for j, (a, b) in enumerate(((0, 2), (2, 4), (4, 6))):
+        k = torch.full((b - a, B, H, S2, D), -1, dtype=torch.int16, device=f"cuda:{G1}")
+        v = torch.full_like(k, -1)
+        dst.append((k, v, dv.cache(k, v, a, 0)))
+    flags = torch.zeros((3, 2), dtype=torch.int64, device=f"cuda:{G1}")
+    sigs = [dv.endpoint(dv.DV_EP_PEER, flags[j].data_ptr(), 16, flags[j].data_ptr(), 2, device=G1) for j in range(3)]
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(G1)
+    s0, s1 = torch.cuda.Stream(device=0), torch.cuda.Stream(device=G1)
+    sets = []
+    for i, (a, b) in enumerate(((0, 3), (3, 6))):
+        st = dv.dv_dplan_stream_out_direct(ctxs[0], src[i][2], reg, ps, i, 0, ts, [d[2] for d in dst], sigs, seq=9)
+        if G1 != 0:
+            assert all(st.plan[q].sys_scope for q in range(st.n))
+        sets.append(st)
+        with torch.cuda.device(0):
+            dv.dvt_fill_rows(src[i][2], seed, dv.region(a, b, 0, B, 0, p), st, 0, stream=s0.cuda_stream)
+    ep1 = [dv.endpoint(dv.DV_EP_DEVICE, flags[j].data_ptr(), 16, flags[j].data_ptr(), 2, device=G1) for j in range(3)]
+    for pc in dv.dv_route(ps, ts, reg, H, D, 2):
+        dv.dv_wait(ctxs[1], ep1[pc.dst_stage], pc.src_stage, 9, stream=s1)
+    snaps = []
+    with torch.cuda.stream(s1):
+        for j in range(3):
+            snaps.append((dst[j][0].clone(), dst[j][1].clone()))
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(G1)
+    odst = {}
+    for j, (a, b) in enumerate(((0, 2), (2, 4), (4, 6))):
+        Ks, Vs = kvgen.sentinel_cache(b - a, B, H, S2, D)
+        odst[(j, 0)] = ok.Cache(Ks, Vs, a, 0, H, S2, D)
+    osrc = {(0, 0): ok.Cache(K[:3], V[:3], 0, 0, H, S, D), (1, 0): ok.Cache(K[3:], V[3:], 3, 0, H, S, D)}
+    ok.stream(osrc, ok.Setup([0, 3, 6], [0, B], S), odst, ok.Setup([0, 2, 4, 6], [0, B], S2), (0, L, 0, B, 0, p))
+    for j in range(3):   # what GPU 1 saw right after its waits
+        assert np.array_equal(to_np(snaps[j][0]), odst[(j, 0)].K) and np.array_equal(to_np(snaps[j][1]), odst[(j, 0)].V), j
+    for st in sets:
+        dv.dv_dplan_free(ctxs[0], st)
+
+
 def test_flag_released_on_one_gpu_observed_on_the_other(ctxs):
     """A5 across GPUs: GPU 0 stores a chunk into GPU 1's memory and releases a seq flag there
     (st.release.sys). Three observers must never see the flag before the payload: (1) GPU 1's
