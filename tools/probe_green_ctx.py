@@ -35,7 +35,8 @@ ck(cu.cuInit(0))
 dev = ck(cu.cuDeviceGet(0))
 SMALL_SMS = int(os.environ.get("GREEN_SMS", "8"))
 res = ck(cu.cuDeviceGetDevResource(dev, cu.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM))
-groups, nb, rest = ck(cu.cuDevSmResourceSplitByCount(1, res, 0, SMALL_SMS))
+SPLIT_FLAGS = int(os.environ.get("SPLIT_FLAGS", "0"))   # cuDevSmResourceSplitByCount useFlags (1 ignore co-scheduling, 2 max cluster)
+groups, nb, rest = ck(cu.cuDevSmResourceSplitByCount(1, res, SPLIT_FLAGS, SMALL_SMS))
 d_small = ck(cu.cuDevResourceGenerateDesc([groups[0]], 1))
 d_big = ck(cu.cuDevResourceGenerateDesc([rest], 1))
 flag = cu.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM
@@ -45,7 +46,8 @@ lo_pr, hi_pr = torch.cuda.Stream.priority_range()
 NB = cu.CUstream_flags.CU_STREAM_NON_BLOCKING
 s_small = torch.cuda.ExternalStream(int(ck(cu.cuGreenCtxStreamCreate(g_small, NB, hi_pr))))
 s_big = torch.cuda.ExternalStream(int(ck(cu.cuGreenCtxStreamCreate(g_big, NB, 0))))
-print(json.dumps({"sms_small": groups[0].sm.smCount, "sms_big": rest.sm.smCount}), flush=True)
+print(json.dumps({"sms_small": groups[0].sm.smCount, "sms_big": rest.sm.smCount, "split_flags": SPLIT_FLAGS}),
+      flush=True)
 
 L, H, D, B, P, S = 40, 40, 128, 8, 1000, 2048
 LAYER = 2 * B * H * D * 2
