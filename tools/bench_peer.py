@@ -368,6 +368,14 @@ class C5:
             us = ((ts[:, 0] - t0).double() / 1e3).tolist()[20:]
             out[arm] = {"start_to_flag_p50_us": env.max(_pct(us, 0.5)), "start_to_flag_p99_us": env.max(_pct(us, 0.99)),
                         "n": len(us)}
+            # every word the predecessor's producer stored into this rank's replica at position q
+            env.barrier()
+            cnt = torch.zeros(1, dtype=torch.int64, device=env.dev)
+            dv.dvt_verify(self.rep, cnt.data_ptr(), seed=SEED_C5,
+                          reg=dv.region(self.pred * self.Ls, self.pred * self.Ls + self.Ls, 0, self.b, q, q + 1),
+                          stream=self.sp)
+            torch.cuda.synchronize()
+            out[arm]["replica_mismatches"] = int(env.max(float(cnt.item())))
         out["bytes"] = self.layer_bytes_tok
         out["release_scope"] = "system" if plans[0].sys_scope else "gpu"
         for pl in plans:
