@@ -1,4 +1,7 @@
-/* dv_device.cuh -- device-side consumer helpers for dvstream sequence flags (header only, CUDA).
+/* dv_device.cuh -- device-side helpers of dvstream (header only, CUDA): consumers acquiring a
+ * sequence flag (below), PRODUCERS storing the K/V rows they compute straight to a stream-out
+ * destination through a device plan and releasing its flag (dv_dplan_*, end of file; include/dv.h),
+ * and producers ringing a persistent-engine doorbell.
  *
  * SURVEY §8(a) A5 / PAPER.md:123-135: a chunk is complete once its 64-bit monotone sequence flag
  * reaches the chunk's seq. Host code waits with dv_wait (a stream-ordered cuStreamWaitValue64);
