@@ -257,3 +257,34 @@ def test_c_program_runs_the_headline_token_steps():
     assert r.returncode == 0, r.stdout + r.stderr
     d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert d["steps"] == 500 and d["c2_token_steps_from_C_gbs"] > 0
+
+
+def test_struct_layouts_match_the_c_header(tmp_path):
+    """Every public struct of include/dv.h has the same size and field offsets in the Python
+    binding (ctypes) as in C (gcc compiles offsetof / sizeof of each field): the binding can only
+    marshal what the C ABI declares."""
+    import ctypes as C
+    import subprocess
+    structs = {"dv_cache": dv.dv_cache, "dv_region": dv.dv_region, "dv_setup": dv.dv_setup,
+               "dv_piece": dv.dv_piece, "dv_endpoint": dv.dv_endpoint, "dv_config": dv.dv_config,
+               "dv_ipc_blob": dv.dv_ipc_blob, "dv_dplan": dv.dv_dplan, "dv_dplan_set": dv.dv_dplan_set}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dv.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} sizeof %zu\\n", sizeof({name}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0]}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for line in out:
+        if line:
+            name, field, val = line.split()
+            got[(name, field)] = int(val)
+    for name, cls in structs.items():
+        assert got[(name, "sizeof")] == C.sizeof(cls), name
+        for f in cls._fields_:
+            assert got[(name, f[0])] == getattr(cls, f[0]).offset, (name, f[0])
