@@ -37,7 +37,7 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
 DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region* region, uint64_t* t_end,
                                uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
 
-/* A vectorised synthetic PRODUCER (kind HASH words of `region` of KV5D cache `c`, 16-byte stores,
+/* A vectorised synthetic PRODUCER (kind HASH words of `region` of cache `c`, KV5D or FT6D key, 16-byte stores,
  * one thread per 16-byte chunk in a grid-stride loop of at most 4 x SMs CTAs of 256 threads -- the
  * shape of a producer's grid, so few CTAs join the plans' release). With `n_plans` plans (include/dv.h
  * dv_dplan_*; <= DV_DPLAN_SET_MAX, disjoint regions, e.g. a dv_dplan_set) it also stores every

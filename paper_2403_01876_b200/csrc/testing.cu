@@ -137,7 +137,10 @@ __global__ void k_fill_rows(const RowsParams rp) {
       w[j] = (uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j) |
              ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
     const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint4*>(base + (int64_t)s * p.D + d0) = v;
+    if (p.ft6d && kv == 0)   // the producer's own FT6D key: packet d0/8 of position s, S*16 bytes apart
+      *reinterpret_cast<uint4*>(base + ((int64_t)(d0 >> 3) * p.S + s) * 8) = v;
+    else
+      *reinterpret_cast<uint4*>(base + (int64_t)s * p.D + d0) = v;
     if (rp.plans.n) {   // packet d0/8 of the row (FT6D-key destinations: packets S*16 bytes apart)
       uint8_t* dst = dv_dplan_set_packet(&rp.plans, rp.step, kv, l, r, h, s, d0 / 8);
       if (dst) *reinterpret_cast<uint4*>(dst) = v;
@@ -330,7 +333,6 @@ extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_re
   RowsParams rp{};
   uint64_t slabs;
   DV_TRY(fill_params(c, DVT_FILL_HASH, seed, nullptr, 0, 1 << 30, region, &rp.f, &slabs));
-  if (c->layout != DV_LAYOUT_KV5D) return fail(DV_ENOTSUP, "dvt_fill_rows writes KV5D caches only");
   if (c->head_dim % 8) return fail(DV_EALIGN, "dvt_fill_rows needs head_dim %% 8 == 0");
   if (!slabs) return fail(DV_EINVAL, "empty region");
   rp.f.t_end = (unsigned long long*)t_end;

@@ -132,6 +132,31 @@ def test_fused_producer_remap_into_an_ft6d_cache():
     assert np.array_equal(to_np(dk), do.K) and np.array_equal(to_np(dvv), do.V)
 
 
+def test_fused_producer_with_an_ft6d_cache():
+    """A producer whose own cache keeps FasterTransformer's 6-D key (packets S*16 bytes apart)
+    streams a region to a device wire through a scatter plan: its cache == kvgen's words in FT6D,
+    the wire == oracle.pack of that cache (position-major: the plan transposes nothing, the
+    producer already holds each row)."""
+    L, B, H, S, D = 2, 3, 4, 40, 64
+    K, V = kvgen.kv5d_cache("hash", 0, L, 0, B, H, S, D, seed=SEED)
+    K6 = kvgen.as_ft6d_key(K)
+    k6 = torch.zeros(K6.shape, dtype=torch.int16, device="cuda")
+    v = torch.zeros(V.shape, dtype=torch.int16, device="cuda")
+    c6 = dv.cache(k6, v)
+    o = ok.Cache(K6, V, 0, 0, H, S, D, ok.LAYOUT_FT6D, 0)
+    reg = (0, L, 1, B, 7, 19, 1, 4)
+    nb = ok.region_bytes(*reg[:6], reg[7] - reg[6], D, 2)
+    buf = sentinel_like((nb // 2,))
+    fl = flags(1)
+    plan = dv.dv_dplan_scatter(ctx(), c6, dv.region(*reg), dv.endpoint_of(buf, fl), 0, flag_slot=0, seq=3)
+    torch.cuda.synchronize()
+    dv.dvt_fill_rows(c6, SEED, dv.region(0, L, 0, B, 0, S), plan, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(k6), K6) and np.array_equal(to_np(v), V)
+    assert np.array_equal(to_np(buf), ok.pack(o, reg)) and int(fl[0]) == 3
+    dv.dv_dplan_free(ctx(), plan)
+
+
 def _blocks(setup):
     for i in range(setup.n_stages):
         for u in range(setup.n_micro):
