@@ -37,7 +37,9 @@ DV_API dv_status dvt_fill(const dv_cache* c, int32_t kind, uint64_t seed, const 
 DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region* region, uint64_t* t_end,
                                uint64_t* doorbell, uint64_t step, uint32_t* ticket, void* stream);
 
-/* A vectorised synthetic PRODUCER (kind HASH words of `region` of cache `c`, KV5D or FT6D key, 16-byte stores,
+/* A vectorised synthetic PRODUCER (dvt_fill's words of `kind` / `seed` / `box` -- HASH is ALU-heavy,
+ * UID a few integer ops per word, i.e. a memory-bound producer -- for `region` of cache `c`, KV5D or
+ * FT6D key, 16-byte stores,
  * one thread per 16-byte chunk in a grid-stride loop of at most 4 x SMs CTAs of 256 threads -- the
  * shape of a producer's grid, so few CTAs join the plans' release). With `n_plans` plans (include/dv.h
  * dv_dplan_*; <= DV_DPLAN_SET_MAX, disjoint regions, e.g. a dv_dplan_set) it also stores every
@@ -46,9 +48,9 @@ DV_API dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_region
  * dv_dplan_set_packet / dv_dplan_set_release). t_start / t_end (optional,
  * device uint64, preset by the caller): min over CTAs of %globaltimer at kernel start / max after
  * the CTA's stores. Triggers programmatic dependent launch at its start. */
-DV_API dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
-                               const dv_dplan* plans, int32_t n_plans, int32_t step, uint64_t* t_start,
-                               uint64_t* t_end, void* stream);
+DV_API dv_status dvt_fill_rows(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                               const dv_region* region, const dv_dplan* plans, int32_t n_plans, int32_t step,
+                               uint64_t* t_start, uint64_t* t_end, void* stream);
 
 /* Verifier (the second, on-device parity check of SURVEY §8(c) C-5 at full sizes): adds to
  * *mismatches (device memory, uint64) the number of words of `region` that differ from the

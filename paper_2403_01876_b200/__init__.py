@@ -179,8 +179,8 @@ _SIGS = {
     "dvt_launch_count": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
     "dvt_fill": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32, C.c_int32,
                            P(dv_region), C.c_void_p, C.c_void_p]),
-    "dvt_fill_rows": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), P(dv_dplan), C.c_int32, C.c_int32,
-                                C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dvt_fill_rows": (C.c_int, [P(dv_cache), C.c_int32, C.c_uint64, P(C.c_int32), P(dv_region), P(dv_dplan),
+                                C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dvt_fill_ring": (C.c_int, [P(dv_cache), C.c_uint64, P(dv_region), C.c_void_p, C.c_void_p, C.c_uint64,
                                 C.c_void_p, C.c_void_p]),
     "dvt_verify": (C.c_int, [P(dv_cache), C.c_void_p, C.c_int32, C.c_uint64, P(C.c_int32), C.c_int32,
@@ -825,8 +825,9 @@ def dvt_fill(c: dv_cache, kind, seed=0, box=None, valid=(0, 1 << 30), reg: dv_re
           _stream(stream))
 
 
-def dvt_fill_rows(c: dv_cache, seed, reg, plan=None, step=0, t_start_ptr=0, t_end_ptr=0, stream=None):
-    """plan: None, a dv_dplan, a dv_dplan_set or a list of dv_dplan."""
+def dvt_fill_rows(c: dv_cache, seed, reg, plan=None, step=0, t_start_ptr=0, t_end_ptr=0, stream=None,
+                  kind=DVT_FILL_HASH, box=None):
+    """plan: None, a dv_dplan, a dv_dplan_set or a list of dv_dplan; kind / box as dvt_fill."""
     if plan is None:
         arr, n = None, 0
     elif isinstance(plan, dv_dplan):
@@ -835,7 +836,8 @@ def dvt_fill_rows(c: dv_cache, seed, reg, plan=None, step=0, t_start_ptr=0, t_en
         arr, n = (plan.plan if plan.n else None), plan.n
     else:
         arr, n = (dv_dplan * len(plan))(*plan), len(plan)
-    _call("dvt_fill_rows", C.byref(c), seed, _reg_ct(reg), arr, n, step, C.c_void_p(t_start_ptr),
+    b = (C.c_int32 * 5)(*box) if box is not None else None
+    _call("dvt_fill_rows", C.byref(c), kind, seed, b, _reg_ct(reg), arr, n, step, C.c_void_p(t_start_ptr),
           C.c_void_p(t_end_ptr), _stream(stream))
 
 

@@ -118,24 +118,33 @@ __global__ void k_fill_rows(const RowsParams rp) {
   const int cpr = p.D / 8;   // 16-byte chunks per row
   const int64_t per_slab = (int64_t)p.n * cpr;
   const int64_t total = 2 * rp.slabs * per_slab;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ks = i / per_slab;              // kv * slabs + slab
-    const int64_t in_slab = i - ks * per_slab;
-    const int kv = (int)(ks / rp.slabs);
-    uint32_t slab = (uint32_t)(ks - (int64_t)kv * rp.slabs);
-    const int h = p.h0 + (int)(slab % p.H);
-    slab /= p.H;
-    const int r = p.r0 + (int)(slab % p.nR);
-    const int l = p.l0 + (int)(slab / p.nR);
-    const int s = p.s0 + (int)(in_slab / cpr);
-    const int d0 = (int)(in_slab % cpr) * 8;
+  // (32-bit index math: the host keeps total < 2^32)
+  const uint32_t ps32 = (uint32_t)per_slab, slabs32 = (uint32_t)rp.slabs;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (uint32_t)total; i += gridDim.x * blockDim.x) {
+    const uint32_t ks = i / ps32;                 // kv * slabs + slab
+    const uint32_t in_slab = i - ks * ps32;
+    const int kv = (int)(ks / slabs32);
+    uint32_t slab = ks - (uint32_t)kv * slabs32;
+    const int h = p.h0 + (int)(slab % (uint32_t)p.H);
+    slab /= (uint32_t)p.H;
+    const int r = p.r0 + (int)(slab % (uint32_t)p.nR);
+    const int l = p.l0 + (int)(slab / (uint32_t)p.nR);
+    const int s = p.s0 + (int)(in_slab / (uint32_t)cpr);
+    const int d0 = (int)(in_slab % (uint32_t)cpr) * 8;
     uint16_t* base = (kv ? p.v : p.k) + (int64_t)(l - p.lb) * p.s_l + (int64_t)(r - p.rb) * p.s_r +
                      (int64_t)(h - p.hb) * p.s_h;
     uint32_t w[4];
+    if (p.kind == DVT_FILL_UID && s >= p.vlo && s < p.vhi) {   // the uid of d0, then + 1 per word
+      const uint32_t u0 = (uint32_t)gen_word(p, kv, l, r, h, s, d0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      w[j] = (uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j) |
-             ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
+      for (int j = 0; j < 4; ++j)
+        w[j] = ((u0 + 2 * j) & 0xFFFFu) | (((u0 + 2 * j + 1) & 0xFFFFu) << 16);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        w[j] = (uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j) |
+               ((uint32_t)gen_word(p, kv, l, r, h, s, d0 + 2 * j + 1) << 16);
+    }
     const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
     if (p.ft6d && kv == 0)   // the producer's own FT6D key: packet d0/8 of position s, S*16 bytes apart
       *reinterpret_cast<uint4*>(base + ((int64_t)(d0 >> 3) * p.S + s) * 8) = v;
@@ -327,12 +336,12 @@ extern "C" dv_status dvt_fill_ring(const dv_cache* c, uint64_t seed, const dv_re
   return DV_OK;
 }
 
-extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_region* region,
-                                   const dv_dplan* plans, int32_t n_plans, int32_t step, uint64_t* t_start,
-                                   uint64_t* t_end, void* stream) {
+extern "C" dv_status dvt_fill_rows(const dv_cache* c, int32_t kind, uint64_t seed, const int32_t* box,
+                                   const dv_region* region, const dv_dplan* plans, int32_t n_plans, int32_t step,
+                                   uint64_t* t_start, uint64_t* t_end, void* stream) {
   RowsParams rp{};
   uint64_t slabs;
-  DV_TRY(fill_params(c, DVT_FILL_HASH, seed, nullptr, 0, 1 << 30, region, &rp.f, &slabs));
+  DV_TRY(fill_params(c, kind, seed, box, 0, 1 << 30, region, &rp.f, &slabs));
   if (c->head_dim % 8) return fail(DV_EALIGN, "dvt_fill_rows needs head_dim %% 8 == 0");
   if (!slabs) return fail(DV_EINVAL, "empty region");
   rp.f.t_end = (unsigned long long*)t_end;
@@ -346,6 +355,8 @@ extern "C" dv_status dvt_fill_rows(const dv_cache* c, uint64_t seed, const dv_re
   rp.plans.n = n_plans;
   rp.step = step;
   rp.slabs = (int64_t)slabs;
+  if (2 * (int64_t)slabs * rp.f.n * (c->head_dim / 8) >= (1ll << 32))
+    return fail(DV_ENOTSUP, "dvt_fill_rows: region too large for one launch (2^32 chunks)");
   // one thread per 16-byte chunk, 256-thread CTAs, at most 4 CTAs per SM (a producer's grid):
   // few CTAs take part in the plans' release ticket chains
   const int64_t chunks = 2 * (int64_t)slabs * rp.f.n * (c->head_dim / 8);
