@@ -288,3 +288,22 @@ def test_struct_layouts_match_the_c_header(tmp_path):
         assert got[(name, "sizeof")] == C.sizeof(cls), name
         for f in cls._fields_:
             assert got[(name, f[0])] == getattr(cls, f[0]).offset, (name, f[0])
+
+
+def test_binding_signatures_match_the_c_prototypes():
+    """Every function the Python binding declares (ctypes argtypes) takes as many arguments as its
+    prototype in include/*.h: the binding cannot drift from the C ABI unnoticed."""
+    import re
+    protos = {}
+    for h in ("dv.h", "dv_trace.h", "dv_testing.h", "dv_baselines.h"):
+        text = open(os.path.join(ROOT, "include", h)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for m in re.finditer(r"DV_API\s+[\w\s\*]+?\b(\w+)\s*\(([^)]*)\)\s*;", text):
+            args = m.group(2).strip()
+            protos[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    checked = 0
+    for name, (_res, argtypes) in dv._SIGS.items():
+        assert name in protos, f"{name} is bound but not declared in include/*.h"
+        assert len(argtypes) == protos[name], (name, len(argtypes), protos[name])
+        checked += 1
+    assert checked >= 60
