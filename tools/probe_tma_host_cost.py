@@ -1,5 +1,8 @@
+"""Host time per dv_scatter call of a C2 FT6D prompt layer with the register transpose and with the
+TMA-row form (tensor-map encode + occupancy query per call), the GPU kept busy by a spin so the
+host time is not hidden: is the TMA form host-bound back to back? (profiles/r02f_tma_host_cost.jsonl)"""
 import os, sys, time, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2403_01876_b200 as dv
 L, H, D, B, P, S = 4, 40, 128, 8, 1000, 2048
